@@ -1,0 +1,328 @@
+"""Benchmark: one FMM evaluate (P2M, M2M, M2L + check->local solve, L2L,
+L2P, P2P) of BASELINE config 2 per step - 1M uniform points in [0,1]^3,
+charges U[0,1), float32, p=4, depth 5, BLAS-M2L with sigma_min 1e-6.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  ``value`` = evaluate Mpoints/s with the
+charges already resident in HBM (device-timed, CUDA events, L2 flushed
+between steps); ``e2e`` = the same through the public API
+(``FmmInstance.evaluate`` on host charges, H2D + D2H inside the timed
+region); ``m2l`` = M2L GFLOP/s from SURVEY 8(d)'s algorithmic flop count;
+``roofline`` = the dominant kernel against its measured pipe peak;
+``cpu_baseline`` = the reference (Cython-compiled, unmodified) evaluate on
+this host's cores.  ``--impl reference`` times that reference alone.
+Multi-GPU (torchrun, N>1): the octree is partitioned by level-2 subtrees,
+M2L multipole halos are exchanged with NCCL; strong scaling of the same 1M
+points (BASELINE metric "1M pts, 1/2/4/8 GPU").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "M2L GFLOP/s (% roofline) & FMM eval Mpoints/s, Laplace 3D, 1M pts, 1/2/4/8 GPU"
+CONFIG = dict(depth=5, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6)
+N_POINTS = 1_000_000
+POINT_SEED, CHARGE_SEED = 7, 11
+
+
+def inputs(n=N_POINTS):
+    pts = np.random.default_rng(POINT_SEED).random((n, 3))     # generate_points("uniform-cube")
+    q = np.random.default_rng(CHARGE_SEED).random(n)
+    return pts, q
+
+
+def workload(n=N_POINTS):
+    return dict(workload="BASELINE config 2: Laplace 3D kiFMM evaluate, N=1,000,000 uniform "
+                         "[0,1]^3 sources=targets, charges U[0,1), float32, p=4 (56-point "
+                         "surfaces), uniform octree depth 5, BLAS-M2L sigma_min 1e-6, potential",
+                n_points=n, seeds={"points": POINT_SEED, "charges": CHARGE_SEED}, **CONFIG)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if "Active" in v
+                          and "Not" not in v})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- work counts
+def m2l_flops(inst):
+    """per level 2 N_s n_e k + 4 k sum_t m_t k_t + 2 N_t k n_c
+    (+ 2 N_t r_d (n_c + n_e) for the solve the reference times inside M2L)."""
+    ops = inst.blas_ops
+    k = ops.k
+    ranks = ops.ranks
+    exp = inst.expansions
+    n_e, n_c, r_d = exp.n_equiv, exp.n_check, exp.down_inv.rank
+    apply_f = solve_f = bucket_f = 0.0
+    per_level = {}
+    for lvl, b in inst.buckets.items():
+        n_s = inst.source_tree.level_keys(lvl).shape[0]
+        n_t = inst.target_tree.level_keys(lvl).shape[0]
+        bk = sum(4.0 * k * p[0].shape[0] * ranks[i] for i, p in enumerate(b.pairs) if p is not None)
+        f = 2.0 * n_s * n_e * k + bk + 2.0 * n_t * k * n_c
+        apply_f += f
+        bucket_f += bk
+        solve_f += 2.0 * n_t * r_d * (n_c + n_e)
+        per_level[lvl] = dict(apply=f, bucket=bk, pairs=int(sum(p[0].shape[0] for p in b.pairs
+                                                              if p is not None)))
+    return apply_f, apply_f + solve_f, per_level
+
+
+def probe_peak(kind):
+    """Measured pipe peak in TFLOP/s (kind 0 FFMA f32, 1 DFMA f64) or
+    Gop/s (kind 2, MUFU rsqrt)."""
+    import torch
+    from paper_2408_07436_b200 import _native as nat
+    nat.load()
+    blocks, threads, iters = 148 * 8, 256, 4096
+    out = torch.empty(blocks * threads, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        nat.call("kifmm_probe", kind, blocks, threads, iters, out.data_ptr(), s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    nat.call("kifmm_probe", kind, blocks, threads, iters, out.data_ptr(), s)
+    e1.record()
+    torch.cuda.synchronize()
+    ops = blocks * threads * iters * 128.0
+    sec = e0.elapsed_time(e1) / 1e3
+    return (2 * ops / sec / 1e12) if kind in (0, 1) else ops / sec / 1e9
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_reference_run(pts, q, steps=1, warmup=0, kw=None):
+    """Unmodified reference evaluate (oracle/_ref, Cython-compiled from
+    /root/reference) on this host; falls back to the oracle port."""
+    kw = kw or CONFIG
+    os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
+    from oracle import reference_available
+    cores = os.cpu_count() or 1
+    if reference_available():
+        from oracle.ref_bridge import make_reference_instance
+        inst = make_reference_instance(pts, pts, threads=cores, **kw)
+        kind = "reference"
+        run = inst.evaluate
+    else:
+        from oracle import port
+        from paper_2408_07436_b200 import FmmConfig, setup
+        inst = setup(pts, pts, FmmConfig(**kw))
+        kind = "port"
+        run = lambda qq: port.evaluate(inst, qq, threads=cores)[:, 0]   # noqa: E731
+    for _ in range(warmup):
+        run(q)
+    times, pot = [], None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        pot = run(q)
+        times.append(time.perf_counter() - t0)
+    return dict(kind=kind, cores=cores, times=times, potentials=pot,
+                timings=getattr(inst, "timings", {}))
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    pts, q = inputs()
+    steps = max(1, args.steps)
+    res = cpu_reference_run(pts, q, steps=steps, warmup=min(args.warmup, 1))
+    sec = float(np.mean(res["times"]))
+    value = N_POINTS / sec / 1e6
+    line = dict(metric=METRIC, value=value, unit="Mpoints/s", impl="reference",
+                n_gpus=args.gpus, steps=steps, warmup=min(args.warmup, 1),
+                ms_per_step=sec * 1e3, higher_is_better=True, scaling="strong",
+                vs_baseline=None, dtype="f32", data="synthetic", config=workload(),
+                cpu_baseline=dict(value=value, unit="Mpoints/s", cores=res["cores"],
+                                  kind=res["kind"],
+                                  sample=f"full workload, {steps} evaluate(s) of 1M points, "
+                                         f"threads={res['cores']}, OMP_WAIT_POLICY=PASSIVE"),
+                e2e=dict(value=value, unit="Mpoints/s", h2d_bytes_per_step=0,
+                         d2h_bytes_per_step=0),
+                m2l_seconds=float(res["timings"].get("m2l", 0.0)),
+                operator_seconds={k: float(v) for k, v in res["timings"].items()})
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ ours
+def run_single(args):
+    import torch
+    from paper_2408_07436_b200 import FmmConfig, setup
+    from paper_2408_07436_b200.device import profile_launches
+
+    torch.cuda.set_device(0)
+    pts, q = inputs()
+    t0 = time.perf_counter()
+    inst = setup(pts, pts, FmmConfig(**CONFIG))
+    setup_s = time.perf_counter() - t0
+    dev = inst.device
+    q_dev = torch.from_numpy(q.reshape(-1, 1)).cuda().reshape(-1)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        dev.evaluate_device(q_dev, 1)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        for e0, e1 in ev:
+            flush.zero_()                      # evict L2 between steps (not timed)
+            e0.record()
+            dev.evaluate_device(q_dev, 1)
+            e1.record()
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    value = N_POINTS / (ms / 1e3) / 1e6
+
+    # per-launch profile of one step (separate, untimed pass)
+    flush.zero_()
+    with profile_launches() as prof:
+        dev.evaluate_device(q_dev, 1, timings=True)
+    launches = prof.times()
+    phases = dev.collect_timings()
+    per_kernel = {}
+    for name, tag, t in launches:
+        key = name.replace("kifmm_", "")
+        per_kernel[key] = per_kernel.get(key, 0.0) + t
+    n_launch = len(launches)
+    pot_dev = dev.evaluate_device(q_dev, 1).cpu().numpy()[:, 0].copy()
+
+    # M2L GFLOP/s: algorithmic flops over the M2L phases (incl. the solve, as
+    # the reference times it)
+    f_apply, f_total, per_level = m2l_flops(inst)
+    m2l_s = phases.get("m2l", 0.0)
+    sweep_t = {t: ms_ for n, t, ms_ in launches if "m2l_sweep" in n}
+    # dominant kernel
+    dom = max(per_kernel.items(), key=lambda kv: kv[1])
+    peak_f32 = probe_peak(0)
+    if "m2l_sweep" in dom[0]:
+        lvl = inst.config.depth
+        achieved = per_level[lvl]["bucket"] / (sweep_t[f"m2l{lvl}"] / 1e3) / 1e12
+        roof = dict(bound="fp32", kernel="m2l_sweep_f32 (finest level)", achieved=achieved,
+                    peak=peak_f32, unit="TFLOP/s", frac=achieved / peak_f32, traffic=None,
+                    algorithmic="4 k sum_t m_t k_t flops at level %d" % lvl)
+    else:
+        inter = inst.n_near_pairs
+        leaf_ms = per_kernel[dom[0]]
+        achieved = 11.0 * inter / (leaf_ms / 1e3) / 1e12
+        roof = dict(bound="fp32", kernel=dom[0], achieved=achieved, peak=peak_f32,
+                    unit="TFLOP/s", frac=achieved / peak_f32, traffic=None,
+                    algorithmic="11 flop x %d P2P interactions (L2P fused, not counted)" % inter)
+    roof["peak_source"] = "kifmm_probe FFMA, measured in this run (MEASURED_PEAKS.json has no FP32 figure)"
+
+    # e2e through the public API (host charges in pinned memory -> host potentials)
+    q_pinned = torch.from_numpy(q).pin_memory().numpy()
+    for _ in range(2):
+        inst.evaluate(q_pinned)
+    e2e_t = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = inst.evaluate(q_pinned)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_value = N_POINTS / float(np.mean(e2e_t)) / 1e6
+
+    # CPU baseline (reference, bounded sample: one full evaluate) + parity of this run
+    cpu = None
+    if not args.no_cpu_baseline:
+        res = cpu_reference_run(pts, q, steps=1)
+        csec = min(res["times"])
+        ref = np.asarray(res["potentials"], dtype=np.float64)
+        rel = np.abs(out.astype(np.float64) - ref) / np.abs(ref)
+        cpu = dict(value=N_POINTS / csec / 1e6, unit="Mpoints/s", cores=res["cores"],
+                   kind=res["kind"], sample="one full 1M-point evaluate, all host threads, "
+                   "OMP_WAIT_POLICY=PASSIVE", seconds=csec,
+                   operator_seconds={k: float(v) for k, v in res["timings"].items()},
+                   parity_max_rel=float(rel.max()), parity_tol=1e-5)
+    line = dict(metric=METRIC, value=value, unit="Mpoints/s", n_gpus=1, steps=args.steps,
+                warmup=args.warmup, ms_per_step=ms, higher_is_better=True, scaling="strong",
+                vs_baseline=None, dtype="f32", data="synthetic (seeded; no dataset involved)",
+                config=dict(workload(), l2="flushed between steps (256 MB write)",
+                            parallelism="1 GPU"),
+                m2l=dict(gflops=f_total / m2l_s / 1e9 if m2l_s else None,
+                         seconds=m2l_s, flops_apply=f_apply, flops_with_solve=f_total),
+                operator_seconds=phases, kernel_ms=per_kernel, roofline=roof,
+                cpu_baseline=cpu,
+                e2e=dict(value=e2e_value, unit="Mpoints/s", h2d_bytes_per_step=int(q.nbytes),
+                         d2h_bytes_per_step=int(out.nbytes)),
+                gpu_launches=n_launch * args.steps, clocks=clk.summary(),
+                setup_seconds=setup_s, p2p_interactions=inst.n_near_pairs)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2408_07436_b200 import distributed
+        return distributed.bench_main(args, sys.modules[__name__])
+    return run_single(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,169 @@
+/*
+ * kifmm_b200.h - C ABI of the B200 (sm_100a) kiFMM hot path.
+ *
+ * All entry points are extern "C", take DEVICE pointers plus sizes and a
+ * CUDA stream handle (cudaStream_t passed as void*), never allocate, and
+ * return an int status: 0 = ok, KIFMM_EARG (10001) = bad argument,
+ * otherwise the cudaError_t of the launch.  Buffers are C-contiguous.
+ * "accumulate" outputs follow the reference semantics (+=).
+ *
+ * Two groups:
+ *  (1) the reference's native plug-in boundary, one function per loop of
+ *      kifmm3d/_hot.pyx, bound in the reference through hotloops.py;
+ *  (2) the level/leaf passes the reference runs through numpy inside
+ *      engine.evaluate (engine.py:270-404), which the device engine chains
+ *      without host round trips.
+ */
+#ifndef KIFMM_B200_H
+#define KIFMM_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KIFMM_EARG 10001
+
+/* ---- (1) kernel-level boundary ------------------------------------------ */
+
+/* Replaces _hot.laplace_potentials (_hot.pyx:24-65, bound at hotloops.py:54-57):
+ * out[i, r] += sum_j K(t_i, s_j) * charges[j, r], K = 1/(4 pi r), 0 if r == 0. */
+int kifmm_laplace_potentials_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
+                                 const float* sx, const float* sy, const float* sz, int64_t ns,
+                                 const float* charges, int64_t nrhs, float* out, void* stream);
+int kifmm_laplace_potentials_f64(const double* tx, const double* ty, const double* tz, int64_t nt,
+                                 const double* sx, const double* sy, const double* sz, int64_t ns,
+                                 const double* charges, int64_t nrhs, double* out, void* stream);
+
+/* Replaces _hot.laplace_matrix (_hot.pyx:68-88, hotloops.py:60-64): out[i, j] = K(t_i, s_j). */
+int kifmm_laplace_matrix_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
+                             const float* sx, const float* sy, const float* sz, int64_t ns,
+                             float* out, void* stream);
+int kifmm_laplace_matrix_f64(const double* tx, const double* ty, const double* tz, int64_t nt,
+                             const double* sx, const double* sy, const double* sz, int64_t ns,
+                             double* out, void* stream);
+
+/* Replaces _hot.p2p_blocked (_hot.pyx:91-138, hotloops.py:67-71): target i sums
+ * the gathered sources src_offsets[b] .. src_offsets[b+1] of its leaf
+ * b = leaf_of_target[i]; out[i, r] += that sum. */
+int kifmm_p2p_blocked_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
+                          const int64_t* leaf_of_target, const float* sx, const float* sy,
+                          const float* sz, const float* charges, int64_t nrhs,
+                          const int64_t* src_offsets, int64_t n_leaves, float* out, void* stream);
+int kifmm_p2p_blocked_f64(const double* tx, const double* ty, const double* tz, int64_t nt,
+                          const int64_t* leaf_of_target, const double* sx, const double* sy,
+                          const double* sz, const double* charges, int64_t nrhs,
+                          const int64_t* src_offsets, int64_t n_leaves, double* out, void* stream);
+
+/* Replaces _hot.hadamard_m2l (_hot.pyx:141-178, hotloops.py:74-77), complex
+ * interleaved (re, im):
+ * phat[f, c, tau, r] += sum_o sum_sigma khat[f, o, tau, sigma] * qhat[f, halo[c, o], sigma, r]
+ * khat (nf, 26, 8, 8), qhat (nf, nsc, 8, nrhs), halo (ntc, 26) (-1 = absent),
+ * phat (nf, ntc, 8, nrhs). */
+int kifmm_hadamard_m2l_c64(const float* khat, const float* qhat, const int64_t* halo, float* phat,
+                           int64_t nf, int64_t nsc, int64_t ntc, int64_t nrhs, void* stream);
+int kifmm_hadamard_m2l_c128(const double* khat, const double* qhat, const int64_t* halo,
+                            double* phat, int64_t nf, int64_t nsc, int64_t ntc, int64_t nrhs,
+                            void* stream);
+
+/* ---- (2) engine passes (device-resident evaluate) ------------------------ */
+
+/* Row-major C[rowmap(m), n] (=|+=) alpha * sum_k A[m, k] B[k, n] * colscale[n].
+ * rowmap NULL -> identity; rowmap[m] < 0 -> row skipped.  colscale may be NULL.
+ * Used for the projection/expansion of BLAS-M2L (m2l_blas.py:285,322) and the
+ * factored pseudo-inverse solves (expansion.py:78-82), M2M/L2L products. */
+int kifmm_gemm_f32(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
+                   const float* B, int64_t ldb, const float* colscale, float* C, int64_t ldc,
+                   const int32_t* rowmap, int accumulate, void* stream);
+int kifmm_gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, const double* colscale, double* C, int64_t ldc,
+                   const int32_t* rowmap, int accumulate, void* stream);
+
+/* P2M check potentials (engine.py:298-319): for source leaf l and check point c,
+ * phi[(l*nrhs + r)*nc + c] = sum_{j in leaf} K(center_l + base_c, s_j) q[j*nrhs + r];
+ * centers (n_leaves, 3) and base (nc, 3) are float64, summed exactly then rounded. */
+int kifmm_p2m_check_f32(const float* sx, const float* sy, const float* sz, const float* q,
+                        int64_t nrhs, const int32_t* leaf_start, const int32_t* leaf_count,
+                        int64_t n_leaves, const double* centers, const double* base, int64_t nc,
+                        float* phi, void* stream);
+int kifmm_p2m_check_f64(const double* sx, const double* sy, const double* sz, const double* q,
+                        int64_t nrhs, const int32_t* leaf_start, const int32_t* leaf_count,
+                        int64_t n_leaves, const double* centers, const double* base, int64_t nc,
+                        double* phi, void* stream);
+
+/* M2M child stacking (engine.py:321-334): out[(p*nrhs + r), c*ne + e] =
+ * mult[(child[p*8+c]*nrhs + r)*ne + e] or 0 where child < 0. */
+int kifmm_stack_children_f32(const float* mult, const int32_t* child, int64_t n_par, int64_t nrhs,
+                             int64_t ne, float* out, void* stream);
+int kifmm_stack_children_f64(const double* mult, const int32_t* child, int64_t n_par,
+                             int64_t nrhs, int64_t ne, double* out, void* stream);
+
+/* BLAS-M2L fused bucket sweep (m2l_blas.py:284-320), target-stationary:
+ * acc[(tgt*nrhs + r)*ko + a] = sum_j sum_b Dt[tv(j), b, a] * qt[(src*nrhs + r)*ki + b]
+ * over the 189 vectors j of each tile's parity class, in ascending order.
+ * qt (n_src*nrhs, ki) zero-padded; Dt (316, ki, ko) transposed dense cores.
+ * tile_targets (n_tiles*128), tile_class (n_tiles), src (n_tiles*128, 189),
+ * class_tv (8, 189).  Padding slots (target -1) are skipped. */
+int kifmm_m2l_sweep_f32(const float* qt, const float* Dt, int64_t ki, int64_t ko,
+                        const int32_t* tile_targets, const int32_t* tile_class,
+                        const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
+                        int64_t nrhs, float* acc, void* stream);
+int kifmm_m2l_sweep_f64(const double* qt, const double* Dt, int64_t ki, int64_t ko,
+                        const int32_t* tile_targets, const int32_t* tile_class,
+                        const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
+                        int64_t nrhs, double* acc, void* stream);
+
+/* FFT-M2L forward (m2l_fft.py:236-247): embed each box's multipole at
+ * lattice+p of the n^3 grid (n = 2p), real 3-D DFT, and write the spectrum
+ * frequency-major into qhat[(f*nsc + cluster)*8 + child)*nrhs + r] (complex).
+ * slot_box (nsc*8): box row of each cluster slot or -1 (zero spectrum). */
+int kifmm_fft_forward_f32(const float* mult, int64_t nrhs, int64_t order, const int32_t* slot_box,
+                          int64_t nsc, float* qhat, void* stream);
+int kifmm_fft_forward_f64(const double* mult, int64_t nrhs, int64_t order,
+                          const int32_t* slot_box, int64_t nsc, double* qhat, void* stream);
+
+/* FFT-M2L inverse (m2l_fft.py:252-261): for each target box b, take the
+ * spectrum phat[f, tgt_slot[b], r], inverse real 3-D DFT, read the
+ * lattice points and scale: check[(b*nrhs + r)*ne + e]. */
+int kifmm_fft_inverse_f32(const float* phat, int64_t nrhs, int64_t order, const int32_t* slot_box,
+                          int64_t ntc, double level_scale, float* check, void* stream);
+int kifmm_fft_inverse_f64(const double* phat, int64_t nrhs, int64_t order,
+                          const int32_t* slot_box, int64_t ntc, double level_scale, double* check,
+                          void* stream);
+
+/* Leaf pass: fused L2P + P2P + un-permute (engine.py:377-404).  For target
+ * leaf b and target i in it:
+ *   out[perm[i]*nrhs + r] = sum_e K(t_i, center_b + base_e) local[(b*nrhs+r)*ne + e]
+ *                         + sum_{near source leaves s of b, in order} sum_{j in s} K(t_i, s_j) q[j]
+ * near_off (n_leaves+1) / near_leaf: source-leaf CSR (own leaf first, then
+ * neighbours by Morton code, engine.py:231-240).  parts: bit 0 = L2P term,
+ * bit 1 = P2P term, bit 2 = accumulate into out instead of overwriting;
+ * perm NULL -> tree order. */
+int kifmm_leaf_pass_f32(const float* tx, const float* ty, const float* tz, const int32_t* tleaf_start,
+                        const int32_t* tleaf_count, int64_t n_tleaves, const double* centers,
+                        const double* base, int64_t ne, const float* local,
+                        const float* sx, const float* sy, const float* sz, const float* q,
+                        const int32_t* sleaf_start, const int32_t* sleaf_count,
+                        const int32_t* near_off, const int32_t* near_leaf, int64_t nrhs,
+                        const int64_t* perm, int parts, float* out, void* stream);
+int kifmm_leaf_pass_f64(const double* tx, const double* ty, const double* tz,
+                        const int32_t* tleaf_start, const int32_t* tleaf_count, int64_t n_tleaves,
+                        const double* centers, const double* base, int64_t ne, const double* local,
+                        const double* sx, const double* sy, const double* sz, const double* q,
+                        const int32_t* sleaf_start, const int32_t* sleaf_count,
+                        const int32_t* near_off, const int32_t* near_leaf, int64_t nrhs,
+                        const int64_t* perm, int parts, double* out, void* stream);
+
+/* Charge intake: q_tree[i*nrhs + r] = (T) q_in[perm[i]*nrhs + r] (float64 in). */
+int kifmm_gather_charges_f32(const double* q_in, const int64_t* perm, int64_t n, int64_t nrhs,
+                             float* q_tree, void* stream);
+int kifmm_gather_charges_f64(const double* q_in, const int64_t* perm, int64_t n, int64_t nrhs,
+                             double* q_tree, void* stream);
+
+/* Library identification: returns the compiled SM target (e.g. 100). */
+int kifmm_sm_target(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KIFMM_B200_H */

@@ -1,0 +1,182 @@
+// Tall-skinny SIMT GEMM for the level operators (projection/expansion of
+// BLAS-M2L, factored pseudo-inverse solves, M2M/L2L kernel products).
+// These are memory-bound (N, K <= a few hundred, M up to 2M rows), so a
+// register-tiled FFMA/DFMA kernel with shared-memory staging is enough; the
+// epilogue fuses the pseudo-inverse's diagonal (colscale), the level scale
+// (alpha), accumulation and the L2L child scatter (rowmap).
+#include "common.cuh"
+
+using namespace kifmm;
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4, NT = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t K, T alpha,
+                                                  const T* __restrict__ A, int64_t lda,
+                                                  const T* __restrict__ B, int64_t ldb,
+                                                  const T* __restrict__ colscale,
+                                                  T* __restrict__ C, int64_t ldc,
+                                                  const int32_t* __restrict__ rowmap,
+                                                  int accumulate) {
+  __shared__ T As[BK][BM + 4];
+  __shared__ T Bs[BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int tn = tid % (BN / TN), tm = tid / (BN / TN);
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+    // A tile: BM x BK, 4 elements per thread, stored transposed.
+#pragma unroll
+    for (int e = 0; e < (BM * BK) / NT; ++e) {
+      int idx = tid + e * NT;
+      int r = idx / BK, c = idx % BK;
+      int64_t gm = m0 + r, gk = k0 + c;
+      As[c][r] = (gm < M && gk < K) ? A[gm * lda + gk] : T(0);
+    }
+#pragma unroll
+    for (int e = 0; e < (BK * BN) / NT; ++e) {
+      int idx = tid + e * NT;
+      int r = idx / BN, c = idx % BN;
+      int64_t gk = k0 + r, gn = n0 + c;
+      Bs[r][c] = (gk < K && gn < N) ? B[gk * ldb + gn] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][tm * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tn + j * (BN / TN)];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    int64_t gm = m0 + tm * TM + i;
+    if (gm >= M) continue;
+    int64_t row = rowmap ? (int64_t)rowmap[gm] : gm;
+    if (row < 0) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      int64_t gn = n0 + tn + j * (BN / TN);
+      if (gn >= N) continue;
+      T v = acc[i][j];
+      if (colscale) v *= colscale[gn];
+      v *= alpha;
+      T* dst = C + row * ldc + gn;
+      *dst = accumulate ? *dst + v : v;
+    }
+  }
+}
+
+template <typename T>
+int gemm(int64_t M, int64_t N, int64_t K, T alpha, const T* A, int64_t lda, const T* B,
+         int64_t ldb, const T* colscale, T* C, int64_t ldc, const int32_t* rowmap, int accumulate,
+         void* stream) {
+  if (M < 0 || N < 0 || K < 0) return KIFMM_EARG;
+  if (M == 0 || N == 0) return 0;
+  dim3 grid(ceil_div(N, BN), ceil_div(M, BM));
+  if (grid.y > 65535u) {
+    // split very tall problems into row chunks
+    const int64_t chunk = (int64_t)65535 * BM;
+    for (int64_t m0 = 0; m0 < M; m0 += chunk) {
+      int64_t mm = M - m0 < chunk ? M - m0 : chunk;
+      int st = gemm<T>(mm, N, K, alpha, A + m0 * lda, lda, B, ldb, colscale,
+                       rowmap ? C : C + m0 * ldc, ldc, rowmap ? rowmap + m0 : nullptr, accumulate,
+                       stream);
+      if (st) return st;
+    }
+    return 0;
+  }
+  gemm_kernel<T><<<grid, NT, 0, (cudaStream_t)stream>>>(M, N, K, alpha, A, lda, B, ldb, colscale,
+                                                        C, ldc, rowmap, accumulate);
+  return launch_status();
+}
+
+template <typename T>
+__global__ void stack_kernel(const T* __restrict__ mult, const int32_t* __restrict__ child,
+                             int64_t n_par, int64_t nrhs, int64_t ne, T* __restrict__ out) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t width = 8 * ne;
+  if (idx >= n_par * nrhs * width) return;
+  int64_t row = idx / width, col = idx - row * width;
+  int64_t p = row / nrhs, r = row - p * nrhs;
+  int c = (int)(col / ne);
+  int64_t e = col - (int64_t)c * ne;
+  int32_t ch = child[p * 8 + c];
+  out[idx] = ch >= 0 ? mult[((int64_t)ch * nrhs + r) * ne + e] : T(0);
+}
+
+template <typename T>
+int stack(const T* mult, const int32_t* child, int64_t n_par, int64_t nrhs, int64_t ne, T* out,
+          void* stream) {
+  if (n_par < 0 || nrhs < 1 || ne < 1) return KIFMM_EARG;
+  int64_t total = n_par * nrhs * 8 * ne;
+  if (total == 0) return 0;
+  stack_kernel<T><<<ceil_div(total, 256), 256, 0, (cudaStream_t)stream>>>(mult, child, n_par,
+                                                                          nrhs, ne, out);
+  return launch_status();
+}
+
+template <typename T>
+__global__ void gather_charges_kernel(const double* __restrict__ qin,
+                                      const int64_t* __restrict__ perm, int64_t n, int64_t nrhs,
+                                      T* __restrict__ qt) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * nrhs) return;
+  int64_t i = idx / nrhs, r = idx - i * nrhs;
+  qt[idx] = (T)qin[perm[i] * nrhs + r];
+}
+
+}  // namespace
+
+extern "C" {
+
+int kifmm_gemm_f32(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
+                   const float* B, int64_t ldb, const float* colscale, float* C, int64_t ldc,
+                   const int32_t* rowmap, int accumulate, void* s) {
+  return gemm<float>(M, N, K, alpha, A, lda, B, ldb, colscale, C, ldc, rowmap, accumulate, s);
+}
+int kifmm_gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, const double* colscale, double* C, int64_t ldc,
+                   const int32_t* rowmap, int accumulate, void* s) {
+  return gemm<double>(M, N, K, alpha, A, lda, B, ldb, colscale, C, ldc, rowmap, accumulate, s);
+}
+int kifmm_stack_children_f32(const float* mult, const int32_t* child, int64_t n_par, int64_t nrhs,
+                             int64_t ne, float* out, void* s) {
+  return stack<float>(mult, child, n_par, nrhs, ne, out, s);
+}
+int kifmm_stack_children_f64(const double* mult, const int32_t* child, int64_t n_par,
+                             int64_t nrhs, int64_t ne, double* out, void* s) {
+  return stack<double>(mult, child, n_par, nrhs, ne, out, s);
+}
+int kifmm_gather_charges_f32(const double* qin, const int64_t* perm, int64_t n, int64_t nrhs,
+                             float* qt, void* s) {
+  if (n < 0 || nrhs < 1) return KIFMM_EARG;
+  if (n == 0) return 0;
+  gather_charges_kernel<float><<<ceil_div(n * nrhs, 256), 256, 0, (cudaStream_t)s>>>(qin, perm, n,
+                                                                                   nrhs, qt);
+  return launch_status();
+}
+int kifmm_gather_charges_f64(const double* qin, const int64_t* perm, int64_t n, int64_t nrhs,
+                             double* qt, void* s) {
+  if (n < 0 || nrhs < 1) return KIFMM_EARG;
+  if (n == 0) return 0;
+  gather_charges_kernel<double><<<ceil_div(n * nrhs, 256), 256, 0, (cudaStream_t)s>>>(
+      qin, perm, n, nrhs, qt);
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,246 @@
+// Kernel-level plug-in boundary: device versions of the four loops of the
+// reference's kifmm3d/_hot.pyx (bound through hotloops.py:54-77).
+//
+// Semantics kept from the reference:
+//  * K(t, s) = (1/4pi)/|t - s|, zero when r2 == 0 (_hot.pyx:44-50);
+//  * outputs accumulate (+=), laplace_matrix overwrites (_hot.pyx:68-88);
+//  * per-target summation follows the source order (_hot.pyx:30-32);
+//  * hadamard: phat[f,c,tau,r] += sum_o sum_sigma khat[f,o,tau,sigma] qhat[f,halo[c,o],sigma,r]
+//    with halo < 0 skipped (_hot.pyx:141-178).
+#include "common.cuh"
+
+using namespace kifmm;
+
+namespace {
+
+constexpr int kTile = 256;
+
+// One thread per target; sources staged through shared memory in tiles.
+template <typename T>
+__global__ void __launch_bounds__(kTile) potentials_kernel(
+    const T* __restrict__ tx, const T* __restrict__ ty, const T* __restrict__ tz, int64_t nt,
+    const T* __restrict__ sx, const T* __restrict__ sy, const T* __restrict__ sz, int64_t ns,
+    const T* __restrict__ q, int64_t nrhs, T* __restrict__ out) {
+  __shared__ T s_x[kTile], s_y[kTile], s_z[kTile];
+  int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  bool live = i < nt;
+  T x = live ? tx[i] : T(0), y = live ? ty[i] : T(0), z = live ? tz[i] : T(0);
+  for (int64_t r = 0; r < nrhs; ++r) {
+    T acc = T(0);
+    for (int64_t j0 = 0; j0 < ns; j0 += kTile) {
+      int64_t j = j0 + threadIdx.x;
+      __syncthreads();
+      if (j < ns) { s_x[threadIdx.x] = sx[j]; s_y[threadIdx.x] = sy[j]; s_z[threadIdx.x] = sz[j]; }
+      __syncthreads();
+      int m = (int)min64(kTile, ns - j0);
+      for (int jj = 0; jj < m; ++jj) {
+        T w = inv_r<T>(x - s_x[jj], y - s_y[jj], z - s_z[jj]);
+        acc += w * __ldg(&q[(j0 + jj) * nrhs + r]);
+      }
+    }
+    if (live) out[i * nrhs + r] += acc * real_traits<T>::inv4pi();
+  }
+}
+
+// out[i, j] = fl(1/4pi) / sqrt(r2): IEEE division and square root, so the
+// matrix is bit-identical to the reference's compiled loop.
+template <typename T>
+__global__ void matrix_kernel(const T* __restrict__ tx, const T* __restrict__ ty,
+                              const T* __restrict__ tz, int64_t nt, const T* __restrict__ sx,
+                              const T* __restrict__ sy, const T* __restrict__ sz, int64_t ns,
+                              T* __restrict__ out) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nt * ns) return;
+  int64_t i = idx / ns, j = idx - i * ns;
+  T dx = tx[i] - sx[j], dy = ty[i] - sy[j], dz = tz[i] - sz[j];
+  T r2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+  out[idx] = r2 > T(0) ? real_traits<T>::inv4pi() / sqrt(r2) : T(0);
+}
+
+template <>
+__global__ void matrix_kernel<double>(const double* __restrict__ tx, const double* __restrict__ ty,
+                                      const double* __restrict__ tz, int64_t nt,
+                                      const double* __restrict__ sx, const double* __restrict__ sy,
+                                      const double* __restrict__ sz, int64_t ns,
+                                      double* __restrict__ out) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nt * ns) return;
+  int64_t i = idx / ns, j = idx - i * ns;
+  double dx = tx[i] - sx[j], dy = ty[i] - sy[j], dz = tz[i] - sz[j];
+  double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  out[idx] = r2 > 0.0 ? KIFMM_INV_4PI_D / sqrt(r2) : 0.0;
+}
+
+// Reference CSR form: target i reads the gathered range of its leaf.
+// Consecutive targets share a leaf, so source loads broadcast within a warp.
+template <typename T>
+__global__ void p2p_csr_kernel(const T* __restrict__ tx, const T* __restrict__ ty,
+                               const T* __restrict__ tz, int64_t nt,
+                               const int64_t* __restrict__ leaf_of_target,
+                               const T* __restrict__ sx, const T* __restrict__ sy,
+                               const T* __restrict__ sz, const T* __restrict__ q, int64_t nrhs,
+                               const int64_t* __restrict__ off, T* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  int64_t b = leaf_of_target[i];
+  int64_t j0 = off[b], j1 = off[b + 1];
+  T x = tx[i], y = ty[i], z = tz[i];
+  for (int64_t r = 0; r < nrhs; ++r) {
+    T acc = T(0);
+    for (int64_t j = j0; j < j1; ++j) {
+      T w = inv_r<T>(x - __ldg(&sx[j]), y - __ldg(&sy[j]), z - __ldg(&sz[j]));
+      acc += w * __ldg(&q[j * nrhs + r]);
+    }
+    out[i * nrhs + r] += acc * real_traits<T>::inv4pi();
+  }
+}
+
+template <typename T> struct cplx;
+template <> struct cplx<float> { using v = float2; };
+template <> struct cplx<double> { using v = double2; };
+
+// Hadamard block MAC.  One CTA per (frequency, chunk of target clusters);
+// khat[f] is staged once in shared memory as [o][sigma][tau] so the 8
+// tau-threads of a cluster read consecutive entries.
+constexpr int kHadThreads = 256;
+constexpr int kHadClusters = 256;   // target clusters per CTA
+
+template <typename T>
+__global__ void __launch_bounds__(kHadThreads) hadamard_kernel(
+    const typename cplx<T>::v* __restrict__ khat, const typename cplx<T>::v* __restrict__ qhat,
+    const int64_t* __restrict__ halo, typename cplx<T>::v* __restrict__ phat, int64_t nsc,
+    int64_t ntc, int64_t nrhs) {
+  using C = typename cplx<T>::v;
+  extern __shared__ unsigned char smem_raw[];
+  C* ks = reinterpret_cast<C*>(smem_raw);       // [26][8 sigma][8 tau]
+  const int64_t f = blockIdx.x;
+  const C* kf = khat + f * (26 * 64);
+  for (int e = threadIdx.x; e < 26 * 64; e += kHadThreads) {
+    int o = e >> 6, tau = (e >> 3) & 7, sig = e & 7;
+    ks[(o * 8 + sig) * 8 + tau] = kf[e];
+  }
+  __syncthreads();
+  const int tau = threadIdx.x & 7;
+  const int64_t c_begin = (int64_t)blockIdx.y * kHadClusters;
+  const int64_t c_end = min64(ntc, c_begin + kHadClusters);
+  const C* qf = qhat + f * nsc * 8 * nrhs;
+  C* pf = phat + f * ntc * 8 * nrhs;
+  for (int64_t c = c_begin + (threadIdx.x >> 3); c < c_end; c += kHadThreads / 8) {
+    for (int64_t r = 0; r < nrhs; ++r) {
+      T re = 0, im = 0;
+      for (int o = 0; o < 26; ++o) {
+        int64_t s = __ldg(&halo[c * 26 + o]);
+        if (s < 0) continue;
+        const C* qs = qf + s * 8 * nrhs + r;
+#pragma unroll
+        for (int sig = 0; sig < 8; ++sig) {
+          C k = ks[(o * 8 + sig) * 8 + tau];
+          C v = qs[sig * nrhs];
+          re += k.x * v.x - k.y * v.y;
+          im += k.x * v.y + k.y * v.x;
+        }
+      }
+      C* p = pf + (c * 8 + tau) * nrhs + r;
+      C old = *p;
+      old.x += re;
+      old.y += im;
+      *p = old;
+    }
+  }
+}
+
+template <typename T>
+int potentials(const T* tx, const T* ty, const T* tz, int64_t nt, const T* sx, const T* sy,
+               const T* sz, int64_t ns, const T* q, int64_t nrhs, T* out, void* stream) {
+  if (nt < 0 || ns < 0 || nrhs < 1) return KIFMM_EARG;
+  if (nt == 0 || ns == 0) return 0;
+  potentials_kernel<T><<<ceil_div(nt, kTile), kTile, 0, (cudaStream_t)stream>>>(
+      tx, ty, tz, nt, sx, sy, sz, ns, q, nrhs, out);
+  return launch_status();
+}
+
+template <typename T>
+int matrix(const T* tx, const T* ty, const T* tz, int64_t nt, const T* sx, const T* sy,
+           const T* sz, int64_t ns, T* out, void* stream) {
+  if (nt < 0 || ns < 0) return KIFMM_EARG;
+  if (nt == 0 || ns == 0) return 0;
+  matrix_kernel<T><<<ceil_div(nt * ns, 256), 256, 0, (cudaStream_t)stream>>>(tx, ty, tz, nt, sx,
+                                                                             sy, sz, ns, out);
+  return launch_status();
+}
+
+template <typename T>
+int p2p(const T* tx, const T* ty, const T* tz, int64_t nt, const int64_t* lot, const T* sx,
+        const T* sy, const T* sz, const T* q, int64_t nrhs, const int64_t* off, int64_t nl, T* out,
+        void* stream) {
+  if (nt < 0 || nl < 0 || nrhs < 1) return KIFMM_EARG;
+  if (nt == 0) return 0;
+  p2p_csr_kernel<T><<<ceil_div(nt, 128), 128, 0, (cudaStream_t)stream>>>(tx, ty, tz, nt, lot, sx,
+                                                                         sy, sz, q, nrhs, off, out);
+  return launch_status();
+}
+
+template <typename T>
+int hadamard(const T* khat, const T* qhat, const int64_t* halo, T* phat, int64_t nf, int64_t nsc,
+             int64_t ntc, int64_t nrhs, void* stream) {
+  using C = typename cplx<T>::v;
+  if (nf < 0 || nsc < 0 || ntc < 0 || nrhs < 1) return KIFMM_EARG;
+  if (nf == 0 || ntc == 0) return 0;
+  size_t smem = 26 * 64 * sizeof(C);
+  auto kern = hadamard_kernel<T>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)nf, ceil_div(ntc, kHadClusters));
+  kern<<<grid, kHadThreads, smem, (cudaStream_t)stream>>>(
+      reinterpret_cast<const C*>(khat), reinterpret_cast<const C*>(qhat), halo,
+      reinterpret_cast<C*>(phat), nsc, ntc, nrhs);
+  return launch_status();
+}
+
+}  // namespace
+
+extern "C" {
+
+int kifmm_laplace_potentials_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
+                                 const float* sx, const float* sy, const float* sz, int64_t ns,
+                                 const float* q, int64_t nrhs, float* out, void* s) {
+  return potentials<float>(tx, ty, tz, nt, sx, sy, sz, ns, q, nrhs, out, s);
+}
+int kifmm_laplace_potentials_f64(const double* tx, const double* ty, const double* tz, int64_t nt,
+                                 const double* sx, const double* sy, const double* sz, int64_t ns,
+                                 const double* q, int64_t nrhs, double* out, void* s) {
+  return potentials<double>(tx, ty, tz, nt, sx, sy, sz, ns, q, nrhs, out, s);
+}
+int kifmm_laplace_matrix_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
+                             const float* sx, const float* sy, const float* sz, int64_t ns,
+                             float* out, void* s) {
+  return matrix<float>(tx, ty, tz, nt, sx, sy, sz, ns, out, s);
+}
+int kifmm_laplace_matrix_f64(const double* tx, const double* ty, const double* tz, int64_t nt,
+                             const double* sx, const double* sy, const double* sz, int64_t ns,
+                             double* out, void* s) {
+  return matrix<double>(tx, ty, tz, nt, sx, sy, sz, ns, out, s);
+}
+int kifmm_p2p_blocked_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
+                          const int64_t* lot, const float* sx, const float* sy, const float* sz,
+                          const float* q, int64_t nrhs, const int64_t* off, int64_t nl, float* out,
+                          void* s) {
+  return p2p<float>(tx, ty, tz, nt, lot, sx, sy, sz, q, nrhs, off, nl, out, s);
+}
+int kifmm_p2p_blocked_f64(const double* tx, const double* ty, const double* tz, int64_t nt,
+                          const int64_t* lot, const double* sx, const double* sy, const double* sz,
+                          const double* q, int64_t nrhs, const int64_t* off, int64_t nl,
+                          double* out, void* s) {
+  return p2p<double>(tx, ty, tz, nt, lot, sx, sy, sz, q, nrhs, off, nl, out, s);
+}
+int kifmm_hadamard_m2l_c64(const float* khat, const float* qhat, const int64_t* halo, float* phat,
+                           int64_t nf, int64_t nsc, int64_t ntc, int64_t nrhs, void* s) {
+  return hadamard<float>(khat, qhat, halo, phat, nf, nsc, ntc, nrhs, s);
+}
+int kifmm_hadamard_m2l_c128(const double* khat, const double* qhat, const int64_t* halo,
+                            double* phat, int64_t nf, int64_t nsc, int64_t ntc, int64_t nrhs,
+                            void* s) {
+  return hadamard<double>(khat, qhat, halo, phat, nf, nsc, ntc, nrhs, s);
+}
+int kifmm_sm_target(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,202 @@
+// Leaf-level passes of evaluate (reference engine.py:298-319 and 377-404).
+//
+//  * p2m_check: check-surface potentials of every source leaf from its own
+//    points (the P2M right-hand side, engine.py:305-318);
+//  * leaf_pass: fused L2P (downward equivalent surface -> targets,
+//    engine.py:377-389) + near-field P2P (_hot.pyx:91-138 via
+//    engine.py:391-397) + the un-permute to caller order (engine.py:399-404).
+//    The near field is walked as the reference orders it: the target's own
+//    leaf first, then its neighbour leaves by Morton code; sources are read
+//    in place from the tree-ordered arrays (no per-leaf duplication).
+//
+// Surface points are formed from a float64 leaf centre and float64 unit
+// offsets with an exact add and one rounding, which reproduces the host's
+// per-leaf surface arrays (engine.py:149-156) bit for bit.
+#include "common.cuh"
+
+using namespace kifmm;
+
+namespace {
+
+template <typename T> struct vec4;
+template <> struct vec4<float> { using v = float4; };
+template <> struct vec4<double> { using v = double4; };
+
+constexpr int kWarps = 4;
+
+template <typename T>
+__global__ void __launch_bounds__(32 * kWarps) p2m_check_kernel(
+    const T* __restrict__ sx, const T* __restrict__ sy, const T* __restrict__ sz,
+    const T* __restrict__ q, int64_t nrhs, const int32_t* __restrict__ leaf_start,
+    const int32_t* __restrict__ leaf_count, int64_t n_leaves, const double* __restrict__ centers,
+    const double* __restrict__ base, int64_t nc, T* __restrict__ phi) {
+  using V = typename vec4<T>::v;
+  __shared__ V buf[kWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t leaf = (int64_t)blockIdx.x * kWarps + w;
+  if (leaf >= n_leaves) return;
+  const int64_t s0 = leaf_start[leaf];
+  const int cnt = leaf_count[leaf];
+  const double cx = centers[leaf * 3], cy = centers[leaf * 3 + 1], cz = centers[leaf * 3 + 2];
+  for (int64_t r = 0; r < nrhs; ++r) {
+    for (int64_t c0 = 0; c0 < nc; c0 += 32) {
+      const int64_t c = c0 + lane;
+      T px = 0, py = 0, pz = 0;
+      if (c < nc) {
+        px = real_traits<T>::from_d(exact_add(cx, base[c * 3]));
+        py = real_traits<T>::from_d(exact_add(cy, base[c * 3 + 1]));
+        pz = real_traits<T>::from_d(exact_add(cz, base[c * 3 + 2]));
+      }
+      T acc = 0;
+      for (int j0 = 0; j0 < cnt; j0 += 32) {
+        __syncwarp();
+        if (j0 + lane < cnt) {
+          int64_t j = s0 + j0 + lane;
+          buf[w][lane] = V{sx[j], sy[j], sz[j], q[j * nrhs + r]};
+        }
+        __syncwarp();
+        const int m = min(32, cnt - j0);
+        for (int k = 0; k < m; ++k) {
+          V s = buf[w][k];
+          acc += inv_r<T>(px - s.x, py - s.y, pz - s.z) * s.w;
+        }
+      }
+      if (c < nc) phi[(leaf * nrhs + r) * nc + c] = acc * real_traits<T>::inv4pi();
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
+    const T* __restrict__ tx, const T* __restrict__ ty, const T* __restrict__ tz,
+    const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
+    const double* __restrict__ centers, const double* __restrict__ base, int64_t ne,
+    const T* __restrict__ local, const T* __restrict__ sx, const T* __restrict__ sy,
+    const T* __restrict__ sz, const T* __restrict__ q, const int32_t* __restrict__ sstart,
+    const int32_t* __restrict__ scount, const int32_t* __restrict__ near_off,
+    const int32_t* __restrict__ near_leaf, int64_t nrhs, const int64_t* __restrict__ perm,
+    int parts, T* __restrict__ out) {
+  using V = typename vec4<T>::v;
+  __shared__ V buf[kWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * kWarps + w;
+  if (b >= n_tleaves) return;
+  const int64_t t0 = tstart[b];
+  const int tc = tcount[b];
+  const double cx = centers[b * 3], cy = centers[b * 3 + 1], cz = centers[b * 3 + 2];
+  const int n0 = near_off[b], n1 = near_off[b + 1];
+  for (int tb = 0; tb < tc; tb += 32) {
+    const bool live = tb + lane < tc;
+    const int64_t i = t0 + tb + lane;
+    const T x = live ? tx[i] : T(0), y = live ? ty[i] : T(0), z = live ? tz[i] : T(0);
+    for (int64_t r = 0; r < nrhs; ++r) {
+      // L2P: downward equivalent densities of the leaf -> its targets.
+      T far = 0;
+      const T* loc = local + (b * nrhs + r) * ne;
+      for (int64_t e0 = 0; (parts & 1) && e0 < ne; e0 += 32) {
+        __syncwarp();
+        const int64_t e = e0 + lane;
+        if (e < ne) {
+          buf[w][lane] = V{real_traits<T>::from_d(exact_add(cx, base[e * 3])),
+                           real_traits<T>::from_d(exact_add(cy, base[e * 3 + 1])),
+                           real_traits<T>::from_d(exact_add(cz, base[e * 3 + 2])), loc[e]};
+        }
+        __syncwarp();
+        const int m = (int)min64(32, ne - e0);
+        for (int k = 0; k < m; ++k) {
+          V s = buf[w][k];
+          far += inv_r<T>(x - s.x, y - s.y, z - s.z) * s.w;
+        }
+      }
+      // P2P: own leaf, then neighbours in Morton order.
+      T near = 0;
+      for (int n = n0; (parts & 2) && n < n1; ++n) {
+        const int sl = near_leaf[n];
+        const int64_t j0 = sstart[sl];
+        const int jc = scount[sl];
+        for (int jb = 0; jb < jc; jb += 32) {
+          __syncwarp();
+          if (jb + lane < jc) {
+            const int64_t j = j0 + jb + lane;
+            buf[w][lane] = V{sx[j], sy[j], sz[j], q[j * nrhs + r]};
+          }
+          __syncwarp();
+          const int m = min(32, jc - jb);
+#pragma unroll 4
+          for (int k = 0; k < m; ++k) {
+            V s = buf[w][k];
+            near += inv_r<T>(x - s.x, y - s.y, z - s.z) * s.w;
+          }
+        }
+      }
+      if (live) {
+        const T c = real_traits<T>::inv4pi();
+        T* o = out + (perm ? perm[i] : i) * nrhs + r;
+        const T v = far * c + near * c;
+        *o = (parts & 4) ? *o + v : v;
+      }
+    }
+  }
+}
+
+template <typename T>
+int p2m_check(const T* sx, const T* sy, const T* sz, const T* q, int64_t nrhs, const int32_t* ls,
+              const int32_t* lc, int64_t nl, const double* centers, const double* base, int64_t nc,
+              T* phi, void* stream) {
+  if (nl < 0 || nc < 1 || nrhs < 1) return KIFMM_EARG;
+  if (nl == 0) return 0;
+  p2m_check_kernel<T><<<ceil_div(nl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
+      sx, sy, sz, q, nrhs, ls, lc, nl, centers, base, nc, phi);
+  return launch_status();
+}
+
+template <typename T>
+int leaf_pass(const T* tx, const T* ty, const T* tz, const int32_t* ts, const int32_t* tcnt,
+              int64_t ntl, const double* centers, const double* base, int64_t ne, const T* local,
+              const T* sx, const T* sy, const T* sz, const T* q, const int32_t* ss,
+              const int32_t* sc, const int32_t* no, const int32_t* nlf, int64_t nrhs,
+              const int64_t* perm, int parts, T* out, void* stream) {
+  if (ntl < 0 || ne < 1 || nrhs < 1 || parts < 1 || parts > 7) return KIFMM_EARG;
+  if (ntl == 0) return 0;
+  leaf_pass_kernel<T><<<ceil_div(ntl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
+      tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local, sx, sy, sz, q, ss, sc, no, nlf, nrhs,
+      perm, parts, out);
+  return launch_status();
+}
+
+}  // namespace
+
+extern "C" {
+
+int kifmm_p2m_check_f32(const float* sx, const float* sy, const float* sz, const float* q,
+                        int64_t nrhs, const int32_t* ls, const int32_t* lc, int64_t nl,
+                        const double* centers, const double* base, int64_t nc, float* phi,
+                        void* s) {
+  return p2m_check<float>(sx, sy, sz, q, nrhs, ls, lc, nl, centers, base, nc, phi, s);
+}
+int kifmm_p2m_check_f64(const double* sx, const double* sy, const double* sz, const double* q,
+                        int64_t nrhs, const int32_t* ls, const int32_t* lc, int64_t nl,
+                        const double* centers, const double* base, int64_t nc, double* phi,
+                        void* s) {
+  return p2m_check<double>(sx, sy, sz, q, nrhs, ls, lc, nl, centers, base, nc, phi, s);
+}
+int kifmm_leaf_pass_f32(const float* tx, const float* ty, const float* tz, const int32_t* ts,
+                        const int32_t* tc, int64_t ntl, const double* centers, const double* base,
+                        int64_t ne, const float* local, const float* sx, const float* sy,
+                        const float* sz, const float* q, const int32_t* ss, const int32_t* sc,
+                        const int32_t* no, const int32_t* nlf, int64_t nrhs, const int64_t* perm,
+                        int parts, float* out, void* s) {
+  return leaf_pass<float>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, sx, sy, sz, q, ss, sc,
+                          no, nlf, nrhs, perm, parts, out, s);
+}
+int kifmm_leaf_pass_f64(const double* tx, const double* ty, const double* tz, const int32_t* ts,
+                        const int32_t* tc, int64_t ntl, const double* centers, const double* base,
+                        int64_t ne, const double* local, const double* sx, const double* sy,
+                        const double* sz, const double* q, const int32_t* ss, const int32_t* sc,
+                        const int32_t* no, const int32_t* nlf, int64_t nrhs, const int64_t* perm,
+                        int parts, double* out, void* s) {
+  return leaf_pass<double>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, sx, sy, sz, q, ss,
+                           sc, no, nlf, nrhs, perm, parts, out, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,192 @@
+// BLAS-M2L fused bucket sweep (replaces the bucket loop of reference
+// m2l_blas.apply_level, m2l_blas.py:284-320).
+//
+// The reference groups pairs by transfer vector t and, per bucket, gathers
+// q~[rows_s], applies (q~ vbar_t) ubar_t^T and scatter-adds into acc[rows_t]
+// (<= 316 gather/GEMM/scatter rounds, numpy-bound on the CPU).  Here the
+// sweep is target-stationary: a CTA owns a tile of 128 target boxes of one
+// parity class (all of which meet the same 189 transfer vectors), keeps the
+// tile's accumulator in registers for the whole sweep and streams, per
+// vector, the gathered source rows and the contracted core
+// D_t = ubar_t vbar_t^T through a double-buffered cp.async pipeline.  No
+// scatter, no atomics; the vector order is the canonical ascending order,
+// so the result is deterministic.
+#include "common.cuh"
+
+using namespace kifmm;
+
+namespace {
+
+constexpr int TMT = 128;   // targets per tile (matches the host plan)
+constexpr int RM = 4;      // accumulator rows per thread (rows tm + 32*i)
+constexpr int RN = 8;      // accumulator columns per thread (contiguous)
+
+template <typename T>
+struct sweep_cfg {
+  static constexpr int VEC = 16 / sizeof(T);
+};
+
+template <typename T>
+__global__ void __launch_bounds__(512) m2l_sweep_kernel(
+    const T* __restrict__ qt, const T* __restrict__ Dt, int kin, int ko_pad, int bk,
+    int nchunks, int kob, const int32_t* __restrict__ tile_targets,
+    const int32_t* __restrict__ tile_class, const int32_t* __restrict__ src,
+    const int32_t* __restrict__ class_tv, int64_t nrhs, T* __restrict__ acc_out) {
+  constexpr int VEC = sweep_cfg<T>::VEC;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int gstride = bk + VEC;                       // padded row stride of Gs
+  T* Gs = reinterpret_cast<T*>(smem_raw);             // [2][TMT][gstride]
+  T* Ds = Gs + 2 * TMT * gstride;                     // [2][bk][kob]
+
+  const int tid = threadIdx.x;
+  const int ng = kob / RN;
+  const int tn = tid % ng, tm = tid / ng;             // tm in [0, 32)
+  const int64_t tile = blockIdx.x;
+  const int64_t r = blockIdx.y;
+  const int c0 = blockIdx.z * kob;
+  const int cls = tile_class[tile];
+  const int32_t* tsrc = src + tile * 189 * TMT;       // [189][TMT]
+  const int32_t* tv_list = class_tv + cls * 189;
+
+  T acc[RM][RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
+
+  const int nsteps = 189 * nchunks;
+  const int gch = bk / VEC;                           // 16-byte chunks per gathered row
+  const int dch = kob / VEC;                          // 16-byte chunks per core row
+
+  auto stage = [&](int st, int buf) {
+    const int j = st / nchunks, ch = st - j * nchunks;
+    const int kk0 = ch * bk;
+    T* g = Gs + buf * TMT * gstride;
+    for (int e = tid; e < TMT * gch; e += blockDim.x) {
+      const int m = e / gch, v = e - m * gch;
+      const int32_t s = __ldg(&tsrc[j * TMT + m]);
+      const T* gp = qt + ((int64_t)(s < 0 ? 0 : s) * nrhs + r) * kin + kk0 + v * VEC;
+      cp_async16(g + m * gstride + v * VEC, gp, s >= 0);
+    }
+    const T* dsrc = Dt + ((int64_t)tv_list[j] * kin + kk0) * ko_pad + c0;
+    T* d = Ds + buf * bk * kob;
+    for (int e = tid; e < bk * dch; e += blockDim.x) {
+      const int row = e / dch, v = e - row * dch;
+      cp_async16(d + row * kob + v * VEC, dsrc + (int64_t)row * ko_pad + v * VEC, true);
+    }
+    cp_async_commit();
+  };
+
+  stage(0, 0);
+  for (int st = 0; st < nsteps; ++st) {
+    const int buf = st & 1;
+    if (st + 1 < nsteps) {
+      stage(st + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const T* g = Gs + buf * TMT * gstride;
+    const T* d = Ds + buf * bk * kob + tn * RN;
+    for (int kk = 0; kk < bk; kk += VEC) {
+      T a[RM][VEC];
+#pragma unroll
+      for (int i = 0; i < RM; ++i) {
+        const T* ap = g + (tm + 32 * i) * gstride + kk;
+        if constexpr (VEC == 4) {
+          float4 t4 = *reinterpret_cast<const float4*>(ap);
+          a[i][0] = t4.x; a[i][1] = t4.y; a[i][2] = t4.z; a[i][3] = t4.w;
+        } else {
+          double2 t2 = *reinterpret_cast<const double2*>(ap);
+          a[i][0] = t2.x; a[i][1] = t2.y;
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        T b[RN];
+        const T* bp = d + (kk + v) * kob;
+#pragma unroll
+        for (int j = 0; j < RN; j += VEC) {
+          if constexpr (VEC == 4) {
+            float4 t4 = *reinterpret_cast<const float4*>(bp + j);
+            b[j] = t4.x; b[j + 1] = t4.y; b[j + 2] = t4.z; b[j + 3] = t4.w;
+          } else {
+            double2 t2 = *reinterpret_cast<const double2*>(bp + j);
+            b[j] = t2.x; b[j + 1] = t2.y;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) acc[i][j] += a[i][v] * b[j];
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < RM; ++i) {
+    const int32_t tgt = tile_targets[tile * TMT + tm + 32 * i];
+    if (tgt < 0) continue;
+    T* o = acc_out + ((int64_t)tgt * nrhs + r) * ko_pad + c0 + tn * RN;
+#pragma unroll
+    for (int j = 0; j < RN; j += VEC) {
+      if constexpr (VEC == 4) {
+        *reinterpret_cast<float4*>(o + j) = float4{acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]};
+      } else {
+        *reinterpret_cast<double2*>(o + j) = double2{acc[i][j], acc[i][j + 1]};
+      }
+    }
+  }
+}
+
+// Host-side launch geometry; must agree with device.py's blas_geometry().
+template <typename T>
+int sweep(const T* qt, const T* Dt, int64_t kin, int64_t ko_pad, const int32_t* tile_targets,
+          const int32_t* tile_class, const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
+          int64_t nrhs, T* acc, void* stream) {
+  constexpr int VEC = sweep_cfg<T>::VEC;
+  constexpr int BKMAX = sizeof(T) == 4 ? 64 : 32;
+  if (kin < VEC || ko_pad < RN || n_tiles < 0 || nrhs < 1) return KIFMM_EARG;
+  if (kin % VEC || ko_pad % RN) return KIFMM_EARG;
+  if (n_tiles == 0) return 0;
+  const int nchunks = (int)((kin + BKMAX - 1) / BKMAX);
+  if (kin % nchunks) return KIFMM_EARG;
+  const int bk = (int)(kin / nchunks);
+  if (bk % VEC) return KIFMM_EARG;
+  const int n_slabs = (int)((ko_pad + 127) / 128);
+  if (ko_pad % n_slabs) return KIFMM_EARG;
+  const int kob = (int)(ko_pad / n_slabs);
+  if (kob % RN) return KIFMM_EARG;
+  const int threads = 32 * (kob / RN);
+  const size_t smem = sizeof(T) * (2 * TMT * (bk + VEC) + 2 * bk * kob);
+  auto kern = m2l_sweep_kernel<T>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)n_slabs);
+  kern<<<grid, threads, smem, (cudaStream_t)stream>>>(qt, Dt, (int)kin, (int)ko_pad, bk, nchunks,
+                                                      kob, tile_targets, tile_class, src,
+                                                      class_tv, nrhs, acc);
+  return launch_status();
+}
+
+}  // namespace
+
+extern "C" {
+
+int kifmm_m2l_sweep_f32(const float* qt, const float* Dt, int64_t kin, int64_t ko_pad,
+                        const int32_t* tile_targets, const int32_t* tile_class, const int32_t* src,
+                        const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, float* acc,
+                        void* s) {
+  return sweep<float>(qt, Dt, kin, ko_pad, tile_targets, tile_class, src, class_tv, n_tiles, nrhs,
+                      acc, s);
+}
+int kifmm_m2l_sweep_f64(const double* qt, const double* Dt, int64_t kin, int64_t ko_pad,
+                        const int32_t* tile_targets, const int32_t* tile_class, const int32_t* src,
+                        const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, double* acc,
+                        void* s) {
+  return sweep<double>(qt, Dt, kin, ko_pad, tile_targets, tile_class, src, class_tv, n_tiles,
+                       nrhs, acc, s);
+}
+
+}  // extern "C"

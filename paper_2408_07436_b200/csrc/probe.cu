@@ -1,0 +1,67 @@
+// Pipe-peak probes for the roofline denominators that MEASURED_PEAKS.json
+// does not carry (FP32 FFMA, FP64 DFMA, MUFU rsqrt).  Each thread runs 8
+// independent dependency chains so the pipe, not latency, is the limit.
+#include "common.cuh"
+
+using namespace kifmm;
+
+namespace {
+
+template <typename T>
+__global__ void fma_probe(T* out, int iters, T b, T c) {
+  T a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = (T)(threadIdx.x + i) * T(1e-3);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = a[i] * b + c;
+  }
+  T s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void rsqrt_probe(float* out, int iters, float c) {
+  float a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = 1.0f + (threadIdx.x + i) * 1e-3f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = rsqrtf(a[i]) + c;
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+}  // namespace
+
+extern "C" {
+
+// kind: 0 = FP32 FFMA, 1 = FP64 DFMA, 2 = MUFU rsqrt (FP32).  out must hold
+// blocks*threads elements of the probe type.  Work per launch:
+// blocks*threads*iters*128 operations (an FMA counts as 2 flops).
+int kifmm_probe(int kind, int64_t blocks, int64_t threads, int64_t iters, void* out,
+                void* stream) {
+  if (blocks < 1 || threads < 1 || iters < 1) return KIFMM_EARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (kind == 0)
+    fma_probe<float><<<(unsigned)blocks, (unsigned)threads, 0, s>>>((float*)out, (int)iters,
+                                                                     0.999f, 1e-4f);
+  else if (kind == 1)
+    fma_probe<double><<<(unsigned)blocks, (unsigned)threads, 0, s>>>((double*)out, (int)iters,
+                                                                      0.999, 1e-4);
+  else if (kind == 2)
+    rsqrt_probe<<<(unsigned)blocks, (unsigned)threads, 0, s>>>((float*)out, (int)iters, 0.5f);
+  else
+    return KIFMM_EARG;
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,482 @@
+"""Device-resident evaluate: uploads the setup plan once, then runs every
+pass of ``evaluate`` (reference ``engine.py:270-404``) on the GPU through the
+C-ABI of ``libkifmm_b200.so``.
+
+PyTorch is used only for allocations and the stream; all arithmetic is in
+our kernels.  There is no CPU path: constructing a :class:`DeviceFmm`
+without a CUDA device raises.
+
+Data layout in HBM (n_rhs = R, T = float32 | float64):
+  sources / targets   SoA x, y, z (T) in leaf-Morton order, int32 leaf starts/counts
+  leaf centres        float64 (n_leaves, 3); surface offsets float64 (n, 3)
+  multipoles[l]       (n_src_boxes(l), R, n_equiv) T
+  locals[l]           (n_tgt_boxes(l), R, n_equiv) T
+  BLAS-M2L            S padded (n_equiv, kin), U^T (k, n_check), transposed dense cores
+                      Dt (316, kin, ko_pad), per-level tile plan (int32)
+  FFT-M2L             khat (n_freq, 26, 8, 8) complex, per-level slot/halo tables,
+                      qhat (n_freq, n_src_clusters, 8, R), phat (n_freq, n_tgt_clusters, 8, R)
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .engine import child_table, leaf_centers, leaf_surface_base
+from .m2l_blas import TILE_TARGETS, dense_cores, level_plan_from_buckets
+from .octree import class_transfer_table
+
+_NP2T = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("kifmm-b200 evaluates on a CUDA device only; none is visible "
+                           "(there is no CPU fallback)")
+    nat.load()
+
+
+def _dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_dev(a, dtype=None):
+    a = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    return torch.from_numpy(a).to(_dev(), non_blocking=False)
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def P(t):
+    return None if t is None else t.data_ptr()
+
+
+# Optional per-launch event profiling (bench.py roofline): when _PROF is a
+# list, every launch appends (entry point, tag, start event, end event).
+_PROF = None
+_TAG = ""
+
+
+def set_tag(tag: str):
+    global _TAG
+    _TAG = tag
+
+
+def launch(name, *args):
+    if _PROF is None:
+        return nat.call(name, *args)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    st = nat.call(name, *args)
+    e1.record()
+    _PROF.append((name, _TAG, e0, e1))
+    return st
+
+
+class profile_launches:
+    """Context manager collecting per-launch CUDA-event times."""
+
+    def __enter__(self):
+        global _PROF
+        _PROF = []
+        self.records = _PROF
+        return self
+
+    def __exit__(self, *exc):
+        global _PROF
+        _PROF = None
+        return False
+
+    def times(self):
+        """[(entry point, tag, milliseconds)] after a synchronize."""
+        torch.cuda.synchronize()
+        return [(n, t, a.elapsed_time(b)) for n, t, a, b in self.records]
+
+
+def blas_geometry(k: int, itemsize: int):
+    """(kin, ko_pad) padding of the compressed rank for the sweep kernel;
+    mirrors the launch checks in csrc/m2l_blas.cu."""
+    vec = 16 // itemsize
+    bkmax = 64 if itemsize == 4 else 32
+    nch = -(-k // bkmax)
+    bk = -(-(-(-k // nch)) // vec) * vec
+    kin = nch * bk
+    n_slabs = -(-k // 128)
+    kob = -(-(-(-k // n_slabs)) // 8) * 8
+    return kin, n_slabs * kob
+
+
+class Linalg:
+    """Thin typed wrappers around the GEMM / solve entry points."""
+
+    def __init__(self, sfx: str):
+        self.sfx = sfx
+
+    def gemm(self, M, N, K, alpha, A, lda, B, ldb, C, ldc, colscale=None, rowmap=None,
+             accumulate=False):
+        launch(f"kifmm_gemm_{self.sfx}", M, N, K, float(alpha), P(A), lda, P(B), ldb,
+                 P(colscale), P(C), ldc, P(rowmap), int(bool(accumulate)), stream_handle())
+
+    def solve(self, inv, phi, M, out, scale, tmp, accumulate=False, rowmap=None):
+        """out[rowmap] (+)= scale * V diag(inv_vals) U^T phi^T, row form
+        (reference expansion.py:78-82 applied through engine._solve_block)."""
+        u, vals, vt = inv
+        n_c, r = u.shape
+        n_e = vt.shape[1]
+        self.gemm(M, r, n_c, 1.0, phi, n_c, u, r, tmp, r, colscale=vals)
+        self.gemm(M, n_e, r, scale, tmp, r, vt, n_e, out, n_e, rowmap=rowmap,
+                  accumulate=accumulate)
+
+
+class DeviceFmm:
+    """GPU-resident copy of an :class:`~.engine.FmmInstance` plan."""
+
+    def __init__(self, inst):
+        require_cuda()
+        self.inst = inst
+        cfg = inst.config
+        self.cfg = cfg
+        self.np_dtype = np.dtype(cfg.dtype)
+        self.T = _NP2T[self.np_dtype]
+        self.sfx = "f32" if self.np_dtype == np.float32 else "f64"
+        self.la = Linalg(self.sfx)
+        st, tt = inst.source_tree, inst.target_tree
+        exp = inst.expansions
+        self.depth = cfg.depth
+        self.n_e, self.n_c = exp.n_equiv, exp.n_check
+        dt = self.np_dtype
+        leaf_side = inst.domain.box_side(cfg.depth)
+        # points
+        self.sx, self.sy, self.sz = (to_dev(v, dt) for v in (st.x, st.y, st.z))
+        self.tx, self.ty, self.tz = (to_dev(v, dt) for v in (tt.x, tt.y, tt.z))
+        self.s_start = to_dev(st.leaf_starts, np.int32)
+        self.s_count = to_dev(st.leaf_counts, np.int32)
+        self.t_start = to_dev(tt.leaf_starts, np.int32)
+        self.t_count = to_dev(tt.leaf_counts, np.int32)
+        self.s_perm = to_dev(st.perm, np.int64)
+        self.t_perm = to_dev(tt.perm, np.int64)
+        self.s_centers = to_dev(leaf_centers(st))
+        self.t_centers = to_dev(leaf_centers(tt))
+        self.check_base = to_dev(leaf_surface_base(cfg.resolved_order_check(), leaf_side,
+                                                   cfg.outer_scale))
+        self.equiv_base = to_dev(leaf_surface_base(cfg.order_equiv, leaf_side, cfg.outer_scale))
+        self.near_off = to_dev(inst.near.offsets, np.int32)
+        self.near_leaf = to_dev(inst.near.leaves, np.int32)
+        # unit-box operators
+        def inv_parts(inv):
+            return (to_dev(inv.u, dt), to_dev(inv.inv_vals, dt),
+                    to_dev(np.ascontiguousarray(inv.v.T), dt))
+        self.up_inv = inv_parts(exp.up_inv)
+        self.dn_inv = inv_parts(exp.down_inv)
+        self.r_up, self.r_dn = exp.up_inv.rank, exp.down_inv.rank
+        self.m2mT = to_dev(np.ascontiguousarray(exp.m2m_kernels.T), dt)
+        self.l2lT = to_dev(np.ascontiguousarray(exp.l2l_kernels.T), dt)
+        # tree levels
+        self.n_src = [st.level_keys(l).shape[0] for l in range(cfg.depth + 1)]
+        self.n_tgt = [tt.level_keys(l).shape[0] for l in range(cfg.depth + 1)]
+        self.src_child = {l: to_dev(child_table(st, l), np.int32) for l in range(3, cfg.depth + 1)}
+        self._tgt_child_np = {l: child_table(tt, l) for l in range(3, cfg.depth + 1)}
+        self._l2l_rowmaps = {}
+        self.side = [inst.domain.box_side(l) for l in range(cfg.depth + 1)]
+        if cfg.backend == "blas":
+            self._init_blas(inst.blas_ops, inst.blas_plans)
+        else:
+            self._init_fft(inst.fft_ops, inst.halo_plans)
+        self._bufs = {}
+        self.last_timings = {}
+        self.last_m2l_calls = []
+
+    # ------------------------------------------------------------ BLAS-M2L
+    def _init_blas(self, ops, plans):
+        dt = self.np_dtype
+        k = ops.k
+        self.k = k
+        self.kin, self.ko_pad = blas_geometry(k, dt.itemsize)
+        s_pad = np.zeros((self.n_e, self.kin), dtype=dt)
+        s_pad[:, :k] = ops.s
+        self.S = to_dev(s_pad)
+        self.UT = to_dev(np.ascontiguousarray(ops.u.T), dt)          # (k, n_c)
+        cores = dense_cores(ops, np.float64)                          # (316, k, k) [out, in]
+        dt_pad = np.zeros((cores.shape[0], self.kin, self.ko_pad), dtype=dt)
+        dt_pad[:, :k, :k] = cores.transpose(0, 2, 1)
+        self.Dt = to_dev(dt_pad)
+        self.class_tv = to_dev(class_transfer_table(), np.int32)
+        self.blas_plan_dev = {l: self._upload_plan(p) for l, p in plans.items()}
+
+    def _upload_plan(self, plan):
+        n_tiles = plan.tile_class.shape[0]
+        src_t = plan.src.reshape(n_tiles, TILE_TARGETS, 189).transpose(0, 2, 1)
+        return dict(n_tiles=n_tiles, tile_targets=to_dev(plan.tile_targets, np.int32),
+                    tile_class=to_dev(plan.tile_class, np.int32),
+                    src=to_dev(np.ascontiguousarray(src_t), np.int32))
+
+    def m2l_blas_level(self, lvl, mult, nrhs, check, plan=None):
+        """check (n_tgt*R, n_c) = level_scale * U^T-expansion of the fused sweep."""
+        b = self._buffers(nrhs)
+        plan = plan if plan is not None else self.blas_plan_dev[lvl]
+        n_s, n_t = self.n_src[lvl], self.n_tgt[lvl]
+        qt = b["qt"][: n_s * nrhs]
+        acc = b["acc"][: n_t * nrhs]
+        self.la.gemm(n_s * nrhs, self.k, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt,
+                     self.kin)
+        launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
+                 P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
+                 P(self.class_tv), plan["n_tiles"], nrhs, P(acc), stream_handle())
+        self.la.gemm(n_t * nrhs, self.n_c, self.k, 1.0 / self.side[lvl], acc, self.ko_pad,
+                     self.UT, self.n_c, check, self.n_c)
+        return 3
+
+    # ------------------------------------------------------------- FFT-M2L
+    def _init_fft(self, ops, plans):
+        self.order = ops.order
+        self.n_freq = ops.n_freq
+        kh = np.ascontiguousarray(ops.khat)
+        self.khat = to_dev(kh.view(np.float32 if kh.dtype == np.complex64 else np.float64))
+        self.fft_plan_dev = {}
+        for l, p in plans.items():
+            sbox = np.full(p.n_src_clusters * 8, -1, dtype=np.int32)
+            sbox[p.src_slot] = np.arange(p.src_slot.shape[0])
+            tbox = np.full(p.n_tgt_clusters * 8, -1, dtype=np.int32)
+            tbox[p.tgt_slot] = np.arange(p.tgt_slot.shape[0])
+            self.fft_plan_dev[l] = dict(nsc=p.n_src_clusters, ntc=p.n_tgt_clusters,
+                                        sbox=to_dev(sbox), tbox=to_dev(tbox),
+                                        halo=to_dev(p.halo, np.int64))
+
+    def m2l_fft_level(self, lvl, mult, nrhs, check, plan=None):
+        plan = plan if plan is not None else self.fft_plan_dev[lvl]
+        b = self._buffers(nrhs)
+        nsc, ntc = plan["nsc"], plan["ntc"]
+        qhat = b["qhat"][: 2 * self.n_freq * nsc * 8 * nrhs]
+        phat = b["phat"][: 2 * self.n_freq * ntc * 8 * nrhs]
+        s = stream_handle()
+        launch(f"kifmm_fft_forward_{self.sfx}", P(mult), nrhs, self.order, P(plan["sbox"]), nsc,
+                 P(qhat), s)
+        phat.zero_()
+        cname = "c64" if self.sfx == "f32" else "c128"
+        launch(f"kifmm_hadamard_m2l_{cname}", P(self.khat), P(qhat), P(plan["halo"]), P(phat),
+                 self.n_freq, nsc, ntc, nrhs, s)
+        launch(f"kifmm_fft_inverse_{self.sfx}", P(phat), nrhs, self.order, P(plan["tbox"]), ntc,
+                 1.0 / self.side[lvl], P(check), s)
+        return 4
+
+    # -------------------------------------------------------------- buffers
+    def _buffers(self, nrhs):
+        if nrhs in self._bufs:
+            return self._bufs[nrhs]
+        T, dev = self.T, _dev()
+        R = nrhs
+        d = self.depth
+        b = {}
+        b["q"] = torch.empty(self.sx.shape[0] * R, dtype=T, device=dev)
+        b["mult"] = [torch.empty(self.n_src[l] * R * self.n_e, dtype=T, device=dev)
+                     for l in range(d + 1)]
+        b["loc"] = [torch.empty(self.n_tgt[l] * R * self.n_e, dtype=T, device=dev)
+                    for l in range(d + 1)]
+        nmax_rows = max(max(self.n_src), max(self.n_tgt)) * R
+        b["phi"] = torch.empty(max(nmax_rows * max(self.n_c, 1),
+                                   max(self.n_tgt[:d] + [1]) * R * 8 * self.n_c), dtype=T,
+                               device=dev)
+        rmax = max(self.r_up, self.r_dn)
+        b["tmp"] = torch.empty(max(nmax_rows, max(self.n_tgt[:d] + [1]) * 8 * R) * rmax,
+                               dtype=T, device=dev)
+        b["stack"] = torch.empty(max(self.n_src[2:d] + [1]) * R * 8 * self.n_e, dtype=T,
+                                 device=dev)
+        if self.cfg.backend == "blas":
+            b["qt"] = torch.zeros(max(self.n_src) * R * self.kin, dtype=T, device=dev)
+            b["acc"] = torch.zeros(max(self.n_tgt) * R * self.ko_pad, dtype=T, device=dev)
+        else:
+            nsc = max(p["nsc"] for p in self.fft_plan_dev.values())
+            ntc = max(p["ntc"] for p in self.fft_plan_dev.values())
+            b["qhat"] = torch.empty(2 * self.n_freq * nsc * 8 * R, dtype=T, device=dev)
+            b["phat"] = torch.empty(2 * self.n_freq * ntc * 8 * R, dtype=T, device=dev)
+        b["out"] = torch.empty(self.tx.shape[0] * R, dtype=T, device=dev)
+        b["qin"] = torch.empty(self.sx.shape[0] * R, dtype=torch.float64, device=dev)
+        self._bufs[nrhs] = b
+        return b
+
+    def _l2l_rowmap(self, lvl, nrhs):
+        """Row map of the L2L solve output (p, r, c) -> child row * R + r."""
+        key = (lvl, nrhs)
+        if key not in self._l2l_rowmaps:
+            ch = self._tgt_child_np[lvl]                           # (n_par, 8)
+            n_par = ch.shape[0]
+            r = np.arange(nrhs)
+            dest = ch[:, None, :] * nrhs + r[None, :, None]        # (n_par, R, 8)
+            dest = np.where(ch[:, None, :] >= 0, dest, -1)
+            self._l2l_rowmaps[key] = to_dev(dest.reshape(n_par * nrhs * 8), np.int32)
+        return self._l2l_rowmaps[key]
+
+    # ------------------------------------------------------------- evaluate
+    def evaluate_device(self, q_dev, nrhs, timings=False):
+        """Full evaluate from float64 charges on the device (caller order,
+        (n_src, R) C-contiguous) to potentials on the device (caller order,
+        (n_tgt, R), working dtype).  Returns the output tensor (a view of an
+        internal buffer)."""
+        b = self._buffers(nrhs)
+        R = nrhs
+        s = stream_handle()
+        d = self.depth
+        n_e, n_c = self.n_e, self.n_c
+        la, sfx = self.la, self.sfx
+        ev = [] if timings else None
+
+        def phase(name):
+            set_tag(name)
+            if ev is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                ev.append((name, e))
+
+        phase("p2m")
+        q = b["q"]
+        launch(f"kifmm_gather_charges_{sfx}", P(q_dev), P(self.s_perm), self.sx.shape[0], R,
+                 P(q), s)
+        # P2M: check potentials, then the up_inv solve scaled by the leaf side.
+        mult, phi, tmp = b["mult"], b["phi"], b["tmp"]
+        nl = self.n_src[d]
+        launch(f"kifmm_p2m_check_{sfx}", P(self.sx), P(self.sy), P(self.sz), P(q), R,
+                 P(self.s_start), P(self.s_count), nl, P(self.s_centers), P(self.check_base),
+                 n_c, P(phi), s)
+        la.solve(self.up_inv, phi, nl * R, mult[d], self.side[d], tmp)
+        phase("m2m")
+        # M2M down to level 2 (levels 0-1 carry no M2L).
+        for lvl in range(d, 2, -1):
+            n_par = self.n_src[lvl - 1]
+            st = b["stack"]
+            launch(f"kifmm_stack_children_{sfx}", P(mult[lvl]), P(self.src_child[lvl]), n_par,
+                     R, n_e, P(st), s)
+            la.gemm(n_par * R, n_c, 8 * n_e, 1.0, st, 8 * n_e, self.m2mT, n_c, phi, n_c)
+            la.solve(self.up_inv, phi, n_par * R, mult[lvl - 1], 1.0, tmp)
+        loc = b["loc"]
+        for lvl in range(2, d + 1):
+            loc[lvl].zero_()
+        calls = []
+        for lvl in range(2, d + 1):
+            n_t = self.n_tgt[lvl]
+            phase(f"m2l{lvl}")
+            check = phi[: n_t * R * n_c]
+            if self.cfg.backend == "blas":
+                calls.append(self.m2l_blas_level(lvl, mult[lvl], R, check))
+            else:
+                calls.append(self.m2l_fft_level(lvl, mult[lvl], R, check))
+            la.solve(self.dn_inv, check, n_t * R, loc[lvl], self.side[lvl], tmp, accumulate=True)
+            if lvl < d:
+                phase(f"l2l{lvl}")
+                n_par = n_t
+                la.gemm(n_par * R, 8 * n_c, n_e, 1.0, loc[lvl], n_e, self.l2lT, 8 * n_c, phi,
+                        8 * n_c)
+                la.solve(self.dn_inv, phi, n_par * R * 8, loc[lvl + 1], 0.5, tmp,
+                         accumulate=True, rowmap=self._l2l_rowmap(lvl + 1, R))
+        phase("leaf")
+        out = b["out"]
+        launch(f"kifmm_leaf_pass_{sfx}", P(self.tx), P(self.ty), P(self.tz), P(self.t_start),
+                 P(self.t_count), self.n_tgt[d], P(self.t_centers), P(self.equiv_base), n_e,
+                 P(loc[d]), P(self.sx), P(self.sy), P(self.sz), P(q), P(self.s_start),
+                 P(self.s_count), P(self.near_off), P(self.near_leaf), R, P(self.t_perm), 3,
+                 P(out), s)
+        phase("end")
+        self.last_m2l_calls = calls
+        self._events = ev
+        return out[: self.tx.shape[0] * R].view(self.tx.shape[0], R)
+
+    def collect_timings(self):
+        ev = getattr(self, "_events", None)
+        if not ev:
+            return {}
+        ev[-1][1].synchronize()
+        t = {k: 0.0 for k in ("p2m", "m2m", "m2l", "l2l", "l2p", "p2p")}
+        for (n0, e0), (n1, e1) in zip(ev[:-1], ev[1:]):
+            dt_s = e0.elapsed_time(e1) / 1e3
+            key = "p2p" if n0 == "leaf" else ("m2l" if n0.startswith("m2l") else
+                                               "l2l" if n0.startswith("l2l") else n0)
+            t[key] += dt_s
+        t["leaf_fused"] = 1.0      # l2p is fused into the p2p leaf pass
+        return t
+
+    def evaluate_host(self, q_host: np.ndarray, timings=False) -> np.ndarray:
+        """Host charges (n_src, R) float64 in caller order -> host potentials."""
+        R = q_host.shape[1]
+        b = self._buffers(R)
+        qin = b["qin"][: q_host.size]
+        qin.copy_(torch.from_numpy(np.ascontiguousarray(q_host, dtype=np.float64)).reshape(-1))
+        out = self.evaluate_device(qin, R, timings=timings)
+        res = out.cpu().numpy().copy()
+        if timings:
+            self.last_timings = self.collect_timings()
+        return res
+
+
+# ---------------------------------------------------------------- shims
+def apply_level_host(ops, buckets, multipoles, n_targets, level_scale, counter=None):
+    """Level-boundary drop-in for reference ``m2l_blas.apply_level``."""
+    require_cuda()
+    mult = np.ascontiguousarray(multipoles)
+    dt = mult.dtype
+    n_src, nrhs, n_e = mult.shape
+    T = _NP2T[np.dtype(dt)]
+    sfx = "f32" if dt == np.float32 else "f64"
+    la = Linalg(sfx)
+    k = ops.k
+    n_c = ops.u.shape[0]
+    kin, ko_pad = blas_geometry(k, dt.itemsize)
+    s_pad = np.zeros((n_e, kin), dtype=dt)
+    s_pad[:, :k] = ops.s
+    cores = dense_cores(ops, np.float64)
+    dt_pad = np.zeros((cores.shape[0], kin, ko_pad), dtype=dt)
+    dt_pad[:, :k, :k] = cores.transpose(0, 2, 1)
+    plan = level_plan_from_buckets(buckets, n_targets)
+    n_tiles = plan.tile_class.shape[0]
+    src_t = plan.src.reshape(n_tiles, TILE_TARGETS, 189).transpose(0, 2, 1)
+    dev = _dev()
+    m = to_dev(mult.reshape(n_src * nrhs, n_e))
+    qt = torch.zeros(max(n_src, 1) * nrhs * kin, dtype=T, device=dev)
+    acc = torch.zeros(max(n_targets, 1) * nrhs * ko_pad, dtype=T, device=dev)
+    check = torch.zeros(max(n_targets, 1) * nrhs * n_c, dtype=T, device=dev)
+    S, Dt_, UT = to_dev(s_pad), to_dev(dt_pad), to_dev(np.ascontiguousarray(ops.u.T), dt)
+    la.gemm(n_src * nrhs, k, n_e, 1.0, m, n_e, S, kin, qt, kin)
+    if n_tiles:
+        launch(f"kifmm_m2l_sweep_{sfx}", P(qt), P(Dt_), kin, ko_pad,
+                 P(to_dev(plan.tile_targets, np.int32)), P(to_dev(plan.tile_class, np.int32)),
+                 P(to_dev(np.ascontiguousarray(src_t), np.int32)),
+                 P(to_dev(class_transfer_table(), np.int32)), n_tiles, nrhs, P(acc),
+                 stream_handle())
+    la.gemm(n_targets * nrhs, n_c, k, level_scale, acc, ko_pad, UT, n_c, check, n_c)
+    if counter is not None:
+        counter.append(3)
+    return check[: n_targets * nrhs * n_c].cpu().numpy().reshape(n_targets, nrhs, n_c)
+
+
+def m2l_fft_level_host(ops, plan, mult, level_scale):
+    """Level-boundary drop-in for reference ``m2l_fft.m2l_fft_level``."""
+    require_cuda()
+    mult = np.ascontiguousarray(mult)
+    dt = mult.dtype
+    n_src, nrhs, n_e = mult.shape
+    T = _NP2T[np.dtype(dt)]
+    sfx = "f32" if dt == np.float32 else "f64"
+    kh = np.ascontiguousarray(ops.khat.astype(np.complex64 if dt == np.float32 else np.complex128))
+    khat = to_dev(kh.view(np.float32 if dt == np.float32 else np.float64))
+    nsc, ntc = plan.n_src_clusters, plan.n_tgt_clusters
+    sbox = np.full(nsc * 8, -1, dtype=np.int32)
+    sbox[plan.src_slot] = np.arange(plan.src_slot.shape[0])
+    tbox = np.full(ntc * 8, -1, dtype=np.int32)
+    tbox[plan.tgt_slot] = np.arange(plan.tgt_slot.shape[0])
+    n_tgt = plan.tgt_slot.shape[0]
+    dev = _dev()
+    nf = ops.n_freq
+    qhat = torch.zeros(2 * nf * max(nsc, 1) * 8 * nrhs, dtype=T, device=dev)
+    phat = torch.zeros(2 * nf * max(ntc, 1) * 8 * nrhs, dtype=T, device=dev)
+    check = torch.zeros(max(n_tgt, 1) * nrhs * n_e, dtype=T, device=dev)
+    s = stream_handle()
+    m = to_dev(mult)
+    launch(f"kifmm_fft_forward_{sfx}", P(m), nrhs, ops.order, P(to_dev(sbox)), nsc, P(qhat), s)
+    cname = "c64" if sfx == "f32" else "c128"
+    launch(f"kifmm_hadamard_m2l_{cname}", P(khat), P(qhat), P(to_dev(plan.halo, np.int64)),
+             P(phat), nf, nsc, ntc, nrhs, s)
+    launch(f"kifmm_fft_inverse_{sfx}", P(phat), nrhs, ops.order, P(to_dev(tbox)), ntc,
+             float(level_scale), P(check), s)
+    return check[: n_tgt * nrhs * n_e].cpu().numpy().reshape(n_tgt, nrhs, n_e)

@@ -1,0 +1,117 @@
+"""Kernel-level drop-in for the reference ``kifmm3d.hotloops`` module
+(``hotloops.py:13-77``): same function names, argument order and
+accumulate/overwrite semantics, with host numpy arrays in and out, but
+every loop runs on the GPU through ``libkifmm_b200.so``.
+
+``BACKEND`` is ``"cuda"``; there is no compiled-CPU or NumPy fallback (the
+reference's ``KIFMM_PURE_PYTHON`` switch has no counterpart).  ``threads``
+arguments are accepted and ignored.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+BACKEND = "cuda"
+COMPILED = True
+
+
+def resolve_threads(threads=None) -> int:
+    from .engine import _resolve_threads
+    return _resolve_threads(threads)
+
+
+def _check_dtype(*arrays):
+    dt = np.asarray(arrays[0]).dtype
+    if dt not in (np.float32, np.float64):
+        raise TypeError(f"unsupported dtype {dt}")
+    for a in arrays[1:]:
+        if np.asarray(a).dtype != dt:
+            raise ValueError("all real arrays must share one dtype")
+    return dt
+
+
+def _dev(a, dtype=None):
+    from .device import to_dev
+    return to_dev(a, dtype)
+
+
+def _sfx(dt):
+    return "f32" if dt == np.float32 else "f64"
+
+
+def laplace_potentials(tx, ty, tz, sx, sy, sz, charges, out, threads=None):
+    """out[i, r] += sum_j K(t_i, s_j) q[j, r]  (reference _hot.pyx:24-65)."""
+    from . import _native as nat
+    from .device import P, require_cuda, stream_handle
+    require_cuda()
+    dt = _check_dtype(tx, ty, tz, sx, sy, sz, charges, out)
+    nt, ns = np.asarray(tx).shape[0], np.asarray(sx).shape[0]
+    q = np.ascontiguousarray(charges).reshape(ns, -1)
+    o = _dev(np.ascontiguousarray(out).reshape(nt, -1))
+    if nt and ns:
+        nat.call(f"kifmm_laplace_potentials_{_sfx(dt)}", P(_dev(tx)), P(_dev(ty)), P(_dev(tz)),
+                 nt, P(_dev(sx)), P(_dev(sy)), P(_dev(sz)), ns, P(_dev(q)), q.shape[1], P(o),
+                 stream_handle())
+    out[...] = o.cpu().numpy().reshape(np.shape(out))
+    return out
+
+
+def laplace_matrix(tx, ty, tz, sx, sy, sz, out=None, threads=None):
+    """out[i, j] = K(t_i, s_j), overwritten (reference _hot.pyx:68-88)."""
+    from . import _native as nat
+    from .device import P, require_cuda, stream_handle
+    require_cuda()
+    dt = _check_dtype(tx, ty, tz, sx, sy, sz)
+    nt, ns = np.asarray(tx).shape[0], np.asarray(sx).shape[0]
+    if out is None:
+        out = np.empty((nt, ns), dtype=dt)
+    import torch
+    o = torch.empty(max(nt * ns, 1), dtype=torch.float32 if dt == np.float32 else torch.float64,
+                    device="cuda")
+    if nt and ns:
+        nat.call(f"kifmm_laplace_matrix_{_sfx(dt)}", P(_dev(tx)), P(_dev(ty)), P(_dev(tz)), nt,
+                 P(_dev(sx)), P(_dev(sy)), P(_dev(sz)), ns, P(o), stream_handle())
+        out[...] = o[: nt * ns].cpu().numpy().reshape(nt, ns)
+    return out
+
+
+def p2p_blocked(tx, ty, tz, leaf_of_target, sx, sy, sz, charges, src_offsets, out, threads=None):
+    """Near-field sweep over the gathered CSR (reference _hot.pyx:91-138)."""
+    from . import _native as nat
+    from .device import P, require_cuda, stream_handle
+    require_cuda()
+    dt = _check_dtype(tx, ty, tz, sx, sy, sz, charges, out)
+    nt = np.asarray(tx).shape[0]
+    ns = np.asarray(sx).shape[0]
+    q = np.ascontiguousarray(charges).reshape(ns, -1)
+    offs = np.ascontiguousarray(src_offsets, dtype=np.int64)
+    o = _dev(np.ascontiguousarray(out).reshape(nt, -1))
+    if nt:
+        nat.call(f"kifmm_p2p_blocked_{_sfx(dt)}", P(_dev(tx)), P(_dev(ty)), P(_dev(tz)), nt,
+                 P(_dev(leaf_of_target, np.int64)), P(_dev(sx)), P(_dev(sy)), P(_dev(sz)),
+                 P(_dev(q)), q.shape[1], P(_dev(offs)), offs.shape[0] - 1, P(o), stream_handle())
+    out[...] = o.cpu().numpy().reshape(np.shape(out))
+    return out
+
+
+def hadamard_m2l(khat, qhat, halo, phat, block=32, threads=None):
+    """phat += frequency-major halo block MAC (reference _hot.pyx:141-178)."""
+    from . import _native as nat
+    from .device import P, require_cuda, stream_handle
+    require_cuda()
+    khat, qhat, phat = (np.asarray(a) for a in (khat, qhat, phat))
+    if khat.dtype not in (np.complex64, np.complex128):
+        raise TypeError(f"unsupported dtype {khat.dtype}")
+    if qhat.dtype != khat.dtype or phat.dtype != khat.dtype:
+        raise ValueError("khat, qhat and phat must share one complex dtype")
+    rdt = np.float32 if khat.dtype == np.complex64 else np.float64
+    nf, nsc, _, nrhs = qhat.shape
+    ntc = np.asarray(halo).shape[0]
+    p = _dev(np.ascontiguousarray(phat).view(rdt))
+    nat.call("kifmm_hadamard_m2l_" + ("c64" if rdt == np.float32 else "c128"),
+             P(_dev(np.ascontiguousarray(khat).view(rdt))),
+             P(_dev(np.ascontiguousarray(qhat).view(rdt))), P(_dev(halo, np.int64)), P(p), nf,
+             nsc, ntc, nrhs, stream_handle())
+    phat[...] = p.cpu().numpy().view(khat.dtype).reshape(phat.shape)
+    return phat
