@@ -99,19 +99,21 @@ int kifmm_stack_children_f64(const double* mult, const int32_t* child, int64_t n
                              int64_t nrhs, int64_t ne, double* out, void* stream);
 
 /* BLAS-M2L fused bucket sweep (m2l_blas.py:284-320), target-stationary:
- * acc[(tgt*nrhs + r)*ko + a] = sum_j sum_b Dt[tv(j), b, a] * qt[(src*nrhs + r)*ki + b]
- * over the 189 vectors j of each tile's parity class, in ascending order.
+ * acc[(tgt*nrhs + r), p*ko + a] = sum_{j in piece p} sum_b Dt[tv(j), b, a] qt[(src*nrhs + r)*ki + b]
+ * over the 189 vectors j of each tile's parity class (ascending), split into
+ * nsplit contiguous pieces p (row stride nsplit*ko); the caller sums the
+ * pieces (the expansion GEMM does, in fixed order).
  * qt (n_src*nrhs, ki) zero-padded; Dt (316, ki, ko) transposed dense cores.
- * tile_targets (n_tiles*128), tile_class (n_tiles), src (n_tiles*128, 189),
+ * tile_targets (n_tiles*128), tile_class (n_tiles), src (n_tiles, 189, 128),
  * class_tv (8, 189).  Padding slots (target -1) are skipped. */
 int kifmm_m2l_sweep_f32(const float* qt, const float* Dt, int64_t ki, int64_t ko,
                         const int32_t* tile_targets, const int32_t* tile_class,
                         const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
-                        int64_t nrhs, float* acc, void* stream);
+                        int64_t nrhs, int64_t nsplit, float* acc, void* stream);
 int kifmm_m2l_sweep_f64(const double* qt, const double* Dt, int64_t ki, int64_t ko,
                         const int32_t* tile_targets, const int32_t* tile_class,
                         const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
-                        int64_t nrhs, double* acc, void* stream);
+                        int64_t nrhs, int64_t nsplit, double* acc, void* stream);
 
 /* FFT-M2L forward (m2l_fft.py:236-247): embed each box's multipole at
  * lattice+p of the n^3 grid (n = 2p), real 3-D DFT, and write the spectrum
@@ -159,6 +161,11 @@ int kifmm_gather_charges_f32(const double* q_in, const int64_t* perm, int64_t n,
                              float* q_tree, void* stream);
 int kifmm_gather_charges_f64(const double* q_in, const int64_t* perm, int64_t n, int64_t nrhs,
                              double* q_tree, void* stream);
+
+/* Pipe-peak probe for roofline denominators: kind 0 FP32 FFMA, 1 FP64 DFMA,
+ * 2 MUFU rsqrt; blocks*threads*iters*128 operations per launch. */
+int kifmm_probe(int kind, int64_t blocks, int64_t threads, int64_t iters, void* out,
+                void* stream);
 
 /* Library identification: returns the compiled SM target (e.g. 100). */
 int kifmm_sm_target(void);

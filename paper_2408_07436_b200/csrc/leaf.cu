@@ -66,6 +66,38 @@ __global__ void __launch_bounds__(32 * kWarps) p2m_check_kernel(
   }
 }
 
+// Near-field staging capacity per warp (sources), see leaf_pass_kernel.
+template <typename T> struct cap_of { static constexpr int v = sizeof(T) == 4 ? 512 : 256; };
+
+// Sum over staged sources [0, m): the first `guarded` entries may coincide
+// with a target (they come from the target's own leaf), the rest cannot: two
+// points in different leaves have distinct coordinates, and every leaf
+// boundary lies >= 1 leaf side away from 0, so r2 cannot underflow either.
+template <typename T, bool TWO>
+__device__ __forceinline__ void near_sum(const typename vec4<T>::v* buf, int m, int guarded,
+                                         T x0, T y0, T z0, T x1, T y1, T z1, T& a0, T& a1) {
+  using V = typename vec4<T>::v;
+  int k = 0;
+  for (; k < guarded; ++k) {
+    V s = buf[k];
+    a0 += inv_r<T>(x0 - s.x, y0 - s.y, z0 - s.z) * s.w;
+    if (TWO) a1 += inv_r<T>(x1 - s.x, y1 - s.y, z1 - s.z) * s.w;
+  }
+  T b0 = 0, b1 = 0;
+#pragma unroll 4
+  for (; k < m; ++k) {
+    V s = buf[k];
+    T dx = x0 - s.x, dy = y0 - s.y, dz = z0 - s.z;
+    a0 += real_traits<T>::rsq(dx * dx + dy * dy + dz * dz) * s.w;
+    if (TWO) {
+      T ex = x1 - s.x, ey = y1 - s.y, ez = z1 - s.z;
+      b1 += real_traits<T>::rsq(ex * ex + ey * ey + ez * ez) * s.w;
+    }
+  }
+  a0 += b0;
+  a1 += b1;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
     const T* __restrict__ tx, const T* __restrict__ ty, const T* __restrict__ tz,
@@ -77,62 +109,79 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
     const int32_t* __restrict__ near_leaf, int64_t nrhs, const int64_t* __restrict__ perm,
     int parts, T* __restrict__ out) {
   using V = typename vec4<T>::v;
-  __shared__ V buf[kWarps][32];
+  constexpr int kCap = cap_of<T>::v;
+  __shared__ V sbuf[kWarps][kCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  V* buf = sbuf[w];
   const int64_t b = (int64_t)blockIdx.x * kWarps + w;
   if (b >= n_tleaves) return;
   const int64_t t0 = tstart[b];
   const int tc = tcount[b];
   const double cx = centers[b * 3], cy = centers[b * 3 + 1], cz = centers[b * 3 + 2];
   const int n0 = near_off[b], n1 = near_off[b + 1];
-  for (int tb = 0; tb < tc; tb += 32) {
-    const bool live = tb + lane < tc;
-    const int64_t i = t0 + tb + lane;
-    const T x = live ? tx[i] : T(0), y = live ? ty[i] : T(0), z = live ? tz[i] : T(0);
+  for (int tb = 0; tb < tc; tb += 64) {
+    const bool two = tc - tb > 32;                 // warp-uniform
+    const bool live0 = tb + lane < tc, live1 = tb + 32 + lane < tc;
+    const int64_t i0 = t0 + tb + lane, i1 = i0 + 32;
+    const T x0 = live0 ? tx[i0] : T(0), y0 = live0 ? ty[i0] : T(0), z0 = live0 ? tz[i0] : T(0);
+    const T x1 = live1 ? tx[i1] : T(0), y1 = live1 ? ty[i1] : T(0), z1 = live1 ? tz[i1] : T(0);
     for (int64_t r = 0; r < nrhs; ++r) {
+      T far0 = 0, far1 = 0, near0 = 0, near1 = 0;
       // L2P: downward equivalent densities of the leaf -> its targets.
-      T far = 0;
       const T* loc = local + (b * nrhs + r) * ne;
-      for (int64_t e0 = 0; (parts & 1) && e0 < ne; e0 += 32) {
+      for (int64_t e0 = 0; (parts & 1) && e0 < ne; e0 += kCap) {
+        const int m = (int)min64(kCap, ne - e0);
         __syncwarp();
-        const int64_t e = e0 + lane;
-        if (e < ne) {
-          buf[w][lane] = V{real_traits<T>::from_d(exact_add(cx, base[e * 3])),
-                           real_traits<T>::from_d(exact_add(cy, base[e * 3 + 1])),
-                           real_traits<T>::from_d(exact_add(cz, base[e * 3 + 2])), loc[e]};
+        for (int k = lane; k < m; k += 32) {
+          const int64_t e = e0 + k;
+          buf[k] = V{real_traits<T>::from_d(exact_add(cx, base[e * 3])),
+                     real_traits<T>::from_d(exact_add(cy, base[e * 3 + 1])),
+                     real_traits<T>::from_d(exact_add(cz, base[e * 3 + 2])), loc[e]};
         }
         __syncwarp();
-        const int m = (int)min64(32, ne - e0);
-        for (int k = 0; k < m; ++k) {
-          V s = buf[w][k];
-          far += inv_r<T>(x - s.x, y - s.y, z - s.z) * s.w;
-        }
+        if (two) near_sum<T, true>(buf, m, m, x0, y0, z0, x1, y1, z1, far0, far1);
+        else near_sum<T, false>(buf, m, m, x0, y0, z0, x1, y1, z1, far0, far1);
       }
-      // P2P: own leaf, then neighbours in Morton order.
-      T near = 0;
-      for (int n = n0; (parts & 2) && n < n1; ++n) {
-        const int sl = near_leaf[n];
-        const int64_t j0 = sstart[sl];
-        const int jc = scount[sl];
-        for (int jb = 0; jb < jc; jb += 32) {
+      // P2P: own leaf first, then neighbours in Morton order, staged in
+      // shared memory up to kCap sources at a time.
+      if (parts & 2) {
+        int fill = 0;
+        int guarded = n1 > n0 ? scount[near_leaf[n0]] : 0;
+        auto flush = [&]() {
           __syncwarp();
-          if (jb + lane < jc) {
-            const int64_t j = j0 + jb + lane;
-            buf[w][lane] = V{sx[j], sy[j], sz[j], q[j * nrhs + r]};
-          }
+          const int g = min(guarded, fill);
+          if (two) near_sum<T, true>(buf, fill, g, x0, y0, z0, x1, y1, z1, near0, near1);
+          else near_sum<T, false>(buf, fill, g, x0, y0, z0, x1, y1, z1, near0, near1);
+          guarded -= g;
+          fill = 0;
           __syncwarp();
-          const int m = min(32, jc - jb);
-#pragma unroll 4
-          for (int k = 0; k < m; ++k) {
-            V s = buf[w][k];
-            near += inv_r<T>(x - s.x, y - s.y, z - s.z) * s.w;
+        };
+        for (int n = n0; n < n1; ++n) {
+          const int sl = near_leaf[n];
+          const int64_t j0 = sstart[sl];
+          const int jc = scount[sl];
+          for (int jb = 0; jb < jc;) {
+            if (fill == kCap) flush();
+            const int m = min(jc - jb, kCap - fill);
+            for (int k = lane; k < m; k += 32) {
+              const int64_t j = j0 + jb + k;
+              buf[fill + k] = V{sx[j], sy[j], sz[j], q[j * nrhs + r]};
+            }
+            fill += m;
+            jb += m;
           }
         }
+        if (fill) flush();
       }
-      if (live) {
-        const T c = real_traits<T>::inv4pi();
-        T* o = out + (perm ? perm[i] : i) * nrhs + r;
-        const T v = far * c + near * c;
+      const T c = real_traits<T>::inv4pi();
+      if (live0) {
+        T* o = out + (perm ? perm[i0] : i0) * nrhs + r;
+        const T v = far0 * c + near0 * c;
+        *o = (parts & 4) ? *o + v : v;
+      }
+      if (two && live1) {
+        T* o = out + (perm ? perm[i1] : i1) * nrhs + r;
+        const T v = far1 * c + near1 * c;
         *o = (parts & 4) ? *o + v : v;
       }
     }

@@ -6,11 +6,15 @@
 // (<= 316 gather/GEMM/scatter rounds, numpy-bound on the CPU).  Here the
 // sweep is target-stationary: a CTA owns a tile of 128 target boxes of one
 // parity class (all of which meet the same 189 transfer vectors), keeps the
-// tile's accumulator in registers for the whole sweep and streams, per
-// vector, the gathered source rows and the contracted core
-// D_t = ubar_t vbar_t^T through a double-buffered cp.async pipeline.  No
-// scatter, no atomics; the vector order is the canonical ascending order,
-// so the result is deterministic.
+// tile's accumulator in registers and streams, per vector, the gathered
+// source rows and the contracted core D_t = ubar_t vbar_t^T through a
+// double-buffered cp.async pipeline.  No scatter, no atomics.
+//
+// The 189-vector range is split into `nsplit` contiguous pieces handled by
+// different CTAs (so small levels still fill the 148 SMs); each piece writes
+// its own partial accumulator column block, and the expansion GEMM that
+// follows (K = nsplit * ko_pad against a stacked U^T) sums them in a fixed
+// order: the result is deterministic run to run.
 #include "common.cuh"
 
 using namespace kifmm;
@@ -20,6 +24,7 @@ namespace {
 constexpr int TMT = 128;   // targets per tile (matches the host plan)
 constexpr int RM = 4;      // accumulator rows per thread (rows tm + 32*i)
 constexpr int RN = 8;      // accumulator columns per thread (contiguous)
+constexpr int MAXG = 12;   // max gather chunks per thread per step (register-cached indices)
 
 template <typename T>
 struct sweep_cfg {
@@ -29,9 +34,9 @@ struct sweep_cfg {
 template <typename T>
 __global__ void __launch_bounds__(512) m2l_sweep_kernel(
     const T* __restrict__ qt, const T* __restrict__ Dt, int kin, int ko_pad, int bk,
-    int nchunks, int kob, const int32_t* __restrict__ tile_targets,
+    int nchunks, int kob, int n_slabs, int jper, const int32_t* __restrict__ tile_targets,
     const int32_t* __restrict__ tile_class, const int32_t* __restrict__ src,
-    const int32_t* __restrict__ class_tv, int64_t nrhs, T* __restrict__ acc_out) {
+    const int32_t* __restrict__ class_tv, int64_t nrhs, int nsplit, T* __restrict__ acc_out) {
   constexpr int VEC = sweep_cfg<T>::VEC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int gstride = bk + VEC;                       // padded row stride of Gs
@@ -39,11 +44,14 @@ __global__ void __launch_bounds__(512) m2l_sweep_kernel(
   T* Ds = Gs + 2 * TMT * gstride;                     // [2][bk][kob]
 
   const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
   const int ng = kob / RN;
   const int tn = tid % ng, tm = tid / ng;             // tm in [0, 32)
   const int64_t tile = blockIdx.x;
   const int64_t r = blockIdx.y;
-  const int c0 = blockIdx.z * kob;
+  const int slab = blockIdx.z % n_slabs, split = blockIdx.z / n_slabs;
+  const int c0 = slab * kob;
+  const int j0 = split * jper, j1 = min(189, j0 + jper);
   const int cls = tile_class[tile];
   const int32_t* tsrc = src + tile * 189 * TMT;       // [189][TMT]
   const int32_t* tv_list = class_tv + cls * 189;
@@ -54,30 +62,41 @@ __global__ void __launch_bounds__(512) m2l_sweep_kernel(
 #pragma unroll
     for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
 
-  const int nsteps = 189 * nchunks;
+  // Staging assignment, fixed for the whole sweep: chunk e = tid + i*nthr.
   const int gch = bk / VEC;                           // 16-byte chunks per gathered row
   const int dch = kob / VEC;                          // 16-byte chunks per core row
+  const int n_g = TMT * gch, n_d = bk * dch;
+  int g_m[MAXG], g_off[MAXG];
+#pragma unroll
+  for (int i = 0; i < MAXG; ++i) {
+    const int e = tid + i * nthr;
+    g_m[i] = e < n_g ? e / gch : -1;
+    g_off[i] = e < n_g ? (e % gch) * VEC : 0;
+  }
 
+  const int nsteps = (j1 - j0) * nchunks;
   auto stage = [&](int st, int buf) {
-    const int j = st / nchunks, ch = st - j * nchunks;
+    const int j = j0 + st / nchunks, ch = st % nchunks;
     const int kk0 = ch * bk;
     T* g = Gs + buf * TMT * gstride;
-    for (int e = tid; e < TMT * gch; e += blockDim.x) {
-      const int m = e / gch, v = e - m * gch;
-      const int32_t s = __ldg(&tsrc[j * TMT + m]);
-      const T* gp = qt + ((int64_t)(s < 0 ? 0 : s) * nrhs + r) * kin + kk0 + v * VEC;
-      cp_async16(g + m * gstride + v * VEC, gp, s >= 0);
+    const int32_t* srow = tsrc + j * TMT;
+#pragma unroll
+    for (int i = 0; i < MAXG; ++i) {
+      if (g_m[i] < 0) break;
+      const int32_t s = __ldg(&srow[g_m[i]]);
+      const T* gp = qt + ((int64_t)(s < 0 ? 0 : s) * nrhs + r) * kin + kk0 + g_off[i];
+      cp_async16(g + g_m[i] * gstride + g_off[i], gp, s >= 0);
     }
     const T* dsrc = Dt + ((int64_t)tv_list[j] * kin + kk0) * ko_pad + c0;
     T* d = Ds + buf * bk * kob;
-    for (int e = tid; e < bk * dch; e += blockDim.x) {
+    for (int e = tid; e < n_d; e += nthr) {
       const int row = e / dch, v = e - row * dch;
       cp_async16(d + row * kob + v * VEC, dsrc + (int64_t)row * ko_pad + v * VEC, true);
     }
     cp_async_commit();
   };
 
-  stage(0, 0);
+  if (nsteps > 0) stage(0, 0);
   for (int st = 0; st < nsteps; ++st) {
     const int buf = st & 1;
     if (st + 1 < nsteps) {
@@ -89,6 +108,7 @@ __global__ void __launch_bounds__(512) m2l_sweep_kernel(
     __syncthreads();
     const T* g = Gs + buf * TMT * gstride;
     const T* d = Ds + buf * bk * kob + tn * RN;
+#pragma unroll 2
     for (int kk = 0; kk < bk; kk += VEC) {
       T a[RM][VEC];
 #pragma unroll
@@ -125,11 +145,12 @@ __global__ void __launch_bounds__(512) m2l_sweep_kernel(
     __syncthreads();
   }
 
+  const int64_t ld = (int64_t)nsplit * ko_pad;
 #pragma unroll
   for (int i = 0; i < RM; ++i) {
     const int32_t tgt = tile_targets[tile * TMT + tm + 32 * i];
     if (tgt < 0) continue;
-    T* o = acc_out + ((int64_t)tgt * nrhs + r) * ko_pad + c0 + tn * RN;
+    T* o = acc_out + ((int64_t)tgt * nrhs + r) * ld + (int64_t)split * ko_pad + c0 + tn * RN;
 #pragma unroll
     for (int j = 0; j < RN; j += VEC) {
       if constexpr (VEC == 4) {
@@ -145,10 +166,11 @@ __global__ void __launch_bounds__(512) m2l_sweep_kernel(
 template <typename T>
 int sweep(const T* qt, const T* Dt, int64_t kin, int64_t ko_pad, const int32_t* tile_targets,
           const int32_t* tile_class, const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
-          int64_t nrhs, T* acc, void* stream) {
+          int64_t nrhs, int64_t nsplit, T* acc, void* stream) {
   constexpr int VEC = sweep_cfg<T>::VEC;
   constexpr int BKMAX = sizeof(T) == 4 ? 64 : 32;
-  if (kin < VEC || ko_pad < RN || n_tiles < 0 || nrhs < 1) return KIFMM_EARG;
+  if (kin < VEC || ko_pad < RN || n_tiles < 0 || nrhs < 1 || nsplit < 1 || nsplit > 189)
+    return KIFMM_EARG;
   if (kin % VEC || ko_pad % RN) return KIFMM_EARG;
   if (n_tiles == 0) return 0;
   const int nchunks = (int)((kin + BKMAX - 1) / BKMAX);
@@ -160,13 +182,16 @@ int sweep(const T* qt, const T* Dt, int64_t kin, int64_t ko_pad, const int32_t* 
   const int kob = (int)(ko_pad / n_slabs);
   if (kob % RN) return KIFMM_EARG;
   const int threads = 32 * (kob / RN);
+  if ((TMT * (bk / VEC) + threads - 1) / threads > MAXG) return KIFMM_EARG;
+  const int jper = (int)((189 + nsplit - 1) / nsplit);
   const size_t smem = sizeof(T) * (2 * TMT * (bk + VEC) + 2 * bk * kob);
   auto kern = m2l_sweep_kernel<T>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)n_slabs);
+  dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)(n_slabs * nsplit));
   kern<<<grid, threads, smem, (cudaStream_t)stream>>>(qt, Dt, (int)kin, (int)ko_pad, bk, nchunks,
-                                                      kob, tile_targets, tile_class, src,
-                                                      class_tv, nrhs, acc);
+                                                      kob, n_slabs, jper, tile_targets,
+                                                      tile_class, src, class_tv, nrhs,
+                                                      (int)nsplit, acc);
   return launch_status();
 }
 
@@ -176,17 +201,17 @@ extern "C" {
 
 int kifmm_m2l_sweep_f32(const float* qt, const float* Dt, int64_t kin, int64_t ko_pad,
                         const int32_t* tile_targets, const int32_t* tile_class, const int32_t* src,
-                        const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, float* acc,
-                        void* s) {
+                        const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, int64_t nsplit,
+                        float* acc, void* s) {
   return sweep<float>(qt, Dt, kin, ko_pad, tile_targets, tile_class, src, class_tv, n_tiles, nrhs,
-                      acc, s);
+                      nsplit, acc, s);
 }
 int kifmm_m2l_sweep_f64(const double* qt, const double* Dt, int64_t kin, int64_t ko_pad,
                         const int32_t* tile_targets, const int32_t* tile_class, const int32_t* src,
-                        const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, double* acc,
-                        void* s) {
+                        const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, int64_t nsplit,
+                        double* acc, void* s) {
   return sweep<double>(qt, Dt, kin, ko_pad, tile_targets, tile_class, src, class_tv, n_tiles,
-                       nrhs, acc, s);
+                       nrhs, nsplit, acc, s);
 }
 
 }  // extern "C"

@@ -132,6 +132,72 @@ class Linalg:
                   accumulate=accumulate)
 
 
+SM_COUNT = 148
+
+
+def sweep_splits(n_tiles: int, n_slabs: int) -> int:
+    """Pieces of the 189-vector range per tile so a level fills ~4 CTAs per SM."""
+    work = max(1, n_tiles * n_slabs)
+    return int(min(63, max(1, -(-4 * SM_COUNT // work))))
+
+
+def upload_blas_plan(plan):
+    n_tiles = plan.tile_class.shape[0]
+    src_t = plan.src.reshape(n_tiles, TILE_TARGETS, 189).transpose(0, 2, 1)
+    return dict(n_tiles=n_tiles, tile_targets=to_dev(plan.tile_targets, np.int32),
+                tile_class=to_dev(plan.tile_class, np.int32),
+                src=to_dev(np.ascontiguousarray(src_t), np.int32))
+
+
+class BlasDevice:
+    """Device copies of the compressed M2L operators and the level apply:
+    projection q~ = M S, fused target-stationary sweep, expansion
+    check = level_scale * acc U^T (reference m2l_blas.py:284-326)."""
+
+    def __init__(self, ops, np_dtype, la):
+        dt = np.dtype(np_dtype)
+        self.la, self.sfx = la, la.sfx
+        self.k = k = ops.k
+        self.n_e, self.n_c = ops.s.shape[0], ops.u.shape[0]
+        self.kin, self.ko_pad = blas_geometry(k, dt.itemsize)
+        self.n_slabs = -(-k // 128)
+        s_pad = np.zeros((self.n_e, self.kin), dtype=dt)
+        s_pad[:, :k] = ops.s
+        self.S = to_dev(s_pad)
+        ut = np.zeros((self.ko_pad, self.n_c), dtype=dt)
+        ut[:k] = ops.u.T
+        self._ut_pad = ut
+        self._ut_rep = {}
+        cores = dense_cores(ops, np.float64)                          # (316, k, k) [out, in]
+        dt_pad = np.zeros((cores.shape[0], self.kin, self.ko_pad), dtype=dt)
+        dt_pad[:, :k, :k] = cores.transpose(0, 2, 1)
+        self.Dt = to_dev(dt_pad)
+        self.class_tv = to_dev(class_transfer_table(), np.int32)
+
+    def ut_rep(self, nsplit):
+        """U^T (zero-padded to ko_pad rows) stacked nsplit times: the
+        expansion GEMM then also sums the sweep's partial accumulators."""
+        if nsplit not in self._ut_rep:
+            self._ut_rep[nsplit] = to_dev(np.ascontiguousarray(np.tile(self._ut_pad, (nsplit, 1))))
+        return self._ut_rep[nsplit]
+
+    def acc_elems(self, n_t, nrhs, n_tiles):
+        return n_t * nrhs * sweep_splits(n_tiles, self.n_slabs) * self.ko_pad
+
+    def run_level(self, plan, mult, n_s, n_t, nrhs, level_scale, check, qt, acc):
+        la = self.la
+        nsplit = sweep_splits(plan["n_tiles"], self.n_slabs)
+        ld = nsplit * self.ko_pad
+        la.gemm(n_s * nrhs, self.k, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
+        if plan["n_tiles"]:
+            launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
+                   P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
+                   P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc), stream_handle())
+        la.gemm(n_t * nrhs, self.n_c, ld, level_scale, acc, ld, self.ut_rep(nsplit), self.n_c,
+                check, self.n_c)
+        return 3
+
+
 class DeviceFmm:
     """GPU-resident copy of an :class:`~.engine.FmmInstance` plan."""
 
@@ -192,43 +258,14 @@ class DeviceFmm:
 
     # ------------------------------------------------------------ BLAS-M2L
     def _init_blas(self, ops, plans):
-        dt = self.np_dtype
-        k = ops.k
-        self.k = k
-        self.kin, self.ko_pad = blas_geometry(k, dt.itemsize)
-        s_pad = np.zeros((self.n_e, self.kin), dtype=dt)
-        s_pad[:, :k] = ops.s
-        self.S = to_dev(s_pad)
-        self.UT = to_dev(np.ascontiguousarray(ops.u.T), dt)          # (k, n_c)
-        cores = dense_cores(ops, np.float64)                          # (316, k, k) [out, in]
-        dt_pad = np.zeros((cores.shape[0], self.kin, self.ko_pad), dtype=dt)
-        dt_pad[:, :k, :k] = cores.transpose(0, 2, 1)
-        self.Dt = to_dev(dt_pad)
-        self.class_tv = to_dev(class_transfer_table(), np.int32)
-        self.blas_plan_dev = {l: self._upload_plan(p) for l, p in plans.items()}
+        self.blas = BlasDevice(ops, self.np_dtype, self.la)
+        self.blas_plan_dev = {l: upload_blas_plan(p) for l, p in plans.items()}
 
-    def _upload_plan(self, plan):
-        n_tiles = plan.tile_class.shape[0]
-        src_t = plan.src.reshape(n_tiles, TILE_TARGETS, 189).transpose(0, 2, 1)
-        return dict(n_tiles=n_tiles, tile_targets=to_dev(plan.tile_targets, np.int32),
-                    tile_class=to_dev(plan.tile_class, np.int32),
-                    src=to_dev(np.ascontiguousarray(src_t), np.int32))
-
-    def m2l_blas_level(self, lvl, mult, nrhs, check, plan=None):
-        """check (n_tgt*R, n_c) = level_scale * U^T-expansion of the fused sweep."""
+    def m2l_blas_level(self, lvl, mult, nrhs, check):
         b = self._buffers(nrhs)
-        plan = plan if plan is not None else self.blas_plan_dev[lvl]
-        n_s, n_t = self.n_src[lvl], self.n_tgt[lvl]
-        qt = b["qt"][: n_s * nrhs]
-        acc = b["acc"][: n_t * nrhs]
-        self.la.gemm(n_s * nrhs, self.k, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt,
-                     self.kin)
-        launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
-                 P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
-                 P(self.class_tv), plan["n_tiles"], nrhs, P(acc), stream_handle())
-        self.la.gemm(n_t * nrhs, self.n_c, self.k, 1.0 / self.side[lvl], acc, self.ko_pad,
-                     self.UT, self.n_c, check, self.n_c)
-        return 3
+        return self.blas.run_level(self.blas_plan_dev[lvl], mult, self.n_src[lvl],
+                                   self.n_tgt[lvl], nrhs, 1.0 / self.side[lvl], check, b["qt"],
+                                   b["acc"])
 
     # ------------------------------------------------------------- FFT-M2L
     def _init_fft(self, ops, plans):
@@ -286,8 +323,10 @@ class DeviceFmm:
         b["stack"] = torch.empty(max(self.n_src[2:d] + [1]) * R * 8 * self.n_e, dtype=T,
                                  device=dev)
         if self.cfg.backend == "blas":
-            b["qt"] = torch.zeros(max(self.n_src) * R * self.kin, dtype=T, device=dev)
-            b["acc"] = torch.zeros(max(self.n_tgt) * R * self.ko_pad, dtype=T, device=dev)
+            b["qt"] = torch.zeros(max(self.n_src) * R * self.blas.kin, dtype=T, device=dev)
+            b["acc"] = torch.zeros(max(self.blas.acc_elems(self.n_tgt[l], R, p["n_tiles"])
+                                       for l, p in self.blas_plan_dev.items()), dtype=T,
+                                   device=dev)
         else:
             nsc = max(p["nsc"] for p in self.fft_plan_dev.values())
             ntc = max(p["ntc"] for p in self.fft_plan_dev.values())
@@ -418,36 +457,18 @@ def apply_level_host(ops, buckets, multipoles, n_targets, level_scale, counter=N
     dt = mult.dtype
     n_src, nrhs, n_e = mult.shape
     T = _NP2T[np.dtype(dt)]
-    sfx = "f32" if dt == np.float32 else "f64"
-    la = Linalg(sfx)
-    k = ops.k
-    n_c = ops.u.shape[0]
-    kin, ko_pad = blas_geometry(k, dt.itemsize)
-    s_pad = np.zeros((n_e, kin), dtype=dt)
-    s_pad[:, :k] = ops.s
-    cores = dense_cores(ops, np.float64)
-    dt_pad = np.zeros((cores.shape[0], kin, ko_pad), dtype=dt)
-    dt_pad[:, :k, :k] = cores.transpose(0, 2, 1)
-    plan = level_plan_from_buckets(buckets, n_targets)
-    n_tiles = plan.tile_class.shape[0]
-    src_t = plan.src.reshape(n_tiles, TILE_TARGETS, 189).transpose(0, 2, 1)
+    la = Linalg("f32" if dt == np.float32 else "f64")
+    bd = BlasDevice(ops, dt, la)
+    plan = upload_blas_plan(level_plan_from_buckets(buckets, n_targets))
     dev = _dev()
     m = to_dev(mult.reshape(n_src * nrhs, n_e))
-    qt = torch.zeros(max(n_src, 1) * nrhs * kin, dtype=T, device=dev)
-    acc = torch.zeros(max(n_targets, 1) * nrhs * ko_pad, dtype=T, device=dev)
-    check = torch.zeros(max(n_targets, 1) * nrhs * n_c, dtype=T, device=dev)
-    S, Dt_, UT = to_dev(s_pad), to_dev(dt_pad), to_dev(np.ascontiguousarray(ops.u.T), dt)
-    la.gemm(n_src * nrhs, k, n_e, 1.0, m, n_e, S, kin, qt, kin)
-    if n_tiles:
-        launch(f"kifmm_m2l_sweep_{sfx}", P(qt), P(Dt_), kin, ko_pad,
-                 P(to_dev(plan.tile_targets, np.int32)), P(to_dev(plan.tile_class, np.int32)),
-                 P(to_dev(np.ascontiguousarray(src_t), np.int32)),
-                 P(to_dev(class_transfer_table(), np.int32)), n_tiles, nrhs, P(acc),
-                 stream_handle())
-    la.gemm(n_targets * nrhs, n_c, k, level_scale, acc, ko_pad, UT, n_c, check, n_c)
+    qt = torch.zeros(max(n_src, 1) * nrhs * bd.kin, dtype=T, device=dev)
+    acc = torch.zeros(max(bd.acc_elems(n_targets, nrhs, plan["n_tiles"]), 1), dtype=T, device=dev)
+    check = torch.zeros(max(n_targets, 1) * nrhs * bd.n_c, dtype=T, device=dev)
+    calls = bd.run_level(plan, m, n_src, n_targets, nrhs, level_scale, check, qt, acc)
     if counter is not None:
-        counter.append(3)
-    return check[: n_targets * nrhs * n_c].cpu().numpy().reshape(n_targets, nrhs, n_c)
+        counter.append(calls)
+    return check[: n_targets * nrhs * bd.n_c].cpu().numpy().reshape(n_targets, nrhs, bd.n_c)
 
 
 def m2l_fft_level_host(ops, plan, mult, level_scale):
@@ -473,10 +494,11 @@ def m2l_fft_level_host(ops, plan, mult, level_scale):
     check = torch.zeros(max(n_tgt, 1) * nrhs * n_e, dtype=T, device=dev)
     s = stream_handle()
     m = to_dev(mult)
-    launch(f"kifmm_fft_forward_{sfx}", P(m), nrhs, ops.order, P(to_dev(sbox)), nsc, P(qhat), s)
+    keep = [to_dev(sbox), to_dev(plan.halo, np.int64), to_dev(tbox)]
+    launch(f"kifmm_fft_forward_{sfx}", P(m), nrhs, ops.order, P(keep[0]), nsc, P(qhat), s)
     cname = "c64" if sfx == "f32" else "c128"
-    launch(f"kifmm_hadamard_m2l_{cname}", P(khat), P(qhat), P(to_dev(plan.halo, np.int64)),
-             P(phat), nf, nsc, ntc, nrhs, s)
-    launch(f"kifmm_fft_inverse_{sfx}", P(phat), nrhs, ops.order, P(to_dev(tbox)), ntc,
-             float(level_scale), P(check), s)
+    launch(f"kifmm_hadamard_m2l_{cname}", P(khat), P(qhat), P(keep[1]), P(phat), nf, nsc, ntc,
+           nrhs, s)
+    launch(f"kifmm_fft_inverse_{sfx}", P(phat), nrhs, ops.order, P(keep[2]), ntc,
+           float(level_scale), P(check), s)
     return check[: n_tgt * nrhs * n_e].cpu().numpy().reshape(n_tgt, nrhs, n_e)

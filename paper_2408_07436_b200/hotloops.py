@@ -31,9 +31,11 @@ def _check_dtype(*arrays):
     return dt
 
 
-def _dev(a, dtype=None):
+def _upload(*arrays, dtype=None):
+    """Device copies, returned as a list the caller keeps alive for the
+    duration of the launch (raw pointers do not hold a reference)."""
     from .device import to_dev
-    return to_dev(a, dtype)
+    return [to_dev(a, dtype) for a in arrays]
 
 
 def _sfx(dt):
@@ -48,17 +50,18 @@ def laplace_potentials(tx, ty, tz, sx, sy, sz, charges, out, threads=None):
     dt = _check_dtype(tx, ty, tz, sx, sy, sz, charges, out)
     nt, ns = np.asarray(tx).shape[0], np.asarray(sx).shape[0]
     q = np.ascontiguousarray(charges).reshape(ns, -1)
-    o = _dev(np.ascontiguousarray(out).reshape(nt, -1))
+    d = _upload(tx, ty, tz, sx, sy, sz, q, np.ascontiguousarray(out).reshape(nt, -1))
     if nt and ns:
-        nat.call(f"kifmm_laplace_potentials_{_sfx(dt)}", P(_dev(tx)), P(_dev(ty)), P(_dev(tz)),
-                 nt, P(_dev(sx)), P(_dev(sy)), P(_dev(sz)), ns, P(_dev(q)), q.shape[1], P(o),
-                 stream_handle())
-    out[...] = o.cpu().numpy().reshape(np.shape(out))
+        nat.call(f"kifmm_laplace_potentials_{_sfx(dt)}", P(d[0]), P(d[1]), P(d[2]), nt, P(d[3]),
+                 P(d[4]), P(d[5]), ns, P(d[6]), q.shape[1], P(d[7]), stream_handle())
+    out[...] = d[7].cpu().numpy().reshape(np.shape(out))
     return out
 
 
 def laplace_matrix(tx, ty, tz, sx, sy, sz, out=None, threads=None):
     """out[i, j] = K(t_i, s_j), overwritten (reference _hot.pyx:68-88)."""
+    import torch
+
     from . import _native as nat
     from .device import P, require_cuda, stream_handle
     require_cuda()
@@ -66,12 +69,12 @@ def laplace_matrix(tx, ty, tz, sx, sy, sz, out=None, threads=None):
     nt, ns = np.asarray(tx).shape[0], np.asarray(sx).shape[0]
     if out is None:
         out = np.empty((nt, ns), dtype=dt)
-    import torch
+    d = _upload(tx, ty, tz, sx, sy, sz)
     o = torch.empty(max(nt * ns, 1), dtype=torch.float32 if dt == np.float32 else torch.float64,
-                    device="cuda")
+                    device=d[0].device)
     if nt and ns:
-        nat.call(f"kifmm_laplace_matrix_{_sfx(dt)}", P(_dev(tx)), P(_dev(ty)), P(_dev(tz)), nt,
-                 P(_dev(sx)), P(_dev(sy)), P(_dev(sz)), ns, P(o), stream_handle())
+        nat.call(f"kifmm_laplace_matrix_{_sfx(dt)}", P(d[0]), P(d[1]), P(d[2]), nt, P(d[3]),
+                 P(d[4]), P(d[5]), ns, P(o), stream_handle())
         out[...] = o[: nt * ns].cpu().numpy().reshape(nt, ns)
     return out
 
@@ -85,13 +88,14 @@ def p2p_blocked(tx, ty, tz, leaf_of_target, sx, sy, sz, charges, src_offsets, ou
     nt = np.asarray(tx).shape[0]
     ns = np.asarray(sx).shape[0]
     q = np.ascontiguousarray(charges).reshape(ns, -1)
-    offs = np.ascontiguousarray(src_offsets, dtype=np.int64)
-    o = _dev(np.ascontiguousarray(out).reshape(nt, -1))
+    d = _upload(tx, ty, tz, sx, sy, sz, q, np.ascontiguousarray(out).reshape(nt, -1))
+    idx = _upload(leaf_of_target, src_offsets, dtype=np.int64)
+    n_leaves = np.asarray(src_offsets).shape[0] - 1
     if nt:
-        nat.call(f"kifmm_p2p_blocked_{_sfx(dt)}", P(_dev(tx)), P(_dev(ty)), P(_dev(tz)), nt,
-                 P(_dev(leaf_of_target, np.int64)), P(_dev(sx)), P(_dev(sy)), P(_dev(sz)),
-                 P(_dev(q)), q.shape[1], P(_dev(offs)), offs.shape[0] - 1, P(o), stream_handle())
-    out[...] = o.cpu().numpy().reshape(np.shape(out))
+        nat.call(f"kifmm_p2p_blocked_{_sfx(dt)}", P(d[0]), P(d[1]), P(d[2]), nt, P(idx[0]),
+                 P(d[3]), P(d[4]), P(d[5]), P(d[6]), q.shape[1], P(idx[1]), n_leaves, P(d[7]),
+                 stream_handle())
+    out[...] = d[7].cpu().numpy().reshape(np.shape(out))
     return out
 
 
@@ -100,18 +104,17 @@ def hadamard_m2l(khat, qhat, halo, phat, block=32, threads=None):
     from . import _native as nat
     from .device import P, require_cuda, stream_handle
     require_cuda()
-    khat, qhat, phat = (np.asarray(a) for a in (khat, qhat, phat))
-    if khat.dtype not in (np.complex64, np.complex128):
-        raise TypeError(f"unsupported dtype {khat.dtype}")
-    if qhat.dtype != khat.dtype or phat.dtype != khat.dtype:
+    k_, q_, p_ = (np.asarray(a) for a in (khat, qhat, phat))
+    if k_.dtype not in (np.complex64, np.complex128):
+        raise TypeError(f"unsupported dtype {k_.dtype}")
+    if q_.dtype != k_.dtype or p_.dtype != k_.dtype:
         raise ValueError("khat, qhat and phat must share one complex dtype")
-    rdt = np.float32 if khat.dtype == np.complex64 else np.float64
-    nf, nsc, _, nrhs = qhat.shape
+    rdt = np.float32 if k_.dtype == np.complex64 else np.float64
+    nf, nsc, _, nrhs = q_.shape
     ntc = np.asarray(halo).shape[0]
-    p = _dev(np.ascontiguousarray(phat).view(rdt))
-    nat.call("kifmm_hadamard_m2l_" + ("c64" if rdt == np.float32 else "c128"),
-             P(_dev(np.ascontiguousarray(khat).view(rdt))),
-             P(_dev(np.ascontiguousarray(qhat).view(rdt))), P(_dev(halo, np.int64)), P(p), nf,
-             nsc, ntc, nrhs, stream_handle())
-    phat[...] = p.cpu().numpy().view(khat.dtype).reshape(phat.shape)
+    d = _upload(*(np.ascontiguousarray(a).view(rdt) for a in (k_, q_, p_)))
+    h = _upload(halo, dtype=np.int64)
+    nat.call("kifmm_hadamard_m2l_" + ("c64" if rdt == np.float32 else "c128"), P(d[0]), P(d[1]),
+             P(h[0]), P(d[2]), nf, nsc, ntc, nrhs, stream_handle())
+    phat[...] = d[2].cpu().numpy().view(k_.dtype).reshape(p_.shape)
     return phat
