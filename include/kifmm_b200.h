@@ -68,16 +68,19 @@ int kifmm_hadamard_m2l_c128(const double* khat, const double* qhat, const int64_
 
 /* ---- (2) engine passes (device-resident evaluate) ------------------------ */
 
-/* Row-major C[rowmap(m), n] (=|+=) alpha * sum_k A[m, k] B[k, n] * colscale[n].
+/* Row-major C[rowmap(m), n] (=|+=) alpha * sum_k A'[m, k] B[k, n] * colscale[n],
+ * A'[m, k] = sum_{s < asum} A[m*lda + s*astride + k] (asum = 1: plain A).
  * rowmap NULL -> identity; rowmap[m] < 0 -> row skipped.  colscale may be NULL.
- * Used for the projection/expansion of BLAS-M2L (m2l_blas.py:285,322) and the
- * factored pseudo-inverse solves (expansion.py:78-82), M2M/L2L products. */
+ * Used for the projection/expansion of BLAS-M2L (m2l_blas.py:285,322; the
+ * A-sum reduces the split sweep's partial accumulators), the factored
+ * pseudo-inverse solves (expansion.py:78-82) and the M2M/L2L products. */
 int kifmm_gemm_f32(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
-                   const float* B, int64_t ldb, const float* colscale, float* C, int64_t ldc,
-                   const int32_t* rowmap, int accumulate, void* stream);
+                   int asum, int64_t astride, const float* B, int64_t ldb, const float* colscale,
+                   float* C, int64_t ldc, const int32_t* rowmap, int accumulate, void* stream);
 int kifmm_gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-                   const double* B, int64_t ldb, const double* colscale, double* C, int64_t ldc,
-                   const int32_t* rowmap, int accumulate, void* stream);
+                   int asum, int64_t astride, const double* B, int64_t ldb,
+                   const double* colscale, double* C, int64_t ldc, const int32_t* rowmap,
+                   int accumulate, void* stream);
 
 /* P2M check potentials (engine.py:298-319): for source leaf l and check point c,
  * phi[(l*nrhs + r)*nc + c] = sum_{j in leaf} K(center_l + base_c, s_j) q[j*nrhs + r];

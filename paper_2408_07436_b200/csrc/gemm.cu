@@ -1,25 +1,32 @@
 // Tall-skinny SIMT GEMM for the level operators (projection/expansion of
 // BLAS-M2L, factored pseudo-inverse solves, M2M/L2L kernel products).
-// These are memory-bound (N, K <= a few hundred, M up to 2M rows), so a
-// register-tiled FFMA/DFMA kernel with shared-memory staging is enough; the
-// epilogue fuses the pseudo-inverse's diagonal (colscale), the level scale
-// (alpha), accumulation and the L2L child scatter (rowmap).
+// These are memory/latency-bound (N, K <= a few hundred, M up to 2M rows),
+// so a register-tiled FFMA/DFMA kernel with shared-memory staging and a
+// register prefetch of the next K-tile is enough.  The epilogue fuses the
+// pseudo-inverse's diagonal (colscale), the level scale (alpha),
+// accumulation and the L2L child scatter (rowmap).  The A loader can sum
+// `asum` column blocks (stride `astride`): that is how the partial
+// accumulators of the split M2L sweep are reduced, in a fixed order.
 #include "common.cuh"
 
 using namespace kifmm;
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4, NT = 256;
+constexpr int BN = 64, BK = 16, TN = 4, NT = 256;
 
-template <typename T>
+template <typename T, int BM>
 __global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t K, T alpha,
                                                   const T* __restrict__ A, int64_t lda,
+                                                  int asum, int64_t astride,
                                                   const T* __restrict__ B, int64_t ldb,
                                                   const T* __restrict__ colscale,
                                                   T* __restrict__ C, int64_t ldc,
                                                   const int32_t* __restrict__ rowmap,
                                                   int accumulate) {
+  constexpr int TM = BM * BN / (NT * TN);        // rows per thread: 4 (BM=64), 2, 1
+  constexpr int AE = BM * BK / NT;               // A elements loaded per thread
+  constexpr int BE = BK * BN / NT;               // B elements loaded per thread (4)
   __shared__ T As[BK][BM + 4];
   __shared__ T Bs[BK][BN + 4];
   const int tid = threadIdx.x;
@@ -31,23 +38,43 @@ __global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t 
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
 
-  for (int64_t k0 = 0; k0 < K; k0 += BK) {
-    // A tile: BM x BK, 4 elements per thread, stored transposed.
+  T ra[AE], rb[BE];
+  auto load = [&](int64_t k0) {
 #pragma unroll
-    for (int e = 0; e < (BM * BK) / NT; ++e) {
-      int idx = tid + e * NT;
-      int r = idx / BK, c = idx % BK;
-      int64_t gm = m0 + r, gk = k0 + c;
-      As[c][r] = (gm < M && gk < K) ? A[gm * lda + gk] : T(0);
+    for (int e = 0; e < AE; ++e) {
+      const int idx = tid + e * NT;
+      const int r = idx / BK, c = idx % BK;
+      const int64_t gm = m0 + r, gk = k0 + c;
+      T v = T(0);
+      if (gm < M && gk < K) {
+        const T* p = A + gm * lda + gk;
+        v = p[0];
+        for (int s = 1; s < asum; ++s) v += p[s * astride];
+      }
+      ra[e] = v;
     }
 #pragma unroll
-    for (int e = 0; e < (BK * BN) / NT; ++e) {
-      int idx = tid + e * NT;
-      int r = idx / BN, c = idx % BN;
-      int64_t gk = k0 + r, gn = n0 + c;
-      Bs[r][c] = (gk < K && gn < N) ? B[gk * ldb + gn] : T(0);
+    for (int e = 0; e < BE; ++e) {
+      const int idx = tid + e * NT;
+      const int r = idx / BN, c = idx % BN;
+      const int64_t gk = k0 + r, gn = n0 + c;
+      rb[e] = (gk < K && gn < N) ? B[gk * ldb + gn] : T(0);
+    }
+  };
+  load(0);
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int e = 0; e < AE; ++e) {
+      const int idx = tid + e * NT;
+      As[idx % BK][idx / BK] = ra[e];
+    }
+#pragma unroll
+    for (int e = 0; e < BE; ++e) {
+      const int idx = tid + e * NT;
+      Bs[idx / BN][idx % BN] = rb[e];
     }
     __syncthreads();
+    if (k0 + BK < K) load(k0 + BK);              // overlap the next tile's loads
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
       T a[TM], b[TN];
@@ -64,13 +91,13 @@ __global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t 
   }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    int64_t gm = m0 + tm * TM + i;
+    const int64_t gm = m0 + tm * TM + i;
     if (gm >= M) continue;
-    int64_t row = rowmap ? (int64_t)rowmap[gm] : gm;
+    const int64_t row = rowmap ? (int64_t)rowmap[gm] : gm;
     if (row < 0) continue;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      int64_t gn = n0 + tn + j * (BN / TN);
+      const int64_t gn = n0 + tn + j * (BN / TN);
       if (gn >= N) continue;
       T v = acc[i][j];
       if (colscale) v *= colscale[gn];
@@ -81,28 +108,38 @@ __global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t 
   }
 }
 
-template <typename T>
-int gemm(int64_t M, int64_t N, int64_t K, T alpha, const T* A, int64_t lda, const T* B,
-         int64_t ldb, const T* colscale, T* C, int64_t ldc, const int32_t* rowmap, int accumulate,
-         void* stream) {
-  if (M < 0 || N < 0 || K < 0) return KIFMM_EARG;
-  if (M == 0 || N == 0) return 0;
-  dim3 grid(ceil_div(N, BN), ceil_div(M, BM));
-  if (grid.y > 65535u) {
-    // split very tall problems into row chunks
-    const int64_t chunk = (int64_t)65535 * BM;
-    for (int64_t m0 = 0; m0 < M; m0 += chunk) {
-      int64_t mm = M - m0 < chunk ? M - m0 : chunk;
-      int st = gemm<T>(mm, N, K, alpha, A + m0 * lda, lda, B, ldb, colscale,
-                       rowmap ? C : C + m0 * ldc, ldc, rowmap ? rowmap + m0 : nullptr, accumulate,
-                       stream);
-      if (st) return st;
-    }
-    return 0;
+template <typename T, int BM>
+int launch_gemm(int64_t M, int64_t N, int64_t K, T alpha, const T* A, int64_t lda, int asum,
+                int64_t astride, const T* B, int64_t ldb, const T* colscale, T* C, int64_t ldc,
+                const int32_t* rowmap, int accumulate, cudaStream_t s) {
+  const int64_t max_rows = (int64_t)65535 * BM;
+  for (int64_t r0 = 0; r0 < M; r0 += max_rows) {
+    const int64_t mm = M - r0 < max_rows ? M - r0 : max_rows;
+    dim3 grid(ceil_div(N, BN), ceil_div(mm, BM));
+    gemm_kernel<T, BM><<<grid, NT, 0, s>>>(mm, N, K, alpha, A + r0 * lda, lda, asum, astride, B,
+                                           ldb, colscale, rowmap ? C : C + r0 * ldc, ldc,
+                                           rowmap ? rowmap + r0 : nullptr, accumulate);
   }
-  gemm_kernel<T><<<grid, NT, 0, (cudaStream_t)stream>>>(M, N, K, alpha, A, lda, B, ldb, colscale,
-                                                        C, ldc, rowmap, accumulate);
   return launch_status();
+}
+
+template <typename T>
+int gemm(int64_t M, int64_t N, int64_t K, T alpha, const T* A, int64_t lda, int asum,
+         int64_t astride, const T* B, int64_t ldb, const T* colscale, T* C, int64_t ldc,
+         const int32_t* rowmap, int accumulate, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || asum < 1) return KIFMM_EARG;
+  if (M == 0 || N == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  // Pick the row tile so that the grid covers the 148 SMs when possible.
+  const int64_t ncol = (N + BN - 1) / BN;
+  if (M * ncol >= 64 * 148 * 2)
+    return launch_gemm<T, 64>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc,
+                              rowmap, accumulate, s);
+  if (M * ncol >= 32 * 148)
+    return launch_gemm<T, 32>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc,
+                              rowmap, accumulate, s);
+  return launch_gemm<T, 16>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc,
+                            rowmap, accumulate, s);
 }
 
 template <typename T>
@@ -145,14 +182,17 @@ __global__ void gather_charges_kernel(const double* __restrict__ qin,
 extern "C" {
 
 int kifmm_gemm_f32(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
-                   const float* B, int64_t ldb, const float* colscale, float* C, int64_t ldc,
-                   const int32_t* rowmap, int accumulate, void* s) {
-  return gemm<float>(M, N, K, alpha, A, lda, B, ldb, colscale, C, ldc, rowmap, accumulate, s);
+                   int asum, int64_t astride, const float* B, int64_t ldb, const float* colscale,
+                   float* C, int64_t ldc, const int32_t* rowmap, int accumulate, void* s) {
+  return gemm<float>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,
+                     accumulate, s);
 }
 int kifmm_gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-                   const double* B, int64_t ldb, const double* colscale, double* C, int64_t ldc,
-                   const int32_t* rowmap, int accumulate, void* s) {
-  return gemm<double>(M, N, K, alpha, A, lda, B, ldb, colscale, C, ldc, rowmap, accumulate, s);
+                   int asum, int64_t astride, const double* B, int64_t ldb,
+                   const double* colscale, double* C, int64_t ldc, const int32_t* rowmap,
+                   int accumulate, void* s) {
+  return gemm<double>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,
+                      accumulate, s);
 }
 int kifmm_stack_children_f32(const float* mult, const int32_t* child, int64_t n_par, int64_t nrhs,
                              int64_t ne, float* out, void* s) {

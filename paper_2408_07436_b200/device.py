@@ -117,9 +117,10 @@ class Linalg:
         self.sfx = sfx
 
     def gemm(self, M, N, K, alpha, A, lda, B, ldb, C, ldc, colscale=None, rowmap=None,
-             accumulate=False):
-        launch(f"kifmm_gemm_{self.sfx}", M, N, K, float(alpha), P(A), lda, P(B), ldb,
-                 P(colscale), P(C), ldc, P(rowmap), int(bool(accumulate)), stream_handle())
+             accumulate=False, asum=1, astride=0):
+        launch(f"kifmm_gemm_{self.sfx}", M, N, K, float(alpha), P(A), lda, int(asum), astride,
+               P(B), ldb, P(colscale), P(C), ldc, P(rowmap), int(bool(accumulate)),
+               stream_handle())
 
     def solve(self, inv, phi, M, out, scale, tmp, accumulate=False, rowmap=None):
         """out[rowmap] (+)= scale * V diag(inv_vals) U^T phi^T, row form
@@ -164,22 +165,12 @@ class BlasDevice:
         s_pad = np.zeros((self.n_e, self.kin), dtype=dt)
         s_pad[:, :k] = ops.s
         self.S = to_dev(s_pad)
-        ut = np.zeros((self.ko_pad, self.n_c), dtype=dt)
-        ut[:k] = ops.u.T
-        self._ut_pad = ut
-        self._ut_rep = {}
+        self.UT = to_dev(np.ascontiguousarray(ops.u.T), dt)          # (k, n_c)
         cores = dense_cores(ops, np.float64)                          # (316, k, k) [out, in]
         dt_pad = np.zeros((cores.shape[0], self.kin, self.ko_pad), dtype=dt)
         dt_pad[:, :k, :k] = cores.transpose(0, 2, 1)
         self.Dt = to_dev(dt_pad)
         self.class_tv = to_dev(class_transfer_table(), np.int32)
-
-    def ut_rep(self, nsplit):
-        """U^T (zero-padded to ko_pad rows) stacked nsplit times: the
-        expansion GEMM then also sums the sweep's partial accumulators."""
-        if nsplit not in self._ut_rep:
-            self._ut_rep[nsplit] = to_dev(np.ascontiguousarray(np.tile(self._ut_pad, (nsplit, 1))))
-        return self._ut_rep[nsplit]
 
     def acc_elems(self, n_t, nrhs, n_tiles):
         return n_t * nrhs * sweep_splits(n_tiles, self.n_slabs) * self.ko_pad
@@ -193,8 +184,8 @@ class BlasDevice:
             launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
                    P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
                    P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc), stream_handle())
-        la.gemm(n_t * nrhs, self.n_c, ld, level_scale, acc, ld, self.ut_rep(nsplit), self.n_c,
-                check, self.n_c)
+        la.gemm(n_t * nrhs, self.n_c, self.k, level_scale, acc, ld, self.UT, self.n_c, check,
+                self.n_c, asum=nsplit, astride=self.ko_pad)
         return 3
 
 
