@@ -118,6 +118,20 @@ int kifmm_m2l_sweep_f64(const double* qt, const double* Dt, int64_t ki, int64_t 
                         const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
                         int64_t nrhs, int64_t nsplit, double* acc, void* stream);
 
+/* Same sweep on the tcgen05 tensor cores for float32 (3xTF32): the caller
+ * passes q~ split into TF32 hi/lo parts (kifmm_split_tf32) and the cores
+ * split into hi/lo and packed per (vector, 32-wide K chunk) in the
+ * canonical K-major UMMA layout [a/8][b/4][a%8][b%4] (device.py
+ * pack_tc_cores).  kin % 8 == 0, n_out % 16 == 0, n_out <= 256.
+ * acc layout as kifmm_m2l_sweep_f32 with ko = n_out. */
+int kifmm_m2l_sweep_tc_f32(const float* qhi, const float* qlo, const float* bhi, const float* blo,
+                           int64_t kin, int64_t n_out, const int32_t* tile_targets,
+                           const int32_t* tile_class, const int32_t* src, const int32_t* class_tv,
+                           int64_t n_tiles, int64_t nrhs, int64_t nsplit, float* acc, void* stream);
+
+/* x = hi + lo with hi, lo TF32 (cvt.rna.tf32.f32), elementwise. */
+int kifmm_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stream);
+
 /* FFT-M2L forward (m2l_fft.py:236-247): embed each box's multipole at
  * lattice+p of the n^3 grid (n = 2p), real 3-D DFT, and write the spectrum
  * frequency-major into qhat[(f*nsc + cluster)*8 + child)*nrhs + r] (complex).

@@ -150,16 +150,62 @@ def upload_blas_plan(plan):
                 src=to_dev(np.ascontiguousarray(src_t), np.int32))
 
 
+def tf32_split(x: np.ndarray):
+    """Host twin of cvt.rna.tf32.f32: x (float32) -> (hi, lo) with hi, lo
+    TF32-representable and x = hi + lo + O(2^-22 |x|)."""
+    def rna(v):
+        bits = np.ascontiguousarray(v, dtype=np.float32).view(np.uint32)
+        return ((bits + np.uint32(0x1000)) & np.uint32(0xFFFFE000)).view(np.float32)
+    x = np.asarray(x, dtype=np.float32)
+    hi = rna(x)
+    lo = rna((x - hi).astype(np.float32))
+    return hi, lo
+
+
+def pack_tc_cores(cores: np.ndarray, kin: int, n_out: int, kc_max: int = 32) -> np.ndarray:
+    """(316, k, k) float32 cores [out a, in b] -> per vector, per K-chunk, the
+    canonical K-major no-swizzle UMMA layout [a/8][b/4][a%8][b%4] the
+    tcgen05 sweep copies verbatim into shared memory (csrc/m2l_tc.cu)."""
+    nt, k, _ = cores.shape
+    d = np.zeros((nt, n_out, kin), dtype=np.float32)
+    d[:, :k, :k] = cores
+    blocks = []
+    for c0 in range(0, kin, kc_max):
+        kc = min(kc_max, kin - c0)
+        blk = d[:, :, c0:c0 + kc].reshape(nt, n_out // 8, 8, kc // 4, 4).transpose(0, 1, 3, 2, 4)
+        blocks.append(blk.reshape(nt, -1))
+    return np.ascontiguousarray(np.concatenate(blocks, axis=1))
+
+
 class BlasDevice:
     """Device copies of the compressed M2L operators and the level apply:
     projection q~ = M S, fused target-stationary sweep, expansion
     check = level_scale * acc U^T (reference m2l_blas.py:284-326)."""
 
-    def __init__(self, ops, np_dtype, la):
+    def __init__(self, ops, np_dtype, la, tensor_cores=None):
+        import os
         dt = np.dtype(np_dtype)
         self.la, self.sfx = la, la.sfx
         self.k = k = ops.k
         self.n_e, self.n_c = ops.s.shape[0], ops.u.shape[0]
+        if tensor_cores is None:
+            tensor_cores = os.environ.get("KIFMM_SWEEP", "tc") != "simt"
+        # float32: tcgen05 3xTF32 sweep (csrc/m2l_tc.cu); float64: FP64 SIMT sweep.
+        self.tc = bool(tensor_cores) and dt == np.float32 and k <= 256
+        if self.tc:
+            self.kin = -(-k // 8) * 8
+            self.ko_pad = -(-k // 16) * 16
+            self.n_slabs = 1
+            cores32 = dense_cores(ops, np.float64).astype(np.float32)
+            hi, lo = tf32_split(cores32)
+            self.Bhi = to_dev(pack_tc_cores(hi, self.kin, self.ko_pad))
+            self.Blo = to_dev(pack_tc_cores(lo, self.kin, self.ko_pad))
+            s_pad = np.zeros((self.n_e, self.kin), dtype=dt)
+            s_pad[:, :k] = ops.s
+            self.S = to_dev(s_pad)
+            self.UT = to_dev(np.ascontiguousarray(ops.u.T), dt)
+            self.class_tv = to_dev(class_transfer_table(), np.int32)
+            return
         self.kin, self.ko_pad = blas_geometry(k, dt.itemsize)
         self.n_slabs = -(-k // 128)
         s_pad = np.zeros((self.n_e, self.kin), dtype=dt)
@@ -180,7 +226,16 @@ class BlasDevice:
         nsplit = sweep_splits(plan["n_tiles"], self.n_slabs)
         ld = nsplit * self.ko_pad
         la.gemm(n_s * nrhs, self.k, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
-        if plan["n_tiles"]:
+        if self.tc:
+            nq = n_s * nrhs * self.kin
+            qhi, qlo = qt[nq: 2 * nq], qt[2 * nq: 3 * nq]
+            launch("kifmm_split_tf32", P(qt), nq, P(qhi), P(qlo), stream_handle())
+            if plan["n_tiles"]:
+                launch("kifmm_m2l_sweep_tc_f32", P(qhi), P(qlo), P(self.Bhi), P(self.Blo),
+                       self.kin, self.ko_pad, P(plan["tile_targets"]), P(plan["tile_class"]),
+                       P(plan["src"]), P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc),
+                       stream_handle())
+        elif plan["n_tiles"]:
             launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
                    P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
                    P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc), stream_handle())
@@ -314,7 +369,8 @@ class DeviceFmm:
         b["stack"] = torch.empty(max(self.n_src[2:d] + [1]) * R * 8 * self.n_e, dtype=T,
                                  device=dev)
         if self.cfg.backend == "blas":
-            b["qt"] = torch.zeros(max(self.n_src) * R * self.blas.kin, dtype=T, device=dev)
+            b["qt"] = torch.zeros(max(self.n_src) * R * self.blas.kin * (3 if self.blas.tc else 1),
+                                  dtype=T, device=dev)
             b["acc"] = torch.zeros(max(self.blas.acc_elems(self.n_tgt[l], R, p["n_tiles"])
                                        for l, p in self.blas_plan_dev.items()), dtype=T,
                                    device=dev)
@@ -453,7 +509,7 @@ def apply_level_host(ops, buckets, multipoles, n_targets, level_scale, counter=N
     plan = upload_blas_plan(level_plan_from_buckets(buckets, n_targets))
     dev = _dev()
     m = to_dev(mult.reshape(n_src * nrhs, n_e))
-    qt = torch.zeros(max(n_src, 1) * nrhs * bd.kin, dtype=T, device=dev)
+    qt = torch.zeros(max(n_src, 1) * nrhs * bd.kin * 3, dtype=T, device=dev)
     acc = torch.zeros(max(bd.acc_elems(n_targets, nrhs, plan["n_tiles"]), 1), dtype=T, device=dev)
     check = torch.zeros(max(n_targets, 1) * nrhs * bd.n_c, dtype=T, device=dev)
     calls = bd.run_level(plan, m, n_src, n_targets, nrhs, level_scale, check, qt, acc)
