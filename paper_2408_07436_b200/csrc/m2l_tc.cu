@@ -10,16 +10,19 @@
 // into a TF32 "hi" part and a TF32 residual "lo" part, so the result keeps
 // ~fp32 accuracy (the TF32 products themselves would lose ~3 digits).
 //
-// Roles (160 threads):
+// Roles (288 threads):
 //   warps 0-3  producers: thread m gathers row m of A_hi/A_lo with cp.async
 //              into the canonical K-major no-swizzle layout (8-row x 16-byte
 //              core matrices) and copies its share of the pre-laid-out
 //              B_hi/B_lo block; completion is tracked on the stage's "full"
-//              mbarrier (cp.async.mbarrier.arrive.noinc).  After the sweep
-//              they are the epilogue: tcgen05.ld of their 32 TMEM lanes.
-//   warp 4     allocates TMEM (accumulator: 128 lanes x N fp32 columns) and
-//              one elected thread issues tcgen05.mma.kind::tf32, releasing
-//              each stage with tcgen05.commit -> "empty" mbarrier.
+//              mbarrier (cp.async.mbarrier.arrive.noinc).
+//   warp 4     allocates TMEM (two 128 x N fp32 MMA buffers + one long-lived
+//              accumulator) and one elected thread issues
+//              tcgen05.mma.kind::tf32, releasing each stage with
+//              tcgen05.commit -> "empty" mbarrier.
+//   warps 5-8  accumulators/epilogue: every FLUSH_V vectors they add the
+//              finished MMA buffer into the long-lived accumulator with IEEE
+//              fp32 adds (tcgen05.ld / tcgen05.st), then write the result.
 #include "common.cuh"
 
 using namespace kifmm;
@@ -29,7 +32,7 @@ namespace {
 constexpr int TMT = 128;        // targets per tile = MMA M
 constexpr int KC = 32;          // K (floats) per pipeline stage
 constexpr int NPROD = 128;      // producer threads
-constexpr int NTHREADS = 160;
+constexpr int NTHREADS = 288;   // 4 producer + 1 MMA + 4 accumulator warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -51,6 +54,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
     if (!done && ++spins > (1u << 26)) __trap();   // watchdog: a lost arrive faults, never hangs
+  }
+}
+
+// Wait for non-latency-critical roles: back off with nanosleep so the
+// spinning warp does not steal issue slots from the producers sharing its
+// SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  uint32_t spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(256);
+    if (++spins > (1u << 24)) __trap();
   }
 }
 
@@ -84,6 +107,28 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// TMEM accumulation is periodically promoted: the MMA accumulates FLUSH_V
+// vectors into one of two TMEM buffers, then the accumulator warps add that
+// buffer into a long-lived TMEM region with IEEE fp32 adds (tensor-core
+// accumulation over the ~3*189*k products of a full sweep loses ~1e-5).
+constexpr int FLUSH_V = 4;
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
+        "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]),
+        "r"(v[14]), "r"(v[15]));
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tc_kernel(
     const float* __restrict__ qhi, const float* __restrict__ qlo, const float* __restrict__ bhi,
     const float* __restrict__ blo, int kin, int n_out, int stages,
@@ -98,25 +143,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tc_kernel(
   const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
   uint64_t* empty = full + stages;
-  uint64_t* done = empty + stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + stages;                      // [2] MMA -> accumulators
+  uint64_t* tempty = tfull + 2;                          // [2] accumulators -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int64_t tile = blockIdx.x;
   const int64_t r = blockIdx.y;
   const int split = blockIdx.z;
   const int j0 = split * jper, j1 = min(189, j0 + jper);
-  const int nsteps = (j1 - j0) * nchunks;
+  const int nvec = max(0, j1 - j0);
+  const int nsteps = nvec * nchunks;
+  const int nblocks = (nvec + FLUSH_V - 1) / FLUSH_V;
   const int cls = tile_class[tile];
   const int32_t* tsrc = src + tile * 189 * TMT;
   const int32_t* tv_list = class_tv + cls * 189;
-  const uint32_t tmem_cols = n_out <= 32 ? 32 : n_out <= 64 ? 64 : n_out <= 128 ? 128 : 256;
+  // columns: [0, n) and [n, 2n) MMA buffers, [2n, 3n) long-lived accumulator
+  const uint32_t need = 3u * (uint32_t)n_out;
+  const uint32_t tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], NPROD);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tfull[1], 1);
+    mbar_init(&tempty[0], NPROD);
+    mbar_init(&tempty[1], NPROD);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 4) {
@@ -157,32 +210,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tc_kernel(
       }
       cp_async_arrive_noinc(&full[stage]);
     }
-    // ------------------------------------------------------------- epilogue
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int32_t tgt = tile_targets[tile * TMT + m];
-    const int64_t ld = (int64_t)nsplit * n_out;
-    float* o = acc_out + ((int64_t)(tgt < 0 ? 0 : tgt) * nrhs + r) * ld + (int64_t)split * n_out;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    for (int c0 = 0; c0 < n_out; c0 += 8) {
-      uint32_t v[8];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7])
-          : "r"(tmem + lane_base + (uint32_t)c0));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (nsteps == 0) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = 0u;           // empty piece: zero partial
-      }
-      if (tgt >= 0) {
-        *reinterpret_cast<float4*>(o + c0) = make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]),
-                                                         __uint_as_float(v[2]), __uint_as_float(v[3]));
-        *reinterpret_cast<float4*>(o + c0 + 4) = make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]),
-                                                             __uint_as_float(v[6]), __uint_as_float(v[7]));
-      }
-    }
   } else if (warp == 4) {
     // ----------------------------------------------------------- MMA issue
     // idesc: D f32 (bit 4), A/B tf32 (bits 7, 10), K-major A and B,
@@ -190,30 +217,85 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tc_kernel(
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n_out >> 3) << 17) |
                            ((uint32_t)(TMT >> 4) << 24);
     if (lane == 0) {
-      uint32_t acc_flag = 0;
-      for (int st = 0; st < nsteps; ++st) {
-        const int stage = st % stages;
-        mbar_wait(&full[stage], (st / stages) & 1);
+      int st = 0;
+      for (int bi = 0; bi < nblocks; ++bi) {
+        const int buf = bi & 1;
+        if (bi >= 2) mbar_wait(&tempty[buf], ((bi >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int c = st % nchunks;
-        const int kc = min(KC, kin - c * KC);
-        const uint32_t base = smem_u32(smem + stage * stage_bytes);
-        const uint32_t a_hi = base, a_lo = base + a_bytes;
-        const uint32_t b_hi = base + 2 * a_bytes, b_lo = b_hi + b_bytes;
-        const uint32_t sbo_a = (KC / 4) * 128, sbo_b = (uint32_t)(kc / 4) * 128;
-        for (int ks = 0; ks < kc / 8; ++ks) {
-          const uint32_t ko = ks * 256;
-          mma_tf32(tmem, smem_desc(a_lo + ko, 128, sbo_a), smem_desc(b_hi + ko, 128, sbo_b), idesc,
-                   acc_flag);
-          acc_flag = 1;
-          mma_tf32(tmem, smem_desc(a_hi + ko, 128, sbo_a), smem_desc(b_lo + ko, 128, sbo_b), idesc, 1);
-          mma_tf32(tmem, smem_desc(a_hi + ko, 128, sbo_a), smem_desc(b_hi + ko, 128, sbo_b), idesc, 1);
+        const uint32_t dcol = tmem + (uint32_t)(buf * n_out);
+        const int vend = min(nvec, (bi + 1) * FLUSH_V);
+        uint32_t acc_flag = 0;
+        for (; st < vend * nchunks; ++st) {
+          const int stage = st % stages;
+          mbar_wait(&full[stage], (st / stages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const int c = st % nchunks;
+          const int kc = min(KC, kin - c * KC);
+          const uint32_t base = smem_u32(smem + stage * stage_bytes);
+          const uint32_t a_hi = base, a_lo = base + a_bytes;
+          const uint32_t b_hi = base + 2 * a_bytes, b_lo = b_hi + b_bytes;
+          const uint32_t sbo_a = (KC / 4) * 128, sbo_b = (uint32_t)(kc / 4) * 128;
+          for (int ks = 0; ks < kc / 8; ++ks) {
+            const uint32_t ko = ks * 256;
+            mma_tf32(dcol, smem_desc(a_lo + ko, 128, sbo_a), smem_desc(b_hi + ko, 128, sbo_b),
+                     idesc, acc_flag);
+            acc_flag = 1;
+            mma_tf32(dcol, smem_desc(a_hi + ko, 128, sbo_a), smem_desc(b_lo + ko, 128, sbo_b),
+                     idesc, 1);
+            mma_tf32(dcol, smem_desc(a_hi + ko, 128, sbo_a), smem_desc(b_hi + ko, 128, sbo_b),
+                     idesc, 1);
+          }
+          mma_commit(&empty[stage]);
         }
-        mma_commit(&empty[stage]);
+        mma_commit(&tfull[buf]);
       }
-      mma_commit(done);
     }
     __syncwarp();
+  } else {
+    // ------------------------------------- accumulator warps (5..8) + epilogue
+    const int sub = warp & 3;                            // TMEM sub-partition of this warp
+    const int m = sub * 32 + lane;                       // accumulator row = target slot
+    const uint32_t lane_base = (uint32_t)(sub * 32) << 16;
+    const uint32_t acc_col = tmem + lane_base + 2u * (uint32_t)n_out;
+    for (int bi = 0; bi < nblocks; ++bi) {
+      const int buf = bi & 1;
+      mbar_wait_sleep(&tfull[buf], (bi >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t bcol = tmem + lane_base + (uint32_t)(buf * n_out);
+      for (int c0 = 0; c0 < n_out; c0 += 16) {
+        uint32_t v[16], a[16];
+        tmem_ld16(bcol + c0, v);
+        if (bi > 0) tmem_ld16(acc_col + c0, a);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          a[i] = bi > 0 ? __float_as_uint(__uint_as_float(a[i]) + __uint_as_float(v[i])) : v[i];
+        tmem_st16(acc_col + c0, a);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf]))
+                   : "memory");
+    }
+    const int32_t tgt = tile_targets[tile * TMT + m];
+    const int64_t ld = (int64_t)nsplit * n_out;
+    float* o = acc_out + ((int64_t)(tgt < 0 ? 0 : tgt) * nrhs + r) * ld + (int64_t)split * n_out;
+    for (int c0 = 0; c0 < n_out; c0 += 16) {
+      uint32_t a[16];
+      tmem_ld16(acc_col + c0, a);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (nblocks == 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) a[i] = 0u;          // empty piece: zero partial
+      }
+      if (tgt >= 0) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(o + c0 + i) =
+              make_float4(__uint_as_float(a[i]), __uint_as_float(a[i + 1]),
+                          __uint_as_float(a[i + 2]), __uint_as_float(a[i + 3]));
+      }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -252,7 +334,7 @@ int kifmm_m2l_sweep_tc_f32(const float* qhi, const float* qlo, const float* bhi,
                            int64_t kin, int64_t n_out, const int32_t* tile_targets,
                            const int32_t* tile_class, const int32_t* src, const int32_t* class_tv,
                            int64_t n_tiles, int64_t nrhs, int64_t nsplit, float* acc, void* stream) {
-  if (kin < 8 || kin % 8 || n_out < 16 || n_out > 256 || n_out % 16 || n_tiles < 0 || nrhs < 1 ||
+  if (kin < 8 || kin % 8 || n_out < 16 || n_out > 160 || n_out % 16 || n_tiles < 0 || nrhs < 1 ||
       nsplit < 1 || nsplit > 189)
     return KIFMM_EARG;
   if (n_tiles == 0) return 0;
@@ -260,7 +342,7 @@ int kifmm_m2l_sweep_tc_f32(const float* qhi, const float* qlo, const float* bhi,
   int stages = (int)((220 * 1024) / stage_bytes);
   if (stages > 6) stages = 6;
   if (stages < 2) return KIFMM_EARG;
-  const size_t smem = stages * stage_bytes + (2 * stages + 1) * 8 + 16;
+  const size_t smem = stages * stage_bytes + (2 * stages + 4) * 8 + 16;
   const int jper = (int)((189 + nsplit - 1) / nsplit);
   cudaFuncSetAttribute(m2l_sweep_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)nsplit);
