@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tc_kernel(
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], NPROD);
+      mbar_init(&full[s], NPROD + 1);   // 128 cp.async arrivals + the bulk-copy expect_tx
       mbar_init(&empty[s], 1);
     }
     mbar_init(&tfull[0], 1);
@@ -185,28 +185,55 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tc_kernel(
 
   if (warp < 4) {
     // ------------------------------------------------------------ producers
-    const int m = tid;                                   // gathered row
-    const uint32_t a_row_off = (m >> 3) * (KC / 4) * 128 + (m & 7) * 16;
-    int32_t s_row = -1;
+    // Warp w gathers rows [32w, 32w+32).  Lane l owns the source index of row
+    // 32w+l (prefetched one vector ahead); the copies go 8 lanes per row, so
+    // one instruction moves 4 full 128-byte row segments (whole sectors).
+    const int sub_row = lane >> 3, sub_ch = lane & 7;
+    int32_t s_cur = nvec > 0 ? __ldg(&tsrc[j0 * TMT + tid]) : -1;
+    int32_t s_next = nvec > 1 ? __ldg(&tsrc[(j0 + 1) * TMT + tid]) : -1;
     for (int st = 0; st < nsteps; ++st) {
       const int stage = st % stages;
       const int round = st / stages;
       if (round > 0) mbar_wait(&empty[stage], (round - 1) & 1);
-      const int j = j0 + st / nchunks, c = st % nchunks;
-      if (c == 0) s_row = __ldg(&tsrc[j * TMT + m]);
+      const int jl = st / nchunks, c = st % nchunks;
+      const int j = j0 + jl;
+      if (c == 0 && jl > 0) {
+        s_cur = s_next;
+        s_next = jl + 1 < nvec ? __ldg(&tsrc[(j + 1) * TMT + tid]) : -1;
+      }
       const int kc = min(KC, kin - c * KC);              // multiple of 8
       unsigned char* sb = smem + stage * stage_bytes;
-      const int64_t g = ((int64_t)(s_row < 0 ? 0 : s_row) * nrhs + r) * kin + c * KC;
-      for (int ch = 0; ch < kc / 4; ++ch) {
-        cp_async16(sb + a_row_off + ch * 128, qhi + g + ch * 4, s_row >= 0);
-        cp_async16(sb + a_bytes + a_row_off + ch * 128, qlo + g + ch * 4, s_row >= 0);
+      if (tid == 0) {
+        // B block of (vector, chunk): already in smem layout, contiguous.
+        const uint32_t bbytes = (uint32_t)(n_out * kc * 4);
+        const int64_t boff = (int64_t)tv_list[j] * n_out * kin + (int64_t)n_out * KC * c;
+        const uint32_t fb = smem_u32(&full[stage]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                     "r"(2 * bbytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sb + 2 * a_bytes)),
+            "l"(bhi + boff), "r"(bbytes), "r"(fb)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sb + 2 * a_bytes + b_bytes)),
+            "l"(blo + boff), "r"(bbytes), "r"(fb)
+            : "memory");
       }
-      // B block of (vector, chunk): already in smem layout, contiguous.
-      const int64_t boff = (int64_t)tv_list[j] * n_out * kin + (int64_t)n_out * KC * c;
-      const int units = n_out * kc / 4;
-      for (int u = m; u < units; u += NPROD) {
-        cp_async16(sb + 2 * a_bytes + u * 16, bhi + boff + u * 4, true);
-        cp_async16(sb + 2 * a_bytes + b_bytes + u * 16, blo + boff + u * 4, true);
+      const bool ch_live = sub_ch < kc / 4;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rl = i * 4 + sub_row;                  // row within the warp's 32
+        const int32_t s = __shfl_sync(0xffffffffu, s_cur, rl);
+        if (ch_live) {
+          const int m = warp * 32 + rl;
+          const uint32_t off = (m >> 3) * (KC / 4) * 128 + (m & 7) * 16 + sub_ch * 128;
+          const int64_t g = ((int64_t)(s < 0 ? 0 : s) * nrhs + r) * kin + c * KC + sub_ch * 4;
+          cp_async16(sb + off, qhi + g, s >= 0);
+          cp_async16(sb + a_bytes + off, qlo + g, s >= 0);
+        }
       }
       cp_async_arrive_noinc(&full[stage]);
     }
