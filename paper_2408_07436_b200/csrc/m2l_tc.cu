@@ -23,6 +23,8 @@
 //   warps 5-8  accumulators/epilogue: every FLUSH_V vectors they add the
 //              finished MMA buffer into the long-lived accumulator with IEEE
 //              fp32 adds (tcgen05.ld / tcgen05.st), then write the result.
+#include <cstdlib>
+
 #include "common.cuh"
 
 using namespace kifmm;
@@ -129,12 +131,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]
         "r"(v[14]), "r"(v[15]));
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tc_kernel(
+__global__ void __launch_bounds__(NTHREADS) m2l_sweep_tc_kernel(
     const float* __restrict__ qhi, const float* __restrict__ qlo, const float* __restrict__ bhi,
     const float* __restrict__ blo, int kin, int n_out, int stages,
     const int32_t* __restrict__ tile_targets, const int32_t* __restrict__ tile_class,
     const int32_t* __restrict__ src, const int32_t* __restrict__ class_tv, int64_t nrhs,
-    int nsplit, int jper, float* __restrict__ acc_out) {
+    int nsplit, int jper, int l1_gather, float* __restrict__ acc_out) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nchunks = (kin + KC - 1) / KC;
@@ -231,8 +233,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tc_kernel(
           const int m = warp * 32 + rl;
           const uint32_t off = (m >> 3) * (KC / 4) * 128 + (m & 7) * 16 + sub_ch * 128;
           const int64_t g = ((int64_t)(s < 0 ? 0 : s) * nrhs + r) * kin + c * KC + sub_ch * 4;
-          cp_async16(sb + off, qhi + g, s >= 0);
-          cp_async16(sb + a_bytes + off, qlo + g, s >= 0);
+          if (l1_gather) {
+            cp_async16_ca(sb + off, qhi + g, s >= 0);
+            cp_async16_ca(sb + a_bytes + off, qlo + g, s >= 0);
+          } else {
+            cp_async16(sb + off, qhi + g, s >= 0);
+            cp_async16(sb + a_bytes + off, qlo + g, s >= 0);
+          }
         }
       }
       cp_async_arrive_noinc(&full[stage]);
@@ -366,8 +373,19 @@ int kifmm_m2l_sweep_tc_f32(const float* qhi, const float* qlo, const float* bhi,
     return KIFMM_EARG;
   if (n_tiles == 0) return 0;
   const size_t stage_bytes = 2 * (size_t)TMT * KC * 4 + 2 * (size_t)n_out * KC * 4;
-  int stages = (int)((220 * 1024) / stage_bytes);
-  if (stages > 6) stages = 6;
+  // Pipeline depth / CTAs per SM (tuning knobs, defaults measured on B200).
+  static int ctas_per_sm = -1, max_stages = -1, l1 = 0;
+  if (ctas_per_sm < 0) {
+    const char* e = getenv("KIFMM_TC_CTAS");
+    ctas_per_sm = e ? atoi(e) : 2;
+    if (ctas_per_sm < 1) ctas_per_sm = 1;
+    const char* f = getenv("KIFMM_TC_STAGES");
+    max_stages = f ? atoi(f) : 6;
+    const char* g = getenv("KIFMM_TC_L1");
+    l1 = g ? atoi(g) : 0;
+  }
+  int stages = (int)((220 * 1024 / ctas_per_sm) / stage_bytes);
+  if (stages > max_stages) stages = max_stages;
   if (stages < 2) return KIFMM_EARG;
   const size_t smem = stages * stage_bytes + (2 * stages + 4) * 8 + 16;
   const int jper = (int)((189 + nsplit - 1) / nsplit);
@@ -375,7 +393,7 @@ int kifmm_m2l_sweep_tc_f32(const float* qhi, const float* qlo, const float* bhi,
   dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)nsplit);
   m2l_sweep_tc_kernel<<<grid, NTHREADS, smem, (cudaStream_t)stream>>>(
       qhi, qlo, bhi, blo, (int)kin, (int)n_out, stages, tile_targets, tile_class, src, class_tv,
-      nrhs, (int)nsplit, jper, acc);
+      nrhs, (int)nsplit, jper, l1, acc);
   return launch_status();
 }
 
