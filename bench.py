@@ -314,11 +314,13 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the partitioned (torchrun) path even for one rank")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference_arm(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or args.force_dist:
         from paper_2408_07436_b200 import distributed
         return distributed.bench_main(args, sys.modules[__name__])
     return run_single(args)

@@ -135,11 +135,25 @@ int kifmm_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stre
 /* FFT-M2L forward (m2l_fft.py:236-247): embed each box's multipole at
  * lattice+p of the n^3 grid (n = 2p), real 3-D DFT, and write the spectrum
  * frequency-major into qhat[(f*nsc + cluster)*8 + child)*nrhs + r] (complex).
- * slot_box (nsc*8): box row of each cluster slot or -1 (zero spectrum). */
+ * slot_box (nsc*8): box row of each cluster slot or -1 (zero spectrum).
+ * cluster_list (n_list) restricts the transform to those clusters (NULL = all). */
 int kifmm_fft_forward_f32(const float* mult, int64_t nrhs, int64_t order, const int32_t* slot_box,
-                          int64_t nsc, float* qhat, void* stream);
+                          int64_t nsc, const int32_t* cluster_list, int64_t n_list, float* qhat,
+                          void* stream);
 int kifmm_fft_forward_f64(const double* mult, int64_t nrhs, int64_t order,
-                          const int32_t* slot_box, int64_t nsc, double* qhat, void* stream);
+                          const int32_t* slot_box, int64_t nsc, const int32_t* cluster_list,
+                          int64_t n_list, double* qhat, void* stream);
+
+/* Multipole halo pack/unpack for the multi-GPU exchange:
+ * gather: dst[i*width + e] = src[rows[i]*width + e]; scatter: the reverse. */
+int kifmm_gather_rows_f32(const float* src, const int32_t* rows, int64_t n_rows, int64_t width,
+                          float* dst, void* stream);
+int kifmm_gather_rows_f64(const double* src, const int32_t* rows, int64_t n_rows, int64_t width,
+                          double* dst, void* stream);
+int kifmm_scatter_rows_f32(const float* src, const int32_t* rows, int64_t n_rows, int64_t width,
+                           float* dst, void* stream);
+int kifmm_scatter_rows_f64(const double* src, const int32_t* rows, int64_t n_rows, int64_t width,
+                           double* dst, void* stream);
 
 /* FFT-M2L inverse (m2l_fft.py:252-261): for each target box b, take the
  * spectrum phat[f, tgt_slot[b], r], inverse real 3-D DFT, read the

@@ -203,11 +203,12 @@ def _solve(inv, phi, scale):
 
 
 # -------------------------------------------------------------- full evaluate
-def evaluate(inst, charges, threads=None, timings=None):
+def evaluate(inst, charges, threads=None, timings=None, state=None):
     """engine.evaluate (engine.py:270-404) on the product's host plan.
 
     Returns potentials in the caller's target order, in the working dtype.
-    ``timings`` (dict) receives per-operator wall seconds like the reference.
+    ``timings`` (dict) receives per-operator wall seconds like the reference;
+    ``state`` (dict) receives the per-level ``multipoles`` and ``locals``.
     """
     import time
 
@@ -331,6 +332,9 @@ def evaluate(inst, charges, threads=None, timings=None):
     p2p_blocked(tx, ty, tz, leaf_of_target, sx[near_idx], sy[near_idx], sz[near_idx],
                 np.ascontiguousarray(q_tree[near_idx]), near_off, pot, threads)
     tm["p2p"] = time.perf_counter() - t0
+    if state is not None:
+        state["multipoles"] = mult
+        state["locals"] = loc
     out = np.empty_like(pot)
     out[tt.perm] = pot
     return out

@@ -177,9 +177,48 @@ __global__ void gather_charges_kernel(const double* __restrict__ qin,
   qt[idx] = (T)qin[perm[i] * nrhs + r];
 }
 
+// Row gather/scatter of width-element rows (multipole halo pack/unpack).
+template <typename T>
+__global__ void rows_kernel(const T* __restrict__ src, const int32_t* __restrict__ rows,
+                            int64_t n_rows, int64_t width, T* __restrict__ dst, int scatter) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_rows * width) return;
+  const int64_t i = idx / width, e = idx - i * width;
+  const int64_t g = rows[i];
+  if (scatter) dst[g * width + e] = src[idx];
+  else dst[idx] = src[g * width + e];
+}
+
+template <typename T>
+int rows_op(const T* src, const int32_t* rows, int64_t n_rows, int64_t width, T* dst, int scatter,
+            void* stream) {
+  if (n_rows < 0 || width < 1) return KIFMM_EARG;
+  if (n_rows == 0) return 0;
+  rows_kernel<T><<<ceil_div(n_rows * width, 256), 256, 0, (cudaStream_t)stream>>>(
+      src, rows, n_rows, width, dst, scatter);
+  return launch_status();
+}
+
 }  // namespace
 
 extern "C" {
+
+int kifmm_gather_rows_f32(const float* src, const int32_t* rows, int64_t n_rows, int64_t width,
+                          float* dst, void* s) {
+  return rows_op<float>(src, rows, n_rows, width, dst, 0, s);
+}
+int kifmm_gather_rows_f64(const double* src, const int32_t* rows, int64_t n_rows, int64_t width,
+                          double* dst, void* s) {
+  return rows_op<double>(src, rows, n_rows, width, dst, 0, s);
+}
+int kifmm_scatter_rows_f32(const float* src, const int32_t* rows, int64_t n_rows, int64_t width,
+                           float* dst, void* s) {
+  return rows_op<float>(src, rows, n_rows, width, dst, 1, s);
+}
+int kifmm_scatter_rows_f64(const double* src, const int32_t* rows, int64_t n_rows, int64_t width,
+                           double* dst, void* s) {
+  return rows_op<double>(src, rows, n_rows, width, dst, 1, s);
+}
 
 int kifmm_gemm_f32(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
                    int asum, int64_t astride, const float* B, int64_t ldb, const float* colscale,

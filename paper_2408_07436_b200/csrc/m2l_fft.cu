@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restri
                                                                int64_t nrhs, int p, int bpc,
                                                                const int32_t* __restrict__ slot_box,
                                                                int64_t nsc,
+                                                               const int32_t* __restrict__ cluster_list,
                                                                typename cx<T>::v* __restrict__ qhat) {
   using C = typename cx<T>::v;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -93,7 +94,8 @@ __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restri
   auto X2 = [&](int b) { return reinterpret_cast<C*>(boxes + b * box_bytes + x1_elems * sizeof(C)); };
 
   const int groups = 8 / bpc;
-  const int64_t cluster = blockIdx.x / groups;
+  const int64_t cluster = cluster_list ? (int64_t)cluster_list[blockIdx.x / groups]
+                                       : (int64_t)(blockIdx.x / groups);
   const int child0 = (blockIdx.x % groups) * bpc;
   const int64_t r = blockIdx.y;
   build_twiddles<T>(n, tw);
@@ -249,7 +251,7 @@ int pick_bpc(size_t (*smem)(int, int), int p, size_t limit) {
 
 template <typename T>
 int forward(const T* mult, int64_t nrhs, int64_t order, const int32_t* slot_box, int64_t nsc,
-            T* qhat, void* stream) {
+            const int32_t* cluster_list, int64_t n_list, T* qhat, void* stream) {
   using C = typename cx<T>::v;
   if (order < 2 || order > kMaxP || nrhs < 1 || nsc < 0) return KIFMM_EARG;
   if (nsc == 0) return 0;
@@ -259,9 +261,11 @@ int forward(const T* mult, int64_t nrhs, int64_t order, const int32_t* slot_box,
   size_t smem = forward_smem<T>(p, bpc);
   auto kern = fft_forward_kernel<T>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((unsigned)(nsc * (8 / bpc)), (unsigned)nrhs);
+  const int64_t nclusters = cluster_list ? n_list : nsc;
+  if (nclusters <= 0) return 0;
+  dim3 grid((unsigned)(nclusters * (8 / bpc)), (unsigned)nrhs);
   kern<<<grid, kThreads, smem, (cudaStream_t)stream>>>(mult, nrhs, p, bpc, slot_box, nsc,
-                                                       reinterpret_cast<C*>(qhat));
+                                                       cluster_list, reinterpret_cast<C*>(qhat));
   return launch_status();
 }
 
@@ -288,12 +292,14 @@ int inverse(const T* phat, int64_t nrhs, int64_t order, const int32_t* slot_box,
 extern "C" {
 
 int kifmm_fft_forward_f32(const float* mult, int64_t nrhs, int64_t order, const int32_t* slot_box,
-                          int64_t nsc, float* qhat, void* s) {
-  return forward<float>(mult, nrhs, order, slot_box, nsc, qhat, s);
+                          int64_t nsc, const int32_t* cluster_list, int64_t n_list, float* qhat,
+                          void* s) {
+  return forward<float>(mult, nrhs, order, slot_box, nsc, cluster_list, n_list, qhat, s);
 }
 int kifmm_fft_forward_f64(const double* mult, int64_t nrhs, int64_t order,
-                          const int32_t* slot_box, int64_t nsc, double* qhat, void* s) {
-  return forward<double>(mult, nrhs, order, slot_box, nsc, qhat, s);
+                          const int32_t* slot_box, int64_t nsc, const int32_t* cluster_list,
+                          int64_t n_list, double* qhat, void* s) {
+  return forward<double>(mult, nrhs, order, slot_box, nsc, cluster_list, n_list, qhat, s);
 }
 int kifmm_fft_inverse_f32(const float* phat, int64_t nrhs, int64_t order, const int32_t* slot_box,
                           int64_t ntc, double level_scale, float* check, void* s) {

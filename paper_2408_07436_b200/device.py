@@ -218,6 +218,40 @@ class BlasDevice:
         self.Dt = to_dev(dt_pad)
         self.class_tv = to_dev(class_transfer_table(), np.int32)
 
+    def run_level_rows(self, plan, mult, n_s, lo, hi, nrhs, level_scale, check, qt, acc):
+        """Multi-GPU variant: ``plan`` covers only the target rows [lo, hi)
+        (global row numbering); the expansion runs on those rows only."""
+        la = self.la
+        nsplit = sweep_splits(plan["n_tiles"], self.n_slabs)
+        ld = nsplit * self.ko_pad
+        isz = qt.element_size()
+        la.gemm(n_s * nrhs, self.k, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
+        if self.tc:
+            nq = n_s * nrhs * self.kin
+            qhi, qlo = qt[nq: 2 * nq], qt[2 * nq: 3 * nq]
+            launch("kifmm_split_tf32", P(qt), nq, P(qhi), P(qlo), stream_handle())
+            if plan["n_tiles"]:
+                launch("kifmm_m2l_sweep_tc_f32", P(qhi), P(qlo), P(self.Bhi), P(self.Blo),
+                       self.kin, self.ko_pad, P(plan["tile_targets"]), P(plan["tile_class"]),
+                       P(plan["src"]), P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc),
+                       stream_handle())
+        elif plan["n_tiles"]:
+            launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
+                   P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
+                   P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc), stream_handle())
+
+        class _Off:
+            def __init__(self, t, elems):
+                self.p = t.data_ptr() + elems * isz
+
+            def data_ptr(self):
+                return self.p
+
+        la.gemm((hi - lo) * nrhs, self.n_c, self.k, level_scale, _Off(acc, lo * nrhs * ld), ld,
+                self.UT, self.n_c, _Off(check, lo * nrhs * self.n_c), self.n_c, asum=nsplit,
+                astride=self.ko_pad)
+        return 3
+
     def acc_elems(self, n_t, nrhs, n_tiles):
         return n_t * nrhs * sweep_splits(n_tiles, self.n_slabs) * self.ko_pad
 
@@ -337,7 +371,7 @@ class DeviceFmm:
         phat = b["phat"][: 2 * self.n_freq * ntc * 8 * nrhs]
         s = stream_handle()
         launch(f"kifmm_fft_forward_{self.sfx}", P(mult), nrhs, self.order, P(plan["sbox"]), nsc,
-                 P(qhat), s)
+               None, 0, P(qhat), s)
         phat.zero_()
         cname = "c64" if self.sfx == "f32" else "c128"
         launch(f"kifmm_hadamard_m2l_{cname}", P(self.khat), P(qhat), P(plan["halo"]), P(phat),
@@ -542,7 +576,7 @@ def m2l_fft_level_host(ops, plan, mult, level_scale):
     s = stream_handle()
     m = to_dev(mult)
     keep = [to_dev(sbox), to_dev(plan.halo, np.int64), to_dev(tbox)]
-    launch(f"kifmm_fft_forward_{sfx}", P(m), nrhs, ops.order, P(keep[0]), nsc, P(qhat), s)
+    launch(f"kifmm_fft_forward_{sfx}", P(m), nrhs, ops.order, P(keep[0]), nsc, None, 0, P(qhat), s)
     cname = "c64" if sfx == "f32" else "c128"
     launch(f"kifmm_hadamard_m2l_{cname}", P(khat), P(qhat), P(keep[1]), P(phat), nf, nsc, ntc,
            nrhs, s)
