@@ -159,8 +159,9 @@ def test_evaluate_matches_reference(cuda, name):
     err = inst.relative_error(got)
     if ref_inst is not None:
         ref_err = ref_inst.relative_error(want)
-        # both must show the same error against direct summation
-        assert abs(err.error - ref_err.error) <= 0.01 * ref_err.error + 1e-14, (err, ref_err)
+        # both must show the same error against direct summation: the mean
+        # relative errors can differ by at most the mean per-target gap
+        assert abs(err.error - ref_err.error) <= rep["max_rel"] + 1e-13, (err, ref_err, rep)
         assert err.n_excluded == ref_err.n_excluded
     # and the golden run (another host) agrees to within its own accuracy
     assert abs(err.error - float(g["error"])) <= 0.5 * float(g["error"]) + 1e-12
