@@ -32,6 +32,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+if __name__ == "__main__" and "reference" in sys.argv:
+    # Reference arm thread policy: all cores for the OpenMP
+    # loops, passive waiting, single-threaded OpenBLAS for the many small
+    # per-leaf GEMMs (default threading oversubscribes: P2M 47x slower).
+    _n = str(os.cpu_count() or 1)
+    for _k, _v in (("OMP_WAIT_POLICY", "PASSIVE"), ("OMP_NUM_THREADS", _n),
+                   ("KIFMM_THREADS", _n), ("OPENBLAS_NUM_THREADS", "1")):
+        os.environ.setdefault(_k, _v)
+
 METRIC = "M2L GFLOP/s (% roofline) & FMM eval Mpoints/s, Laplace 3D, 1M pts, 1/2/4/8 GPU"
 CONFIG = dict(depth=5, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6)
 N_POINTS = 1_000_000
@@ -121,6 +130,18 @@ def m2l_flops(inst):
         per_level[lvl] = dict(apply=f, bucket=bk, pairs=int(sum(p[0].shape[0] for p in b.pairs
                                                               if p is not None)))
     return apply_f, apply_f + solve_f, per_level
+
+
+def measured_peaks():
+    """Driver-written MEASURED_PEAKS.json, else the profiling guide's fallback."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return dict(hbm_gbs=float(d["hbm_gbs"]), bf16_tflops=float(d["bf16_tflops"]),
+                    source="MEASURED_PEAKS.json")
+    except Exception:
+        return dict(hbm_gbs=6650.0, bf16_tflops=1590.0, source="fallback (B200_PROFILING.md)")
 
 
 def probe_peak(kind):
@@ -248,23 +269,51 @@ def run_single(args):
     f_apply, f_total, per_level = m2l_flops(inst)
     m2l_s = phases.get("m2l", 0.0)
     sweep_t = {t: ms_ for n, t, ms_ in launches if "m2l_sweep" in n}
-    # dominant kernel
+    # rooflines of the two dominant kernels; `roofline` is the top one
     dom = max(per_kernel.items(), key=lambda kv: kv[1])
     peak_f32 = probe_peak(0)
-    if "m2l_sweep" in dom[0]:
-        lvl = inst.config.depth
-        achieved = per_level[lvl]["bucket"] / (sweep_t[f"m2l{lvl}"] / 1e3) / 1e12
-        roof = dict(bound="fp32", kernel="m2l_sweep_f32 (finest level)", achieved=achieved,
-                    peak=peak_f32, unit="TFLOP/s", frac=achieved / peak_f32, traffic=None,
-                    algorithmic="4 k sum_t m_t k_t flops at level %d" % lvl)
+    peak_mufu = probe_peak(2)                       # Grsqrt/s
+    peaks = measured_peaks()
+    rooflines = {}
+    lvl = inst.config.depth
+    bd = dev.blas
+    sweep_ms = sweep_t[f"m2l{lvl}"]
+    algo = per_level[lvl]["bucket"]
+    if bd.tc:
+        # 3xTF32 on the TF32 tensor pipe: dense TF32 = bf16 / 2 (same datapath),
+        # three MMAs per fp32 product
+        peak_tc = peaks["bf16_tflops"] / 2.0 / 3.0
+        execd = 3 * 2.0 * 128 * bd.kin * bd.ko_pad * 189 * \
+            dev.blas_plan_dev[lvl]["n_tiles"]
+        gather_bytes = 2 * 4.0 * bd.kin * per_level[lvl]["pairs"]
+        rooflines["m2l_sweep_tc_f32"] = dict(
+            bound="tensor", kernel=f"m2l_sweep_tc_f32 (level {lvl})",
+            achieved=algo / (sweep_ms / 1e3) / 1e12, peak=peak_tc, unit="TFLOP/s",
+            frac=algo / (sweep_ms / 1e3) / 1e12 / peak_tc, traffic=None,
+            algorithmic=f"4 k sum_t m_t k_t = {algo:.4g} flop at level {lvl} (SURVEY 8d)",
+            executed_tensor_tflops=execd / (sweep_ms / 1e3) / 1e12,
+            gather_gbs=gather_bytes / (sweep_ms / 1e3) / 1e9,
+            peak_source="MEASURED_PEAKS.json bf16_tflops / 2 (TF32) / 3 (3xTF32)")
     else:
-        inter = inst.n_near_pairs
-        leaf_ms = per_kernel[dom[0]]
-        achieved = 11.0 * inter / (leaf_ms / 1e3) / 1e12
-        roof = dict(bound="fp32", kernel=dom[0], achieved=achieved, peak=peak_f32,
-                    unit="TFLOP/s", frac=achieved / peak_f32, traffic=None,
-                    algorithmic="11 flop x %d P2P interactions (L2P fused, not counted)" % inter)
-    roof["peak_source"] = "kifmm_probe FFMA, measured in this run (MEASURED_PEAKS.json has no FP32 figure)"
+        rooflines["m2l_sweep"] = dict(
+            bound="fp32", kernel=f"m2l_sweep (level {lvl})",
+            achieved=algo / (sweep_ms / 1e3) / 1e12, peak=peak_f32, unit="TFLOP/s",
+            frac=algo / (sweep_ms / 1e3) / 1e12 / peak_f32, traffic=None,
+            algorithmic=f"4 k sum_t m_t k_t = {algo:.4g} flop at level {lvl}",
+            peak_source="kifmm_probe FFMA measured in this run")
+    inter = inst.n_near_pairs
+    leaf_key = [k for k in per_kernel if k.startswith("leaf_pass")][0]
+    leaf_ms = per_kernel[leaf_key]
+    l2p = float(inst.target_tree.n_points) * inst.expansions.n_equiv
+    rooflines[leaf_key] = dict(
+        bound="mufu", kernel=leaf_key, achieved=(inter + l2p) / (leaf_ms / 1e3) / 1e9,
+        peak=peak_mufu, unit="Grsqrt/s", frac=(inter + l2p) / (leaf_ms / 1e3) / 1e9 / peak_mufu,
+        traffic=None,
+        algorithmic=f"{inter} P2P + {l2p:.0f} L2P kernel evaluations (one rsqrt each)",
+        tflops_11_per_interaction=11.0 * inter / (leaf_ms / 1e3) / 1e12, fp32_peak=peak_f32,
+        peak_source="kifmm_probe MUFU.RSQ measured in this run")
+    roof = rooflines["m2l_sweep_tc_f32" if bd.tc else "m2l_sweep"] if "sweep" in dom[0] \
+        else rooflines[leaf_key]
 
     # e2e through the public API (host charges in pinned memory -> host potentials)
     q_pinned = torch.from_numpy(q).pin_memory().numpy()
@@ -298,6 +347,7 @@ def run_single(args):
                 m2l=dict(gflops=f_total / m2l_s / 1e9 if m2l_s else None,
                          seconds=m2l_s, flops_apply=f_apply, flops_with_solve=f_total),
                 operator_seconds=phases, kernel_ms=per_kernel, roofline=roof,
+                roofline_all=rooflines,
                 cpu_baseline=cpu,
                 e2e=dict(value=e2e_value, unit="Mpoints/s", h2d_bytes_per_step=int(q.nbytes),
                          d2h_bytes_per_step=int(out.nbytes)),

@@ -174,18 +174,24 @@ int kifmm_fft_inverse_f64(const double* phat, int64_t nrhs, int64_t order,
  * perm NULL -> tree order. */
 int kifmm_leaf_pass_f32(const float* tx, const float* ty, const float* tz, const int32_t* tleaf_start,
                         const int32_t* tleaf_count, int64_t n_tleaves, const double* centers,
-                        const double* base, int64_t ne, const float* local,
-                        const float* sx, const float* sy, const float* sz, const float* q,
-                        const int32_t* sleaf_start, const int32_t* sleaf_count,
+                        const double* base, int64_t ne, const float* local, const float* src4,
+                        int64_t ns, const int32_t* sleaf_start, const int32_t* sleaf_count,
                         const int32_t* near_off, const int32_t* near_leaf, int64_t nrhs,
                         const int64_t* perm, int parts, float* out, void* stream);
 int kifmm_leaf_pass_f64(const double* tx, const double* ty, const double* tz,
                         const int32_t* tleaf_start, const int32_t* tleaf_count, int64_t n_tleaves,
                         const double* centers, const double* base, int64_t ne, const double* local,
-                        const double* sx, const double* sy, const double* sz, const double* q,
-                        const int32_t* sleaf_start, const int32_t* sleaf_count,
-                        const int32_t* near_off, const int32_t* near_leaf, int64_t nrhs,
-                        const int64_t* perm, int parts, double* out, void* stream);
+                        const double* src4, int64_t ns, const int32_t* sleaf_start,
+                        const int32_t* sleaf_count, const int32_t* near_off,
+                        const int32_t* near_leaf, int64_t nrhs, const int64_t* perm, int parts,
+                        double* out, void* stream);
+
+/* AoS source records for the leaf pass (16/32-byte aligned):
+ * src4[(r*ns + j)*4 + {0,1,2,3}] = (x_j, y_j, z_j, q[j*nrhs + r]). */
+int kifmm_pack_sources_f32(const float* sx, const float* sy, const float* sz, const float* q,
+                           int64_t ns, int64_t nrhs, float* src4, void* stream);
+int kifmm_pack_sources_f64(const double* sx, const double* sy, const double* sz, const double* q,
+                           int64_t ns, int64_t nrhs, double* src4, void* stream);
 
 /* Charge intake: q_tree[i*nrhs + r] = (T) q_in[perm[i]*nrhs + r] (float64 in). */
 int kifmm_gather_charges_f32(const double* q_in, const int64_t* perm, int64_t n, int64_t nrhs,

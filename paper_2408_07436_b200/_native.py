@@ -46,10 +46,12 @@ SIGNATURES = {
     "kifmm_scatter_rows_f64": [_P, _P, _I, _I, _P, _P],
     "kifmm_fft_inverse_f32": [_P, _I, _I, _P, _I, _D, _P, _P],
     "kifmm_fft_inverse_f64": [_P, _I, _I, _P, _I, _D, _P, _P],
-    "kifmm_leaf_pass_f32": [_P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P,
-                            _P, _P, _I, _P, _C, _P, _P],
-    "kifmm_leaf_pass_f64": [_P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P,
-                            _P, _P, _I, _P, _C, _P, _P],
+    "kifmm_leaf_pass_f32": [_P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P,
+                            _I, _P, _C, _P, _P],
+    "kifmm_leaf_pass_f64": [_P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P,
+                            _I, _P, _C, _P, _P],
+    "kifmm_pack_sources_f32": [_P, _P, _P, _P, _I, _I, _P, _P],
+    "kifmm_pack_sources_f64": [_P, _P, _P, _P, _I, _I, _P, _P],
     "kifmm_gather_charges_f32": [_P, _P, _I, _I, _P, _P],
     "kifmm_gather_charges_f64": [_P, _P, _I, _I, _P, _P],
     "kifmm_split_tf32": [_P, _I, _P, _P, _P],

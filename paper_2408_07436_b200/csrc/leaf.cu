@@ -88,7 +88,7 @@ __device__ __forceinline__ void near_sum(const typename vec4<T>::v* buf, int m, 
   for (; k < m; ++k) {
     V s = buf[k];
     T dx = x0 - s.x, dy = y0 - s.y, dz = z0 - s.z;
-    a0 += real_traits<T>::rsq(dx * dx + dy * dy + dz * dz) * s.w;
+    b0 += real_traits<T>::rsq(dx * dx + dy * dy + dz * dz) * s.w;
     if (TWO) {
       T ex = x1 - s.x, ey = y1 - s.y, ez = z1 - s.z;
       b1 += real_traits<T>::rsq(ex * ex + ey * ey + ez * ez) * s.w;
@@ -98,19 +98,33 @@ __device__ __forceinline__ void near_sum(const typename vec4<T>::v* buf, int m, 
   a1 += b1;
 }
 
+// Copy one (x, y, z, q) source record global -> shared asynchronously.
+template <typename T>
+__device__ __forceinline__ void stage_src(typename vec4<T>::v* dst, const typename vec4<T>::v* src) {
+  if constexpr (sizeof(T) == 4) {
+    cp_async16(dst, src, true);
+  } else {
+    cp_async16(dst, src, true);
+    cp_async16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16, true);
+  }
+}
+
+// Leaf pass: one warp per target leaf, up to 64 targets per pass (lane and
+// lane+32).  The near-field sources of the leaf - its own leaf first, then
+// the neighbours by Morton code - are staged from the AoS source array into
+// shared memory with cp.async, all segments in flight at once, then swept.
 template <typename T>
 __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
     const T* __restrict__ tx, const T* __restrict__ ty, const T* __restrict__ tz,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
     const double* __restrict__ centers, const double* __restrict__ base, int64_t ne,
-    const T* __restrict__ local, const T* __restrict__ sx, const T* __restrict__ sy,
-    const T* __restrict__ sz, const T* __restrict__ q, const int32_t* __restrict__ sstart,
-    const int32_t* __restrict__ scount, const int32_t* __restrict__ near_off,
-    const int32_t* __restrict__ near_leaf, int64_t nrhs, const int64_t* __restrict__ perm,
-    int parts, T* __restrict__ out) {
+    const T* __restrict__ local, const typename vec4<T>::v* __restrict__ src4, int64_t ns,
+    const int32_t* __restrict__ sstart, const int32_t* __restrict__ scount,
+    const int32_t* __restrict__ near_off, const int32_t* __restrict__ near_leaf, int64_t nrhs,
+    const int64_t* __restrict__ perm, int parts, T* __restrict__ out) {
   using V = typename vec4<T>::v;
   constexpr int kCap = cap_of<T>::v;
-  __shared__ V sbuf[kWarps][kCap];
+  __shared__ __align__(16) V sbuf[kWarps][kCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   V* buf = sbuf[w];
   const int64_t b = (int64_t)blockIdx.x * kWarps + w;
@@ -142,12 +156,14 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
         if (two) near_sum<T, true>(buf, m, m, x0, y0, z0, x1, y1, z1, far0, far1);
         else near_sum<T, false>(buf, m, m, x0, y0, z0, x1, y1, z1, far0, far1);
       }
-      // P2P: own leaf first, then neighbours in Morton order, staged in
-      // shared memory up to kCap sources at a time.
+      // P2P: own leaf first, then neighbours in Morton order.
       if (parts & 2) {
+        const V* srow = src4 + r * ns;
         int fill = 0;
         int guarded = n1 > n0 ? scount[near_leaf[n0]] : 0;
         auto flush = [&]() {
+          cp_async_commit();
+          cp_async_wait<0>();
           __syncwarp();
           const int g = min(guarded, fill);
           if (two) near_sum<T, true>(buf, fill, g, x0, y0, z0, x1, y1, z1, near0, near1);
@@ -156,6 +172,7 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
           fill = 0;
           __syncwarp();
         };
+        __syncwarp();
         for (int n = n0; n < n1; ++n) {
           const int sl = near_leaf[n];
           const int64_t j0 = sstart[sl];
@@ -163,10 +180,7 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
           for (int jb = 0; jb < jc;) {
             if (fill == kCap) flush();
             const int m = min(jc - jb, kCap - fill);
-            for (int k = lane; k < m; k += 32) {
-              const int64_t j = j0 + jb + k;
-              buf[fill + k] = V{sx[j], sy[j], sz[j], q[j * nrhs + r]};
-            }
+            for (int k = lane; k < m; k += 32) stage_src<T>(buf + fill + k, srow + j0 + jb + k);
             fill += m;
             jb += m;
           }
@@ -188,6 +202,17 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
   }
 }
 
+// AoS source records for the leaf pass: out[r*ns + j] = (x_j, y_j, z_j, q[j*nrhs + r]).
+template <typename T>
+__global__ void pack_sources_kernel(const T* __restrict__ sx, const T* __restrict__ sy,
+                                    const T* __restrict__ sz, const T* __restrict__ q, int64_t ns,
+                                    int64_t nrhs, typename vec4<T>::v* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= ns * nrhs) return;
+  const int64_t r = idx / ns, j = idx - r * ns;
+  out[idx] = typename vec4<T>::v{sx[j], sy[j], sz[j], q[j * nrhs + r]};
+}
+
 template <typename T>
 int p2m_check(const T* sx, const T* sy, const T* sz, const T* q, int64_t nrhs, const int32_t* ls,
               const int32_t* lc, int64_t nl, const double* centers, const double* base, int64_t nc,
@@ -202,14 +227,25 @@ int p2m_check(const T* sx, const T* sy, const T* sz, const T* q, int64_t nrhs, c
 template <typename T>
 int leaf_pass(const T* tx, const T* ty, const T* tz, const int32_t* ts, const int32_t* tcnt,
               int64_t ntl, const double* centers, const double* base, int64_t ne, const T* local,
-              const T* sx, const T* sy, const T* sz, const T* q, const int32_t* ss,
-              const int32_t* sc, const int32_t* no, const int32_t* nlf, int64_t nrhs,
-              const int64_t* perm, int parts, T* out, void* stream) {
-  if (ntl < 0 || ne < 1 || nrhs < 1 || parts < 1 || parts > 7) return KIFMM_EARG;
+              const T* src4, int64_t ns, const int32_t* ss, const int32_t* sc, const int32_t* no,
+              const int32_t* nlf, int64_t nrhs, const int64_t* perm, int parts, T* out,
+              void* stream) {
+  if (ntl < 0 || ne < 1 || nrhs < 1 || parts < 1 || parts > 7 || ns < 0) return KIFMM_EARG;
   if (ntl == 0) return 0;
   leaf_pass_kernel<T><<<ceil_div(ntl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
-      tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local, sx, sy, sz, q, ss, sc, no, nlf, nrhs,
-      perm, parts, out);
+      tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local,
+      reinterpret_cast<const typename vec4<T>::v*>(src4), ns, ss, sc, no, nlf, nrhs, perm, parts,
+      out);
+  return launch_status();
+}
+
+template <typename T>
+int pack_sources(const T* sx, const T* sy, const T* sz, const T* q, int64_t ns, int64_t nrhs,
+                 T* out, void* stream) {
+  if (ns < 0 || nrhs < 1) return KIFMM_EARG;
+  if (ns == 0) return 0;
+  pack_sources_kernel<T><<<ceil_div(ns * nrhs, 256), 256, 0, (cudaStream_t)stream>>>(
+      sx, sy, sz, q, ns, nrhs, reinterpret_cast<typename vec4<T>::v*>(out));
   return launch_status();
 }
 
@@ -231,21 +267,29 @@ int kifmm_p2m_check_f64(const double* sx, const double* sy, const double* sz, co
 }
 int kifmm_leaf_pass_f32(const float* tx, const float* ty, const float* tz, const int32_t* ts,
                         const int32_t* tc, int64_t ntl, const double* centers, const double* base,
-                        int64_t ne, const float* local, const float* sx, const float* sy,
-                        const float* sz, const float* q, const int32_t* ss, const int32_t* sc,
-                        const int32_t* no, const int32_t* nlf, int64_t nrhs, const int64_t* perm,
-                        int parts, float* out, void* s) {
-  return leaf_pass<float>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, sx, sy, sz, q, ss, sc,
-                          no, nlf, nrhs, perm, parts, out, s);
+                        int64_t ne, const float* local, const float* src4, int64_t ns,
+                        const int32_t* ss, const int32_t* sc, const int32_t* no,
+                        const int32_t* nlf, int64_t nrhs, const int64_t* perm, int parts,
+                        float* out, void* s) {
+  return leaf_pass<float>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, src4, ns, ss, sc, no,
+                          nlf, nrhs, perm, parts, out, s);
 }
 int kifmm_leaf_pass_f64(const double* tx, const double* ty, const double* tz, const int32_t* ts,
                         const int32_t* tc, int64_t ntl, const double* centers, const double* base,
-                        int64_t ne, const double* local, const double* sx, const double* sy,
-                        const double* sz, const double* q, const int32_t* ss, const int32_t* sc,
-                        const int32_t* no, const int32_t* nlf, int64_t nrhs, const int64_t* perm,
-                        int parts, double* out, void* s) {
-  return leaf_pass<double>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, sx, sy, sz, q, ss,
-                           sc, no, nlf, nrhs, perm, parts, out, s);
+                        int64_t ne, const double* local, const double* src4, int64_t ns,
+                        const int32_t* ss, const int32_t* sc, const int32_t* no,
+                        const int32_t* nlf, int64_t nrhs, const int64_t* perm, int parts,
+                        double* out, void* s) {
+  return leaf_pass<double>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, src4, ns, ss, sc,
+                           no, nlf, nrhs, perm, parts, out, s);
+}
+int kifmm_pack_sources_f32(const float* sx, const float* sy, const float* sz, const float* q,
+                           int64_t ns, int64_t nrhs, float* out, void* s) {
+  return pack_sources<float>(sx, sy, sz, q, ns, nrhs, out, s);
+}
+int kifmm_pack_sources_f64(const double* sx, const double* sy, const double* sz, const double* q,
+                           int64_t ns, int64_t nrhs, double* out, void* s) {
+  return pack_sources<double>(sx, sy, sz, q, ns, nrhs, out, s);
 }
 
 }  // extern "C"

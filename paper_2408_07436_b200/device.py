@@ -191,7 +191,8 @@ class BlasDevice:
         if tensor_cores is None:
             tensor_cores = os.environ.get("KIFMM_SWEEP", "tc") != "simt"
         # float32: tcgen05 3xTF32 sweep (csrc/m2l_tc.cu); float64: FP64 SIMT sweep.
-        self.tc = bool(tensor_cores) and dt == np.float32 and k <= 256
+        # (3 TMEM accumulators of n_out <= 160 columns fit the 512-column TMEM)
+        self.tc = bool(tensor_cores) and dt == np.float32 and k <= 160
         if self.tc:
             self.kin = -(-k // 8) * 8
             self.ko_pad = -(-k // 16) * 16
@@ -389,6 +390,7 @@ class DeviceFmm:
         d = self.depth
         b = {}
         b["q"] = torch.empty(self.sx.shape[0] * R, dtype=T, device=dev)
+        b["src4"] = torch.empty(self.sx.shape[0] * R * 4, dtype=T, device=dev)
         b["mult"] = [torch.empty(self.n_src[l] * R * self.n_e, dtype=T, device=dev)
                      for l in range(d + 1)]
         b["loc"] = [torch.empty(self.n_tgt[l] * R * self.n_e, dtype=T, device=dev)
@@ -454,7 +456,9 @@ class DeviceFmm:
         phase("p2m")
         q = b["q"]
         launch(f"kifmm_gather_charges_{sfx}", P(q_dev), P(self.s_perm), self.sx.shape[0], R,
-                 P(q), s)
+               P(q), s)
+        launch(f"kifmm_pack_sources_{sfx}", P(self.sx), P(self.sy), P(self.sz), P(q),
+               self.sx.shape[0], R, P(b["src4"]), s)
         # P2M: check potentials, then the up_inv solve scaled by the leaf side.
         mult, phi, tmp = b["mult"], b["phi"], b["tmp"]
         nl = self.n_src[d]
@@ -495,9 +499,8 @@ class DeviceFmm:
         out = b["out"]
         launch(f"kifmm_leaf_pass_{sfx}", P(self.tx), P(self.ty), P(self.tz), P(self.t_start),
                  P(self.t_count), self.n_tgt[d], P(self.t_centers), P(self.equiv_base), n_e,
-                 P(loc[d]), P(self.sx), P(self.sy), P(self.sz), P(q), P(self.s_start),
-                 P(self.s_count), P(self.near_off), P(self.near_leaf), R, P(self.t_perm), 3,
-                 P(out), s)
+               P(loc[d]), P(b["src4"]), self.sx.shape[0], P(self.s_start), P(self.s_count),
+               P(self.near_off), P(self.near_leaf), R, P(self.t_perm), 3, P(out), s)
         phase("end")
         self.last_m2l_calls = calls
         self._events = ev

@@ -299,6 +299,8 @@ class DistributedFmm:
         R, n_e, n_c, depth = nrhs, d.n_e, d.n_c, d.depth
         q = b["q"]
         launch(f"kifmm_gather_charges_{d.sfx}", P(q_dev), P(d.s_perm), d.sx.shape[0], R, P(q), s)
+        launch(f"kifmm_pack_sources_{d.sfx}", P(d.sx), P(d.sy), P(d.sz), P(q), d.sx.shape[0], R,
+               P(b["src4"]), s)
         isz = q.element_size()
         lo, hi = self.plan.src_ranges[depth]
         nl = hi - lo
@@ -361,7 +363,7 @@ class DistributedFmm:
         if hi > lo:
             launch(f"kifmm_leaf_pass_{d.sfx}", P(d.tx), P(d.ty), P(d.tz), P(d.t_start) + 4 * lo,
                    P(d.t_count) + 4 * lo, hi - lo, P(d.t_centers) + 24 * lo, P(d.equiv_base), n_e,
-                   P(loc[depth]) + lo * R * n_e * isz, P(d.sx), P(d.sy), P(d.sz), P(b["q"]),
+                   P(loc[depth]) + lo * R * n_e * isz, P(b["src4"]), d.sx.shape[0],
                    P(d.s_start), P(d.s_count), P(d.near_off) + 4 * lo, P(d.near_leaf), R,
                    P(d.t_perm), 3, P(out), s)
         return out[: d.tx.shape[0] * R]
