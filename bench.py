@@ -33,11 +33,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 if __name__ == "__main__" and "reference" in sys.argv:
-    # Reference arm thread policy: all cores for the OpenMP
-    # loops, passive waiting, single-threaded OpenBLAS for the many small
-    # per-leaf GEMMs (default threading oversubscribes: P2M 47x slower).
+    # Reference arm thread policy: all cores for the OpenMP loops with active
+    # waiting (the per-leaf P2M/L2P loops fork ~65k short parallel regions)
+    # and single-threaded OpenBLAS (threaded OpenBLAS oversubscribes the
+    # cores against the OpenMP team).  Measured on the B200 host (16 cores,
+    # c2): this policy 1.70 s/evaluate; PASSIVE 3.73 s; ACTIVE + threaded
+    # OpenBLAS 9.98 s; see profiles/r1/README.md.
     _n = str(os.cpu_count() or 1)
-    for _k, _v in (("OMP_WAIT_POLICY", "PASSIVE"), ("OMP_NUM_THREADS", _n),
+    for _k, _v in (("OMP_WAIT_POLICY", "ACTIVE"), ("OMP_NUM_THREADS", _n),
                    ("KIFMM_THREADS", _n), ("OPENBLAS_NUM_THREADS", "1")):
         os.environ.setdefault(_k, _v)
 
@@ -170,7 +173,6 @@ def cpu_reference_run(pts, q, steps=1, warmup=0, kw=None):
     """Unmodified reference evaluate (oracle/_ref, Cython-compiled from
     /root/reference) on this host; falls back to the oracle port."""
     kw = kw or CONFIG
-    os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
     from oracle import reference_available
     cores = os.cpu_count() or 1
     if reference_available():
@@ -211,7 +213,8 @@ def run_reference_arm(args):
                 cpu_baseline=dict(value=value, unit="Mpoints/s", cores=res["cores"],
                                   kind=res["kind"],
                                   sample=f"full workload, {steps} evaluate(s) of 1M points, "
-                                         f"threads={res['cores']}, OMP_WAIT_POLICY=PASSIVE"),
+                                         f"threads={res['cores']}, OMP_WAIT_POLICY=ACTIVE, "
+                                         "OPENBLAS_NUM_THREADS=1"),
                 e2e=dict(value=value, unit="Mpoints/s", h2d_bytes_per_step=0,
                          d2h_bytes_per_step=0),
                 m2l_seconds=float(res["timings"].get("m2l", 0.0)),
@@ -335,8 +338,8 @@ def run_single(args):
         ref = np.asarray(res["potentials"], dtype=np.float64)
         rel = np.abs(out.astype(np.float64) - ref) / np.abs(ref)
         cpu = dict(value=N_POINTS / csec / 1e6, unit="Mpoints/s", cores=res["cores"],
-                   kind=res["kind"], sample="one full 1M-point evaluate, all host threads, "
-                   "OMP_WAIT_POLICY=PASSIVE", seconds=csec,
+                   kind=res["kind"], sample="one full 1M-point evaluate, all host threads "
+                   "(in the bench process; default thread policy)", seconds=csec,
                    operator_seconds={k: float(v) for k, v in res["timings"].items()},
                    parity_max_rel=float(rel.max()), parity_tol=1e-5)
     line = dict(metric=METRIC, value=value, unit="Mpoints/s", n_gpus=1, steps=args.steps,
