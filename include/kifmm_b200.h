@@ -82,6 +82,28 @@ int kifmm_gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* 
                    const double* colscale, double* C, int64_t ldc, const int32_t* rowmap,
                    int accumulate, void* stream);
 
+/* Fused operator chain on row tiles (csrc/chain.cu):
+ *   Y0 = X . B0 * cs0 * al0;  Y(s) = Y(s-1) re-read as rows of width K(s) . B(s) * cs(s) * al(s)
+ *   C[rowmap(row)] (=|+=) Y(last)
+ * X rows: A[m*lda + k] summed over asum blocks (stride astride), or, when
+ * a_child is set, the 8 child rows a_child[p*8+c]*a_nrhs + r concatenated
+ * (M2M stacking).  B(s) are (K(s) x N(s)) row-major; cs(s) may be NULL.
+ * Used for the P2M solve, M2M, the M2L expansion + check->local solve and
+ * L2L (kernel product, then the factored pseudo-inverse, as the reference). */
+int kifmm_chain_f32(int64_t M, const float* A, int64_t lda, int asum, int64_t astride,
+                    const int32_t* a_child, int64_t child_w, int64_t a_nrhs, int nstage,
+                    const float* B0, const float* B1, const float* B2, int64_t K0, int64_t N0,
+                    int64_t K1, int64_t N1, int64_t K2, int64_t N2, const float* cs0,
+                    const float* cs1, const float* cs2, double al0, double al1, double al2,
+                    float* C, int64_t ldc, const int32_t* c_rowmap, int accumulate, void* stream);
+int kifmm_chain_f64(int64_t M, const double* A, int64_t lda, int asum, int64_t astride,
+                    const int32_t* a_child, int64_t child_w, int64_t a_nrhs, int nstage,
+                    const double* B0, const double* B1, const double* B2, int64_t K0, int64_t N0,
+                    int64_t K1, int64_t N1, int64_t K2, int64_t N2, const double* cs0,
+                    const double* cs1, const double* cs2, double al0, double al1, double al2,
+                    double* C, int64_t ldc, const int32_t* c_rowmap, int accumulate,
+                    void* stream);
+
 /* P2M check potentials (engine.py:298-319): for source leaf l and check point c,
  * phi[(l*nrhs + r)*nc + c] = sum_{j in leaf} K(center_l + base_c, s_j) q[j*nrhs + r];
  * centers (n_leaves, 3) and base (nc, 3) are float64, summed exactly then rounded. */

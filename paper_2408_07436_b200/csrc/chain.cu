@@ -1,0 +1,195 @@
+// Fused chains of small dense operators applied to a tile of rows:
+//
+//   Y0 = X . B0 (x cs0, x al0) ;  Y1 = Y0' . B1 (x cs1, x al1) ;  Y2 = Y1' . B2 ...
+//
+// where Ys' is Ys re-read as rows of width K(s+1) (K(s+1) divides N(s): the
+// L2L product (parent, 8 children x n_check) becomes 8 child rows of n_check).
+// Intermediates live in shared memory; only X is read and the last stage is
+// written (optionally accumulated, optionally through a destination row map).
+//
+// This covers every operator chain of the evaluate around the hot path:
+//   P2M solve       phi . U_up (x inv) . V_up^T (x side)       (expansion.py:78-82)
+//   M2M             stack(children) . M2M^T . U_up (x inv) . V_up^T   (engine.py:321-334)
+//   M2L epilogue    sum_splits(acc) . U^T (x 1/side) . U_dn (x inv) . V_dn^T (x side)
+//                   (m2l_blas.py:322 + engine.py:355)
+//   L2L             local . L2L^T -> per child . U_dn (x inv) . V_dn^T (x 0.5) -> scatter
+//                   (engine.py:358-374)
+// and keeps the reference's factored order (kernel product, then the solve).
+#include "common.cuh"
+
+using namespace kifmm;
+
+namespace {
+
+constexpr int NT = 256;
+
+struct ChainArgs {
+  int64_t M;                 // input rows
+  int bm;                    // input rows per CTA
+  int nstage;
+  int64_t lda;
+  int asum;
+  int64_t astride;
+  const int32_t* a_child;    // optional: row (p, r) = concat over children c of src row a_child[p*8+c]*R + r
+  int64_t child_rows_w;      // width of one child row when a_child is set
+  int64_t a_nrhs;            // R for the child-stack mode
+  int64_t per_row;           // widest per-input-row footprint over the stages
+  int64_t K[3], N[3];
+  const void* B[3];
+  const void* cs[3];
+  double al[3];
+  int64_t ldc;
+  const int32_t* c_rowmap;
+  int accumulate;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, ChainArgs a,
+                                                   T* __restrict__ C) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int64_t row0 = (int64_t)blockIdx.x * a.bm;
+  const int rows_in = (int)min64(a.bm, a.M - row0);
+  // ping-pong buffers sized by the host to hold the widest stage
+  T* buf0 = reinterpret_cast<T*>(smem_raw);
+  T* buf1 = buf0 + (int64_t)a.bm * a.per_row;
+
+  // load the X tile
+  const int64_t K0 = a.K[0];
+  for (int64_t e = tid; e < (int64_t)a.bm * K0; e += NT) {
+    const int m = (int)(e / K0);
+    const int64_t k = e - (int64_t)m * K0;
+    T v = T(0);
+    if (m < rows_in) {
+      const int64_t g = row0 + m;
+      if (a.a_child) {
+        const int c = (int)(k / a.child_rows_w);
+        const int64_t p = g / a.a_nrhs, r = g - p * a.a_nrhs;
+        const int32_t ch = a.a_child[p * 8 + c];
+        if (ch >= 0) v = A[((int64_t)ch * a.a_nrhs + r) * a.lda + (k - c * a.child_rows_w)];
+      } else {
+        const T* p = A + g * a.lda + k;
+        v = p[0];
+        for (int s = 1; s < a.asum; ++s) v += p[s * a.astride];
+      }
+    }
+    buf0[e] = v;
+  }
+  __syncthreads();
+
+  T* in = buf0;
+  T* outb = buf1;
+  int64_t nrows = a.bm;            // rows of the current stage input
+  int64_t expand = 1;              // output rows per input row of the chain
+  for (int s = 0; s < a.nstage; ++s) {
+    const int64_t K = a.K[s], N = a.N[s];
+    const T* B = reinterpret_cast<const T*>(a.B[s]);
+    const T* cs = reinterpret_cast<const T*>(a.cs[s]);
+    const T al = (T)a.al[s];
+    const bool last = s + 1 == a.nstage;
+    const int64_t live_rows = (int64_t)rows_in * expand;
+    for (int64_t e = tid; e < nrows * N; e += NT) {
+      const int64_t m = e / N, n = e - m * N;
+      if (last && m >= live_rows) continue;
+      const T* x = in + m * K;
+      T acc = T(0);
+#pragma unroll 4
+      for (int64_t k = 0; k < K; ++k) acc += x[k] * __ldg(&B[k * N + n]);
+      if (cs) acc *= __ldg(&cs[n]);
+      acc *= al;
+      if (!last) {
+        outb[e] = acc;
+      } else {
+        const int64_t gr = row0 * expand + m;
+        const int64_t dst = a.c_rowmap ? (int64_t)a.c_rowmap[gr] : gr;
+        if (dst >= 0) {
+          T* o = C + dst * a.ldc + n;
+          *o = a.accumulate ? *o + acc : acc;
+        }
+      }
+    }
+    if (!last) {
+      __syncthreads();
+      const int64_t total = nrows * N;
+      nrows = total / a.K[s + 1];
+      expand = nrows / a.bm;
+      T* t = in;
+      in = outb;
+      outb = t;
+    }
+  }
+}
+
+template <typename T>
+int chain(int64_t M, const T* A, int64_t lda, int asum, int64_t astride, const int32_t* a_child,
+          int64_t child_w, int64_t a_nrhs, int nstage, const T* B0, const T* B1, const T* B2, int64_t K0,
+          int64_t N0, int64_t K1, int64_t N1, int64_t K2, int64_t N2, const T* cs0, const T* cs1,
+          const T* cs2, double al0, double al1, double al2, T* C, int64_t ldc,
+          const int32_t* c_rowmap, int accumulate, void* stream) {
+  if (M < 0 || nstage < 1 || nstage > 3 || asum < 1 || K0 < 1 || N0 < 1) return KIFMM_EARG;
+  if (M == 0) return 0;
+  ChainArgs a{};
+  a.M = M;
+  a.nstage = nstage;
+  a.lda = lda;
+  a.asum = asum;
+  a.astride = astride;
+  a.a_child = a_child;
+  a.child_rows_w = child_w;
+  a.a_nrhs = a_nrhs < 1 ? 1 : a_nrhs;
+  a.K[0] = K0; a.N[0] = N0; a.K[1] = K1; a.N[1] = N1; a.K[2] = K2; a.N[2] = N2;
+  a.B[0] = B0; a.B[1] = B1; a.B[2] = B2;
+  a.cs[0] = cs0; a.cs[1] = cs1; a.cs[2] = cs2;
+  a.al[0] = al0; a.al[1] = al1; a.al[2] = al2;
+  a.ldc = ldc;
+  a.c_rowmap = c_rowmap;
+  a.accumulate = accumulate;
+  // widest per-input-row footprint over the stages
+  int64_t per_row = K0, width = 1;   // width = rows per input row at the current stage
+  for (int s = 0; s < nstage; ++s) {
+    if (a.K[s] < 1 || a.N[s] < 1) return KIFMM_EARG;
+    const int64_t w = width * a.N[s];
+    per_row = per_row > w ? per_row : w;
+    if (s + 1 < nstage) {
+      if (w % a.K[s + 1]) return KIFMM_EARG;
+      width = w / a.K[s + 1];
+    }
+  }
+  a.per_row = per_row;
+  int bm = 32;
+  while (bm > 1 && 2 * (size_t)bm * per_row * sizeof(T) > 200 * 1024) bm /= 2;
+  // keep >= 2 waves of CTAs on 148 SMs when rows are few
+  while (bm > 4 && (M + bm - 1) / bm < 2 * 148) bm /= 2;
+  a.bm = bm;
+  const size_t smem = 2 * (size_t)bm * per_row * sizeof(T);
+  cudaFuncSetAttribute(chain_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  chain_kernel<T><<<ceil_div(M, bm), NT, smem, (cudaStream_t)stream>>>(A, a, C);
+  return launch_status();
+}
+
+}  // namespace
+
+extern "C" {
+
+int kifmm_chain_f32(int64_t M, const float* A, int64_t lda, int asum, int64_t astride,
+                    const int32_t* a_child, int64_t child_w, int64_t a_nrhs, int nstage,
+                    const float* B0,
+                    const float* B1, const float* B2, int64_t K0, int64_t N0, int64_t K1,
+                    int64_t N1, int64_t K2, int64_t N2, const float* cs0, const float* cs1,
+                    const float* cs2, double al0, double al1, double al2, float* C, int64_t ldc,
+                    const int32_t* c_rowmap, int accumulate, void* s) {
+  return chain<float>(M, A, lda, asum, astride, a_child, child_w, a_nrhs, nstage, B0, B1, B2, K0, N0, K1,
+                      N1, K2, N2, cs0, cs1, cs2, al0, al1, al2, C, ldc, c_rowmap, accumulate, s);
+}
+int kifmm_chain_f64(int64_t M, const double* A, int64_t lda, int asum, int64_t astride,
+                    const int32_t* a_child, int64_t child_w, int64_t a_nrhs, int nstage,
+                    const double* B0,
+                    const double* B1, const double* B2, int64_t K0, int64_t N0, int64_t K1,
+                    int64_t N1, int64_t K2, int64_t N2, const double* cs0, const double* cs1,
+                    const double* cs2, double al0, double al1, double al2, double* C, int64_t ldc,
+                    const int32_t* c_rowmap, int accumulate, void* s) {
+  return chain<double>(M, A, lda, asum, astride, a_child, child_w, a_nrhs, nstage, B0, B1, B2, K0, N0, K1,
+                       N1, K2, N2, cs0, cs1, cs2, al0, al1, al2, C, ldc, c_rowmap, accumulate, s);
+}
+
+}  // extern "C"

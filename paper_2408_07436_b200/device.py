@@ -122,6 +122,24 @@ class Linalg:
                P(B), ldb, P(colscale), P(C), ldc, P(rowmap), int(bool(accumulate)),
                stream_handle())
 
+    def chain(self, M, A, lda, stages, C, ldc, rowmap=None, accumulate=False, asum=1,
+              astride=0, a_child=None, child_w=0, a_nrhs=1):
+        """Fused operator chain (csrc/chain.cu): stages = [(B, K, N, colscale, alpha), ...]."""
+        st = list(stages) + [(None, 0, 0, None, 1.0)] * (3 - len(stages))
+        launch(f"kifmm_chain_{self.sfx}", M, P(A), lda, int(asum), astride, P(a_child),
+               child_w, a_nrhs, len(stages), P(st[0][0]), P(st[1][0]), P(st[2][0]),
+               st[0][1], st[0][2], st[1][1], st[1][2], st[2][1], st[2][2],
+               P(st[0][3]), P(st[1][3]), P(st[2][3]), float(st[0][4]), float(st[1][4]),
+               float(st[2][4]), P(C), ldc, P(rowmap), int(bool(accumulate)), stream_handle())
+
+    @staticmethod
+    def solve_stages(inv, scale):
+        """The factored pseudo-inverse as two chain stages (expansion.py:78-82):
+        (x . U) * inv_vals, then . V^T * scale."""
+        u, vals, vt = inv
+        n_c, r = u.shape
+        return [(u, n_c, r, vals, 1.0), (vt, r, vt.shape[1], None, scale)]
+
     def solve(self, inv, phi, M, out, scale, tmp, accumulate=False, rowmap=None):
         """out[rowmap] (+)= scale * V diag(inv_vals) U^T phi^T, row form
         (reference expansion.py:78-82 applied through engine._solve_block)."""
@@ -256,7 +274,7 @@ class BlasDevice:
     def acc_elems(self, n_t, nrhs, n_tiles):
         return n_t * nrhs * sweep_splits(n_tiles, self.n_slabs) * self.ko_pad
 
-    def run_level(self, plan, mult, n_s, n_t, nrhs, level_scale, check, qt, acc):
+    def run_level(self, plan, mult, n_s, n_t, nrhs, level_scale, check, qt, acc, solve=None):
         la = self.la
         nsplit = sweep_splits(plan["n_tiles"], self.n_slabs)
         ld = nsplit * self.ko_pad
@@ -274,6 +292,15 @@ class BlasDevice:
             launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
                    P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
                    P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc), stream_handle())
+        if solve is not None:
+            # fused M2L epilogue: split-sum . U^T * level_scale, then the
+            # check->local solve, accumulated into the locals
+            inv, side, loc = solve
+            la.chain(n_t * nrhs, acc, ld,
+                     [(self.UT, self.k, self.n_c, None, level_scale)]
+                     + Linalg.solve_stages(inv, side), loc, inv[2].shape[1], accumulate=True,
+                     asum=nsplit, astride=self.ko_pad)
+            return 3
         la.gemm(n_t * nrhs, self.n_c, self.k, level_scale, acc, ld, self.UT, self.n_c, check,
                 self.n_c, asum=nsplit, astride=self.ko_pad)
         return 3
@@ -342,11 +369,11 @@ class DeviceFmm:
         self.blas = BlasDevice(ops, self.np_dtype, self.la)
         self.blas_plan_dev = {l: upload_blas_plan(p) for l, p in plans.items()}
 
-    def m2l_blas_level(self, lvl, mult, nrhs, check):
+    def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None):
         b = self._buffers(nrhs)
         return self.blas.run_level(self.blas_plan_dev[lvl], mult, self.n_src[lvl],
                                    self.n_tgt[lvl], nrhs, 1.0 / self.side[lvl], check, b["qt"],
-                                   b["acc"])
+                                   b["acc"], solve=solve)
 
     # ------------------------------------------------------------- FFT-M2L
     def _init_fft(self, ops, plans):
@@ -465,16 +492,16 @@ class DeviceFmm:
         launch(f"kifmm_p2m_check_{sfx}", P(self.sx), P(self.sy), P(self.sz), P(q), R,
                  P(self.s_start), P(self.s_count), nl, P(self.s_centers), P(self.check_base),
                  n_c, P(phi), s)
-        la.solve(self.up_inv, phi, nl * R, mult[d], self.side[d], tmp)
+        la.chain(nl * R, phi, n_c, Linalg.solve_stages(self.up_inv, self.side[d]), mult[d], n_e)
         phase("m2m")
-        # M2M down to level 2 (levels 0-1 carry no M2L).
+        # M2M down to level 2 (levels 0-1 carry no M2L): children stacked in
+        # the chain's loader, kernel product, then the up_inv solve.
         for lvl in range(d, 2, -1):
             n_par = self.n_src[lvl - 1]
-            st = b["stack"]
-            launch(f"kifmm_stack_children_{sfx}", P(mult[lvl]), P(self.src_child[lvl]), n_par,
-                     R, n_e, P(st), s)
-            la.gemm(n_par * R, n_c, 8 * n_e, 1.0, st, 8 * n_e, self.m2mT, n_c, phi, n_c)
-            la.solve(self.up_inv, phi, n_par * R, mult[lvl - 1], 1.0, tmp)
+            la.chain(n_par * R, mult[lvl], n_e,
+                     [(self.m2mT, 8 * n_e, n_c, None, 1.0)]
+                     + Linalg.solve_stages(self.up_inv, 1.0), mult[lvl - 1], n_e,
+                     a_child=self.src_child[lvl], child_w=n_e, a_nrhs=R)
         loc = b["loc"]
         for lvl in range(2, d + 1):
             loc[lvl].zero_()
@@ -484,17 +511,18 @@ class DeviceFmm:
             phase(f"m2l{lvl}")
             check = phi[: n_t * R * n_c]
             if self.cfg.backend == "blas":
-                calls.append(self.m2l_blas_level(lvl, mult[lvl], R, check))
+                calls.append(self.m2l_blas_level(
+                    lvl, mult[lvl], R, check, solve=(self.dn_inv, self.side[lvl], loc[lvl])))
             else:
                 calls.append(self.m2l_fft_level(lvl, mult[lvl], R, check))
-            la.solve(self.dn_inv, check, n_t * R, loc[lvl], self.side[lvl], tmp, accumulate=True)
+                la.chain(n_t * R, check, n_c, Linalg.solve_stages(self.dn_inv, self.side[lvl]),
+                         loc[lvl], n_e, accumulate=True)
             if lvl < d:
                 phase(f"l2l{lvl}")
-                n_par = n_t
-                la.gemm(n_par * R, 8 * n_c, n_e, 1.0, loc[lvl], n_e, self.l2lT, 8 * n_c, phi,
-                        8 * n_c)
-                la.solve(self.dn_inv, phi, n_par * R * 8, loc[lvl + 1], 0.5, tmp,
-                         accumulate=True, rowmap=self._l2l_rowmap(lvl + 1, R))
+                la.chain(n_t * R, loc[lvl], n_e,
+                         [(self.l2lT, n_e, 8 * n_c, None, 1.0)]
+                         + Linalg.solve_stages(self.dn_inv, 0.5), loc[lvl + 1], n_e,
+                         rowmap=self._l2l_rowmap(lvl + 1, R), accumulate=True)
         phase("leaf")
         out = b["out"]
         launch(f"kifmm_leaf_pass_{sfx}", P(self.tx), P(self.ty), P(self.tz), P(self.t_start),
