@@ -88,23 +88,60 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
     const T al = (T)a.al[s];
     const bool last = s + 1 == a.nstage;
     const int64_t live_rows = (int64_t)rows_in * expand;
-    for (int64_t e = tid; e < nrows * N; e += NT) {
-      const int64_t m = e / N, n = e - m * N;
-      if (last && m >= live_rows) continue;
-      const T* x = in + m * K;
-      T acc = T(0);
-#pragma unroll 4
-      for (int64_t k = 0; k < K; ++k) acc += x[k] * __ldg(&B[k * N + n]);
-      if (cs) acc *= __ldg(&cs[n]);
-      acc *= al;
-      if (!last) {
-        outb[e] = acc;
-      } else {
-        const int64_t gr = row0 * expand + m;
-        const int64_t dst = a.c_rowmap ? (int64_t)a.c_rowmap[gr] : gr;
-        if (dst >= 0) {
-          T* o = C + dst * a.ldc + n;
-          *o = a.accumulate ? *o + acc : acc;
+    // register tile: RR rows x RC consecutive columns per work item
+    constexpr int RR = 2, RC = 4;
+    const int64_t ncg = (N + RC - 1) / RC, nrg = (nrows + RR - 1) / RR;
+    const bool vec_b = (N % RC == 0) && (sizeof(T) == 4);
+    for (int64_t it = tid; it < ncg * nrg; it += NT) {
+      const int64_t rg = it / ncg, cg = it - rg * ncg;
+      const int64_t m0 = rg * RR, n0 = cg * RC;
+      if (last && m0 >= live_rows) continue;
+      T acc[RR][RC];
+#pragma unroll
+      for (int i = 0; i < RR; ++i)
+#pragma unroll
+        for (int j = 0; j < RC; ++j) acc[i][j] = T(0);
+      const T* x0 = in + m0 * K;
+      const T* x1 = in + (m0 + 1 < nrows ? m0 + 1 : m0) * K;
+#pragma unroll 2
+      for (int64_t k = 0; k < K; ++k) {
+        T b[RC];
+        const T* bp = B + k * N + n0;
+        if (vec_b) {
+          const float4 t4 = __ldg(reinterpret_cast<const float4*>(bp));
+          b[0] = t4.x; b[1] = t4.y; b[2] = t4.z; b[3] = t4.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < RC; ++j) b[j] = n0 + j < N ? __ldg(bp + j) : T(0);
+        }
+        const T xa = x0[k], xb = x1[k];
+#pragma unroll
+        for (int j = 0; j < RC; ++j) {
+          acc[0][j] += xa * b[j];
+          acc[1][j] += xb * b[j];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RR; ++i) {
+        const int64_t m = m0 + i;
+        if (m >= nrows || (last && m >= live_rows)) continue;
+#pragma unroll
+        for (int j = 0; j < RC; ++j) {
+          const int64_t n = n0 + j;
+          if (n >= N) continue;
+          T v = acc[i][j];
+          if (cs) v *= __ldg(&cs[n]);
+          v *= al;
+          if (!last) {
+            outb[m * N + n] = v;
+          } else {
+            const int64_t gr = row0 * expand + m;
+            const int64_t dst = a.c_rowmap ? (int64_t)a.c_rowmap[gr] : gr;
+            if (dst >= 0) {
+              T* o = C + dst * a.ldc + n;
+              *o = a.accumulate ? *o + v : v;
+            }
+          }
         }
       }
     }
