@@ -199,7 +199,7 @@ int chain(int64_t M, const T* A, int64_t lda, int asum, int64_t astride, const i
   while (bm > 4 && (M + bm - 1) / bm < 2 * 148) bm /= 2;
   a.bm = bm;
   const size_t smem = 2 * (size_t)bm * per_row * sizeof(T);
-  cudaFuncSetAttribute(chain_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_max_smem((const void*)chain_kernel<T>, smem);
   chain_kernel<T><<<ceil_div(M, bm), NT, smem, (cudaStream_t)stream>>>(A, a, C);
   return launch_status();
 }

@@ -188,7 +188,7 @@ int hadamard(const T* khat, const T* qhat, const int64_t* halo, T* phat, int64_t
   if (nf == 0 || ntc == 0) return 0;
   size_t smem = 26 * 64 * sizeof(C);
   auto kern = hadamard_kernel<T>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_max_smem((const void*)kern, smem);
   dim3 grid((unsigned)nf, ceil_div(ntc, kHadClusters));
   kern<<<grid, kHadThreads, smem, (cudaStream_t)stream>>>(
       reinterpret_cast<const C*>(khat), reinterpret_cast<const C*>(qhat), halo,

@@ -186,7 +186,7 @@ int sweep(const T* qt, const T* Dt, int64_t kin, int64_t ko_pad, const int32_t* 
   const int jper = (int)((189 + nsplit - 1) / nsplit);
   const size_t smem = sizeof(T) * (2 * TMT * (bk + VEC) + 2 * bk * kob);
   auto kern = m2l_sweep_kernel<T>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_max_smem((const void*)kern, smem);
   dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)(n_slabs * nsplit));
   kern<<<grid, threads, smem, (cudaStream_t)stream>>>(qt, Dt, (int)kin, (int)ko_pad, bk, nchunks,
                                                       kob, n_slabs, jper, tile_targets,

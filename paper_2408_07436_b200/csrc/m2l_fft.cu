@@ -260,7 +260,7 @@ int forward(const T* mult, int64_t nrhs, int64_t order, const int32_t* slot_box,
   if (!bpc) return KIFMM_EARG;
   size_t smem = forward_smem<T>(p, bpc);
   auto kern = fft_forward_kernel<T>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_max_smem((const void*)kern, smem);
   const int64_t nclusters = cluster_list ? n_list : nsc;
   if (nclusters <= 0) return 0;
   dim3 grid((unsigned)(nclusters * (8 / bpc)), (unsigned)nrhs);
@@ -280,7 +280,7 @@ int inverse(const T* phat, int64_t nrhs, int64_t order, const int32_t* slot_box,
   if (!bpc) return KIFMM_EARG;
   size_t smem = inverse_smem<T>(p, bpc);
   auto kern = fft_inverse_kernel<T>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_max_smem((const void*)kern, smem);
   dim3 grid((unsigned)(ntc * (8 / bpc)), (unsigned)nrhs);
   kern<<<grid, kThreads, smem, (cudaStream_t)stream>>>(reinterpret_cast<const C*>(phat), nrhs, p,
                                                        bpc, slot_box, ntc, (T)level_scale, check);

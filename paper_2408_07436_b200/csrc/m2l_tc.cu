@@ -389,7 +389,7 @@ int kifmm_m2l_sweep_tc_f32(const float* qhi, const float* qlo, const float* bhi,
   if (stages < 2) return KIFMM_EARG;
   const size_t smem = stages * stage_bytes + (2 * stages + 4) * 8 + 16;
   const int jper = (int)((189 + nsplit - 1) / nsplit);
-  cudaFuncSetAttribute(m2l_sweep_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_max_smem((const void*)m2l_sweep_tc_kernel, smem);
   dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)nsplit);
   m2l_sweep_tc_kernel<<<grid, NTHREADS, smem, (cudaStream_t)stream>>>(
       qhi, qlo, bhi, blo, (int)kin, (int)n_out, stages, tile_targets, tile_class, src, class_tv,

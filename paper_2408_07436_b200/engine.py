@@ -196,6 +196,9 @@ class FmmInstance:
     n_near_pairs: int = 0
     _last_charges: np.ndarray | None = None
     _device: object = None
+    # per-operator CUDA-event timings (operator_timings) cost an eager,
+    # un-graphed evaluate; off by default
+    profile: bool = False
 
     def evaluate(self, charges):
         return evaluate(self, charges)
@@ -276,8 +279,9 @@ def evaluate(inst: FmmInstance, charges) -> np.ndarray:
     q_in = np.asarray(charges)
     q = np.ascontiguousarray(as_charge_matrix(q_in, inst.source_tree.n_points), dtype=np.float64)
     inst._last_charges = q
-    out = inst.device.evaluate_host(q, timings=True)
-    inst.timings = dict(inst.device.last_timings)
+    out = inst.device.evaluate_host(q, timings=inst.profile)
+    if inst.profile:
+        inst.timings = dict(inst.device.last_timings)
     inst.m2l_calls = list(inst.device.last_m2l_calls)
     if q_in.ndim == 1 and q.shape[1] == 1:
         return out[:, 0]
