@@ -43,6 +43,10 @@ struct ChainArgs {
   int accumulate;
 };
 
+constexpr int RC = 4;          // consecutive output columns per work item
+constexpr int MAXIPT = 8;      // work items per thread
+constexpr int BS_BYTES = 48 * 1024;   // operator K-chunk staged in shared memory
+
 template <typename T>
 __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, ChainArgs a,
                                                    T* __restrict__ C) {
@@ -50,9 +54,9 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
   const int tid = threadIdx.x;
   const int64_t row0 = (int64_t)blockIdx.x * a.bm;
   const int rows_in = (int)min64(a.bm, a.M - row0);
-  // ping-pong buffers sized by the host to hold the widest stage
   T* buf0 = reinterpret_cast<T*>(smem_raw);
   T* buf1 = buf0 + (int64_t)a.bm * a.per_row;
+  T* Bs = buf1 + (int64_t)a.bm * a.per_row;
 
   // load the X tile
   const int64_t K0 = a.K[0];
@@ -75,7 +79,6 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
     }
     buf0[e] = v;
   }
-  __syncthreads();
 
   T* in = buf0;
   T* outb = buf1;
@@ -88,65 +91,68 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
     const T al = (T)a.al[s];
     const bool last = s + 1 == a.nstage;
     const int64_t live_rows = (int64_t)rows_in * expand;
-    // register tile: RR rows x RC consecutive columns per work item
-    constexpr int RR = 2, RC = 4;
-    const int64_t ncg = (N + RC - 1) / RC, nrg = (nrows + RR - 1) / RR;
-    const bool vec_b = (N % RC == 0) && (sizeof(T) == 4);
-    for (int64_t it = tid; it < ncg * nrg; it += NT) {
-      const int64_t rg = it / ncg, cg = it - rg * ncg;
-      const int64_t m0 = rg * RR, n0 = cg * RC;
-      if (last && m0 >= live_rows) continue;
-      T acc[RR][RC];
+    const int64_t ncg = (N + RC - 1) / RC;
+    const int64_t items = nrows * ncg;
+    const int64_t kch = (BS_BYTES / (int64_t)sizeof(T)) / N;   // operator rows per chunk
+    T acc[MAXIPT][RC];
 #pragma unroll
-      for (int i = 0; i < RR; ++i)
+    for (int i = 0; i < MAXIPT; ++i)
 #pragma unroll
-        for (int j = 0; j < RC; ++j) acc[i][j] = T(0);
-      const T* x0 = in + m0 * K;
-      const T* x1 = in + (m0 + 1 < nrows ? m0 + 1 : m0) * K;
-#pragma unroll 2
-      for (int64_t k = 0; k < K; ++k) {
-        T b[RC];
-        const T* bp = B + k * N + n0;
-        if (vec_b) {
-          const float4 t4 = __ldg(reinterpret_cast<const float4*>(bp));
-          b[0] = t4.x; b[1] = t4.y; b[2] = t4.z; b[3] = t4.w;
-        } else {
+      for (int j = 0; j < RC; ++j) acc[i][j] = T(0);
+    for (int64_t k0 = 0; k0 < K; k0 += kch) {
+      const int64_t kc = min64(kch, K - k0);
+      __syncthreads();                                 // previous chunk consumed / X ready
+      for (int64_t e = tid; e < kc * N; e += NT) Bs[e] = __ldg(&B[k0 * N + e]);
+      __syncthreads();
 #pragma unroll
-          for (int j = 0; j < RC; ++j) b[j] = n0 + j < N ? __ldg(bp + j) : T(0);
-        }
-        const T xa = x0[k], xb = x1[k];
+      for (int i = 0; i < MAXIPT; ++i) {
+        const int64_t it = tid + (int64_t)i * NT;
+        if (it >= items) break;
+        const int64_t m = it / ncg, n0 = (it - m * ncg) * RC;
+        const T* x = in + m * K + k0;
+        const T* bp = Bs + n0;
+        const bool full = n0 + RC <= N;
+        for (int64_t k = 0; k < kc; ++k) {
+          const T xv = x[k];
+          const T* br = bp + k * N;
+          if (full) {
 #pragma unroll
-        for (int j = 0; j < RC; ++j) {
-          acc[0][j] += xa * b[j];
-          acc[1][j] += xb * b[j];
+            for (int j = 0; j < RC; ++j) acc[i][j] += xv * br[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < RC; ++j)
+              if (n0 + j < N) acc[i][j] += xv * br[j];
+          }
         }
       }
+    }
+    // epilogue of the stage
 #pragma unroll
-      for (int i = 0; i < RR; ++i) {
-        const int64_t m = m0 + i;
-        if (m >= nrows || (last && m >= live_rows)) continue;
+    for (int i = 0; i < MAXIPT; ++i) {
+      const int64_t it = tid + (int64_t)i * NT;
+      if (it >= items) break;
+      const int64_t m = it / ncg, n0 = (it - m * ncg) * RC;
+      if (last && m >= live_rows) continue;
 #pragma unroll
-        for (int j = 0; j < RC; ++j) {
-          const int64_t n = n0 + j;
-          if (n >= N) continue;
-          T v = acc[i][j];
-          if (cs) v *= __ldg(&cs[n]);
-          v *= al;
-          if (!last) {
-            outb[m * N + n] = v;
-          } else {
-            const int64_t gr = row0 * expand + m;
-            const int64_t dst = a.c_rowmap ? (int64_t)a.c_rowmap[gr] : gr;
-            if (dst >= 0) {
-              T* o = C + dst * a.ldc + n;
-              *o = a.accumulate ? *o + v : v;
-            }
+      for (int j = 0; j < RC; ++j) {
+        const int64_t n = n0 + j;
+        if (n >= N) continue;
+        T v = acc[i][j];
+        if (cs) v *= __ldg(&cs[n]);
+        v *= al;
+        if (!last) {
+          outb[m * N + n] = v;
+        } else {
+          const int64_t gr = row0 * expand + m;
+          const int64_t dst = a.c_rowmap ? (int64_t)a.c_rowmap[gr] : gr;
+          if (dst >= 0) {
+            T* o = C + dst * a.ldc + n;
+            *o = a.accumulate ? *o + v : v;
           }
         }
       }
     }
     if (!last) {
-      __syncthreads();
       const int64_t total = nrows * N;
       nrows = total / a.K[s + 1];
       expand = nrows / a.bm;
@@ -193,12 +199,24 @@ int chain(int64_t M, const T* A, int64_t lda, int asum, int64_t astride, const i
     }
   }
   a.per_row = per_row;
-  int bm = 32;
-  while (bm > 1 && 2 * (size_t)bm * per_row * sizeof(T) > 200 * 1024) bm /= 2;
-  // keep >= 2 waves of CTAs on 148 SMs when rows are few
-  while (bm > 4 && (M + bm - 1) / bm < 2 * 148) bm /= 2;
+  // rows per CTA: <= MAXIPT*NT work items per stage, smem for the ping-pong
+  // tiles plus the operator chunk, and about one wave when rows are few
+  auto fits = [&](int bm_) {
+    int64_t rows_s = bm_;
+    for (int s = 0; s < nstage; ++s) {
+      if (rows_s * ((a.N[s] + RC - 1) / RC) > (int64_t)MAXIPT * NT) return false;
+      if (s + 1 < nstage) rows_s = rows_s * a.N[s] / a.K[s + 1];
+    }
+    return 2 * (size_t)bm_ * per_row * sizeof(T) + BS_BYTES <= 200 * 1024;
+  };
+  int bm = 128;
+  while (bm > 1 && !fits(bm)) bm /= 2;
+  while (bm > 8 && (M + bm - 1) / bm < 148) bm /= 2;
+  if (!fits(bm)) return KIFMM_EARG;
+  for (int s = 0; s < nstage; ++s)
+    if ((int64_t)(BS_BYTES / sizeof(T)) / a.N[s] < 1) return KIFMM_EARG;
   a.bm = bm;
-  const size_t smem = 2 * (size_t)bm * per_row * sizeof(T);
+  const size_t smem = 2 * (size_t)bm * per_row * sizeof(T) + BS_BYTES;
   set_max_smem((const void*)chain_kernel<T>, smem);
   chain_kernel<T><<<ceil_div(M, bm), NT, smem, (cudaStream_t)stream>>>(A, a, C);
   return launch_status();
