@@ -44,7 +44,8 @@ struct ChainArgs {
 };
 
 constexpr int RC = 4;          // consecutive output columns per work item
-constexpr int MAXIPT = 8;      // work items per thread
+constexpr int RR = 4;          // rows per work item
+constexpr int MAXIPT = 4;      // work items per thread
 constexpr int BS_BYTES = 48 * 1024;   // operator K-chunk staged in shared memory
 
 template <typename T>
@@ -92,13 +93,17 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
     const bool last = s + 1 == a.nstage;
     const int64_t live_rows = (int64_t)rows_in * expand;
     const int64_t ncg = (N + RC - 1) / RC;
-    const int64_t items = nrows * ncg;
+    const int64_t nrg = (nrows + RR - 1) / RR;
+    const int64_t items = nrg * ncg;
     const int64_t kch = (BS_BYTES / (int64_t)sizeof(T)) / N;   // operator rows per chunk
-    T acc[MAXIPT][RC];
+    const bool vec = (N % RC == 0) && sizeof(T) == 4;
+    T acc[MAXIPT][RR][RC];
 #pragma unroll
     for (int i = 0; i < MAXIPT; ++i)
 #pragma unroll
-      for (int j = 0; j < RC; ++j) acc[i][j] = T(0);
+      for (int r = 0; r < RR; ++r)
+#pragma unroll
+        for (int j = 0; j < RC; ++j) acc[i][r][j] = T(0);
     for (int64_t k0 = 0; k0 < K; k0 += kch) {
       const int64_t kc = min64(kch, K - k0);
       __syncthreads();                                 // previous chunk consumed / X ready
@@ -107,21 +112,29 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
 #pragma unroll
       for (int i = 0; i < MAXIPT; ++i) {
         const int64_t it = tid + (int64_t)i * NT;
-        if (it >= items) break;
-        const int64_t m = it / ncg, n0 = (it - m * ncg) * RC;
-        const T* x = in + m * K + k0;
-        const T* bp = Bs + n0;
-        const bool full = n0 + RC <= N;
-        for (int64_t k = 0; k < kc; ++k) {
-          const T xv = x[k];
-          const T* br = bp + k * N;
-          if (full) {
+        if (it < items) {
+          const int64_t rg = it / ncg, n0 = (it - rg * ncg) * RC;
+          const int64_t m0 = rg * RR;
+          const T* x[RR];
 #pragma unroll
-            for (int j = 0; j < RC; ++j) acc[i][j] += xv * br[j];
-          } else {
+          for (int r = 0; r < RR; ++r)
+            x[r] = in + (m0 + r < nrows ? m0 + r : m0) * K + k0;
+          const T* bp = Bs + n0;
+          for (int64_t k = 0; k < kc; ++k) {
+            T bv[RC];
+            if (vec) {
+              const float4 t4 = *reinterpret_cast<const float4*>(bp + k * N);
+              bv[0] = t4.x; bv[1] = t4.y; bv[2] = t4.z; bv[3] = t4.w;
+            } else {
 #pragma unroll
-            for (int j = 0; j < RC; ++j)
-              if (n0 + j < N) acc[i][j] += xv * br[j];
+              for (int j = 0; j < RC; ++j) bv[j] = n0 + j < N ? bp[k * N + j] : T(0);
+            }
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+              const T xv = x[r][k];
+#pragma unroll
+              for (int j = 0; j < RC; ++j) acc[i][r][j] += xv * bv[j];
+            }
           }
         }
       }
@@ -130,24 +143,28 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
 #pragma unroll
     for (int i = 0; i < MAXIPT; ++i) {
       const int64_t it = tid + (int64_t)i * NT;
-      if (it >= items) break;
-      const int64_t m = it / ncg, n0 = (it - m * ncg) * RC;
-      if (last && m >= live_rows) continue;
+      if (it >= items) continue;
+      const int64_t rg = it / ncg, n0 = (it - rg * ncg) * RC;
 #pragma unroll
-      for (int j = 0; j < RC; ++j) {
-        const int64_t n = n0 + j;
-        if (n >= N) continue;
-        T v = acc[i][j];
-        if (cs) v *= __ldg(&cs[n]);
-        v *= al;
-        if (!last) {
-          outb[m * N + n] = v;
-        } else {
-          const int64_t gr = row0 * expand + m;
-          const int64_t dst = a.c_rowmap ? (int64_t)a.c_rowmap[gr] : gr;
-          if (dst >= 0) {
-            T* o = C + dst * a.ldc + n;
-            *o = a.accumulate ? *o + v : v;
+      for (int r = 0; r < RR; ++r) {
+        const int64_t m = rg * RR + r;
+        if (m >= nrows || (last && m >= live_rows)) continue;
+#pragma unroll
+        for (int j = 0; j < RC; ++j) {
+          const int64_t n = n0 + j;
+          if (n >= N) continue;
+          T v = acc[i][r][j];
+          if (cs) v *= __ldg(&cs[n]);
+          v *= al;
+          if (!last) {
+            outb[m * N + n] = v;
+          } else {
+            const int64_t gr = row0 * expand + m;
+            const int64_t dst = a.c_rowmap ? (int64_t)a.c_rowmap[gr] : gr;
+            if (dst >= 0) {
+              T* o = C + dst * a.ldc + n;
+              *o = a.accumulate ? *o + v : v;
+            }
           }
         }
       }
@@ -204,7 +221,8 @@ int chain(int64_t M, const T* A, int64_t lda, int asum, int64_t astride, const i
   auto fits = [&](int bm_) {
     int64_t rows_s = bm_;
     for (int s = 0; s < nstage; ++s) {
-      if (rows_s * ((a.N[s] + RC - 1) / RC) > (int64_t)MAXIPT * NT) return false;
+      if (((rows_s + RR - 1) / RR) * ((a.N[s] + RC - 1) / RC) > (int64_t)MAXIPT * NT)
+        return false;
       if (s + 1 < nstage) rows_s = rows_s * a.N[s] / a.K[s + 1];
     }
     return 2 * (size_t)bm_ * per_row * sizeof(T) + BS_BYTES <= 200 * 1024;
