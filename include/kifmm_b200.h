@@ -151,6 +151,23 @@ int kifmm_m2l_sweep_tc_f32(const float* qhi, const float* qlo, const float* bhi,
                            const int32_t* tile_class, const int32_t* src, const int32_t* class_tv,
                            int64_t n_tiles, int64_t nrhs, int64_t nsplit, float* acc, void* stream);
 
+/* TMA-fed variant for the engine (csrc/m2l_tma.cu): q~ hi/lo live in dense
+ * parity sub-lattice arrays (8*nrhs, h, h, h, kin) (kifmm_dense_split_tf32);
+ * tile_ids (n_tiles) select class tiles of 4x4x8 same-parity targets
+ * (class-major, then x, y, z tile index), tile_targets (n_tiles*128) map each
+ * tile row (x*32 + y*8 + z) to a target row or -1; offsets (316, 3) int8 are
+ * the transfer vectors.  kin % 8 == 0 and kin <= 128. */
+int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi, const float* blo,
+                            int64_t kin, int64_t n_out, int64_t h, const int32_t* tile_targets,
+                            const int32_t* tile_ids, int64_t n_tiles, const int32_t* class_tv,
+                            const int8_t* offsets, int64_t nrhs, int64_t nsplit, float* acc,
+                            void* stream);
+
+/* q~ rows (n_boxes*nrhs, kin) -> TF32 hi/lo parts scattered into the dense
+ * sub-lattice arrays at slot[box] = parity*h^3 + (ix*h + iy)*h + iz. */
+int kifmm_dense_split_tf32(const float* qt, const int32_t* slot, int64_t n_boxes, int64_t nrhs,
+                           int64_t kin, int64_t h, float* hi, float* lo, void* stream);
+
 /* x = hi + lo with hi, lo TF32 (cvt.rna.tf32.f32), elementwise. */
 int kifmm_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stream);
 

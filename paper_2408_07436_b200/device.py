@@ -195,6 +195,30 @@ def pack_tc_cores(cores: np.ndarray, kin: int, n_out: int, kc_max: int = 32) -> 
     return np.ascontiguousarray(np.concatenate(blocks, axis=1))
 
 
+def tma_level_plan(src_codes, tgt_codes, level):
+    """Plan of the TMA-fed tcgen05 sweep (csrc/m2l_tma.cu) for one level:
+    class tiles of 4 x 4 x 8 same-parity targets, the target row of every
+    tile slot, and the dense sub-lattice slot of every source box."""
+    from .octree import decode_codes
+    h = 1 << (level - 1)
+    tx, ty, tz = -(-h // 4), -(-h // 4), -(-h // 8)
+    ta, _ = decode_codes(tgt_codes)
+    cls = ((ta[:, 0] & 1) << 2) | ((ta[:, 1] & 1) << 1) | (ta[:, 2] & 1)
+    i = ta >> 1
+    tile = cls * (tx * ty * tz) + ((i[:, 0] // 4) * ty + i[:, 1] // 4) * tz + i[:, 2] // 8
+    row = ((i[:, 0] % 4) * 4 + i[:, 1] % 4) * 8 + i[:, 2] % 8
+    tile_ids = np.unique(tile)
+    slot = np.searchsorted(tile_ids, tile)
+    tile_targets = np.full(tile_ids.shape[0] * 128, -1, dtype=np.int32)
+    tile_targets[slot * 128 + row] = np.arange(tgt_codes.shape[0])
+    sa, _ = decode_codes(src_codes)
+    sp = ((sa[:, 0] & 1) << 2) | ((sa[:, 1] & 1) << 1) | (sa[:, 2] & 1)
+    si = sa >> 1
+    src_slot = sp * h ** 3 + (si[:, 0] * h + si[:, 1]) * h + si[:, 2]
+    return dict(h=h, n_tiles=int(tile_ids.shape[0]), tile_ids=to_dev(tile_ids, np.int32),
+                tile_targets=to_dev(tile_targets, np.int32), src_slot=to_dev(src_slot, np.int32))
+
+
 class BlasDevice:
     """Device copies of the compressed M2L operators and the level apply:
     projection q~ = M S, fused target-stationary sweep, expansion
@@ -210,7 +234,7 @@ class BlasDevice:
             tensor_cores = os.environ.get("KIFMM_SWEEP", "tc") != "simt"
         # float32: tcgen05 3xTF32 sweep (csrc/m2l_tc.cu); float64: FP64 SIMT sweep.
         # (3 TMEM accumulators of n_out <= 160 columns fit the 512-column TMEM)
-        self.tc = bool(tensor_cores) and dt == np.float32 and k <= 160
+        self.tc = bool(tensor_cores) and dt == np.float32 and k <= 160 and -(-k // 8) * 8 <= 128
         if self.tc:
             self.kin = -(-k // 8) * 8
             self.ko_pad = -(-k // 16) * 16
@@ -224,6 +248,8 @@ class BlasDevice:
             self.S = to_dev(s_pad)
             self.UT = to_dev(np.ascontiguousarray(ops.u.T), dt)
             self.class_tv = to_dev(class_transfer_table(), np.int32)
+            from .octree import transfer_offsets
+            self.offsets = to_dev(transfer_offsets(), np.int8)
             return
         self.kin, self.ko_pad = blas_geometry(k, dt.itemsize)
         self.n_slabs = -(-k // 128)
@@ -270,6 +296,27 @@ class BlasDevice:
                 self.UT, self.n_c, _Off(check, lo * nrhs * self.n_c), self.n_c, asum=nsplit,
                 astride=self.ko_pad)
         return 3
+
+    def run_level_tma(self, plan, mult, n_s, n_t, nrhs, level_scale, qt, dense, acc, solve):
+        """Engine path for float32: projection -> dense hi/lo sub-lattice
+        arrays -> TMA-fed tcgen05 sweep -> fused epilogue into the locals."""
+        la = self.la
+        nsplit = sweep_splits(plan["n_tiles"], 1)
+        ld = nsplit * self.ko_pad
+        la.gemm(n_s * nrhs, self.k, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
+        hi, lo = dense
+        launch("kifmm_dense_split_tf32", P(qt), P(plan["src_slot"]), n_s, nrhs, self.kin,
+               plan["h"], P(hi), P(lo), stream_handle())
+        launch("kifmm_m2l_sweep_tma_f32", P(hi), P(lo), P(self.Bhi), P(self.Blo), self.kin,
+               self.ko_pad, plan["h"], P(plan["tile_targets"]), P(plan["tile_ids"]),
+               plan["n_tiles"], P(self.class_tv), P(self.offsets), nrhs, nsplit, P(acc),
+               stream_handle())
+        inv, side, loc = solve
+        la.chain(n_t * nrhs, acc, ld,
+                 [(self.UT, self.k, self.n_c, None, level_scale)]
+                 + Linalg.solve_stages(inv, side), loc, inv[2].shape[1], accumulate=True,
+                 asum=nsplit, astride=self.ko_pad)
+        return 4
 
     def acc_elems(self, n_t, nrhs, n_tiles):
         return n_t * nrhs * sweep_splits(n_tiles, self.n_slabs) * self.ko_pad
@@ -366,11 +413,23 @@ class DeviceFmm:
 
     # ------------------------------------------------------------ BLAS-M2L
     def _init_blas(self, ops, plans):
+        import os
         self.blas = BlasDevice(ops, self.np_dtype, self.la)
         self.blas_plan_dev = {l: upload_blas_plan(p) for l, p in plans.items()}
+        # float32 engine path: TMA-fed sweep on dense sub-lattice arrays
+        self.tma = self.blas.tc and os.environ.get("KIFMM_SWEEP", "tma") == "tma"
+        if self.tma:
+            st, tt = self.inst.source_tree, self.inst.target_tree
+            self.tma_plan = {l: tma_level_plan(st.level_keys(l), tt.level_keys(l), l)
+                             for l in plans}
 
     def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None):
         b = self._buffers(nrhs)
+        if self.tma and solve is not None:
+            plan = self.tma_plan[lvl]
+            return self.blas.run_level_tma(plan, mult, self.n_src[lvl], self.n_tgt[lvl], nrhs,
+                                           1.0 / self.side[lvl], b["qt"], b["dense"][lvl],
+                                           b["acc"], solve)
         return self.blas.run_level(self.blas_plan_dev[lvl], mult, self.n_src[lvl],
                                    self.n_tgt[lvl], nrhs, 1.0 / self.side[lvl], check, b["qt"],
                                    b["acc"], solve=solve)
@@ -437,6 +496,13 @@ class DeviceFmm:
             b["acc"] = torch.zeros(max(self.blas.acc_elems(self.n_tgt[l], R, p["n_tiles"])
                                        for l, p in self.blas_plan_dev.items()), dtype=T,
                                    device=dev)
+            if self.tma:
+                b["acc"] = torch.zeros(max(b["acc"].numel(), max(
+                    self.blas.acc_elems(self.n_tgt[l], R, p["n_tiles"])
+                    for l, p in self.tma_plan.items())), dtype=T, device=dev)
+                b["dense"] = {l: tuple(torch.zeros(8 * R * p["h"] ** 3 * self.blas.kin, dtype=T,
+                                                   device=dev) for _ in range(2))
+                              for l, p in self.tma_plan.items()}
         else:
             nsc = max(p["nsc"] for p in self.fft_plan_dev.values())
             ntc = max(p["ntc"] for p in self.fft_plan_dev.values())
