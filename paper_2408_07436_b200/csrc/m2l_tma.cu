@@ -401,7 +401,7 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
     const char* e = getenv("KIFMM_TMA_STAGES");
     max_stages = e ? atoi(e) : 4;
     const char* f = getenv("KIFMM_TMA_CTAS");
-    ctas = f ? atoi(f) : 1;
+    ctas = f ? atoi(f) : 2;
     if (ctas < 1) ctas = 1;
   }
   int stages = (int)(((200 * 1024) / ctas) / stage_bytes);
