@@ -66,6 +66,26 @@ int kifmm_hadamard_m2l_c128(const double* khat, const double* qhat, const int64_
                             double* phat, int64_t nf, int64_t nsc, int64_t ntc, int64_t nrhs,
                             void* stream);
 
+/* The same product over a tile plan of the halo table (m2l_fft.py
+ * plan_hadamard_tiles): tile t owns target clusters [tile_begin[t],
+ * tile_begin[t+1]); tcol (n_tiles, 256) int16 = tile-local target of each
+ * slot-table column (-1 = empty; column 32w + 4g + j holds a target of
+ * coordinate parity class g); src[src_off[t] .. src_off[t+1]) = source
+ * cluster of each shared-memory slot (at most 600, -1 = hole, slot % 8 =
+ * the source's parity class); slots (n_tiles, 26, 256) int16 = slot of
+ * (offset, column), 600 + class = absent.  Each frequency's sources are
+ * staged once per tile.  accumulate = 0 stores (phat need not be zeroed),
+ * 1 adds. */
+int kifmm_hadamard_tiled_c64(const float* khat, const float* qhat, const int64_t* tile_begin,
+                             const int64_t* src_off, const int64_t* src, const int16_t* slots,
+                             const int16_t* tcol, int64_t n_tiles, int64_t nf, int64_t nsc,
+                             int64_t ntc, int64_t nrhs, int accumulate, float* phat, void* stream);
+int kifmm_hadamard_tiled_c128(const double* khat, const double* qhat, const int64_t* tile_begin,
+                              const int64_t* src_off, const int64_t* src, const int16_t* slots,
+                              const int16_t* tcol, int64_t n_tiles, int64_t nf, int64_t nsc,
+                              int64_t ntc, int64_t nrhs, int accumulate, double* phat,
+                              void* stream);
+
 /* ---- (2) engine passes (device-resident evaluate) ------------------------ */
 
 /* Row-major C[rowmap(m), n] (=|+=) alpha * sum_k A'[m, k] B[k, n] * colscale[n],

@@ -30,6 +30,8 @@ SIGNATURES = {
     "kifmm_p2p_blocked_f64": [_P, _P, _P, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P],
     "kifmm_hadamard_m2l_c64": [_P, _P, _P, _P, _I, _I, _I, _I, _P],
     "kifmm_hadamard_m2l_c128": [_P, _P, _P, _P, _I, _I, _I, _I, _P],
+    "kifmm_hadamard_tiled_c64": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _C, _P, _P],
+    "kifmm_hadamard_tiled_c128": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _C, _P, _P],
     "kifmm_gemm_f32": [_I, _I, _I, _F, _P, _I, _C, _I, _P, _I, _P, _P, _I, _P, _C, _P],
     "kifmm_gemm_f64": [_I, _I, _I, _D, _P, _I, _C, _I, _P, _I, _P, _P, _I, _P, _C, _P],
     "kifmm_p2m_check_f32": [_P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _P, _P],

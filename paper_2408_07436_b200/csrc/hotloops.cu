@@ -5,8 +5,7 @@
 //  * K(t, s) = (1/4pi)/|t - s|, zero when r2 == 0 (_hot.pyx:44-50);
 //  * outputs accumulate (+=), laplace_matrix overwrites (_hot.pyx:68-88);
 //  * per-target summation follows the source order (_hot.pyx:30-32);
-//  * hadamard: phat[f,c,tau,r] += sum_o sum_sigma khat[f,o,tau,sigma] qhat[f,halo[c,o],sigma,r]
-//    with halo < 0 skipped (_hot.pyx:141-178).
+//  * the fourth loop, hadamard_m2l (_hot.pyx:141-178), lives in hadamard.cu.
 #include "common.cuh"
 
 using namespace kifmm;
@@ -95,60 +94,6 @@ __global__ void p2p_csr_kernel(const T* __restrict__ tx, const T* __restrict__ t
   }
 }
 
-template <typename T> struct cplx;
-template <> struct cplx<float> { using v = float2; };
-template <> struct cplx<double> { using v = double2; };
-
-// Hadamard block MAC.  One CTA per (frequency, chunk of target clusters);
-// khat[f] is staged once in shared memory as [o][sigma][tau] so the 8
-// tau-threads of a cluster read consecutive entries.
-constexpr int kHadThreads = 256;
-constexpr int kHadClusters = 256;   // target clusters per CTA
-
-template <typename T>
-__global__ void __launch_bounds__(kHadThreads) hadamard_kernel(
-    const typename cplx<T>::v* __restrict__ khat, const typename cplx<T>::v* __restrict__ qhat,
-    const int64_t* __restrict__ halo, typename cplx<T>::v* __restrict__ phat, int64_t nsc,
-    int64_t ntc, int64_t nrhs) {
-  using C = typename cplx<T>::v;
-  extern __shared__ unsigned char smem_raw[];
-  C* ks = reinterpret_cast<C*>(smem_raw);       // [26][8 sigma][8 tau]
-  const int64_t f = blockIdx.x;
-  const C* kf = khat + f * (26 * 64);
-  for (int e = threadIdx.x; e < 26 * 64; e += kHadThreads) {
-    int o = e >> 6, tau = (e >> 3) & 7, sig = e & 7;
-    ks[(o * 8 + sig) * 8 + tau] = kf[e];
-  }
-  __syncthreads();
-  const int tau = threadIdx.x & 7;
-  const int64_t c_begin = (int64_t)blockIdx.y * kHadClusters;
-  const int64_t c_end = min64(ntc, c_begin + kHadClusters);
-  const C* qf = qhat + f * nsc * 8 * nrhs;
-  C* pf = phat + f * ntc * 8 * nrhs;
-  for (int64_t c = c_begin + (threadIdx.x >> 3); c < c_end; c += kHadThreads / 8) {
-    for (int64_t r = 0; r < nrhs; ++r) {
-      T re = 0, im = 0;
-      for (int o = 0; o < 26; ++o) {
-        int64_t s = __ldg(&halo[c * 26 + o]);
-        if (s < 0) continue;
-        const C* qs = qf + s * 8 * nrhs + r;
-#pragma unroll
-        for (int sig = 0; sig < 8; ++sig) {
-          C k = ks[(o * 8 + sig) * 8 + tau];
-          C v = qs[sig * nrhs];
-          re += k.x * v.x - k.y * v.y;
-          im += k.x * v.y + k.y * v.x;
-        }
-      }
-      C* p = pf + (c * 8 + tau) * nrhs + r;
-      C old = *p;
-      old.x += re;
-      old.y += im;
-      *p = old;
-    }
-  }
-}
-
 template <typename T>
 int potentials(const T* tx, const T* ty, const T* tz, int64_t nt, const T* sx, const T* sy,
                const T* sz, int64_t ns, const T* q, int64_t nrhs, T* out, void* stream) {
@@ -177,22 +122,6 @@ int p2p(const T* tx, const T* ty, const T* tz, int64_t nt, const int64_t* lot, c
   if (nt == 0) return 0;
   p2p_csr_kernel<T><<<ceil_div(nt, 128), 128, 0, (cudaStream_t)stream>>>(tx, ty, tz, nt, lot, sx,
                                                                          sy, sz, q, nrhs, off, out);
-  return launch_status();
-}
-
-template <typename T>
-int hadamard(const T* khat, const T* qhat, const int64_t* halo, T* phat, int64_t nf, int64_t nsc,
-             int64_t ntc, int64_t nrhs, void* stream) {
-  using C = typename cplx<T>::v;
-  if (nf < 0 || nsc < 0 || ntc < 0 || nrhs < 1) return KIFMM_EARG;
-  if (nf == 0 || ntc == 0) return 0;
-  size_t smem = 26 * 64 * sizeof(C);
-  auto kern = hadamard_kernel<T>;
-  set_max_smem((const void*)kern, smem);
-  dim3 grid((unsigned)nf, ceil_div(ntc, kHadClusters));
-  kern<<<grid, kHadThreads, smem, (cudaStream_t)stream>>>(
-      reinterpret_cast<const C*>(khat), reinterpret_cast<const C*>(qhat), halo,
-      reinterpret_cast<C*>(phat), nsc, ntc, nrhs);
   return launch_status();
 }
 
@@ -231,15 +160,6 @@ int kifmm_p2p_blocked_f64(const double* tx, const double* ty, const double* tz, 
                           const double* q, int64_t nrhs, const int64_t* off, int64_t nl,
                           double* out, void* s) {
   return p2p<double>(tx, ty, tz, nt, lot, sx, sy, sz, q, nrhs, off, nl, out, s);
-}
-int kifmm_hadamard_m2l_c64(const float* khat, const float* qhat, const int64_t* halo, float* phat,
-                           int64_t nf, int64_t nsc, int64_t ntc, int64_t nrhs, void* s) {
-  return hadamard<float>(khat, qhat, halo, phat, nf, nsc, ntc, nrhs, s);
-}
-int kifmm_hadamard_m2l_c128(const double* khat, const double* qhat, const int64_t* halo,
-                            double* phat, int64_t nf, int64_t nsc, int64_t ntc, int64_t nrhs,
-                            void* s) {
-  return hadamard<double>(khat, qhat, halo, phat, nf, nsc, ntc, nrhs, s);
 }
 int kifmm_sm_target(void) { return 100; }
 

@@ -122,15 +122,57 @@ class Linalg:
                P(B), ldb, P(colscale), P(C), ldc, P(rowmap), int(bool(accumulate)),
                stream_handle())
 
+    # widest operator (elements) the fused chain kernel handles well; wider
+    # chains (p >= 6 in float64) run as tiled GEMM stages instead
+    CHAIN_MAX_N = 256
+
     def chain(self, M, A, lda, stages, C, ldc, rowmap=None, accumulate=False, asum=1,
               astride=0, a_child=None, child_w=0, a_nrhs=1):
         """Fused operator chain (csrc/chain.cu): stages = [(B, K, N, colscale, alpha), ...]."""
+        if max(s[2] for s in stages) > self.CHAIN_MAX_N or max(s[1] for s in stages) > 512:
+            return self._chain_gemms(M, A, lda, stages, C, ldc, rowmap, accumulate, asum,
+                                     astride, a_child, child_w, a_nrhs)
         st = list(stages) + [(None, 0, 0, None, 1.0)] * (3 - len(stages))
         launch(f"kifmm_chain_{self.sfx}", M, P(A), lda, int(asum), astride, P(a_child),
                child_w, a_nrhs, len(stages), P(st[0][0]), P(st[1][0]), P(st[2][0]),
                st[0][1], st[0][2], st[1][1], st[1][2], st[2][1], st[2][2],
                P(st[0][3]), P(st[1][3]), P(st[2][3]), float(st[0][4]), float(st[1][4]),
                float(st[2][4]), P(C), ldc, P(rowmap), int(bool(accumulate)), stream_handle())
+
+    def _chain_gemms(self, M, A, lda, stages, C, ldc, rowmap, accumulate, asum, astride,
+                     a_child, child_w, a_nrhs):
+        """Same chain as sequential tiled GEMMs through scratch buffers."""
+        T = torch.float32 if self.sfx == "f32" else torch.float64
+        dev = torch.device("cuda", torch.cuda.current_device())
+        if a_child is not None:
+            n_par = M // a_nrhs
+            x = self.scratch(0, M * 8 * child_w, T, dev)
+            launch(f"kifmm_stack_children_{self.sfx}", P(A), P(a_child), n_par, a_nrhs, child_w,
+                   P(x), stream_handle())
+            A, lda, asum = x, 8 * child_w, 1
+        rows = M
+        for i, (B, K, N, cs, al) in enumerate(stages):
+            last = i + 1 == len(stages)
+            if last:
+                self.gemm(rows, N, K, al, A, lda, B, N, C, ldc, colscale=cs, rowmap=rowmap,
+                          accumulate=accumulate, asum=asum, astride=astride)
+            else:
+                y = self.scratch(1 + (i & 1), rows * N, T, dev)
+                self.gemm(rows, N, K, al, A, lda, B, N, y, N, colscale=cs, asum=asum,
+                          astride=astride)
+                rows = rows * N // stages[i + 1][1]
+                A, lda, asum, astride = y, stages[i + 1][1], 1, 0
+
+    def scratch(self, slot, n, T, dev):
+        """Grow-only scratch buffers (allocated outside graph capture on the
+        eager warm-up pass, reused afterwards)."""
+        if not hasattr(self, "_scratch"):
+            self._scratch = {}
+        t = self._scratch.get(slot)
+        if t is None or t.numel() < n or t.dtype != T:
+            t = torch.empty(n, dtype=T, device=dev)
+            self._scratch[slot] = t
+        return t
 
     @staticmethod
     def solve_stages(inv, scale):
@@ -448,7 +490,8 @@ class DeviceFmm:
             tbox[p.tgt_slot] = np.arange(p.tgt_slot.shape[0])
             self.fft_plan_dev[l] = dict(nsc=p.n_src_clusters, ntc=p.n_tgt_clusters,
                                         sbox=to_dev(sbox), tbox=to_dev(tbox),
-                                        halo=to_dev(p.halo, np.int64))
+                                        halo=to_dev(p.halo, np.int64),
+                                        tiles=upload_hadamard_tiles(p.halo, p.src_color, p.tgt_color))
 
     def m2l_fft_level(self, lvl, mult, nrhs, check, plan=None):
         plan = plan if plan is not None else self.fft_plan_dev[lvl]
@@ -459,10 +502,8 @@ class DeviceFmm:
         s = stream_handle()
         launch(f"kifmm_fft_forward_{self.sfx}", P(mult), nrhs, self.order, P(plan["sbox"]), nsc,
                None, 0, P(qhat), s)
-        phat.zero_()
-        cname = "c64" if self.sfx == "f32" else "c128"
-        launch(f"kifmm_hadamard_m2l_{cname}", P(self.khat), P(qhat), P(plan["halo"]), P(phat),
-                 self.n_freq, nsc, ntc, nrhs, s)
+        hadamard_tiled(self.sfx, self.khat, qhat, plan["tiles"], self.n_freq, nsc, ntc, nrhs,
+                       phat, s)
         launch(f"kifmm_fft_inverse_{self.sfx}", P(phat), nrhs, self.order, P(plan["tbox"]), ntc,
                  1.0 / self.side[lvl], P(check), s)
         return 4
@@ -689,6 +730,25 @@ def apply_level_host(ops, buckets, multipoles, n_targets, level_scale, counter=N
     return check[: n_targets * nrhs * bd.n_c].cpu().numpy().reshape(n_targets, nrhs, bd.n_c)
 
 
+def upload_hadamard_tiles(halo_rows, src_color, tgt_color):
+    """Device copy of plan_hadamard_tiles (the tiled Hadamard's plan)."""
+    from .m2l_fft import plan_hadamard_tiles
+    t = plan_hadamard_tiles(halo_rows, src_color, tgt_color)
+    return dict(n_tiles=t.n_tiles, begin=to_dev(t.begin), src_off=to_dev(t.src_off),
+                src=to_dev(t.src if t.src.size else np.zeros(1, np.int64)),
+                slots=to_dev(t.slots if t.slots.size else np.zeros(1, np.int16)),
+                tcol=to_dev(t.tcol if t.tcol.size else np.zeros(1, np.int16)))
+
+
+def hadamard_tiled(sfx, khat, qhat, tiles, nf, nsc, ntc, nrhs, phat, stream, accumulate=0):
+    """phat (=|+=) Hadamard M2L over a tile plan (csrc/hadamard.cu)."""
+    cname = "c64" if sfx == "f32" else "c128"
+    launch(f"kifmm_hadamard_tiled_{cname}", P(khat), P(qhat), P(tiles["begin"]),
+           P(tiles["src_off"]), P(tiles["src"]), P(tiles["slots"]), P(tiles["tcol"]),
+           tiles["n_tiles"], nf, nsc,
+           ntc, nrhs, accumulate, P(phat), stream)
+
+
 def m2l_fft_level_host(ops, plan, mult, level_scale):
     """Level-boundary drop-in for reference ``m2l_fft.m2l_fft_level``."""
     require_cuda()
@@ -712,11 +772,10 @@ def m2l_fft_level_host(ops, plan, mult, level_scale):
     check = torch.zeros(max(n_tgt, 1) * nrhs * n_e, dtype=T, device=dev)
     s = stream_handle()
     m = to_dev(mult)
-    keep = [to_dev(sbox), to_dev(plan.halo, np.int64), to_dev(tbox)]
+    keep = [to_dev(sbox), upload_hadamard_tiles(plan.halo, plan.src_color, plan.tgt_color),
+            to_dev(tbox)]
     launch(f"kifmm_fft_forward_{sfx}", P(m), nrhs, ops.order, P(keep[0]), nsc, None, 0, P(qhat), s)
-    cname = "c64" if sfx == "f32" else "c128"
-    launch(f"kifmm_hadamard_m2l_{cname}", P(khat), P(qhat), P(keep[1]), P(phat), nf, nsc, ntc,
-           nrhs, s)
+    hadamard_tiled(sfx, khat, qhat, keep[1], nf, nsc, ntc, nrhs, phat, s)
     launch(f"kifmm_fft_inverse_{sfx}", P(phat), nrhs, ops.order, P(keep[2]), ntc,
            float(level_scale), P(check), s)
     return check[: n_tgt * nrhs * n_e].cpu().numpy().reshape(n_tgt, nrhs, n_e)

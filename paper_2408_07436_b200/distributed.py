@@ -214,7 +214,7 @@ class DistributedFmm:
     def __init__(self, inst, rank_plan: RankPlan, device_fmm=None):
         import torch
 
-        from .device import DeviceFmm, to_dev, upload_blas_plan
+        from .device import DeviceFmm, to_dev, upload_blas_plan, upload_hadamard_tiles
         self.inst = inst
         self.plan = rank_plan
         self.dev = device_fmm if device_fmm is not None else DeviceFmm(inst)
@@ -233,7 +233,10 @@ class DistributedFmm:
         else:
             self.fft_sub = {}
             for l, (clo, chi, scl) in rank_plan.fft_clusters.items():
-                self.fft_sub[l] = (clo, chi, to_dev(scl, np.int32), int(scl.shape[0]))
+                self.fft_sub[l] = (clo, chi, to_dev(scl, np.int32), int(scl.shape[0]),
+                                   upload_hadamard_tiles(inst.halo_plans[l].halo[clo:chi],
+                                                         inst.halo_plans[l].src_color,
+                                                         inst.halo_plans[l].tgt_color[clo:chi]))
         del R
 
     # -- exchange buffers: one flat buffer per peer holding all levels' rows
@@ -369,11 +372,11 @@ class DistributedFmm:
         return out[: d.tx.shape[0] * R]
 
     def _fft_level(self, lvl, mult, nrhs, check):
-        from .device import P, launch, stream_handle
+        from .device import P, hadamard_tiled, launch, stream_handle
         d = self.dev
         b = d._buffers(nrhs)
         plan = d.fft_plan_dev[lvl]
-        clo, chi, scl, n_scl = self.fft_sub[lvl]
+        clo, chi, scl, n_scl, tiles = self.fft_sub[lvl]
         nsc = plan["nsc"]
         n_sub = chi - clo
         qhat = b["qhat"][: 2 * d.n_freq * nsc * 8 * nrhs]
@@ -381,10 +384,7 @@ class DistributedFmm:
         s = stream_handle()
         launch(f"kifmm_fft_forward_{d.sfx}", P(mult), nrhs, d.order, P(plan["sbox"]), nsc, P(scl),
                n_scl, P(qhat), s)
-        phat.zero_()
-        cname = "c64" if d.sfx == "f32" else "c128"
-        launch(f"kifmm_hadamard_m2l_{cname}", P(d.khat), P(qhat), P(plan["halo"]) + 8 * 26 * clo,
-               P(phat), d.n_freq, nsc, n_sub, nrhs, s)
+        hadamard_tiled(d.sfx, d.khat, qhat, tiles, d.n_freq, nsc, n_sub, nrhs, phat, s)
         launch(f"kifmm_fft_inverse_{d.sfx}", P(phat), nrhs, d.order, P(plan["tbox"]) + 4 * 8 * clo,
                n_sub, 1.0 / d.side[lvl], P(check), s)
 

@@ -117,6 +117,8 @@ class HaloPlan:
     src_slot: np.ndarray      # (n_src_boxes,) cluster*8 + child
     tgt_slot: np.ndarray      # (n_tgt_boxes,)
     halo: np.ndarray          # (n_tgt_clusters, 26) source cluster or -1
+    src_color: np.ndarray = None   # (n_src_clusters,) coordinate parity class (x&1|y&1<<1|z&1<<2)
+    tgt_color: np.ndarray = None   # (n_tgt_clusters,) same for the target clusters
 
 
 def build_halo_plan(source_tree: Octree, target_tree: Octree, level: int) -> HaloPlan:
@@ -139,8 +141,113 @@ def build_halo_plan(source_tree: Octree, target_tree: Octree, level: int) -> Hal
         posc = np.minimum(pos, spu.shape[0] - 1)
         hit = spu[posc] == codes
         halo[rows[hit], i] = posc[hit]
+    sa, _ = decode_codes(spu)
     return HaloPlan(level, int(spu.shape[0]), int(tpu.shape[0]), src_slot.astype(np.int64),
-                    tgt_slot.astype(np.int64), halo)
+                    tgt_slot.astype(np.int64), halo, parity_class(sa), parity_class(anchors))
+
+
+def parity_class(anchors: np.ndarray) -> np.ndarray:
+    """Coordinate parity class x&1 | (y&1)<<1 | (z&1)<<2 of integer anchors."""
+    a = np.asarray(anchors, dtype=np.int64).reshape(-1, 3)
+    return (a[:, 0] & 1) | ((a[:, 1] & 1) << 1) | ((a[:, 2] & 1) << 2)
+
+
+HAD_TILE = 256      # target clusters per tile (csrc/hadamard.cu TT)
+HAD_UMAX = 600      # source slots per tile (UMAX); UMAX + class = absent (zero rows)
+HAD_OFFSET_PARITY = parity_class(np.array(halo_offsets()))
+
+
+@dataclass
+class HadamardTiles:
+    """Tile plan of a halo table for the tiled Hadamard kernel
+    (csrc/hadamard.cu hadamard_tiled_kernel, which documents the layout).
+
+    Per tile of consecutive target clusters: ``tcol`` places each target in
+    a slot-table column of its parity class (column 32w + 4g + j <-> class
+    g), ``src`` lists the distinct sources in shared-memory slots with
+    slot % 8 = the source's parity class, and ``slots`` maps each (offset,
+    column) to its source's slot.  At a fixed offset the 8 lane groups of a
+    warp then read sources of 8 different classes -> 8 different banks."""
+    begin: np.ndarray        # (n_tiles + 1,) target-cluster offsets
+    src_off: np.ndarray      # (n_tiles + 1,) offsets into src
+    src: np.ndarray          # per tile: source cluster of each slot (-1 = hole)
+    slots: np.ndarray        # (n_tiles, 26, HAD_TILE) int16
+    tcol: np.ndarray         # (n_tiles, HAD_TILE) int16 tile-local target, -1 = empty
+
+    @property
+    def n_tiles(self) -> int:
+        return int(self.begin.shape[0] - 1)
+
+
+def _slot_layout(u: np.ndarray, color: np.ndarray):
+    """Slots for sorted distinct sources u: slot = 8 * (rank within its class) + class."""
+    c = color[u]
+    order = np.argsort(c, kind="stable")
+    counts = np.bincount(c, minlength=8)
+    rank = np.empty(u.shape[0], dtype=np.int64)
+    rank[order] = np.arange(u.shape[0]) - np.repeat(np.cumsum(counts) - counts, counts)
+    slot = 8 * rank + c
+    n_slots = int(8 * counts.max()) if u.shape[0] else 0
+    return slot, n_slots
+
+
+def _columns(tc: np.ndarray, tile: int) -> np.ndarray:
+    """Column of each tile-local target: the k-th target of class g goes to
+    column 32 (k // 4) + 4 g + k % 4."""
+    col = np.empty(tc.shape[0], dtype=np.int64)
+    for g in range(8):
+        idx = np.flatnonzero(tc == g)
+        k = np.arange(idx.shape[0])
+        col[idx] = 32 * (k // 4) + 4 * g + (k % 4)
+    return col
+
+
+def plan_hadamard_tiles(halo: np.ndarray, src_color: np.ndarray, tgt_color: np.ndarray,
+                        tile: int = HAD_TILE, umax: int = HAD_UMAX) -> HadamardTiles:
+    """Greedy tiling of the (Morton-ordered) target clusters: take up to
+    ``tile`` consecutive clusters, halve while a parity class holds more than
+    tile/8 of them or their sources need more than ``umax`` slots (a full
+    256-cluster brick: 32 targets per class, 600 sources = 75 per class =
+    exactly 600 slots)."""
+    halo = np.asarray(halo, dtype=np.int64)
+    src_color = np.asarray(src_color, dtype=np.int64)
+    tgt_color = np.asarray(tgt_color, dtype=np.int64)
+    n = halo.shape[0]
+    per_class = tile // 8
+    begin, src_off, srcs, slots, tcols = [0], [0], [], [], []
+    b = 0
+    while b < n:
+        e = min(n, b + tile)
+        while True:
+            h = halo[b:e]
+            tc = tgt_color[b:e]
+            u = np.unique(h[h >= 0])
+            slot, n_slots = _slot_layout(u, src_color)
+            if (n_slots <= umax and np.bincount(tc, minlength=8).max() <= per_class) or e - b == 1:
+                break
+            e = b + (e - b) // 2
+        table = np.full(n_slots, -1, dtype=np.int64)
+        table[slot] = u
+        loc = slot[np.searchsorted(u, h)] if u.shape[0] else np.zeros(h.shape, np.int64)
+        absent = umax + (tc[:, None] ^ HAD_OFFSET_PARITY[None, :])
+        loc = np.where(h < 0, absent, loc)
+        col = _columns(tc, tile)
+        sl = np.empty((26, tile), dtype=np.int16)
+        col_class = (np.arange(tile) >> 2) & 7
+        sl[:] = (umax + (col_class[None, :] ^ HAD_OFFSET_PARITY[:, None])).astype(np.int16)
+        sl[:, col] = loc.T
+        tcol = np.full(tile, -1, dtype=np.int16)
+        tcol[col] = np.arange(e - b)
+        srcs.append(table)
+        slots.append(sl)
+        tcols.append(tcol)
+        begin.append(e)
+        src_off.append(src_off[-1] + n_slots)
+        b = e
+    return HadamardTiles(np.asarray(begin, dtype=np.int64), np.asarray(src_off, dtype=np.int64),
+                         np.concatenate(srcs).astype(np.int64) if srcs else np.zeros(0, np.int64),
+                         np.stack(slots) if slots else np.zeros((0, 26, tile), np.int16),
+                         np.stack(tcols) if tcols else np.zeros((0, tile), np.int16))
 
 
 def m2l_fft_level(ops: M2lFftOperators, plan: HaloPlan, multipoles, level_scale: float = 1.0,

@@ -68,6 +68,41 @@ def test_bucket_plan_covers_every_pair(case):
                               np.arange(inst.target_tree.level_keys(lvl).shape[0]))
 
 
+def test_hadamard_tiles_reproduce_halo(case):
+    """The tiled Hadamard's plan (csrc/hadamard.cu) addresses exactly the
+    halo table's sources, with the bank invariants the kernel relies on:
+    column 32w + 4g + j holds a target of parity class g, a source sits in a
+    slot of its own class, and absent sources map to zero row UMAX + class."""
+    from paper_2408_07436_b200.m2l_fft import (HAD_OFFSET_PARITY, HAD_TILE, HAD_UMAX,
+                                               plan_hadamard_tiles)
+    name, g, inst = case
+    if inst.config.backend != "fft":
+        pytest.skip("fft only")
+    col_class = (np.arange(HAD_TILE) >> 2) & 7
+    for lvl, hp in inst.halo_plans.items():
+        for umax in (HAD_UMAX, 64):                    # 64 forces tile splitting
+            t = plan_hadamard_tiles(hp.halo, hp.src_color, hp.tgt_color, umax=umax)
+            assert t.begin[0] == 0 and t.begin[-1] == hp.halo.shape[0]
+            for k in range(t.n_tiles):
+                b, e = t.begin[k], t.begin[k + 1]
+                assert 0 < e - b <= HAD_TILE
+                table = t.src[t.src_off[k]:t.src_off[k + 1]]
+                assert table.shape[0] <= umax or e - b == 1
+                used = table >= 0
+                assert np.array_equal(hp.src_color[table[used]], np.flatnonzero(used) % 8)
+                tcol = t.tcol[k].astype(np.int64)
+                filled = tcol >= 0
+                assert np.array_equal(np.sort(tcol[filled]), np.arange(e - b))
+                assert np.array_equal(hp.tgt_color[b + tcol[filled]], col_class[filled])
+                sl = t.slots[k].astype(np.int64)              # (26, HAD_TILE)
+                want_class = col_class[None, :] ^ HAD_OFFSET_PARITY[:, None]
+                assert np.array_equal(sl % 8, want_class)
+                absent = sl >= umax
+                assert np.array_equal(sl[absent], umax + want_class[absent])
+                got = np.where(absent, -1, table[np.minimum(sl, table.shape[0] - 1)])
+                assert np.array_equal(got[:, filled].T, hp.halo[b + tcol[filled]])
+
+
 def test_config_validation_mirrors_reference():
     for bad in (dict(depth=1), dict(order_equiv=1), dict(order_equiv=6, order_check=5),
                 dict(backend="magic"), dict(backend="fft", order_equiv=6, order_check=8),

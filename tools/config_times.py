@@ -1,0 +1,33 @@
+"""Device evaluate time + per-phase breakdown for a BASELINE-style config."""
+import os, sys, time
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2408_07436_b200 import FmmConfig, setup
+from paper_2408_07436_b200.device import profile_launches
+
+n = int(sys.argv[1]); kw = eval(sys.argv[2]); signed = len(sys.argv) > 3 and sys.argv[3] == "signed"
+pts = np.random.default_rng(7).random((n, 3))
+rng = np.random.default_rng(11)
+q = rng.uniform(-1, 1, n) if signed else rng.random(n)
+t0 = time.perf_counter(); inst = setup(pts, pts, FmmConfig(**kw)); ts = time.perf_counter() - t0
+dev = inst.device
+qd = torch.from_numpy(q).cuda()
+for _ in range(2):
+    dev.evaluate_graphed(qd, 1)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    dev.evaluate_graphed(qd, 1)
+e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+with profile_launches() as p:
+    dev.evaluate_device(qd, 1)
+agg = {}
+for name, tag, t in p.times():
+    key = tag[:3] + ":" + name.replace("kifmm_", "")
+    agg[key] = agg.get(key, 0) + t
+print(f"n={n} {kw} setup {ts:.1f}s evaluate {ms:.3f} ms -> {n/ms/1e3:.1f} Mpts/s")
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:12]:
+    print(f"   {k:40s} {v*1e3:9.1f} us")
