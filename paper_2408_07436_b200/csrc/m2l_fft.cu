@@ -53,238 +53,285 @@ __device__ void build_lattice(int p, int* lat) {
   }
 }
 
+// Twiddle table TW[k][m] = e^{-2 pi i (k m mod n) / n}, k, m < n: with the
+// order a template constant every DFT loop below is unrolled and a twiddle
+// read is (row base + immediate).
 template <typename T>
 __device__ void build_twiddles(int n, typename cx<T>::v* tw) {
-  for (int m = threadIdx.x; m < n; m += blockDim.x) {
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int k = e / n, m = e % n;
     double s, c;
-    sincospi(2.0 * m / n, &s, &c);
-    tw[m] = typename cx<T>::v{(T)c, (T)(-s)};   // e^{-2 pi i m / n}
+    sincospi(2.0 * ((k * m) % n) / n, &s, &c);
+    tw[e] = typename cx<T>::v{(T)c, (T)(-s)};
   }
 }
 
-template <typename T>
-size_t forward_smem(int p, int bpc) {
-  using C = typename cx<T>::v;
-  int n = 2 * p, nh = p + 1, ne = 6 * (p - 1) * (p - 1) + 2;
-  size_t per_box_x1 = (size_t)p * p * nh * sizeof(C);
-  size_t cube = (size_t)p * p * p * sizeof(T);
-  size_t x2 = (size_t)p * n * nh * sizeof(C);
-  size_t per_box = per_box_x1 + (cube > x2 ? cube : x2);
-  return n * sizeof(C) + ((ne * sizeof(int) + 15) / 16) * 16 + bpc * per_box;
+// Per-box scratch strides are padded to (multiple of 128 B) + sizeof(C) so
+// the 8 boxes a warp's lanes touch at the same offset sit in 8 different
+// bank groups.
+template <typename C>
+constexpr size_t pad_box(size_t bytes) {
+  return ((bytes + 127) / 128) * 128 + sizeof(C);
 }
 
-template <typename T>
+template <typename T, int P>
+struct FftShape {
+  using C = typename cx<T>::v;
+  static constexpr int N = 2 * P, NH = P + 1, NE = 6 * (P - 1) * (P - 1) + 2, P3 = P * P * P;
+  static constexpr size_t head = ((N * N * sizeof(C) + NE * sizeof(int) + 127) / 128) * 128;
+  // forward: X1 [P][P][NH] complex, then CUBE [P^3] real / X2 [P][N][NH] complex
+  static constexpr size_t fx1 = (size_t)P * P * NH * sizeof(C);
+  static constexpr size_t fu = (size_t)P * N * NH * sizeof(C) > (size_t)P3 * sizeof(T)
+                                   ? (size_t)P * N * NH * sizeof(C) : (size_t)P3 * sizeof(T);
+  static constexpr size_t fbox = pad_box<C>(fx1 + fu);
+  // inverse: Y1 [P][N][NH], Y2 [P][P][NH]
+  static constexpr size_t iy1 = (size_t)P * N * NH * sizeof(C);
+  static constexpr size_t ibox = pad_box<C>(iy1 + (size_t)P * P * NH * sizeof(C));
+};
+
+template <typename T, int P>
 __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restrict__ mult,
-                                                               int64_t nrhs, int p, int bpc,
+                                                               int64_t nrhs, int bpc,
                                                                const int32_t* __restrict__ slot_box,
                                                                int64_t nsc,
                                                                const int32_t* __restrict__ cluster_list,
                                                                typename cx<T>::v* __restrict__ qhat) {
+  using S = FftShape<T, P>;
   using C = typename cx<T>::v;
+  constexpr int N = S::N, NH = S::NH, NE = S::NE, P3 = S::P3;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int n = 2 * p, nh = p + 1, ne = 6 * (p - 1) * (p - 1) + 2, p3 = p * p * p;
   C* tw = reinterpret_cast<C*>(smem_raw);
-  int* lat = reinterpret_cast<int*>(smem_raw + n * sizeof(C));
-  unsigned char* boxes = smem_raw + n * sizeof(C) + ((ne * sizeof(int) + 15) / 16) * 16;
-  const size_t x1_elems = (size_t)p * p * nh;
-  const size_t u_bytes = max((size_t)p3 * sizeof(T), (size_t)p * n * nh * sizeof(C));
-  const size_t box_bytes = x1_elems * sizeof(C) + u_bytes;
-  auto X1 = [&](int b) { return reinterpret_cast<C*>(boxes + b * box_bytes); };
-  auto CUBE = [&](int b) { return reinterpret_cast<T*>(boxes + b * box_bytes + x1_elems * sizeof(C)); };
-  auto X2 = [&](int b) { return reinterpret_cast<C*>(boxes + b * box_bytes + x1_elems * sizeof(C)); };
+  int* lat = reinterpret_cast<int*>(smem_raw + N * N * sizeof(C));
+  unsigned char* boxes = smem_raw + S::head;
+  auto X1 = [&](int b) { return reinterpret_cast<C*>(boxes + b * S::fbox); };
+  auto CUBE = [&](int b) { return reinterpret_cast<T*>(boxes + b * S::fbox + S::fx1); };
+  auto X2 = [&](int b) { return reinterpret_cast<C*>(boxes + b * S::fbox + S::fx1); };
 
   const int groups = 8 / bpc;
   const int64_t cluster = cluster_list ? (int64_t)cluster_list[blockIdx.x / groups]
                                        : (int64_t)(blockIdx.x / groups);
   const int child0 = (blockIdx.x % groups) * bpc;
   const int64_t r = blockIdx.y;
-  build_twiddles<T>(n, tw);
-  build_lattice(p, lat);
-  for (int e = threadIdx.x; e < bpc * p3; e += kThreads) CUBE(e / p3)[e % p3] = T(0);
+  build_twiddles<T>(N, tw);
+  build_lattice(P, lat);
+  for (int e = threadIdx.x; e < bpc * P3; e += kThreads) CUBE(e % bpc)[e / bpc] = T(0);
   __syncthreads();
-  for (int e = threadIdx.x; e < bpc * ne; e += kThreads) {
-    const int b = e / ne, s = e - b * ne;
+  for (int e = threadIdx.x; e < bpc * NE; e += kThreads) {
+    const int b = e / NE, s = e - b * NE;
     const int32_t box = slot_box[cluster * 8 + child0 + b];
-    if (box >= 0) CUBE(b)[lat[s]] = mult[((int64_t)box * nrhs + r) * ne + s];
+    if (box >= 0) CUBE(b)[lat[s]] = mult[((int64_t)box * nrhs + r) * NE + s];
   }
   __syncthreads();
-  // z: X1[i0][i1][k2] = sum_{i2} cube[i0][i1][i2] w^{k2 (i2 + p)}
-  for (int e = threadIdx.x; e < bpc * p * p * nh; e += kThreads) {
-    const int b = e / (p * p * nh);
-    int rem = e - b * p * p * nh;
-    const int k2 = rem % nh, i01 = rem / nh;
-    const T* line = CUBE(b) + i01 * p;
-    C acc{0, 0};
-    for (int i2 = 0; i2 < p; ++i2) {
-      C w = tw[(k2 * (i2 + p)) % n];
-      acc.x += line[i2] * w.x;
-      acc.y += line[i2] * w.y;
+  // z: X1[i0][i1][k2] = sum_{i2} cube[i0][i1][i2] w^{k2 (i2 + P)}; thread per line.
+  for (int e = threadIdx.x; e < bpc * P * P; e += kThreads) {
+    const int b = e % bpc, i01 = e / bpc;
+    T line[P];
+#pragma unroll
+    for (int i2 = 0; i2 < P; ++i2) line[i2] = CUBE(b)[i01 * P + i2];
+    C* out = X1(b) + i01 * NH;
+#pragma unroll 1
+    for (int k2 = 0; k2 < NH; ++k2) {
+      const C* w = tw + k2 * N + P;
+      C acc{0, 0};
+#pragma unroll
+      for (int i2 = 0; i2 < P; ++i2) {
+        acc.x = fma(line[i2], w[i2].x, acc.x);
+        acc.y = fma(line[i2], w[i2].y, acc.y);
+      }
+      out[k2] = acc;
     }
-    X1(b)[i01 * nh + k2] = acc;
   }
   __syncthreads();
-  // y: X2[i0][k1][k2] = sum_{i1} X1[i0][i1][k2] w^{k1 (i1 + p)}   (overwrites the cube)
-  for (int e = threadIdx.x; e < bpc * p * n * nh; e += kThreads) {
-    const int b = e / (p * n * nh);
-    int rem = e - b * p * n * nh;
-    const int k2 = rem % nh, k1 = (rem / nh) % n, i0 = rem / (nh * n);
-    C acc{0, 0};
-    for (int i1 = 0; i1 < p; ++i1) cfma(acc, X1(b)[(i0 * p + i1) * nh + k2], tw[(k1 * (i1 + p)) % n]);
-    X2(b)[(i0 * n + k1) * nh + k2] = acc;
+  // y: X2[i0][k1][k2] = sum_{i1} X1[i0][i1][k2] w^{k1 (i1 + P)} (overwrites the cube).
+  for (int e = threadIdx.x; e < bpc * P * NH; e += kThreads) {
+    const int b = e % bpc, rem = e / bpc;
+    const int k2 = rem % NH, i0 = rem / NH;
+    C in[P];
+#pragma unroll
+    for (int i1 = 0; i1 < P; ++i1) in[i1] = X1(b)[(i0 * P + i1) * NH + k2];
+#pragma unroll 1
+    for (int k1 = 0; k1 < N; ++k1) {
+      const C* w = tw + k1 * N + P;
+      C acc{0, 0};
+#pragma unroll
+      for (int i1 = 0; i1 < P; ++i1) cfma(acc, in[i1], w[i1]);
+      X2(b)[(i0 * N + k1) * NH + k2] = acc;
+    }
   }
   __syncthreads();
-  // x: spectrum[k0][k1][k2] = sum_{i0} X2[i0][k1][k2] w^{k0 (i0 + p)}, child fastest
-  const int nf = n * n * nh;
-  for (int e = threadIdx.x; e < nf * bpc; e += kThreads) {
-    const int b = e % bpc, f = e / bpc;
-    const int k0 = f / (n * nh), k12 = f % (n * nh);
-    C acc{0, 0};
-    for (int i0 = 0; i0 < p; ++i0) cfma(acc, X2(b)[i0 * n * nh + k12], tw[(k0 * (i0 + p)) % n]);
-    qhat[(((int64_t)f * nsc + cluster) * 8 + child0 + b) * nrhs + r] = acc;
+  // x: spectrum[k0][k1][k2] = sum_{i0} X2[i0][k1][k2] w^{k0 (i0 + P)}, child fastest.
+  for (int e = threadIdx.x; e < N * NH * bpc; e += kThreads) {
+    const int b = e % bpc, k12 = e / bpc;
+    C in[P];
+#pragma unroll
+    for (int i0 = 0; i0 < P; ++i0) in[i0] = X2(b)[i0 * N * NH + k12];
+    C* dst = qhat + (((int64_t)k12 * nsc + cluster) * 8 + child0 + b) * nrhs + r;
+    const int64_t fstride = (int64_t)N * NH * nsc * 8 * nrhs;
+#pragma unroll 1
+    for (int k0 = 0; k0 < N; ++k0) {
+      const C* w = tw + k0 * N + P;
+      C acc{0, 0};
+#pragma unroll
+      for (int i0 = 0; i0 < P; ++i0) cfma(acc, in[i0], w[i0]);
+      dst[k0 * fstride] = acc;
+    }
   }
 }
 
-template <typename T>
-size_t inverse_smem(int p, int bpc) {
-  using C = typename cx<T>::v;
-  int n = 2 * p, nh = p + 1, ne = 6 * (p - 1) * (p - 1) + 2;
-  size_t y1 = (size_t)p * n * nh * sizeof(C), y2 = (size_t)p * p * nh * sizeof(C);
-  return n * sizeof(C) + ((ne * sizeof(int) + 15) / 16) * 16 + bpc * (y1 + y2);
-}
-
-template <typename T>
+template <typename T, int P>
 __global__ void __launch_bounds__(kThreads) fft_inverse_kernel(const typename cx<T>::v* __restrict__ phat,
-                                                               int64_t nrhs, int p, int bpc,
+                                                               int64_t nrhs, int bpc,
                                                                const int32_t* __restrict__ slot_box,
                                                                int64_t ntc, T scale,
                                                                T* __restrict__ check) {
+  using S = FftShape<T, P>;
   using C = typename cx<T>::v;
+  constexpr int N = S::N, NH = S::NH, NE = S::NE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int n = 2 * p, nh = p + 1, ne = 6 * (p - 1) * (p - 1) + 2;
   C* tw = reinterpret_cast<C*>(smem_raw);
-  int* lat = reinterpret_cast<int*>(smem_raw + n * sizeof(C));
-  unsigned char* boxes = smem_raw + n * sizeof(C) + ((ne * sizeof(int) + 15) / 16) * 16;
-  const size_t y1e = (size_t)p * n * nh, y2e = (size_t)p * p * nh;
-  auto Y1 = [&](int b) { return reinterpret_cast<C*>(boxes) + b * (y1e + y2e); };
-  auto Y2 = [&](int b) { return reinterpret_cast<C*>(boxes) + b * (y1e + y2e) + y1e; };
+  int* lat = reinterpret_cast<int*>(smem_raw + N * N * sizeof(C));
+  unsigned char* boxes = smem_raw + S::head;
+  auto Y1 = [&](int b) { return reinterpret_cast<C*>(boxes + b * S::ibox); };
+  auto Y2 = [&](int b) { return reinterpret_cast<C*>(boxes + b * S::ibox + S::iy1); };
 
   const int groups = 8 / bpc;
   const int64_t cluster = blockIdx.x / groups;
   const int child0 = (blockIdx.x % groups) * bpc;
   const int64_t r = blockIdx.y;
-  build_twiddles<T>(n, tw);
-  build_lattice(p, lat);
+  build_twiddles<T>(N, tw);
+  build_lattice(P, lat);
   __syncthreads();
-  // x: Y1[i0][k1][k2] = sum_{k0} X[k0][k1][k2] w^{-k0 i0}, i0 < p; child fastest.
-  for (int e = threadIdx.x; e < n * nh * bpc; e += kThreads) {
+  // x: Y1[i0][k1][k2] = sum_{k0} X[k0][k1][k2] w^{-k0 i0}, i0 < P; child fastest.
+  for (int e = threadIdx.x; e < N * NH * bpc; e += kThreads) {
     const int b = e % bpc, k12 = e / bpc;
-    C acc[kMaxP];
+    const C* src = phat + (((int64_t)k12 * ntc + cluster) * 8 + child0 + b) * nrhs + r;
+    const int64_t fstride = (int64_t)N * NH * ntc * 8 * nrhs;
+    C in[N];
 #pragma unroll
-    for (int i = 0; i < kMaxP; ++i) acc[i] = C{0, 0};
-    for (int k0 = 0; k0 < n; ++k0) {
-      const int64_t f = (int64_t)k0 * n * nh + k12;
-      const C v = phat[((f * ntc + cluster) * 8 + child0 + b) * nrhs + r];
+    for (int k0 = 0; k0 < N; ++k0) in[k0] = src[k0 * fstride];
+#pragma unroll 1
+    for (int i0 = 0; i0 < P; ++i0) {
+      C acc{0, 0};
 #pragma unroll
-      for (int i0 = 0; i0 < kMaxP; ++i0) {
-        if (i0 < p) {
-          C w = tw[(k0 * i0) % n];
-          w.y = -w.y;
-          cfma(acc[i0], v, w);
-        }
+      for (int k0 = 0; k0 < N; ++k0) {
+        const C w = tw[i0 * N + k0];           // conj(w) applied below
+        acc.x = fma(in[k0].x, w.x, fma(in[k0].y, w.y, acc.x));
+        acc.y = fma(in[k0].y, w.x, fma(-in[k0].x, w.y, acc.y));
       }
+      Y1(b)[i0 * N * NH + k12] = acc;
     }
-#pragma unroll
-    for (int i0 = 0; i0 < kMaxP; ++i0)
-      if (i0 < p) Y1(b)[i0 * n * nh + k12] = acc[i0];
   }
   __syncthreads();
-  // y: Y2[i0][i1][k2] = sum_{k1} Y1[i0][k1][k2] w^{-k1 i1}, i1 < p.
-  for (int e = threadIdx.x; e < p * nh * bpc; e += kThreads) {
+  // y: Y2[i0][i1][k2] = sum_{k1} Y1[i0][k1][k2] w^{-k1 i1}, i1 < P.
+  for (int e = threadIdx.x; e < P * NH * bpc; e += kThreads) {
     const int b = e % bpc, rem = e / bpc;
-    const int k2 = rem % nh, i0 = rem / nh;
-    C acc[kMaxP];
+    const int k2 = rem % NH, i0 = rem / NH;
+    C in[N];
 #pragma unroll
-    for (int i = 0; i < kMaxP; ++i) acc[i] = C{0, 0};
-    for (int k1 = 0; k1 < n; ++k1) {
-      const C v = Y1(b)[(i0 * n + k1) * nh + k2];
+    for (int k1 = 0; k1 < N; ++k1) in[k1] = Y1(b)[(i0 * N + k1) * NH + k2];
+#pragma unroll 1
+    for (int i1 = 0; i1 < P; ++i1) {
+      C acc{0, 0};
 #pragma unroll
-      for (int i1 = 0; i1 < kMaxP; ++i1) {
-        if (i1 < p) {
-          C w = tw[(k1 * i1) % n];
-          w.y = -w.y;
-          cfma(acc[i1], v, w);
-        }
+      for (int k1 = 0; k1 < N; ++k1) {
+        const C w = tw[i1 * N + k1];
+        acc.x = fma(in[k1].x, w.x, fma(in[k1].y, w.y, acc.x));
+        acc.y = fma(in[k1].y, w.x, fma(-in[k1].x, w.y, acc.y));
       }
+      Y2(b)[(i0 * P + i1) * NH + k2] = acc;
     }
-#pragma unroll
-    for (int i1 = 0; i1 < kMaxP; ++i1)
-      if (i1 < p) Y2(b)[(i0 * p + i1) * nh + k2] = acc[i1];
   }
   __syncthreads();
   // z (complex -> real, Hermitian half spectrum; the imaginary parts of the
   // k2 = 0 and Nyquist bins are ignored as in pocketfft's c2r), read the
   // lattice, normalise by n^3 and apply the level scale.
-  const T norm = T(1) / (T)(n * n * n);
-  for (int e = threadIdx.x; e < ne * bpc; e += kThreads) {
+  const T norm = T(1) / (T)(N * N * N);
+  for (int e = threadIdx.x; e < NE * bpc; e += kThreads) {
     const int b = e % bpc, s = e / bpc;
     const int32_t box = slot_box[cluster * 8 + child0 + b];
     if (box < 0) continue;
     const int li = lat[s];
-    const int i0 = li / (p * p), i1 = (li / p) % p, i2 = li % p;
-    const C* y = Y2(b) + (i0 * p + i1) * nh;
-    T acc = y[0].x + ((i2 & 1) ? -y[p].x : y[p].x);
+    const int i01 = li / P, i2 = li - i01 * P;
+    const C* y = Y2(b) + i01 * NH;
+    const C* w = tw + i2 * N;                  // Re(y e^{+i theta}) = y.x cos + y.y (-sin)
+    T acc = y[0].x + ((i2 & 1) ? -y[P].x : y[P].x);
     T mid = 0;
-    for (int k2 = 1; k2 < p; ++k2) {
-      C w = tw[(k2 * i2) % n];   // e^{-i theta}; Re(y e^{+i theta}) = y.x cos + y.y (-sin)
-      mid += y[k2].x * w.x + y[k2].y * w.y;
-    }
+#pragma unroll
+    for (int k2 = 1; k2 < P; ++k2) mid = fma(y[k2].x, w[k2].x, fma(y[k2].y, w[k2].y, mid));
     acc += T(2) * mid;
-    check[((int64_t)box * nrhs + r) * ne + s] = (acc * norm) * scale;
+    check[((int64_t)box * nrhs + r) * NE + s] = (acc * norm) * scale;
   }
 }
 
-int pick_bpc(size_t (*smem)(int, int), int p, size_t limit) {
+template <typename T, int P>
+size_t forward_smem(int bpc) { return FftShape<T, P>::head + bpc * FftShape<T, P>::fbox; }
+template <typename T, int P>
+size_t inverse_smem(int bpc) { return FftShape<T, P>::head + bpc * FftShape<T, P>::ibox; }
+
+int pick_bpc(size_t (*smem)(int), size_t limit) {
   for (int bpc = 8; bpc >= 1; bpc /= 2)
-    if (smem(p, bpc) <= limit) return bpc;
+    if (smem(bpc) <= limit) return bpc;
   return 0;
 }
+
+template <typename T, int P>
+int forward_p(const T* mult, int64_t nrhs, const int32_t* slot_box, int64_t nsc,
+              const int32_t* cluster_list, int64_t nclusters, T* qhat, cudaStream_t stream) {
+  using C = typename cx<T>::v;
+  const int bpc = pick_bpc(forward_smem<T, P>, 227 * 1024);
+  if (!bpc) return KIFMM_EARG;
+  const size_t smem = forward_smem<T, P>(bpc);
+  set_max_smem((const void*)fft_forward_kernel<T, P>, smem);
+  dim3 grid((unsigned)(nclusters * (8 / bpc)), (unsigned)nrhs);
+  fft_forward_kernel<T, P><<<grid, kThreads, smem, stream>>>(
+      mult, nrhs, bpc, slot_box, nsc, cluster_list, reinterpret_cast<C*>(qhat));
+  return launch_status();
+}
+
+template <typename T, int P>
+int inverse_p(const T* phat, int64_t nrhs, const int32_t* slot_box, int64_t ntc, double scale,
+              T* check, cudaStream_t stream) {
+  using C = typename cx<T>::v;
+  const int bpc = pick_bpc(inverse_smem<T, P>, 227 * 1024);
+  if (!bpc) return KIFMM_EARG;
+  const size_t smem = inverse_smem<T, P>(bpc);
+  set_max_smem((const void*)fft_inverse_kernel<T, P>, smem);
+  dim3 grid((unsigned)(ntc * (8 / bpc)), (unsigned)nrhs);
+  fft_inverse_kernel<T, P><<<grid, kThreads, smem, stream>>>(
+      reinterpret_cast<const C*>(phat), nrhs, bpc, slot_box, ntc, (T)scale, check);
+  return launch_status();
+}
+
+#define KIFMM_ORDERS(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12)
 
 template <typename T>
 int forward(const T* mult, int64_t nrhs, int64_t order, const int32_t* slot_box, int64_t nsc,
             const int32_t* cluster_list, int64_t n_list, T* qhat, void* stream) {
-  using C = typename cx<T>::v;
   if (order < 2 || order > kMaxP || nrhs < 1 || nsc < 0) return KIFMM_EARG;
   if (nsc == 0) return 0;
-  const int p = (int)order;
-  const int bpc = pick_bpc(forward_smem<T>, p, 227 * 1024);
-  if (!bpc) return KIFMM_EARG;
-  size_t smem = forward_smem<T>(p, bpc);
-  auto kern = fft_forward_kernel<T>;
-  set_max_smem((const void*)kern, smem);
   const int64_t nclusters = cluster_list ? n_list : nsc;
   if (nclusters <= 0) return 0;
-  dim3 grid((unsigned)(nclusters * (8 / bpc)), (unsigned)nrhs);
-  kern<<<grid, kThreads, smem, (cudaStream_t)stream>>>(mult, nrhs, p, bpc, slot_box, nsc,
-                                                       cluster_list, reinterpret_cast<C*>(qhat));
-  return launch_status();
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (order) {
+#define X(P_) case P_: return forward_p<T, P_>(mult, nrhs, slot_box, nsc, cluster_list, nclusters, qhat, s);
+    KIFMM_ORDERS(X)
+#undef X
+  }
+  return KIFMM_EARG;
 }
 
 template <typename T>
 int inverse(const T* phat, int64_t nrhs, int64_t order, const int32_t* slot_box, int64_t ntc,
             double level_scale, T* check, void* stream) {
-  using C = typename cx<T>::v;
   if (order < 2 || order > kMaxP || nrhs < 1 || ntc < 0) return KIFMM_EARG;
   if (ntc == 0) return 0;
-  const int p = (int)order;
-  const int bpc = pick_bpc(inverse_smem<T>, p, 227 * 1024);
-  if (!bpc) return KIFMM_EARG;
-  size_t smem = inverse_smem<T>(p, bpc);
-  auto kern = fft_inverse_kernel<T>;
-  set_max_smem((const void*)kern, smem);
-  dim3 grid((unsigned)(ntc * (8 / bpc)), (unsigned)nrhs);
-  kern<<<grid, kThreads, smem, (cudaStream_t)stream>>>(reinterpret_cast<const C*>(phat), nrhs, p,
-                                                       bpc, slot_box, ntc, (T)level_scale, check);
-  return launch_status();
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (order) {
+#define X(P_) case P_: return inverse_p<T, P_>(phat, nrhs, slot_box, ntc, level_scale, check, s);
+    KIFMM_ORDERS(X)
+#undef X
+  }
+  return KIFMM_EARG;
 }
 
 }  // namespace
