@@ -165,7 +165,7 @@ def probe_peak(kind):
     torch.cuda.synchronize()
     ops = blocks * threads * iters * 128.0
     sec = e0.elapsed_time(e1) / 1e3
-    return (2 * ops / sec / 1e12) if kind in (0, 1) else ops / sec / 1e9
+    return (2 * ops / sec / 1e12) if kind != 2 else ops / sec / 1e9
 
 
 # ------------------------------------------------------------- CPU baseline

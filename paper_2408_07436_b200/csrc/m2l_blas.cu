@@ -23,7 +23,7 @@ namespace {
 
 constexpr int TMT = 128;   // targets per tile (matches the host plan)
 constexpr int RM = 4;      // accumulator rows per thread (rows tm + 32*i)
-constexpr int RN = 8;      // accumulator columns per thread (contiguous)
+constexpr int RN = 8;      // accumulator columns per thread: RN/VEC vectors, lane-interleaved
 constexpr int MAXG = 12;   // max gather chunks per thread per step (register-cached indices)
 
 template <typename T>
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(512) m2l_sweep_kernel(
     }
     __syncthreads();
     const T* g = Gs + buf * TMT * gstride;
-    const T* d = Ds + buf * bk * kob + tn * RN;
+    const T* d = Ds + buf * bk * kob + tn * VEC;
 #pragma unroll 2
     for (int kk = 0; kk < bk; kk += VEC) {
       T a[RM][VEC];
@@ -129,10 +129,10 @@ __global__ void __launch_bounds__(512) m2l_sweep_kernel(
 #pragma unroll
         for (int j = 0; j < RN; j += VEC) {
           if constexpr (VEC == 4) {
-            float4 t4 = *reinterpret_cast<const float4*>(bp + j);
+            float4 t4 = *reinterpret_cast<const float4*>(bp + (j / VEC) * ng * VEC);
             b[j] = t4.x; b[j + 1] = t4.y; b[j + 2] = t4.z; b[j + 3] = t4.w;
           } else {
-            double2 t2 = *reinterpret_cast<const double2*>(bp + j);
+            double2 t2 = *reinterpret_cast<const double2*>(bp + (j / VEC) * ng * VEC);
             b[j] = t2.x; b[j + 1] = t2.y;
           }
         }
@@ -150,13 +150,14 @@ __global__ void __launch_bounds__(512) m2l_sweep_kernel(
   for (int i = 0; i < RM; ++i) {
     const int32_t tgt = tile_targets[tile * TMT + tm + 32 * i];
     if (tgt < 0) continue;
-    T* o = acc_out + ((int64_t)tgt * nrhs + r) * ld + (int64_t)split * ko_pad + c0 + tn * RN;
+    T* o = acc_out + ((int64_t)tgt * nrhs + r) * ld + (int64_t)split * ko_pad + c0 + tn * VEC;
 #pragma unroll
     for (int j = 0; j < RN; j += VEC) {
+      T* oj = o + (j / VEC) * ng * VEC;
       if constexpr (VEC == 4) {
-        *reinterpret_cast<float4*>(o + j) = float4{acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]};
+        *reinterpret_cast<float4*>(oj) = float4{acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]};
       } else {
-        *reinterpret_cast<double2*>(o + j) = double2{acc[i][j], acc[i][j + 1]};
+        *reinterpret_cast<double2*>(oj) = double2{acc[i][j], acc[i][j + 1]};
       }
     }
   }
@@ -195,6 +196,164 @@ int sweep(const T* qt, const T* Dt, int64_t kin, int64_t ko_pad, const int32_t* 
   return launch_status();
 }
 
+// ---------------------------------------------------------------------------
+// FP64 sweep on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64): same
+// target-stationary structure, but each warp owns a 32 x (kob/2) block of
+// the tile's accumulator as 4 x NTW m8n8 fragments, and every k4 step is
+// 4 + NTW fragment loads for 4 * NTW DMMAs (256 FMAs each) -- the FP64
+// pipe, not instruction issue or shared memory, sets the pace.  Exact IEEE
+// fp64 products and sums (only the summation order differs from SIMT).
+// Geometry (device.py blas_geometry): kin % 16 == 0; ko_pad = n_slabs * kob,
+// kob % 16 == 0, kob <= 160, n_slabs = ceil(ko_pad / 160).
+namespace dm {
+constexpr int BK = 16;          // k-chunk per pipeline stage
+constexpr int GS = BK + 4;      // Gs row stride (doubles): rows 8r..8r+3 -> distinct bank quarters
+constexpr int KOB_MAX = 160;
+}
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+template <int NTW>
+__global__ void __launch_bounds__(256, NTW > 6 ? 1 : 2) m2l_sweep_dmma_kernel(
+    const double* __restrict__ qt, const double* __restrict__ Dt, int kin, int ko_pad,
+    int nchunks, int n_slabs, int jper, const int32_t* __restrict__ tile_targets,
+    const int32_t* __restrict__ tile_class, const int32_t* __restrict__ src,
+    const int32_t* __restrict__ class_tv, int64_t nrhs, int nsplit, double* __restrict__ acc_out) {
+  using namespace dm;
+  constexpr int KOB = 16 * NTW;
+  constexpr int DS = KOB + 8;                         // Ds row stride: rows k, k+1 in opposite bank halves
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* Gs = reinterpret_cast<double*>(smem_raw);   // [2][TMT][GS]
+  double* Ds = Gs + 2 * TMT * GS;                     // [2][BK][DS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int64_t tile = blockIdx.x;
+  const int64_t r = blockIdx.y;
+  const int slab = blockIdx.z % n_slabs, split = blockIdx.z / n_slabs;
+  const int c0 = slab * KOB;
+  const int j0 = split * jper, j1 = min(189, j0 + jper);
+  const int32_t* tsrc = src + tile * 189 * TMT;
+  const int32_t* tv_list = class_tv + tile_class[tile] * 189;
+
+  double acc[4][NTW][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // Gather assignment: rows (tid >> 3) + 32 i, 16-byte chunk tid & 7.
+  const int grow = tid >> 3, gch = tid & 7;
+  int ids_cur[4], ids_next[4];
+  auto load_ids = [&](int j, int (&ids)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ids[i] = j < j1 ? __ldg(&tsrc[j * TMT + grow + 32 * i]) : -1;
+  };
+  const int nsteps = (j1 - j0) * nchunks;
+  auto stage = [&](int st, int buf) {
+    const int j = j0 + st / nchunks, ch = st % nchunks;
+    if (ch == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ids_cur[i] = ids_next[i];
+      load_ids(j + 1, ids_next);
+    }
+    const int kk0 = ch * BK;
+    double* g = Gs + buf * TMT * GS;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int s = ids_cur[i];
+      const double* gp = qt + ((int64_t)(s < 0 ? 0 : s) * nrhs + r) * kin + kk0 + 2 * gch;
+      cp_async16(g + (grow + 32 * i) * GS + 2 * gch, gp, s >= 0);
+    }
+    const double* dsrc = Dt + ((int64_t)tv_list[j] * kin + kk0) * ko_pad + c0;
+    double* d = Ds + buf * BK * DS;
+    constexpr int DCH = BK * KOB / 2;
+    for (int e = tid; e < DCH; e += 256) {
+      const int row = e / (KOB / 2), v = e - row * (KOB / 2);
+      cp_async16(d + row * DS + 2 * v, dsrc + (int64_t)row * ko_pad + 2 * v, true);
+    }
+    cp_async_commit();
+  };
+
+  load_ids(j0, ids_next);
+  if (nsteps > 0) stage(0, 0);
+  const int arow = 32 * wm + (lane >> 2), acol = lane & 3;
+  const int bcol = wn * (KOB / 2) + (lane >> 2), brow = lane & 3;
+  for (int st = 0; st < nsteps; ++st) {
+    const int buf = st & 1;
+    if (st + 1 < nsteps) {
+      stage(st + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* g = Gs + buf * TMT * GS + arow * GS + acol;
+    const double* d = Ds + buf * BK * DS + brow * DS + bcol;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double a[4], b[NTW];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) a[mt] = g[mt * 8 * GS + ks];
+#pragma unroll
+      for (int nt = 0; nt < NTW; ++nt) b[nt] = d[ks * DS + nt * 8];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
+    }
+    __syncthreads();
+  }
+
+  const int64_t ld = (int64_t)nsplit * ko_pad;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int32_t tgt = tile_targets[tile * TMT + 32 * wm + 8 * mt + (lane >> 2)];
+    if (tgt < 0) continue;
+    double* o = acc_out + ((int64_t)tgt * nrhs + r) * ld + (int64_t)split * ko_pad + c0 +
+                wn * (KOB / 2) + 2 * (lane & 3);
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt)
+      *reinterpret_cast<double2*>(o + nt * 8) = double2{acc[mt][nt][0], acc[mt][nt][1]};
+  }
+}
+
+int sweep_dmma(const double* qt, const double* Dt, int64_t kin, int64_t ko_pad,
+               const int32_t* tile_targets, const int32_t* tile_class, const int32_t* src,
+               const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, int64_t nsplit, double* acc,
+               void* stream) {
+  using namespace dm;
+  if (kin < BK || kin % BK || ko_pad < 16 || n_tiles < 0 || nrhs < 1 || nsplit < 1 || nsplit > 189)
+    return KIFMM_EARG;
+  if (n_tiles == 0) return 0;
+  const int n_slabs = (int)((ko_pad + KOB_MAX - 1) / KOB_MAX);
+  if (ko_pad % n_slabs) return KIFMM_EARG;
+  const int kob = (int)(ko_pad / n_slabs);
+  if (kob % 16 || kob > KOB_MAX) return KIFMM_EARG;
+  const int nchunks = (int)(kin / BK);
+  const int jper = (int)((189 + nsplit - 1) / nsplit);
+  const size_t smem = sizeof(double) * (2 * TMT * GS + 2 * BK * (kob + 8));
+  dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)(n_slabs * nsplit));
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (kob / 16) {
+#define KIFMM_DMMA(NT_)                                                                          \
+  case NT_:                                                                                      \
+    set_max_smem((const void*)m2l_sweep_dmma_kernel<NT_>, smem);                                \
+    m2l_sweep_dmma_kernel<NT_><<<grid, 256, smem, s>>>(qt, Dt, (int)kin, (int)ko_pad, nchunks, \
+                                                       n_slabs, jper, tile_targets, tile_class, \
+                                                       src, class_tv, nrhs, (int)nsplit, acc);  \
+    break;
+    KIFMM_DMMA(1) KIFMM_DMMA(2) KIFMM_DMMA(3) KIFMM_DMMA(4) KIFMM_DMMA(5)
+    KIFMM_DMMA(6) KIFMM_DMMA(7) KIFMM_DMMA(8) KIFMM_DMMA(9) KIFMM_DMMA(10)
+#undef KIFMM_DMMA
+    default:
+      return KIFMM_EARG;
+  }
+  return launch_status();
+}
+
 }  // namespace
 
 extern "C" {
@@ -210,8 +369,8 @@ int kifmm_m2l_sweep_f64(const double* qt, const double* Dt, int64_t kin, int64_t
                         const int32_t* tile_targets, const int32_t* tile_class, const int32_t* src,
                         const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, int64_t nsplit,
                         double* acc, void* s) {
-  return sweep<double>(qt, Dt, kin, ko_pad, tile_targets, tile_class, src, class_tv, n_tiles,
-                       nrhs, nsplit, acc, s);
+  return sweep_dmma(qt, Dt, kin, ko_pad, tile_targets, tile_class, src, class_tv, n_tiles, nrhs,
+                    nsplit, acc, s);
 }
 
 }  // extern "C"

@@ -98,16 +98,21 @@ class profile_launches:
 
 
 def blas_geometry(k: int, itemsize: int):
-    """(kin, ko_pad) padding of the compressed rank for the sweep kernel;
-    mirrors the launch checks in csrc/m2l_blas.cu."""
+    """(kin, ko_pad, n_slabs) padding of the compressed rank for the SIMT /
+    DMMA sweep kernels; mirrors the launch checks in csrc/m2l_blas.cu."""
+    if itemsize == 8:                       # DMMA sweep: 16-wide k chunks, slabs of <= 160
+        kin = -(-k // 16) * 16
+        n_slabs = -(-k // 160)
+        kob = -(-(-(-k // n_slabs)) // 16) * 16
+        return kin, n_slabs * kob, n_slabs
     vec = 16 // itemsize
-    bkmax = 64 if itemsize == 4 else 32
+    bkmax = 64
     nch = -(-k // bkmax)
     bk = -(-(-(-k // nch)) // vec) * vec
     kin = nch * bk
     n_slabs = -(-k // 128)
     kob = -(-(-(-k // n_slabs)) // 8) * 8
-    return kin, n_slabs * kob
+    return kin, n_slabs * kob, n_slabs
 
 
 class Linalg:
@@ -293,8 +298,7 @@ class BlasDevice:
             from .octree import transfer_offsets
             self.offsets = to_dev(transfer_offsets(), np.int8)
             return
-        self.kin, self.ko_pad = blas_geometry(k, dt.itemsize)
-        self.n_slabs = -(-k // 128)
+        self.kin, self.ko_pad, self.n_slabs = blas_geometry(k, dt.itemsize)
         s_pad = np.zeros((self.n_e, self.kin), dtype=dt)
         s_pad[:, :k] = ops.s
         self.S = to_dev(s_pad)
@@ -312,7 +316,7 @@ class BlasDevice:
         nsplit = sweep_splits(plan["n_tiles"], self.n_slabs)
         ld = nsplit * self.ko_pad
         isz = qt.element_size()
-        la.gemm(n_s * nrhs, self.k, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
+        la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
         if self.tc:
             nq = n_s * nrhs * self.kin
             qhi, qlo = qt[nq: 2 * nq], qt[2 * nq: 3 * nq]
@@ -345,7 +349,7 @@ class BlasDevice:
         la = self.la
         nsplit = sweep_splits(plan["n_tiles"], 1)
         ld = nsplit * self.ko_pad
-        la.gemm(n_s * nrhs, self.k, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
+        la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
         hi, lo = dense
         launch("kifmm_dense_split_tf32", P(qt), P(plan["src_slot"]), n_s, nrhs, self.kin,
                plan["h"], P(hi), P(lo), stream_handle())
@@ -367,7 +371,7 @@ class BlasDevice:
         la = self.la
         nsplit = sweep_splits(plan["n_tiles"], self.n_slabs)
         ld = nsplit * self.ko_pad
-        la.gemm(n_s * nrhs, self.k, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
+        la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
         if self.tc:
             nq = n_s * nrhs * self.kin
             qhi, qlo = qt[nq: 2 * nq], qt[2 * nq: 3 * nq]
