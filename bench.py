@@ -27,22 +27,23 @@ import sys
 import threading
 import time
 
-import numpy as np
-
-ROOT = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, ROOT)
-
-if __name__ == "__main__" and "reference" in sys.argv:
+if __name__ == "__main__" and any(a.endswith("reference") for a in sys.argv[1:]):
     # Reference arm thread policy: all cores for the OpenMP loops with active
     # waiting (the per-leaf P2M/L2P loops fork ~65k short parallel regions)
     # and single-threaded OpenBLAS (threaded OpenBLAS oversubscribes the
     # cores against the OpenMP team).  Measured on the B200 host (16 cores,
     # c2): this policy 1.70 s/evaluate; PASSIVE 3.73 s; ACTIVE + threaded
-    # OpenBLAS 9.98 s; see profiles/r1/README.md.
+    # OpenBLAS 9.98 s; see profiles/r1/README.md.  Must run before numpy loads
+    # OpenBLAS (it reads the thread count once, at load).
     _n = str(os.cpu_count() or 1)
     for _k, _v in (("OMP_WAIT_POLICY", "ACTIVE"), ("OMP_NUM_THREADS", _n),
                    ("KIFMM_THREADS", _n), ("OPENBLAS_NUM_THREADS", "1")):
         os.environ.setdefault(_k, _v)
+
+import numpy as np  # noqa: E402  (after the reference-arm thread policy)
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
 
 METRIC = "M2L GFLOP/s (% roofline) & FMM eval Mpoints/s, Laplace 3D, 1M pts, 1/2/4/8 GPU"
 CONFIG = dict(depth=5, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6)
@@ -286,11 +287,12 @@ def run_single(args):
         # 3xTF32 on the TF32 tensor pipe: dense TF32 = bf16 / 2 (same datapath),
         # three MMAs per fp32 product
         peak_tc = peaks["bf16_tflops"] / 2.0 / 3.0
-        execd = 3 * 2.0 * 128 * bd.kin * bd.ko_pad * 189 * \
-            dev.blas_plan_dev[lvl]["n_tiles"]
+        n_tiles = (dev.tma_plan if dev.tma else dev.blas_plan_dev)[lvl]["n_tiles"]
+        execd = 3 * 2.0 * 128 * bd.kin * bd.ko_pad * 189 * n_tiles
         gather_bytes = 2 * 4.0 * bd.kin * per_level[lvl]["pairs"]
         rooflines["m2l_sweep_tc_f32"] = dict(
-            bound="tensor", kernel=f"m2l_sweep_tc_f32 (level {lvl})",
+            bound="tensor",
+            kernel=f"m2l_sweep_{'tma' if dev.tma else 'tc'}_f32 (level {lvl})",
             achieved=algo / (sweep_ms / 1e3) / 1e12, peak=peak_tc, unit="TFLOP/s",
             frac=algo / (sweep_ms / 1e3) / 1e12 / peak_tc, traffic=None,
             algorithmic=f"4 k sum_t m_t k_t = {algo:.4g} flop at level {lvl} (SURVEY 8d)",
