@@ -35,6 +35,19 @@ int kifmm_laplace_potentials_f64(const double* tx, const double* ty, const doubl
                                  const double* sx, const double* sy, const double* sz, int64_t ns,
                                  const double* charges, int64_t nrhs, double* out, void* stream);
 
+/* Extension (no reference counterpart: the reference is potential-only;
+ * BASELINE config 3 asks for potential and gradient): direct sum of both,
+ * phi[i, r] += sum_j K q_j, grad[i, r, :] += sum_j q_j grad_t K(t_i, s_j)
+ * = -sum_j q_j (t_i - s_j) / (4 pi r^3), pairs with r == 0 skipped. */
+int kifmm_laplace_gradients_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
+                                const float* sx, const float* sy, const float* sz, int64_t ns,
+                                const float* charges, int64_t nrhs, float* phi, float* grad,
+                                void* stream);
+int kifmm_laplace_gradients_f64(const double* tx, const double* ty, const double* tz, int64_t nt,
+                                const double* sx, const double* sy, const double* sz, int64_t ns,
+                                const double* charges, int64_t nrhs, double* phi, double* grad,
+                                void* stream);
+
 /* Replaces _hot.laplace_matrix (_hot.pyx:68-88, hotloops.py:60-64): out[i, j] = K(t_i, s_j). */
 int kifmm_laplace_matrix_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
                              const float* sx, const float* sy, const float* sz, int64_t ns,
@@ -244,6 +257,25 @@ int kifmm_leaf_pass_f64(const double* tx, const double* ty, const double* tz,
                         const int32_t* sleaf_count, const int32_t* near_off,
                         const int32_t* near_leaf, int64_t nrhs, const int64_t* perm, int parts,
                         double* out, void* stream);
+/* Same pass with the potential gradient as well (config 3): grad[(perm[i] *
+ * nrhs + r) * 3 + c] (=|+= with parts & 4) from the same L2P densities and
+ * P2P sources.  grad must be non-NULL. */
+int kifmm_leaf_pass_grad_f32(const float* tx, const float* ty, const float* tz,
+                             const int32_t* tleaf_start, const int32_t* tleaf_count,
+                             int64_t n_tleaves, const double* centers, const double* base,
+                             int64_t ne, const float* local, const float* src4, int64_t ns,
+                             const int32_t* sleaf_start, const int32_t* sleaf_count,
+                             const int32_t* near_off, const int32_t* near_leaf, int64_t nrhs,
+                             const int64_t* perm, int parts, float* out, float* grad,
+                             void* stream);
+int kifmm_leaf_pass_grad_f64(const double* tx, const double* ty, const double* tz,
+                             const int32_t* tleaf_start, const int32_t* tleaf_count,
+                             int64_t n_tleaves, const double* centers, const double* base,
+                             int64_t ne, const double* local, const double* src4, int64_t ns,
+                             const int32_t* sleaf_start, const int32_t* sleaf_count,
+                             const int32_t* near_off, const int32_t* near_leaf, int64_t nrhs,
+                             const int64_t* perm, int parts, double* out, double* grad,
+                             void* stream);
 
 /* AoS source records for the leaf pass (16/32-byte aligned):
  * src4[(r*ns + j)*4 + {0,1,2,3}] = (x_j, y_j, z_j, q[j*nrhs + r]). */

@@ -340,6 +340,60 @@ def evaluate(inst, charges, threads=None, timings=None, state=None):
     return out
 
 
+def gradient_matrix(t, s):
+    """grad_t K(t, s) for K = 1/(4 pi |t - s|): (nt, ns, 3) float64, zero where
+    t == s.  No reference counterpart (the reference is potential-only); the
+    gradient of config 3 is checked against this and direct_gradient."""
+    d = np.asarray(t, dtype=np.float64)[:, None, :] - np.asarray(s, dtype=np.float64)[None, :, :]
+    r2 = np.einsum("ijk,ijk->ij", d, d)
+    with np.errstate(divide="ignore"):
+        w = np.where(r2 > 0, 1.0 / (4.0 * np.pi * r2 * np.sqrt(np.where(r2 > 0, r2, 1.0))), 0.0)
+    return -d * w[:, :, None]
+
+
+def direct_gradient(sources, charges, targets, chunk=2048):
+    """Float64 direct-sum potential gradient at every target: (nt, n_rhs, 3)."""
+    src = np.asarray(sources, dtype=np.float64).reshape(-1, 3)
+    tgt = np.asarray(targets, dtype=np.float64).reshape(-1, 3)
+    q = np.asarray(charges, dtype=np.float64).reshape(src.shape[0], -1)
+    out = np.zeros((tgt.shape[0], q.shape[1], 3))
+    for i0 in range(0, tgt.shape[0], chunk):
+        g = gradient_matrix(tgt[i0:i0 + chunk], src)          # (c, ns, 3)
+        out[i0:i0 + chunk] = np.einsum("isk,sr->irk", g, q)
+    return out
+
+
+def fmm_gradient(inst, charges, state):
+    """The FMM gradient in float64 from the local expansions a previous
+    ``evaluate(..., state=state)`` left in ``state["locals"]``: per target
+    leaf, grad of the downward-equivalent-surface field (the L2P operator
+    differentiated) plus the near-field direct gradient over the reference's
+    P2P source rows (engine.py:224-256).  Caller order, (nt, n_rhs, 3)."""
+    from paper_2408_07436_b200.engine import as_charge_matrix, leaf_centers, leaf_surface_base
+    cfg = inst.config
+    st, tt = inst.source_tree, inst.target_tree
+    depth = cfg.depth
+    q = as_charge_matrix(np.asarray(charges), st.n_points)
+    q_tree = np.asarray(q, dtype=np.float64)[st.perm]
+    loc = np.asarray(state["locals"][depth], dtype=np.float64)        # (n_leaves, n_rhs, n_e)
+    equiv = leaf_centers(tt)[:, None, :] + leaf_surface_base(
+        cfg.order_equiv, inst.domain.box_side(depth), cfg.outer_scale)[None]
+    near_idx, near_off = inst.near.source_rows(st)
+    tpts = np.stack([tt.x, tt.y, tt.z], axis=1)
+    spts = np.stack([st.x, st.y, st.z], axis=1)
+    grad = np.zeros((tt.n_points, q.shape[1], 3))
+    for i in range(tt.leaves.shape[0]):
+        s0 = int(tt.leaf_starts[i])
+        s1 = s0 + int(tt.leaf_counts[i])
+        t = tpts[s0:s1]
+        grad[s0:s1] += np.einsum("tsk,rs->trk", gradient_matrix(t, equiv[i]), loc[i])
+        rows = near_idx[near_off[i]:near_off[i + 1]]
+        grad[s0:s1] += np.einsum("tsk,sr->trk", gradient_matrix(t, spts[rows]), q_tree[rows])
+    out = np.empty_like(grad)
+    out[tt.perm] = grad
+    return out
+
+
 def direct(sources, charges, targets, dtype=np.float64, threads=None):
     """kernel.direct_potentials (kernel.py:83-103): the O(N^2) oracle."""
     src = np.asarray(sources, dtype=np.float64).reshape(-1, 3)

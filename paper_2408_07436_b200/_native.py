@@ -24,6 +24,8 @@ _C = ctypes.c_int
 SIGNATURES = {
     "kifmm_laplace_potentials_f32": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P],
     "kifmm_laplace_potentials_f64": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P],
+    "kifmm_laplace_gradients_f32": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P, _P],
+    "kifmm_laplace_gradients_f64": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P, _P],
     "kifmm_laplace_matrix_f32": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _P],
     "kifmm_laplace_matrix_f64": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _P],
     "kifmm_p2p_blocked_f32": [_P, _P, _P, _I, _P, _P, _P, _P, _P, _I, _P, _I, _P, _P],
@@ -52,6 +54,10 @@ SIGNATURES = {
                             _I, _P, _C, _P, _P],
     "kifmm_leaf_pass_f64": [_P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P,
                             _I, _P, _C, _P, _P],
+    "kifmm_leaf_pass_grad_f32": [_P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _P, _P, _P,
+                                 _P, _I, _P, _C, _P, _P, _P],
+    "kifmm_leaf_pass_grad_f64": [_P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _P, _P, _P,
+                                 _P, _I, _P, _C, _P, _P, _P],
     "kifmm_pack_sources_f32": [_P, _P, _P, _P, _I, _I, _P, _P],
     "kifmm_pack_sources_f64": [_P, _P, _P, _P, _I, _I, _P, _P],
     "kifmm_gather_charges_f32": [_P, _P, _I, _I, _P, _P],

@@ -41,6 +41,43 @@ __global__ void __launch_bounds__(kTile) potentials_kernel(
   }
 }
 
+// Potential and gradient by direct summation (the gradient is an extension:
+// the reference is potential-only; config 3 asks for both).  phi += sum q K,
+// grad += sum q grad_t K = -sum q (t - s) / (4 pi r^3); r2 == 0 skipped.
+template <typename T>
+__global__ void __launch_bounds__(kTile) gradients_kernel(
+    const T* __restrict__ tx, const T* __restrict__ ty, const T* __restrict__ tz, int64_t nt,
+    const T* __restrict__ sx, const T* __restrict__ sy, const T* __restrict__ sz, int64_t ns,
+    const T* __restrict__ q, int64_t nrhs, T* __restrict__ phi, T* __restrict__ grad) {
+  __shared__ T s_x[kTile], s_y[kTile], s_z[kTile];
+  int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  bool live = i < nt;
+  T x = live ? tx[i] : T(0), y = live ? ty[i] : T(0), z = live ? tz[i] : T(0);
+  for (int64_t r = 0; r < nrhs; ++r) {
+    T acc = T(0), gx = T(0), gy = T(0), gz = T(0);
+    for (int64_t j0 = 0; j0 < ns; j0 += kTile) {
+      int64_t j = j0 + threadIdx.x;
+      __syncthreads();
+      if (j < ns) { s_x[threadIdx.x] = sx[j]; s_y[threadIdx.x] = sy[j]; s_z[threadIdx.x] = sz[j]; }
+      __syncthreads();
+      int m = (int)min64(kTile, ns - j0);
+      for (int jj = 0; jj < m; ++jj) {
+        const T dx = x - s_x[jj], dy = y - s_y[jj], dz = z - s_z[jj];
+        const T w = inv_r<T>(dx, dy, dz);
+        const T qw = w * __ldg(&q[(j0 + jj) * nrhs + r]), qw3 = qw * w * w;
+        acc += qw;
+        gx -= dx * qw3; gy -= dy * qw3; gz -= dz * qw3;
+      }
+    }
+    if (live) {
+      const T c = real_traits<T>::inv4pi();
+      phi[i * nrhs + r] += acc * c;
+      T* g = grad + (i * nrhs + r) * 3;
+      g[0] += gx * c; g[1] += gy * c; g[2] += gz * c;
+    }
+  }
+}
+
 // out[i, j] = fl(1/4pi) / sqrt(r2): IEEE division and square root, so the
 // matrix is bit-identical to the reference's compiled loop.
 template <typename T>
@@ -95,6 +132,16 @@ __global__ void p2p_csr_kernel(const T* __restrict__ tx, const T* __restrict__ t
 }
 
 template <typename T>
+int gradients(const T* tx, const T* ty, const T* tz, int64_t nt, const T* sx, const T* sy,
+              const T* sz, int64_t ns, const T* q, int64_t nrhs, T* phi, T* grad, void* stream) {
+  if (nt < 0 || ns < 0 || nrhs < 1) return KIFMM_EARG;
+  if (nt == 0 || ns == 0) return 0;
+  gradients_kernel<T><<<ceil_div(nt, kTile), kTile, 0, (cudaStream_t)stream>>>(
+      tx, ty, tz, nt, sx, sy, sz, ns, q, nrhs, phi, grad);
+  return launch_status();
+}
+
+template <typename T>
 int potentials(const T* tx, const T* ty, const T* tz, int64_t nt, const T* sx, const T* sy,
                const T* sz, int64_t ns, const T* q, int64_t nrhs, T* out, void* stream) {
   if (nt < 0 || ns < 0 || nrhs < 1) return KIFMM_EARG;
@@ -138,6 +185,17 @@ int kifmm_laplace_potentials_f64(const double* tx, const double* ty, const doubl
                                  const double* sx, const double* sy, const double* sz, int64_t ns,
                                  const double* q, int64_t nrhs, double* out, void* s) {
   return potentials<double>(tx, ty, tz, nt, sx, sy, sz, ns, q, nrhs, out, s);
+}
+int kifmm_laplace_gradients_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
+                                const float* sx, const float* sy, const float* sz, int64_t ns,
+                                const float* q, int64_t nrhs, float* phi, float* grad, void* s) {
+  return gradients<float>(tx, ty, tz, nt, sx, sy, sz, ns, q, nrhs, phi, grad, s);
+}
+int kifmm_laplace_gradients_f64(const double* tx, const double* ty, const double* tz, int64_t nt,
+                                const double* sx, const double* sy, const double* sz, int64_t ns,
+                                const double* q, int64_t nrhs, double* phi, double* grad,
+                                void* s) {
+  return gradients<double>(tx, ty, tz, nt, sx, sy, sz, ns, q, nrhs, phi, grad, s);
 }
 int kifmm_laplace_matrix_f32(const float* tx, const float* ty, const float* tz, int64_t nt,
                              const float* sx, const float* sy, const float* sz, int64_t ns,

@@ -8,6 +8,9 @@
 //    The near field is walked as the reference orders it: the target's own
 //    leaf first, then its neighbour leaves by Morton code; sources are read
 //    in place from the tree-ordered arrays (no per-leaf duplication).
+//    The gradient variant (config 3, "potential and gradient"; the reference
+//    is potential-only) adds grad = sum q grad_t(1/(4 pi |t - s|)) over the
+//    same L2P and P2P sources.
 //
 // Surface points are formed from a float64 leaf centre and float64 unit
 // offsets with an exact add and one rounding, which reproduces the host's
@@ -73,25 +76,54 @@ template <typename T> struct cap_of { static constexpr int v = sizeof(T) == 4 ? 
 // with a target (they come from the target's own leaf), the rest cannot: two
 // points in different leaves have distinct coordinates, and every leaf
 // boundary lies >= 1 leaf side away from 0, so r2 cannot underflow either.
-template <typename T, bool TWO>
+// GRAD also accumulates g -= (t - s) q / r^3 (the gradient of q / r at t).
+template <typename T, bool TWO, bool GRAD>
 __device__ __forceinline__ void near_sum(const typename vec4<T>::v* buf, int m, int guarded,
-                                         T x0, T y0, T z0, T x1, T y1, T z1, T& a0, T& a1) {
+                                         T x0, T y0, T z0, T x1, T y1, T z1, T& a0, T& a1,
+                                         T (&g0)[3], T (&g1)[3]) {
   using V = typename vec4<T>::v;
   int k = 0;
   for (; k < guarded; ++k) {
     V s = buf[k];
-    a0 += inv_r<T>(x0 - s.x, y0 - s.y, z0 - s.z) * s.w;
-    if (TWO) a1 += inv_r<T>(x1 - s.x, y1 - s.y, z1 - s.z) * s.w;
+    if constexpr (GRAD) {
+      const T dx = x0 - s.x, dy = y0 - s.y, dz = z0 - s.z;
+      const T r2 = dx * dx + dy * dy + dz * dz;
+      const T ri = r2 > T(0) ? real_traits<T>::rsq(r2) : T(0);
+      const T w = ri * s.w, w3 = w * ri * ri;
+      a0 += w;
+      g0[0] -= dx * w3; g0[1] -= dy * w3; g0[2] -= dz * w3;
+      if (TWO) {
+        const T ex = x1 - s.x, ey = y1 - s.y, ez = z1 - s.z;
+        const T q2 = ex * ex + ey * ey + ez * ez;
+        const T qi = q2 > T(0) ? real_traits<T>::rsq(q2) : T(0);
+        const T v = qi * s.w, v3 = v * qi * qi;
+        a1 += v;
+        g1[0] -= ex * v3; g1[1] -= ey * v3; g1[2] -= ez * v3;
+      }
+    } else {
+      a0 += inv_r<T>(x0 - s.x, y0 - s.y, z0 - s.z) * s.w;
+      if (TWO) a1 += inv_r<T>(x1 - s.x, y1 - s.y, z1 - s.z) * s.w;
+    }
   }
   T b0 = 0, b1 = 0;
 #pragma unroll 4
   for (; k < m; ++k) {
     V s = buf[k];
     T dx = x0 - s.x, dy = y0 - s.y, dz = z0 - s.z;
-    b0 += real_traits<T>::rsq(dx * dx + dy * dy + dz * dz) * s.w;
+    const T ri = real_traits<T>::rsq(dx * dx + dy * dy + dz * dz);
+    b0 += ri * s.w;
+    if constexpr (GRAD) {
+      const T w3 = ri * ri * ri * s.w;
+      g0[0] -= dx * w3; g0[1] -= dy * w3; g0[2] -= dz * w3;
+    }
     if (TWO) {
       T ex = x1 - s.x, ey = y1 - s.y, ez = z1 - s.z;
-      b1 += real_traits<T>::rsq(ex * ex + ey * ey + ez * ez) * s.w;
+      const T qi = real_traits<T>::rsq(ex * ex + ey * ey + ez * ez);
+      b1 += qi * s.w;
+      if constexpr (GRAD) {
+        const T v3 = qi * qi * qi * s.w;
+        g1[0] -= ex * v3; g1[1] -= ey * v3; g1[2] -= ez * v3;
+      }
     }
   }
   a0 += b0;
@@ -113,7 +145,9 @@ __device__ __forceinline__ void stage_src(typename vec4<T>::v* dst, const typena
 // lane+32).  The near-field sources of the leaf - its own leaf first, then
 // the neighbours by Morton code - are staged from the AoS source array into
 // shared memory with cp.async, all segments in flight at once, then swept.
-template <typename T>
+// GRAD: also the potential gradient, grad[(perm[i] * nrhs + r) * 3 + c]
+// (L2P from the same downward equivalent densities + P2P gradient kernel).
+template <typename T, bool GRAD>
 __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
     const T* __restrict__ tx, const T* __restrict__ ty, const T* __restrict__ tz,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
@@ -121,7 +155,7 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
     const T* __restrict__ local, const typename vec4<T>::v* __restrict__ src4, int64_t ns,
     const int32_t* __restrict__ sstart, const int32_t* __restrict__ scount,
     const int32_t* __restrict__ near_off, const int32_t* __restrict__ near_leaf, int64_t nrhs,
-    const int64_t* __restrict__ perm, int parts, T* __restrict__ out) {
+    const int64_t* __restrict__ perm, int parts, T* __restrict__ out, T* __restrict__ grad) {
   using V = typename vec4<T>::v;
   constexpr int kCap = cap_of<T>::v;
   __shared__ __align__(16) V sbuf[kWarps][kCap];
@@ -141,6 +175,7 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
     const T x1 = live1 ? tx[i1] : T(0), y1 = live1 ? ty[i1] : T(0), z1 = live1 ? tz[i1] : T(0);
     for (int64_t r = 0; r < nrhs; ++r) {
       T far0 = 0, far1 = 0, near0 = 0, near1 = 0;
+      T gf0[3] = {0, 0, 0}, gf1[3] = {0, 0, 0}, gn0[3] = {0, 0, 0}, gn1[3] = {0, 0, 0};
       // L2P: downward equivalent densities of the leaf -> its targets.
       const T* loc = local + (b * nrhs + r) * ne;
       for (int64_t e0 = 0; (parts & 1) && e0 < ne; e0 += kCap) {
@@ -153,8 +188,8 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
                      real_traits<T>::from_d(exact_add(cz, base[e * 3 + 2])), loc[e]};
         }
         __syncwarp();
-        if (two) near_sum<T, true>(buf, m, m, x0, y0, z0, x1, y1, z1, far0, far1);
-        else near_sum<T, false>(buf, m, m, x0, y0, z0, x1, y1, z1, far0, far1);
+        if (two) near_sum<T, true, GRAD>(buf, m, m, x0, y0, z0, x1, y1, z1, far0, far1, gf0, gf1);
+        else near_sum<T, false, GRAD>(buf, m, m, x0, y0, z0, x1, y1, z1, far0, far1, gf0, gf1);
       }
       // P2P: own leaf first, then neighbours in Morton order.
       if (parts & 2) {
@@ -166,8 +201,8 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
           cp_async_wait<0>();
           __syncwarp();
           const int g = min(guarded, fill);
-          if (two) near_sum<T, true>(buf, fill, g, x0, y0, z0, x1, y1, z1, near0, near1);
-          else near_sum<T, false>(buf, fill, g, x0, y0, z0, x1, y1, z1, near0, near1);
+          if (two) near_sum<T, true, GRAD>(buf, fill, g, x0, y0, z0, x1, y1, z1, near0, near1, gn0, gn1);
+          else near_sum<T, false, GRAD>(buf, fill, g, x0, y0, z0, x1, y1, z1, near0, near1, gn0, gn1);
           guarded -= g;
           fill = 0;
           __syncwarp();
@@ -189,14 +224,32 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
       }
       const T c = real_traits<T>::inv4pi();
       if (live0) {
-        T* o = out + (perm ? perm[i0] : i0) * nrhs + r;
+        const int64_t row = (perm ? perm[i0] : i0) * nrhs + r;
+        T* o = out + row;
         const T v = far0 * c + near0 * c;
         *o = (parts & 4) ? *o + v : v;
+        if constexpr (GRAD) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            T* gp = grad + row * 3 + d;
+            const T gv = gf0[d] * c + gn0[d] * c;
+            *gp = (parts & 4) ? *gp + gv : gv;
+          }
+        }
       }
       if (two && live1) {
-        T* o = out + (perm ? perm[i1] : i1) * nrhs + r;
+        const int64_t row = (perm ? perm[i1] : i1) * nrhs + r;
+        T* o = out + row;
         const T v = far1 * c + near1 * c;
         *o = (parts & 4) ? *o + v : v;
+        if constexpr (GRAD) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            T* gp = grad + row * 3 + d;
+            const T gv = gf1[d] * c + gn1[d] * c;
+            *gp = (parts & 4) ? *gp + gv : gv;
+          }
+        }
       }
     }
   }
@@ -229,13 +282,18 @@ int leaf_pass(const T* tx, const T* ty, const T* tz, const int32_t* ts, const in
               int64_t ntl, const double* centers, const double* base, int64_t ne, const T* local,
               const T* src4, int64_t ns, const int32_t* ss, const int32_t* sc, const int32_t* no,
               const int32_t* nlf, int64_t nrhs, const int64_t* perm, int parts, T* out,
-              void* stream) {
+              T* grad, void* stream) {
   if (ntl < 0 || ne < 1 || nrhs < 1 || parts < 1 || parts > 7 || ns < 0) return KIFMM_EARG;
   if (ntl == 0) return 0;
-  leaf_pass_kernel<T><<<ceil_div(ntl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
-      tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local,
-      reinterpret_cast<const typename vec4<T>::v*>(src4), ns, ss, sc, no, nlf, nrhs, perm, parts,
-      out);
+  const auto* s4 = reinterpret_cast<const typename vec4<T>::v*>(src4);
+  if (grad)
+    leaf_pass_kernel<T, true><<<ceil_div(ntl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
+        tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local, s4, ns, ss, sc, no, nlf, nrhs, perm,
+        parts, out, grad);
+  else
+    leaf_pass_kernel<T, false><<<ceil_div(ntl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
+        tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local, s4, ns, ss, sc, no, nlf, nrhs, perm,
+        parts, out, nullptr);
   return launch_status();
 }
 
@@ -272,7 +330,7 @@ int kifmm_leaf_pass_f32(const float* tx, const float* ty, const float* tz, const
                         const int32_t* nlf, int64_t nrhs, const int64_t* perm, int parts,
                         float* out, void* s) {
   return leaf_pass<float>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, src4, ns, ss, sc, no,
-                          nlf, nrhs, perm, parts, out, s);
+                          nlf, nrhs, perm, parts, out, nullptr, s);
 }
 int kifmm_leaf_pass_f64(const double* tx, const double* ty, const double* tz, const int32_t* ts,
                         const int32_t* tc, int64_t ntl, const double* centers, const double* base,
@@ -281,7 +339,28 @@ int kifmm_leaf_pass_f64(const double* tx, const double* ty, const double* tz, co
                         const int32_t* nlf, int64_t nrhs, const int64_t* perm, int parts,
                         double* out, void* s) {
   return leaf_pass<double>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, src4, ns, ss, sc,
-                           no, nlf, nrhs, perm, parts, out, s);
+                           no, nlf, nrhs, perm, parts, out, nullptr, s);
+}
+int kifmm_leaf_pass_grad_f32(const float* tx, const float* ty, const float* tz, const int32_t* ts,
+                             const int32_t* tc, int64_t ntl, const double* centers,
+                             const double* base, int64_t ne, const float* local, const float* src4,
+                             int64_t ns, const int32_t* ss, const int32_t* sc, const int32_t* no,
+                             const int32_t* nlf, int64_t nrhs, const int64_t* perm, int parts,
+                             float* out, float* grad, void* s) {
+  if (!grad) return KIFMM_EARG;
+  return leaf_pass<float>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, src4, ns, ss, sc, no,
+                          nlf, nrhs, perm, parts, out, grad, s);
+}
+int kifmm_leaf_pass_grad_f64(const double* tx, const double* ty, const double* tz,
+                             const int32_t* ts, const int32_t* tc, int64_t ntl,
+                             const double* centers, const double* base, int64_t ne,
+                             const double* local, const double* src4, int64_t ns,
+                             const int32_t* ss, const int32_t* sc, const int32_t* no,
+                             const int32_t* nlf, int64_t nrhs, const int64_t* perm, int parts,
+                             double* out, double* grad, void* s) {
+  if (!grad) return KIFMM_EARG;
+  return leaf_pass<double>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, src4, ns, ss, sc,
+                           no, nlf, nrhs, perm, parts, out, grad, s);
 }
 int kifmm_pack_sources_f32(const float* sx, const float* sy, const float* sz, const float* q,
                            int64_t ns, int64_t nrhs, float* out, void* s) {

@@ -571,7 +571,7 @@ class DeviceFmm:
         return self._l2l_rowmaps[key]
 
     # ------------------------------------------------------------- evaluate
-    def evaluate_device(self, q_dev, nrhs, timings=False):
+    def evaluate_device(self, q_dev, nrhs, timings=False, gradient=False):
         """Full evaluate from float64 charges on the device (caller order,
         (n_src, R) C-contiguous) to potentials on the device (caller order,
         (n_tgt, R), working dtype).  Returns the output tensor (a view of an
@@ -636,41 +636,51 @@ class DeviceFmm:
                          rowmap=self._l2l_rowmap(lvl + 1, R), accumulate=True)
         phase("leaf")
         out = b["out"]
-        launch(f"kifmm_leaf_pass_{sfx}", P(self.tx), P(self.ty), P(self.tz), P(self.t_start),
-                 P(self.t_count), self.n_tgt[d], P(self.t_centers), P(self.equiv_base), n_e,
-               P(loc[d]), P(b["src4"]), self.sx.shape[0], P(self.s_start), P(self.s_count),
-               P(self.near_off), P(self.near_leaf), R, P(self.t_perm), 3, P(out), s)
+        leaf_args = [P(self.tx), P(self.ty), P(self.tz), P(self.t_start), P(self.t_count),
+                     self.n_tgt[d], P(self.t_centers), P(self.equiv_base), n_e, P(loc[d]),
+                     P(b["src4"]), self.sx.shape[0], P(self.s_start), P(self.s_count),
+                     P(self.near_off), P(self.near_leaf), R, P(self.t_perm), 3, P(out)]
+        nt = self.tx.shape[0]
+        if gradient:
+            if "grad" not in b:
+                b["grad"] = torch.empty(nt * R * 3, dtype=self.T, device=out.device)
+            launch(f"kifmm_leaf_pass_grad_{sfx}", *leaf_args, P(b["grad"]), s)
+        else:
+            launch(f"kifmm_leaf_pass_{sfx}", *leaf_args, s)
         phase("end")
         self.last_m2l_calls = calls
         self._events = ev
-        return out[: self.tx.shape[0] * R].view(self.tx.shape[0], R)
+        if gradient:
+            return out[: nt * R].view(nt, R), b["grad"][: nt * R * 3].view(nt, R, 3)
+        return out[: nt * R].view(nt, R)
 
     # ------------------------------------------------------------ CUDA graph
-    def graph_for(self, nrhs):
+    def graph_for(self, nrhs, gradient=False):
         """The whole evaluate captured once as a CUDA graph (one launch per
         evaluate instead of ~30 host-side kernel launches).  Returns
-        (graph, static float64 charge buffer (n_src*R,), output tensor)."""
+        (graph, static float64 charge buffer (n_src*R,), output tensor(s))."""
         if not hasattr(self, "_graphs"):
             self._graphs = {}
-        if nrhs not in self._graphs:
+        key = (nrhs, bool(gradient))
+        if key not in self._graphs:
             static_q = torch.zeros(self.sx.shape[0] * nrhs, dtype=torch.float64,
                                    device=self.sx.device)
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
                 for _ in range(2):                   # allocate buffers, cache plans
-                    self.evaluate_device(static_q, nrhs)
+                    self.evaluate_device(static_q, nrhs, gradient=gradient)
             torch.cuda.current_stream().wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                out = self.evaluate_device(static_q, nrhs)
-            self._graphs[nrhs] = (g, static_q, out)
-        return self._graphs[nrhs]
+                out = self.evaluate_device(static_q, nrhs, gradient=gradient)
+            self._graphs[key] = (g, static_q, out)
+        return self._graphs[key]
 
-    def evaluate_graphed(self, q_dev, nrhs):
+    def evaluate_graphed(self, q_dev, nrhs, gradient=False):
         """evaluate_device through the captured graph (q_dev: float64 device
-        charges, caller order).  Returns the graph's output tensor."""
-        g, static_q, out = self.graph_for(nrhs)
+        charges, caller order).  Returns the graph's output tensor(s)."""
+        g, static_q, out = self.graph_for(nrhs, gradient)
         static_q.copy_(q_dev.reshape(-1))
         g.replay()
         return out
@@ -689,7 +699,7 @@ class DeviceFmm:
         t["leaf_fused"] = 1.0      # l2p is fused into the p2p leaf pass
         return t
 
-    def evaluate_host(self, q_host: np.ndarray, timings=False) -> np.ndarray:
+    def evaluate_host(self, q_host: np.ndarray, timings=False, gradient=False):
         """Host charges (n_src, R) float64 in caller order -> host potentials.
 
         The charges are copied straight into the captured graph's input
@@ -702,13 +712,16 @@ class DeviceFmm:
             b = self._buffers(R)
             qin = b["qin"][: q_host.size]
             qin.copy_(src)
-            out = self.evaluate_device(qin, R, timings=True)
-            res = out.cpu().numpy().copy()
+            out = self.evaluate_device(qin, R, timings=True, gradient=gradient)
             self.last_timings = self.collect_timings()
-            return res
-        g, static_q, out = self.graph_for(R)
+            if gradient:
+                return out[0].cpu().numpy().copy(), out[1].cpu().numpy().copy()
+            return out.cpu().numpy().copy()
+        g, static_q, out = self.graph_for(R, gradient)
         static_q.copy_(src)
         g.replay()
+        if gradient:
+            return out[0].cpu().numpy(), out[1].cpu().numpy()
         return out.cpu().numpy()
 
 

@@ -200,8 +200,8 @@ class FmmInstance:
     # un-graphed evaluate; off by default
     profile: bool = False
 
-    def evaluate(self, charges):
-        return evaluate(self, charges)
+    def evaluate(self, charges, gradient=False):
+        return evaluate(self, charges, gradient)
 
     def attach_charges(self, charges):
         return evaluate(self, charges)
@@ -273,19 +273,27 @@ def as_charge_matrix(charges, n_sources: int) -> np.ndarray:
     raise ValueError(f"charge array shape {q.shape} does not match {n_sources} sources")
 
 
-def evaluate(inst: FmmInstance, charges) -> np.ndarray:
+def evaluate(inst: FmmInstance, charges, gradient=False):
     """Potentials at every target (caller order) for one or more charge
-    columns; the whole evaluate runs on the GPU."""
+    columns; the whole evaluate runs on the GPU.
+
+    ``gradient=True`` (an extension: the reference is potential-only,
+    BASELINE config 3 asks for both) returns ``(potentials, gradients)``
+    with ``gradients.shape == potentials.shape + (3,)``: the gradient of the
+    potential at each target, from the same local expansions (L2P) and near
+    field (P2P)."""
     q_in = np.asarray(charges)
     q = np.ascontiguousarray(as_charge_matrix(q_in, inst.source_tree.n_points), dtype=np.float64)
     inst._last_charges = q
-    out = inst.device.evaluate_host(q, timings=inst.profile)
+    res = inst.device.evaluate_host(q, timings=inst.profile, gradient=gradient)
+    out, grad = res if gradient else (res, None)
     if inst.profile:
         inst.timings = dict(inst.device.last_timings)
     inst.m2l_calls = list(inst.device.last_m2l_calls)
     if q_in.ndim == 1 and q.shape[1] == 1:
-        return out[:, 0]
-    return out
+        out = out[:, 0]
+        grad = grad[:, 0] if grad is not None else None
+    return (out, grad) if gradient else out
 
 
 def relative_error(inst: FmmInstance, potentials, leaf=None) -> ErrorStats:

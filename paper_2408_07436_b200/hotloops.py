@@ -58,6 +58,28 @@ def laplace_potentials(tx, ty, tz, sx, sy, sz, charges, out, threads=None):
     return out
 
 
+def laplace_gradients(tx, ty, tz, sx, sy, sz, charges, out, grad, threads=None):
+    """out[i, r] += sum_j K q, grad[i, r, :] += sum_j q grad_t K (extension of
+    laplace_potentials; the reference has no gradient loop).  ``grad`` is
+    shaped ``out.shape + (3,)``."""
+    from . import _native as nat
+    from .device import P, require_cuda, stream_handle
+    require_cuda()
+    dt = _check_dtype(tx, ty, tz, sx, sy, sz, charges, out, grad)
+    nt, ns = np.asarray(tx).shape[0], np.asarray(sx).shape[0]
+    q = np.ascontiguousarray(charges).reshape(ns, -1)
+    if np.shape(grad) != tuple(np.shape(out)) + (3,):
+        raise ValueError("grad must be shaped out.shape + (3,)")
+    d = _upload(tx, ty, tz, sx, sy, sz, q, np.ascontiguousarray(out).reshape(nt, -1),
+                np.ascontiguousarray(grad).reshape(nt, -1))
+    if nt and ns:
+        nat.call(f"kifmm_laplace_gradients_{_sfx(dt)}", P(d[0]), P(d[1]), P(d[2]), nt, P(d[3]),
+                 P(d[4]), P(d[5]), ns, P(d[6]), q.shape[1], P(d[7]), P(d[8]), stream_handle())
+    out[...] = d[7].cpu().numpy().reshape(np.shape(out))
+    grad[...] = d[8].cpu().numpy().reshape(np.shape(grad))
+    return out, grad
+
+
 def laplace_matrix(tx, ty, tz, sx, sy, sz, out=None, threads=None):
     """out[i, j] = K(t_i, s_j), overwritten (reference _hot.pyx:68-88)."""
     import torch

@@ -227,3 +227,62 @@ def test_partitioned_evaluate_matches_single_device(cuda, backend, precision):
         got = evaluate_local(inst, world, q)[:, 0]
         rel = np.abs(got - ref) / np.abs(ref)
         assert rel.max() <= TOL[precision], (world, rel.max())
+
+
+# ------------------------------------------------------------------ gradient
+# The reference is potential-only: the gradient (BASELINE config 3) has no
+# reference oracle ("parity unpinned").  It is checked against
+# the oracle's float64 restatement of the same FMM gradient (oracle/port.py
+# fmm_gradient, from the oracle's own local expansions) and against the
+# float64 direct-sum gradient.
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_direct_gradient_kernel(cuda, precision):
+    from oracle import port
+    from paper_2408_07436_b200 import hotloops
+    dt = np.float32 if precision == "f32" else np.float64
+    rng = np.random.default_rng(3)
+    t, s = rng.random((700, 3)), rng.random((900, 3))
+    s[:50] = t[:50]                                       # coincident pairs are skipped
+    q = rng.uniform(-1, 1, (900, 2))
+    phi = np.zeros((700, 2), dt)
+    grad = np.zeros((700, 2, 3), dt)
+    c = lambda a, k: np.ascontiguousarray(a[:, k], dtype=dt)
+    hotloops.laplace_gradients(c(t, 0), c(t, 1), c(t, 2), c(s, 0), c(s, 1), c(s, 2),
+                               q.astype(dt), phi, grad)
+    want = port.direct_gradient(s.astype(dt), q.astype(dt), t.astype(dt))
+    tol = 2e-5 if dt == np.float32 else 1e-12
+    assert np.linalg.norm(grad - want) / np.linalg.norm(want) < tol
+    assert np.linalg.norm(phi - port.direct(s, q, t)) / np.linalg.norm(phi) < tol
+
+
+@pytest.mark.parametrize("kw,tol_port,tol_direct", [
+    (dict(depth=3, order_equiv=8, backend="fft", precision="f64"), 1e-10, 2e-6),
+    (dict(depth=3, order_equiv=6, backend="blas", precision="f64", sigma_min=1e-12), 1e-10, 1e-4),
+    (dict(depth=3, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6), 2e-5, 3e-3),
+])
+def test_evaluate_gradient(cuda, kw, tol_port, tol_direct):
+    from oracle import port
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(7)
+    pts = rng.random((5000, 3))
+    q = np.random.default_rng(11).uniform(-1, 1, 5000)
+    inst = setup(pts, pts, FmmConfig(**kw))
+    phi, grad = inst.evaluate(q, gradient=True)
+    assert phi.shape == (5000,) and grad.shape == (5000, 3)
+    # the potential agrees with the potential-only pass (the gradient pass
+    # rounds the own-leaf terms through one more product)
+    ptol = 1e-6 if kw["precision"] == "f32" else 1e-13
+    assert np.allclose(phi, inst.evaluate(q), rtol=ptol, atol=ptol * np.abs(phi).max())
+    st = {}
+    port.evaluate(inst, q, state=st)
+    want = port.fmm_gradient(inst, q, st)[:, 0]
+    assert np.linalg.norm(grad - want) / np.linalg.norm(want) < tol_port
+    exact = port.direct_gradient(pts, q, pts)[:, 0]
+    assert np.linalg.norm(grad - exact) / np.linalg.norm(exact) < tol_direct
+    # multi-RHS: columns are independent
+    q2 = np.stack([q, 2.0 * q], axis=1)
+    phi2, grad2 = inst.evaluate(q2, gradient=True)
+    assert grad2.shape == (5000, 2, 3)
+    assert np.allclose(grad2[:, 0], grad, rtol=1e-6 if kw["precision"] == "f32" else 1e-12,
+                       atol=1e-6 * np.abs(grad).max())
+    assert np.allclose(grad2[:, 1], 2.0 * grad2[:, 0], rtol=1e-5, atol=1e-5 * np.abs(grad).max())

@@ -45,3 +45,30 @@ def test_evaluate(name):
     # same host as the generator -> bit-identical; elsewhere BLAS rounding may differ
     tol = 1e-6 if want.dtype == np.float32 else 1e-13
     assert np.abs(got - want).max() <= tol * np.abs(want).max()
+
+
+def test_gradient_restatement_against_direct_sum():
+    """The oracle's FMM gradient (no reference counterpart) converges to the
+    float64 direct-sum gradient at the accuracy of the expansion order."""
+    from oracle import port
+    from paper_2408_07436_b200 import FmmConfig, setup
+    pts = np.random.default_rng(7).random((2000, 3))
+    q = np.random.default_rng(11).uniform(-1, 1, 2000)
+    exact = port.direct_gradient(pts, q, pts)
+    errs = []
+    for p in (4, 6):
+        inst = setup(pts, pts, FmmConfig(depth=3, order_equiv=p, backend="fft", precision="f64"))
+        st = {}
+        port.evaluate(inst, q, state=st)
+        g = port.fmm_gradient(inst, q, st)
+        errs.append(np.linalg.norm(g - exact) / np.linalg.norm(exact))
+    assert errs[0] < 1e-3 and errs[1] < errs[0] / 10
+    # finite-difference check of the direct gradient itself (off-source points)
+    h = 1e-5
+    t = np.random.default_rng(5).random((5, 3))
+    g = port.direct_gradient(pts, q, t)
+    for k in range(3):
+        e = np.zeros(3)
+        e[k] = h
+        fd = (port.direct(pts, q, t + e) - port.direct(pts, q, t - e)) / (2 * h)
+        assert np.allclose(fd[:, 0], g[:, 0, k], rtol=1e-5, atol=1e-8 * np.abs(g).max())
