@@ -15,11 +15,23 @@
 // Surface points are formed from a float64 leaf centre and float64 unit
 // offsets with an exact add and one rounding, which reproduces the host's
 // per-leaf surface arrays (engine.py:149-156) bit for bit.
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 
 using namespace kifmm;
 
 namespace {
+
+inline bool getenv_flag(const char* name) {
+  static int cached = -1;
+  if (cached < 0) {
+    const char* v = std::getenv(name);
+    cached = (v && *v && *v != '0') ? 1 : 0;
+  }
+  return cached == 1;
+}
 
 template <typename T> struct vec4;
 template <> struct vec4<float> { using v = float4; };
@@ -255,6 +267,219 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// float32 leaf pass on packed FP32 (FFMA2/FADD2/FMUL2, sm_100's f32x2 ops).
+// The scalar pass is issue-bound (~8 instructions per interaction); here two
+// interactions share each vector instruction:
+//  * leaves of <= 32 targets: a lane's target against a PAIR of sources,
+//    staged as [xA xB yA yB zA zB qA qB] so two LDS.128 yield packed pairs;
+//  * leaves of 33..64 targets: a PAIR of targets (lane, lane + 32) against
+//    one source, its coordinates used as broadcast scalars (no moves).
+// 9 vector/MUFU instructions per 2 interactions.  Same sources, order of
+// traversal and guard semantics as leaf_pass_kernel (the sums are split
+// into two interleaved partial sums, so rounding differs in the last bits).
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 up2(u64 v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+// 1/sqrt of both halves; GUARD: 0 where r2 == 0 (coincident points).
+template <bool GUARD>
+__device__ __forceinline__ u64 rsq2(u64 r2) {
+  const float2 v = up2(r2);
+  float a = real_traits<float>::rsq(v.x), b = real_traits<float>::rsq(v.y);
+  if (GUARD) {
+    a = v.x > 0.f ? a : 0.f;
+    b = v.y > 0.f ? b : 0.f;
+  }
+  return pk2(a, b);
+}
+
+constexpr int kPairCap = 256;              // source pairs staged per warp (512 sources)
+constexpr float kFar = 1e18f;              // padding source: r2 ~ 1e36, charge 0
+
+// Stage source record j of the current fill into the paired layout.
+__device__ __forceinline__ void stage_pair(float* buf, int j, const float4* src) {
+  float* rec = buf + (j >> 1) * 8 + (j & 1);
+  const float* g = reinterpret_cast<const float*>(src);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(rec + 2 * c);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(g + c));
+  }
+}
+
+// Sum over pairs [0, np); pairs below `gpairs` may hold coincident points.
+// Two accumulators alternate so consecutive pairs do not serialise on one
+// FFMA2 dependency chain.
+template <bool TWO>
+__device__ __forceinline__ void pair_sum(const float* buf, int np, int gpairs, u64 X, u64 Y,
+                                         u64 Z, float x0, float y0, float z0, u64& acc) {
+  const float4* b4 = reinterpret_cast<const float4*>(buf);
+  u64 acc2 = pk2(0.f, 0.f);
+  auto body = [&](int p, u64& a_, auto guard) {
+    constexpr bool G = decltype(guard)::value;
+    const float4 a = b4[2 * p], b = b4[2 * p + 1];   // (xA xB yA yB), (zA zB qA qB)
+    if (TWO) {
+      // targets (lane, lane+32) against source A, then source B
+      u64 dx = sub2(X, pk2(a.x, a.x)), dy = sub2(Y, pk2(a.z, a.z)), dz = sub2(Z, pk2(b.x, b.x));
+      u64 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+      a_ = fma2(rsq2<G>(r2), pk2(b.z, b.z), a_);
+      dx = sub2(X, pk2(a.y, a.y)); dy = sub2(Y, pk2(a.w, a.w)); dz = sub2(Z, pk2(b.y, b.y));
+      r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+      a_ = fma2(rsq2<G>(r2), pk2(b.w, b.w), a_);
+    } else {
+      // this lane's target against sources (A, B)
+      const u64 dx = sub2(pk2(x0, x0), pk2(a.x, a.y));
+      const u64 dy = sub2(pk2(y0, y0), pk2(a.z, a.w));
+      const u64 dz = sub2(pk2(z0, z0), pk2(b.x, b.y));
+      const u64 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+      a_ = fma2(rsq2<G>(r2), pk2(b.z, b.w), a_);
+    }
+  };
+  int p = 0;
+  for (; p < gpairs; ++p) body(p, acc, std::true_type{});
+#pragma unroll 2
+  for (; p + 1 < np; p += 2) {
+    body(p, acc, std::false_type{});
+    body(p + 1, acc2, std::false_type{});
+  }
+  if (p < np) body(p, acc, std::false_type{});
+  const float2 u = up2(acc), v = up2(acc2);
+  acc = pk2(u.x + v.x, u.y + v.y);
+}
+
+__global__ void __launch_bounds__(32 * kWarps) leaf_pass_x2_kernel(
+    const float* __restrict__ tx, const float* __restrict__ ty, const float* __restrict__ tz,
+    const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
+    const double* __restrict__ centers, const double* __restrict__ base, int64_t ne,
+    const float* __restrict__ local, const float4* __restrict__ src4, int64_t ns,
+    const int32_t* __restrict__ sstart, const int32_t* __restrict__ scount,
+    const int32_t* __restrict__ near_off, const int32_t* __restrict__ near_leaf, int64_t nrhs,
+    const int64_t* __restrict__ perm, int parts, float* __restrict__ out) {
+  constexpr int kCap = 2 * kPairCap;
+  __shared__ __align__(16) float sbuf[kWarps][kPairCap * 8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* buf = sbuf[w];
+  const int64_t b = (int64_t)blockIdx.x * kWarps + w;
+  if (b >= n_tleaves) return;
+  const int64_t t0 = tstart[b];
+  const int tc = tcount[b];
+  const double cx = centers[b * 3], cy = centers[b * 3 + 1], cz = centers[b * 3 + 2];
+  const int n0 = near_off[b], n1 = near_off[b + 1];
+  // The near-field segments (<= 27 leaves) are looked up by all lanes at
+  // once and broadcast with shuffles: no serial chain of dependent loads.
+  int seg_start = 0, seg_cnt = 0;
+  if (lane < n1 - n0) {
+    const int sl = near_leaf[n0 + lane];
+    seg_start = sstart[sl];
+    seg_cnt = scount[sl];
+  }
+  // pad slot m (odd fills): far away, zero charge
+  auto pad = [&](int m) {
+    if ((m & 1) && lane == 0) {
+      float* rec = buf + (m >> 1) * 8 + 1;
+      rec[0] = kFar; rec[2] = kFar; rec[4] = kFar; rec[6] = 0.f;
+    }
+  };
+  for (int tb = 0; tb < tc; tb += 64) {
+    const bool two = tc - tb > 32;                 // warp-uniform
+    const bool live0 = tb + lane < tc, live1 = tb + 32 + lane < tc;
+    const int64_t i0 = t0 + tb + lane, i1 = i0 + 32;
+    const float x0 = live0 ? tx[i0] : 0.f, y0 = live0 ? ty[i0] : 0.f, z0 = live0 ? tz[i0] : 0.f;
+    const float x1 = live1 ? tx[i1] : 0.f, y1 = live1 ? ty[i1] : 0.f, z1 = live1 ? tz[i1] : 0.f;
+    const u64 X = pk2(x0, x1), Y = pk2(y0, y1), Z = pk2(z0, z1);
+    for (int64_t r = 0; r < nrhs; ++r) {
+      u64 far = pk2(0.f, 0.f), near = pk2(0.f, 0.f);
+      // L2P: downward equivalent densities of the leaf -> its targets.
+      const float* loc = local + (b * nrhs + r) * ne;
+      for (int64_t e0 = 0; (parts & 1) && e0 < ne; e0 += kCap) {
+        const int m = (int)min64(kCap, ne - e0);
+        __syncwarp();
+        for (int k = lane; k < m; k += 32) {
+          const int64_t e = e0 + k;
+          float* rec = buf + (k >> 1) * 8 + (k & 1);
+          rec[0] = real_traits<float>::from_d(exact_add(cx, base[e * 3]));
+          rec[2] = real_traits<float>::from_d(exact_add(cy, base[e * 3 + 1]));
+          rec[4] = real_traits<float>::from_d(exact_add(cz, base[e * 3 + 2]));
+          rec[6] = loc[e];
+        }
+        pad(m);
+        __syncwarp();
+        if (two) pair_sum<true>(buf, (m + 1) >> 1, 0, X, Y, Z, x0, y0, z0, far);
+        else pair_sum<false>(buf, (m + 1) >> 1, 0, X, Y, Z, x0, y0, z0, far);
+      }
+      // P2P: own leaf first, then neighbours in Morton order.
+      if (parts & 2) {
+        const float4* srow = src4 + r * ns;
+        int fill = 0;
+        int guarded = __shfl_sync(0xffffffffu, seg_cnt, 0);
+        auto flush = [&]() {
+          cp_async_commit();
+          cp_async_wait<0>();
+          pad(fill);
+          __syncwarp();
+          const int g = min(guarded, fill);
+          const int np = (fill + 1) >> 1, gp = (g + 1) >> 1;
+          if (two) pair_sum<true>(buf, np, gp, X, Y, Z, x0, y0, z0, near);
+          else pair_sum<false>(buf, np, gp, X, Y, Z, x0, y0, z0, near);
+          guarded -= g;
+          fill = 0;
+          __syncwarp();
+        };
+        __syncwarp();
+        for (int n = 0; n < n1 - n0; ++n) {
+          const int64_t j0 = __shfl_sync(0xffffffffu, seg_start, n & 31);
+          const int jc = __shfl_sync(0xffffffffu, seg_cnt, n & 31);
+          for (int jb = 0; jb < jc;) {
+            if (fill == kCap) flush();
+            const int m = min(jc - jb, kCap - fill);
+            for (int k = lane; k < m; k += 32) stage_pair(buf, fill + k, srow + j0 + jb + k);
+            fill += m;
+            jb += m;
+          }
+        }
+        if (fill) flush();
+      }
+      const float c = real_traits<float>::inv4pi();
+      const float2 fv = up2(far), nv = up2(near);
+      // single mode: (x, y) halves are two partial sums of the same target;
+      // two mode: they are the two targets.
+      const float v0 = two ? fv.x * c + nv.x * c : (fv.x + fv.y) * c + (nv.x + nv.y) * c;
+      if (live0) {
+        float* o = out + (perm ? perm[i0] : i0) * nrhs + r;
+        *o = (parts & 4) ? *o + v0 : v0;
+      }
+      if (two && live1) {
+        float* o = out + (perm ? perm[i1] : i1) * nrhs + r;
+        const float v1 = fv.y * c + nv.y * c;
+        *o = (parts & 4) ? *o + v1 : v1;
+      }
+    }
+  }
+}
+
 // AoS source records for the leaf pass: out[r*ns + j] = (x_j, y_j, z_j, q[j*nrhs + r]).
 template <typename T>
 __global__ void pack_sources_kernel(const T* __restrict__ sx, const T* __restrict__ sy,
@@ -286,6 +511,14 @@ int leaf_pass(const T* tx, const T* ty, const T* tz, const int32_t* ts, const in
   if (ntl < 0 || ne < 1 || nrhs < 1 || parts < 1 || parts > 7 || ns < 0) return KIFMM_EARG;
   if (ntl == 0) return 0;
   const auto* s4 = reinterpret_cast<const typename vec4<T>::v*>(src4);
+  if constexpr (sizeof(T) == 4) {
+    if (!grad && !getenv_flag("KIFMM_LEAF_SCALAR")) {
+      leaf_pass_x2_kernel<<<ceil_div(ntl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
+          tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local, s4, ns, ss, sc, no, nlf, nrhs,
+          perm, parts, out);
+      return launch_status();
+    }
+  }
   if (grad)
     leaf_pass_kernel<T, true><<<ceil_div(ntl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
         tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local, s4, ns, ss, sc, no, nlf, nrhs, perm,

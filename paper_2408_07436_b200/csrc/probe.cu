@@ -79,12 +79,39 @@ __global__ void dmma16816_probe(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// Packed FP32 (FFMA2, fma.rn.f32x2): 128 FMAs per thread per iteration.
+__global__ void ffma2_probe(float* out, int iters) {
+  unsigned long long a[4];
+  const float2 b2{0.999f, 0.998f}, c2{1e-4f, 2e-4f};
+  const unsigned long long b = *reinterpret_cast<const unsigned long long*>(&b2);
+  const unsigned long long c = *reinterpret_cast<const unsigned long long*>(&c2);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 v{1e-3f * (threadIdx.x + i), 2e-3f * (threadIdx.x + i)};
+    a[i] = *reinterpret_cast<unsigned long long*>(&v);
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[i]) : "l"(b), "l"(c));
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 v = *reinterpret_cast<float2*>(&a[i]);
+    s += v.x + v.y;
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 }  // namespace
 
 extern "C" {
 
 // kind: 0 = FP32 FFMA, 1 = FP64 DFMA, 2 = MUFU rsqrt (FP32), 3 = DMMA m8n8k4,
-// 4 = DMMA m16n8k16 (FP64 tensor cores).  out must hold
+// 4 = DMMA m16n8k16 (FP64 tensor cores), 5 = packed FP32 FFMA2.  out must hold
 // blocks*threads elements of the probe type.  Work per launch:
 // blocks*threads*iters*128 operations (an FMA counts as 2 flops).
 int kifmm_probe(int kind, int64_t blocks, int64_t threads, int64_t iters, void* out,
@@ -103,6 +130,8 @@ int kifmm_probe(int kind, int64_t blocks, int64_t threads, int64_t iters, void* 
     dmma884_probe<<<(unsigned)blocks, (unsigned)threads, 0, s>>>((double*)out, (int)iters);
   else if (kind == 4)
     dmma16816_probe<<<(unsigned)blocks, (unsigned)threads, 0, s>>>((double*)out, (int)iters);
+  else if (kind == 5)
+    ffma2_probe<<<(unsigned)blocks, (unsigned)threads, 0, s>>>((float*)out, (int)iters);
   else
     return KIFMM_EARG;
   return launch_status();

@@ -431,6 +431,8 @@ class DeviceFmm:
         self.check_base = to_dev(leaf_surface_base(cfg.resolved_order_check(), leaf_side,
                                                    cfg.outer_scale))
         self.equiv_base = to_dev(leaf_surface_base(cfg.order_equiv, leaf_side, cfg.outer_scale))
+        if inst.near.offsets.shape[0] > 1 and int(np.diff(inst.near.offsets).max()) > 32:
+            raise ValueError("a leaf's near field spans more than 32 leaves (leaf pass limit)")
         self.near_off = to_dev(inst.near.offsets, np.int32)
         self.near_leaf = to_dev(inst.near.leaves, np.int32)
         # unit-box operators
