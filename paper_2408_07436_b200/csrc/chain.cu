@@ -59,26 +59,48 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
   T* buf1 = buf0 + (int64_t)a.bm * a.per_row;
   T* Bs = buf1 + (int64_t)a.bm * a.per_row;
 
-  // load the X tile
+  // load the X tile: U independent loads in flight per thread (the split-sum
+  // and child-stack reads are latency-bound when the tile is small).
   const int64_t K0 = a.K[0];
-  for (int64_t e = tid; e < (int64_t)a.bm * K0; e += NT) {
+  auto load_x = [&](int64_t e) -> T {
     const int m = (int)(e / K0);
     const int64_t k = e - (int64_t)m * K0;
-    T v = T(0);
-    if (m < rows_in) {
-      const int64_t g = row0 + m;
-      if (a.a_child) {
-        const int c = (int)(k / a.child_rows_w);
-        const int64_t p = g / a.a_nrhs, r = g - p * a.a_nrhs;
-        const int32_t ch = a.a_child[p * 8 + c];
-        if (ch >= 0) v = A[((int64_t)ch * a.a_nrhs + r) * a.lda + (k - c * a.child_rows_w)];
-      } else {
-        const T* p = A + g * a.lda + k;
-        v = p[0];
-        for (int s = 1; s < a.asum; ++s) v += p[s * a.astride];
+    if (m >= rows_in) return T(0);
+    const int64_t g = row0 + m;
+    if (a.a_child) {
+      const int c = (int)(k / a.child_rows_w);
+      const int64_t p = g / a.a_nrhs, r = g - p * a.a_nrhs;
+      const int32_t ch = a.a_child[p * 8 + c];
+      return ch >= 0 ? __ldg(&A[((int64_t)ch * a.a_nrhs + r) * a.lda + (k - c * a.child_rows_w)])
+                     : T(0);
+    }
+    const T* p = A + g * a.lda + k;
+    T v = __ldg(p);
+    int s = 1;
+    for (; s + 4 <= a.asum; s += 4) {
+      const T v1 = __ldg(p + s * a.astride), v2 = __ldg(p + (s + 1) * a.astride);
+      const T v3 = __ldg(p + (s + 2) * a.astride), v4 = __ldg(p + (s + 3) * a.astride);
+      v += v1; v += v2; v += v3; v += v4;
+    }
+    for (; s < a.asum; ++s) v += __ldg(p + s * a.astride);
+    return v;
+  };
+  {
+    constexpr int U = 8;
+    const int64_t total = (int64_t)a.bm * K0;
+    for (int64_t e0 = tid; e0 < total; e0 += (int64_t)NT * U) {
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = e0 + (int64_t)u * NT;
+        v[u] = e < total ? load_x(e) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = e0 + (int64_t)u * NT;
+        if (e < total) buf0[e] = v[u];
       }
     }
-    buf0[e] = v;
   }
 
   T* in = buf0;
@@ -95,6 +117,13 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
     const int64_t ncg = (N + RC - 1) / RC;
     const int64_t nrg = (nrows + RR - 1) / RR;
     const int64_t items = nrg * ncg;
+    // Small tiles: split K over `ks` thread groups (reduced in shared memory
+    // below) so the serial K loop per thread shrinks by ks.
+    int ks = 1;
+    while (ks < 8 && items * ks * 2 <= NT &&
+           (int64_t)ks * 2 * nrows * N * (int64_t)sizeof(T) <= BS_BYTES)
+      ks *= 2;
+    const int64_t witems = items * ks;
     const int64_t kch = (BS_BYTES / (int64_t)sizeof(T)) / N;   // operator rows per chunk
     const bool vec = (N % RC == 0) && sizeof(T) == 4;
     T acc[MAXIPT][RR][RC];
@@ -107,12 +136,34 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
     for (int64_t k0 = 0; k0 < K; k0 += kch) {
       const int64_t kc = min64(kch, K - k0);
       __syncthreads();                                 // previous chunk consumed / X ready
-      for (int64_t e = tid; e < kc * N; e += NT) Bs[e] = __ldg(&B[k0 * N + e]);
+      // operator chunk: contiguous kc*N elements, all copies in flight at once
+      {
+        const T* src = B + k0 * N;
+        const int64_t bytes = kc * N * (int64_t)sizeof(T);
+        if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(Bs)) & 15) == 0 &&
+            (bytes & 15) == 0) {
+          for (int64_t e = tid; e < bytes / 16; e += NT)
+            cp_async16(reinterpret_cast<char*>(Bs) + 16 * e,
+                       reinterpret_cast<const char*>(src) + 16 * e, true);
+        } else {
+          for (int64_t e = tid; e < kc * N; e += NT) {
+            unsigned sa = (unsigned)__cvta_generic_to_shared(Bs + e);
+            if constexpr (sizeof(T) == 8)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + e));
+            else
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src + e));
+          }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+      }
       __syncthreads();
 #pragma unroll
       for (int i = 0; i < MAXIPT; ++i) {
-        const int64_t it = tid + (int64_t)i * NT;
-        if (it < items) {
+        const int64_t wit = tid + (int64_t)i * NT;
+        if (wit < witems) {
+          const int64_t it = wit % items;
+          const int ksl = (int)(wit / items);
           const int64_t rg = it / ncg, n0 = (it - rg * ncg) * RC;
           const int64_t m0 = rg * RR;
           const T* x[RR];
@@ -120,7 +171,7 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
           for (int r = 0; r < RR; ++r)
             x[r] = in + (m0 + r < nrows ? m0 + r : m0) * K + k0;
           const T* bp = Bs + n0;
-          for (int64_t k = 0; k < kc; ++k) {
+          for (int64_t k = ksl; k < kc; k += ks) {
             T bv[RC];
             if (vec) {
               const float4 t4 = *reinterpret_cast<const float4*>(bp + k * N);
@@ -140,33 +191,62 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
       }
     }
     // epilogue of the stage
-#pragma unroll
-    for (int i = 0; i < MAXIPT; ++i) {
-      const int64_t it = tid + (int64_t)i * NT;
-      if (it >= items) continue;
-      const int64_t rg = it / ncg, n0 = (it - rg * ncg) * RC;
-#pragma unroll
-      for (int r = 0; r < RR; ++r) {
-        const int64_t m = rg * RR + r;
-        if (m >= nrows || (last && m >= live_rows)) continue;
-#pragma unroll
-        for (int j = 0; j < RC; ++j) {
-          const int64_t n = n0 + j;
-          if (n >= N) continue;
-          T v = acc[i][r][j];
-          if (cs) v *= __ldg(&cs[n]);
-          v *= al;
-          if (!last) {
-            outb[m * N + n] = v;
-          } else {
-            const int64_t gr = row0 * expand + m;
-            const int64_t dst = a.c_rowmap ? (int64_t)a.c_rowmap[gr] : gr;
-            if (dst >= 0) {
-              T* o = C + dst * a.ldc + n;
-              *o = a.accumulate ? *o + v : v;
-            }
-          }
+    auto apply = [&](int64_t m, int64_t n, T v) {
+      if (cs) v *= __ldg(&cs[n]);
+      v *= al;
+      if (!last) {
+        outb[m * N + n] = v;
+      } else {
+        const int64_t gr = row0 * expand + m;
+        const int64_t dst = a.c_rowmap ? (int64_t)a.c_rowmap[gr] : gr;
+        if (dst >= 0) {
+          T* o = C + dst * a.ldc + n;
+          *o = a.accumulate ? *o + v : v;
         }
+      }
+    };
+    if (ks == 1) {
+#pragma unroll
+      for (int i = 0; i < MAXIPT; ++i) {
+        const int64_t it = tid + (int64_t)i * NT;
+        if (it >= items) continue;
+        const int64_t rg = it / ncg, n0 = (it - rg * ncg) * RC;
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+          const int64_t m = rg * RR + r;
+          if (m >= nrows || (last && m >= live_rows)) continue;
+#pragma unroll
+          for (int j = 0; j < RC; ++j)
+            if (n0 + j < N) apply(m, n0 + j, acc[i][r][j]);
+        }
+      }
+    } else {
+      // split-K partials -> Bs (free once every thread is past the K loop)
+      T* red = Bs;
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < MAXIPT; ++i) {
+        const int64_t wit = tid + (int64_t)i * NT;
+        if (wit >= witems) continue;
+        const int64_t it = wit % items;
+        const int ksl = (int)(wit / items);
+        const int64_t rg = it / ncg, n0 = (it - rg * ncg) * RC;
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+          const int64_t m = rg * RR + r;
+          if (m >= nrows) continue;
+#pragma unroll
+          for (int j = 0; j < RC; ++j)
+            if (n0 + j < N) red[((int64_t)ksl * nrows + m) * N + n0 + j] = acc[i][r][j];
+        }
+      }
+      __syncthreads();
+      for (int64_t e = tid; e < nrows * N; e += NT) {
+        const int64_t m = e / N, n = e - m * N;
+        if (last && m >= live_rows) continue;
+        T v = red[e];
+        for (int q = 1; q < ks; ++q) v += red[(int64_t)q * nrows * N + e];
+        apply(m, n, v);
       }
     }
     if (!last) {

@@ -19,6 +19,8 @@ Data layout in HBM (n_rhs = R, T = float32 | float64):
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -129,7 +131,7 @@ class Linalg:
 
     # widest operator (elements) the fused chain kernel handles well; wider
     # chains (p >= 6 in float64) run as tiled GEMM stages instead
-    CHAIN_MAX_N = 256
+    CHAIN_MAX_N = int(os.environ.get("KIFMM_CHAIN_MAX_N", "256"))
 
     def chain(self, M, A, lda, stages, C, ldc, rowmap=None, accumulate=False, asum=1,
               astride=0, a_child=None, child_w=0, a_nrhs=1):
@@ -173,6 +175,7 @@ class Linalg:
         eager warm-up pass, reused afterwards)."""
         if not hasattr(self, "_scratch"):
             self._scratch = {}
+        slot = (torch.cuda.current_stream().cuda_stream, slot)   # per stream: levels overlap
         t = self._scratch.get(slot)
         if t is None or t.numel() < n or t.dtype != T:
             t = torch.empty(n, dtype=T, device=dev)
@@ -415,6 +418,13 @@ class DeviceFmm:
         exp = inst.expansions
         self.depth = cfg.depth
         self.n_e, self.n_c = exp.n_equiv, exp.n_check
+        # near field concurrent with the far field (see evaluate_device)
+        self.overlap = os.environ.get("KIFMM_OVERLAP", "1") != "0"
+        least, greatest = torch.cuda.Stream.priority_range()
+        self.side_stream = torch.cuda.Stream(priority=least)
+        self.hi_stream = torch.cuda.Stream(priority=greatest)
+        self.bulk_stream = torch.cuda.Stream(priority=max(greatest, least - 1)
+                                             if least > greatest else least)
         dt = self.np_dtype
         leaf_side = inst.domain.box_side(cfg.depth)
         # points
@@ -471,16 +481,18 @@ class DeviceFmm:
             self.tma_plan = {l: tma_level_plan(st.level_keys(l), tt.level_keys(l), l)
                              for l in plans}
 
-    def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None):
+    def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None, bulk=False):
+        """``bulk``: the finest level running concurrently with the coarser
+        ones (evaluate_device overlap) uses its own scratch (qt, acc)."""
         b = self._buffers(nrhs)
+        qt, acc = (b["qt_bulk"], b["acc_bulk"]) if bulk else (b["qt"], b["acc"])
         if self.tma and solve is not None:
             plan = self.tma_plan[lvl]
             return self.blas.run_level_tma(plan, mult, self.n_src[lvl], self.n_tgt[lvl], nrhs,
-                                           1.0 / self.side[lvl], b["qt"], b["dense"][lvl],
-                                           b["acc"], solve)
+                                           1.0 / self.side[lvl], qt, b["dense"][lvl], acc, solve)
         return self.blas.run_level(self.blas_plan_dev[lvl], mult, self.n_src[lvl],
-                                   self.n_tgt[lvl], nrhs, 1.0 / self.side[lvl], check, b["qt"],
-                                   b["acc"], solve=solve)
+                                   self.n_tgt[lvl], nrhs, 1.0 / self.side[lvl], check, qt, acc,
+                                   solve=solve)
 
     # ------------------------------------------------------------- FFT-M2L
     def _init_fft(self, ops, plans):
@@ -499,12 +511,13 @@ class DeviceFmm:
                                         halo=to_dev(p.halo, np.int64),
                                         tiles=upload_hadamard_tiles(p.halo, p.src_color, p.tgt_color))
 
-    def m2l_fft_level(self, lvl, mult, nrhs, check, plan=None):
+    def m2l_fft_level(self, lvl, mult, nrhs, check, plan=None, bulk=False):
         plan = plan if plan is not None else self.fft_plan_dev[lvl]
         b = self._buffers(nrhs)
         nsc, ntc = plan["nsc"], plan["ntc"]
-        qhat = b["qhat"][: 2 * self.n_freq * nsc * 8 * nrhs]
-        phat = b["phat"][: 2 * self.n_freq * ntc * 8 * nrhs]
+        qh, ph = (b["qhat_bulk"], b["phat_bulk"]) if bulk else (b["qhat"], b["phat"])
+        qhat = qh[: 2 * self.n_freq * nsc * 8 * nrhs]
+        phat = ph[: 2 * self.n_freq * ntc * 8 * nrhs]
         s = stream_handle()
         launch(f"kifmm_fft_forward_{self.sfx}", P(mult), nrhs, self.order, P(plan["sbox"]), nsc,
                None, 0, P(qhat), s)
@@ -537,24 +550,39 @@ class DeviceFmm:
                                dtype=T, device=dev)
         b["stack"] = torch.empty(max(self.n_src[2:d] + [1]) * R * 8 * self.n_e, dtype=T,
                                  device=dev)
+        # scratch of the M2L levels: one set for the coarse levels (run in
+        # sequence) and one for the finest level (may run concurrently, see
+        # evaluate_device); check rows of the finest level in phi_bulk
+        coarse = [l for l in range(2, d)] or [d]
+        b["phi_bulk"] = torch.empty(max(self.n_tgt[d] * R * self.n_c, 1), dtype=T, device=dev)
         if self.cfg.backend == "blas":
-            b["qt"] = torch.zeros(max(self.n_src) * R * self.blas.kin * (3 if self.blas.tc else 1),
-                                  dtype=T, device=dev)
-            b["acc"] = torch.zeros(max(self.blas.acc_elems(self.n_tgt[l], R, p["n_tiles"])
-                                       for l, p in self.blas_plan_dev.items()), dtype=T,
-                                   device=dev)
+            def acc_need(levels):
+                n = max(self.blas.acc_elems(self.n_tgt[l], R, self.blas_plan_dev[l]["n_tiles"])
+                        for l in levels)
+                if self.tma:
+                    n = max(n, max(self.blas.acc_elems(self.n_tgt[l], R,
+                                                       self.tma_plan[l]["n_tiles"])
+                                   for l in levels))
+                return max(n, 1)
+            qt_w = R * self.blas.kin * (3 if self.blas.tc else 1)
+            b["qt"] = torch.zeros(max(self.n_src[l] for l in coarse) * qt_w, dtype=T, device=dev)
+            b["acc"] = torch.zeros(acc_need(coarse), dtype=T, device=dev)
+            b["qt_bulk"] = torch.zeros(self.n_src[d] * qt_w, dtype=T, device=dev)
+            b["acc_bulk"] = torch.zeros(acc_need([d]), dtype=T, device=dev)
             if self.tma:
-                b["acc"] = torch.zeros(max(b["acc"].numel(), max(
-                    self.blas.acc_elems(self.n_tgt[l], R, p["n_tiles"])
-                    for l, p in self.tma_plan.items())), dtype=T, device=dev)
                 b["dense"] = {l: tuple(torch.zeros(8 * R * p["h"] ** 3 * self.blas.kin, dtype=T,
                                                    device=dev) for _ in range(2))
                               for l, p in self.tma_plan.items()}
         else:
-            nsc = max(p["nsc"] for p in self.fft_plan_dev.values())
-            ntc = max(p["ntc"] for p in self.fft_plan_dev.values())
+            fp = self.fft_plan_dev
+            nsc = max(fp[l]["nsc"] for l in coarse)
+            ntc = max(fp[l]["ntc"] for l in coarse)
             b["qhat"] = torch.empty(2 * self.n_freq * nsc * 8 * R, dtype=T, device=dev)
             b["phat"] = torch.empty(2 * self.n_freq * ntc * 8 * R, dtype=T, device=dev)
+            b["qhat_bulk"] = torch.empty(2 * self.n_freq * fp[d]["nsc"] * 8 * R, dtype=T,
+                                         device=dev)
+            b["phat_bulk"] = torch.empty(2 * self.n_freq * fp[d]["ntc"] * 8 * R, dtype=T,
+                                         device=dev)
         b["out"] = torch.empty(self.tx.shape[0] * R, dtype=T, device=dev)
         b["qin"] = torch.empty(self.sx.shape[0] * R, dtype=torch.float64, device=dev)
         self._bufs[nrhs] = b
@@ -577,7 +605,22 @@ class DeviceFmm:
         """Full evaluate from float64 charges on the device (caller order,
         (n_src, R) C-contiguous) to potentials on the device (caller order,
         (n_tgt, R), working dtype).  Returns the output tensor (a view of an
-        internal buffer)."""
+        internal buffer).
+
+        With ``overlap`` the far-field pipeline runs on a high-priority stream
+        and the near field on a low-priority one, so the block scheduler
+        serves the (latency-bound) far-field kernels first and fills the
+        rest of the machine with P2P work."""
+        if self.overlap and not timings and _PROF is None:
+            caller = torch.cuda.current_stream()
+            self.hi_stream.wait_stream(caller)
+            with torch.cuda.stream(self.hi_stream):
+                res = self._evaluate(q_dev, nrhs, False, gradient, True)
+            caller.wait_stream(self.hi_stream)
+            return res
+        return self._evaluate(q_dev, nrhs, timings, gradient, False)
+
+    def _evaluate(self, q_dev, nrhs, timings, gradient, overlap):
         b = self._buffers(nrhs)
         R = nrhs
         s = stream_handle()
@@ -599,6 +642,30 @@ class DeviceFmm:
                P(q), s)
         launch(f"kifmm_pack_sources_{sfx}", P(self.sx), P(self.sy), P(self.sz), P(q),
                self.sx.shape[0], R, P(b["src4"]), s)
+        # The near field (P2P) needs only the packed sources: with `overlap`
+        # it runs on a low-priority side stream concurrently with the whole
+        # far-field pipeline (mostly latency-bound small-level kernels), and
+        # the L2P pass adds the far field at the end.  Eager timing/profiling
+        # passes keep the fused sequential leaf pass.
+        out = b["out"]
+        nt = self.tx.shape[0]
+        if gradient and "grad" not in b:
+            b["grad"] = torch.empty(nt * R * 3, dtype=self.T, device=out.device)
+        grad_ptr = [P(b["grad"])] if gradient else []
+        leaf_name = f"kifmm_leaf_pass_grad_{sfx}" if gradient else f"kifmm_leaf_pass_{sfx}"
+
+        def leaf_args(parts):
+            return [P(self.tx), P(self.ty), P(self.tz), P(self.t_start), P(self.t_count),
+                    self.n_tgt[d], P(self.t_centers), P(self.equiv_base), n_e,
+                    P(b["loc"][d]), P(b["src4"]), self.sx.shape[0], P(self.s_start),
+                    P(self.s_count), P(self.near_off), P(self.near_leaf), R, P(self.t_perm),
+                    parts, P(out)] + grad_ptr
+
+        if overlap:
+            main = torch.cuda.current_stream()
+            side = self.side_stream
+            side.wait_stream(main)
+            launch(leaf_name, *leaf_args(2), side.cuda_stream)       # P2P, overwrite
         # P2M: check potentials, then the up_inv solve scaled by the leaf side.
         mult, phi, tmp = b["mult"], b["phi"], b["tmp"]
         nl = self.n_src[d]
@@ -606,6 +673,35 @@ class DeviceFmm:
                  P(self.s_start), P(self.s_count), nl, P(self.s_centers), P(self.check_base),
                  n_c, P(phi), s)
         la.chain(nl * R, phi, n_c, Linalg.solve_stages(self.up_inv, self.side[d]), mult[d], n_e)
+        loc = b["loc"]
+        for lvl in range(2, d + 1):
+            loc[lvl].zero_()
+        calls = {}
+
+        def m2l(lvl, bulk):
+            n_t = self.n_tgt[lvl]
+            check = (b["phi_bulk"] if bulk else phi)[: n_t * R * n_c]
+            if self.cfg.backend == "blas":
+                calls[lvl] = self.m2l_blas_level(lvl, mult[lvl], R, check,
+                                                 solve=(self.dn_inv, self.side[lvl], loc[lvl]),
+                                                 bulk=bulk)
+            else:
+                calls[lvl] = self.m2l_fft_level(lvl, mult[lvl], R, check, bulk=bulk)
+                la.chain(n_t * R, check, n_c, Linalg.solve_stages(self.dn_inv, self.side[lvl]),
+                         loc[lvl], n_e, accumulate=True)
+
+        # With `overlap`, the finest level's M2L (the bulk of the far-field
+        # work; it needs only mult[d]) runs on its own stream, concurrently
+        # with the M2M pass and the coarser levels; the L2L into level d
+        # waits for it (both accumulate into loc[d]).
+        joined = True
+        bulk_run = overlap and d >= 3
+        if bulk_run:
+            bulk = self.bulk_stream
+            bulk.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(bulk):
+                m2l(d, True)
+            joined = False
         phase("m2m")
         # M2M down to level 2 (levels 0-1 carry no M2L): children stacked in
         # the chain's loader, kernel product, then the up_inv solve.
@@ -615,40 +711,29 @@ class DeviceFmm:
                      [(self.m2mT, 8 * n_e, n_c, None, 1.0)]
                      + Linalg.solve_stages(self.up_inv, 1.0), mult[lvl - 1], n_e,
                      a_child=self.src_child[lvl], child_w=n_e, a_nrhs=R)
-        loc = b["loc"]
-        for lvl in range(2, d + 1):
-            loc[lvl].zero_()
-        calls = []
         for lvl in range(2, d + 1):
             n_t = self.n_tgt[lvl]
             phase(f"m2l{lvl}")
-            check = phi[: n_t * R * n_c]
-            if self.cfg.backend == "blas":
-                calls.append(self.m2l_blas_level(
-                    lvl, mult[lvl], R, check, solve=(self.dn_inv, self.side[lvl], loc[lvl])))
-            else:
-                calls.append(self.m2l_fft_level(lvl, mult[lvl], R, check))
-                la.chain(n_t * R, check, n_c, Linalg.solve_stages(self.dn_inv, self.side[lvl]),
-                         loc[lvl], n_e, accumulate=True)
+            if not (lvl == d and bulk_run):
+                m2l(lvl, lvl == d)        # the finest level always uses its own scratch set
             if lvl < d:
+                if lvl + 1 == d and not joined:
+                    torch.cuda.current_stream().wait_stream(bulk)
+                    joined = True
                 phase(f"l2l{lvl}")
                 la.chain(n_t * R, loc[lvl], n_e,
                          [(self.l2lT, n_e, 8 * n_c, None, 1.0)]
                          + Linalg.solve_stages(self.dn_inv, 0.5), loc[lvl + 1], n_e,
                          rowmap=self._l2l_rowmap(lvl + 1, R), accumulate=True)
+        if not joined:
+            torch.cuda.current_stream().wait_stream(bulk)
+        calls = [calls[l] for l in sorted(calls)]
         phase("leaf")
-        out = b["out"]
-        leaf_args = [P(self.tx), P(self.ty), P(self.tz), P(self.t_start), P(self.t_count),
-                     self.n_tgt[d], P(self.t_centers), P(self.equiv_base), n_e, P(loc[d]),
-                     P(b["src4"]), self.sx.shape[0], P(self.s_start), P(self.s_count),
-                     P(self.near_off), P(self.near_leaf), R, P(self.t_perm), 3, P(out)]
-        nt = self.tx.shape[0]
-        if gradient:
-            if "grad" not in b:
-                b["grad"] = torch.empty(nt * R * 3, dtype=self.T, device=out.device)
-            launch(f"kifmm_leaf_pass_grad_{sfx}", *leaf_args, P(b["grad"]), s)
+        if overlap:
+            main.wait_stream(side)
+            launch(leaf_name, *leaf_args(1 | 4), s)                  # L2P, accumulate
         else:
-            launch(f"kifmm_leaf_pass_{sfx}", *leaf_args, s)
+            launch(leaf_name, *leaf_args(3), s)                      # fused L2P + P2P
         phase("end")
         self.last_m2l_calls = calls
         self._events = ev
