@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(NT) chain_kernel(const T* __restrict__ A, Chai
           for (int r = 0; r < RR; ++r)
             x[r] = in + (m0 + r < nrows ? m0 + r : m0) * K + k0;
           const T* bp = Bs + n0;
-          for (int64_t k = ksl; k < kc; k += ks) {
+#pragma unroll 4
+          for (int k = ksl; k < (int)kc; k += ks) {
             T bv[RC];
             if (vec) {
               const float4 t4 = *reinterpret_cast<const float4*>(bp + k * N);

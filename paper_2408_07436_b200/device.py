@@ -132,11 +132,14 @@ class Linalg:
     # widest operator (elements) the fused chain kernel handles well; wider
     # chains (p >= 6 in float64) run as tiled GEMM stages instead
     CHAIN_MAX_N = int(os.environ.get("KIFMM_CHAIN_MAX_N", "256"))
+    # row count from which the stages run as separate (throughput) GEMMs
+    CHAIN_GEMM_ROWS = int(os.environ.get("KIFMM_CHAIN_GEMM_ROWS", "16384"))
 
     def chain(self, M, A, lda, stages, C, ldc, rowmap=None, accumulate=False, asum=1,
               astride=0, a_child=None, child_w=0, a_nrhs=1):
         """Fused operator chain (csrc/chain.cu): stages = [(B, K, N, colscale, alpha), ...]."""
-        if max(s[2] for s in stages) > self.CHAIN_MAX_N or max(s[1] for s in stages) > 512:
+        if max(s[2] for s in stages) > self.CHAIN_MAX_N or max(s[1] for s in stages) > 512 \
+                or M >= self.CHAIN_GEMM_ROWS:
             return self._chain_gemms(M, A, lda, stages, C, ldc, rowmap, accumulate, asum,
                                      astride, a_child, child_w, a_nrhs)
         st = list(stages) + [(None, 0, 0, None, 1.0)] * (3 - len(stages))
