@@ -384,7 +384,10 @@ int kifmm_m2l_sweep_tc_f32(const float* qhi, const float* qlo, const float* bhi,
     const char* g = getenv("KIFMM_TC_L1");
     l1 = g ? atoi(g) : 0;
   }
-  int stages = (int)((220 * 1024 / ctas_per_sm) / stage_bytes);
+  // 3 * n_out accumulator columns > 256 take the whole 512-column TMEM:
+  // one CTA per SM then (a second one would wait in tcgen05.alloc).
+  const int ctas = 3 * n_out > 256 ? 1 : ctas_per_sm;
+  int stages = (int)((220 * 1024 / ctas) / stage_bytes);
   if (stages > max_stages) stages = max_stages;
   if (stages < 2) return KIFMM_EARG;
   const size_t smem = stages * stage_bytes + (2 * stages + 4) * 8 + 16;

@@ -387,7 +387,7 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
                             const int32_t* tile_ids, int64_t n_tiles, const int32_t* class_tv,
                             const int8_t* offsets, int64_t nrhs, int64_t nsplit, float* acc,
                             void* stream) {
-  if (kin < 8 || kin % 8 || kin > 4 * KC || n_out < 16 || n_out > 160 || n_out % 16 ||
+  if (kin < 8 || kin % 8 || n_out < 16 || n_out > 160 || n_out % 16 ||
       n_tiles < 0 || nrhs < 1 || nsplit < 1 || nsplit > 189 || h < 1)
     return KIFMM_EARG;
   if (n_tiles == 0) return 0;
@@ -404,7 +404,10 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
     ctas = f ? atoi(f) : 2;
     if (ctas < 1) ctas = 1;
   }
-  int stages = (int)(((200 * 1024) / ctas) / stage_bytes);
+  // 3 * n_out accumulator columns > 256 take the whole 512-column TMEM:
+  // one CTA per SM then, with the shared memory for deeper pipelining.
+  const int cps = 3 * n_out > 256 ? 1 : ctas;
+  int stages = (int)(((cps == 1 ? 222 * 1024 : 200 * 1024) / cps) / stage_bytes);
   if (stages > max_stages) stages = max_stages;
   if (stages < 2) return KIFMM_EARG;
   const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;

@@ -286,8 +286,9 @@ class BlasDevice:
         if tensor_cores is None:
             tensor_cores = os.environ.get("KIFMM_SWEEP", "tc") != "simt"
         # float32: tcgen05 3xTF32 sweep (csrc/m2l_tc.cu); float64: FP64 SIMT sweep.
-        # (3 TMEM accumulators of n_out <= 160 columns fit the 512-column TMEM)
-        self.tc = bool(tensor_cores) and dt == np.float32 and k <= 160 and -(-k // 8) * 8 <= 128
+        # (3 TMEM accumulators of n_out <= 160 columns fit the 512-column TMEM;
+        # above 256 columns the kernels run one CTA per SM)
+        self.tc = bool(tensor_cores) and dt == np.float32 and -(-k // 16) * 16 <= 160
         if self.tc:
             self.kin = -(-k // 8) * 8
             self.ko_pad = -(-k // 16) * 16

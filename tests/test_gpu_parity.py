@@ -167,6 +167,24 @@ def test_evaluate_matches_reference(cuda, name):
     assert abs(err.error - float(g["error"])) <= 0.5 * float(g["error"]) + 1e-12
 
 
+@pytest.mark.parametrize("order,depth", [(6, 3), (6, 4)])
+def test_wide_rank_tensor_core_sweep(cuda, order, depth):
+    """float32 p=6 (BASELINE config 4): shared rank k=147 > 128, so the
+    tcgen05 sweeps run with 160-column accumulators (whole TMEM, one CTA per
+    SM); checked against the reference on the same inputs."""
+    rng = np.random.default_rng(5)
+    pts = rng.random((20000, 3))
+    q = np.random.default_rng(6).random(20000)
+    kw = dict(depth=depth, order_equiv=order, backend="blas", precision="f32")
+    from paper_2408_07436_b200 import FmmConfig, setup
+    inst = setup(pts, pts, FmmConfig(**kw))
+    assert inst.device.blas.tc and inst.device.blas.ko_pad > 128
+    got = inst.evaluate(q)
+    want, _ = _reference_run(pts, q, kw)
+    rep = parity_report(got, want)
+    assert rep["max_rel"] <= TOL["f32"], rep
+
+
 def test_evaluate_is_deterministic_and_linear(cuda):
     from paper_2408_07436_b200 import FmmConfig, setup
     from conftest import uniform_points

@@ -6,10 +6,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2408_07436_b200 import FmmConfig, setup
 from paper_2408_07436_b200.device import profile_launches
 
-n = int(sys.argv[1]); kw = eval(sys.argv[2]); signed = len(sys.argv) > 3 and sys.argv[3] == "signed"
-pts = np.random.default_rng(7).random((n, 3))
-rng = np.random.default_rng(11)
-q = rng.uniform(-1, 1, n) if signed else rng.random(n)
+n = int(sys.argv[1]); kw = eval(sys.argv[2]); mode = sys.argv[3] if len(sys.argv) > 3 else ""
+if "sphere" in mode:       # BASELINE config 5: unit-sphere surface scaled into [0,1]^3, N(0,1)
+    g = np.random.default_rng(7).standard_normal((n, 3))
+    pts = (g / np.linalg.norm(g, axis=1, keepdims=True) + 1.0) / 2.0
+    q = np.random.default_rng(11).standard_normal(n)
+else:
+    pts = np.random.default_rng(7).random((n, 3))
+    rng = np.random.default_rng(11)
+    q = rng.uniform(-1, 1, n) if "signed" in mode else rng.random(n)
 t0 = time.perf_counter(); inst = setup(pts, pts, FmmConfig(**kw)); ts = time.perf_counter() - t0
 dev = inst.device
 qd = torch.from_numpy(q).cuda()
