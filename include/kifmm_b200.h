@@ -298,6 +298,39 @@ int kifmm_probe(int kind, int64_t blocks, int64_t threads, int64_t iters, void* 
 /* Library identification: returns the compiled SM target (e.g. 100). */
 int kifmm_sm_target(void);
 
+/* ---- (5) device tree and plan build (octree.py:274-329,
+ * engine.py:224-256, m2l_blas.py:232-258), bit-exact with the host build.
+ * Codes are the reference's Morton keys: interleave(x, y, z) << 5 | level. */
+/* Scratch bytes for op 0 = sort (incl. its index buffer), 1 = run-length
+ * encode, 2 = unique; written to *bytes (host pointer). */
+int kifmm_tree_temp_bytes(int op, int64_t n, int end_bit, int64_t* bytes);
+/* Leaf codes of n points (n x 3 float64) in the domain (origin, side);
+ * *bad (device int, zeroed by the caller) counts points outside it. */
+int kifmm_tree_encode(const double* pts, int64_t n, double ox, double oy, double oz, double side,
+                      int64_t depth, uint64_t* codes, int* bad, void* stream);
+/* Stable radix sort of codes (bits [0, end_bit)); perm_out = original indices
+ * (the reference's stable argsort). */
+int kifmm_tree_sort(const uint64_t* codes_in, int64_t n, int end_bit, uint64_t* codes_out,
+                    int64_t* perm_out, void* temp, int64_t temp_bytes, void* stream);
+/* Runs of a sorted key array: unique keys, counts, *n_runs (device). */
+int kifmm_tree_rle(const uint64_t* keys, int64_t n, uint64_t* unique, int64_t* counts,
+                   int64_t* n_runs, void* temp, int64_t temp_bytes, void* stream);
+/* Distinct parent codes of a sorted level (*n_out device; scratch: n codes). */
+int kifmm_tree_parents(const uint64_t* codes, int64_t n, uint64_t* scratch, uint64_t* parents,
+                       int64_t* n_out, void* temp, int64_t temp_bytes, void* stream);
+/* Binary search: rows[i] = index of queries[i] in the sorted table or -1. */
+int kifmm_lookup_codes(const uint64_t* table, int64_t n, const uint64_t* queries, int64_t nq,
+                       int64_t* rows, void* stream);
+/* Near-field candidates (engine.py:231-240): rows (ntl, 27), own leaf first,
+ * then the in-domain neighbours by ascending code, -1 = absent. */
+int kifmm_near_field_rows(const uint64_t* tleaf, int64_t ntl, int64_t depth,
+                          const uint64_t* sleaf, int64_t nsl, int64_t* rows, void* stream);
+/* BLAS-M2L source table in the sweep layout src[tile][j][m] (n_slots % 128
+ * == 0): source row at anchor(slot_target) + offset(class_tv[class][j]). */
+int kifmm_blas_src_table(const uint64_t* tcodes, const int32_t* slot_target, int64_t n_slots,
+                         int64_t level, const int32_t* class_tv, const int8_t* offsets,
+                         const uint64_t* scodes, int64_t ns, int32_t* src, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

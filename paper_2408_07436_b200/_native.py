@@ -24,6 +24,14 @@ _C = ctypes.c_int
 SIGNATURES = {
     "kifmm_laplace_potentials_f32": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P],
     "kifmm_laplace_potentials_f64": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P],
+    "kifmm_tree_temp_bytes": [_C, _I, _C, _P],
+    "kifmm_tree_encode": [_P, _I, _D, _D, _D, _D, _I, _P, _P, _P],
+    "kifmm_tree_sort": [_P, _I, _C, _P, _P, _P, _I, _P],
+    "kifmm_tree_rle": [_P, _I, _P, _P, _P, _P, _I, _P],
+    "kifmm_tree_parents": [_P, _I, _P, _P, _P, _P, _I, _P],
+    "kifmm_lookup_codes": [_P, _I, _P, _I, _P, _P],
+    "kifmm_near_field_rows": [_P, _I, _I, _P, _I, _P, _P],
+    "kifmm_blas_src_table": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P],
     "kifmm_laplace_gradients_f32": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P, _P],
     "kifmm_laplace_gradients_f64": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P, _P],
     "kifmm_laplace_matrix_f32": [_P, _P, _P, _I, _P, _P, _P, _I, _P, _P],

@@ -215,10 +215,12 @@ def sweep_splits(n_tiles: int, n_slabs: int) -> int:
 
 def upload_blas_plan(plan):
     n_tiles = plan.tile_class.shape[0]
-    src_t = plan.src.reshape(n_tiles, TILE_TARGETS, 189).transpose(0, 2, 1)
+    src_dev = getattr(plan, "src_dev", None)          # built on the device (device_setup)
+    if src_dev is None:
+        src_t = plan.src.reshape(n_tiles, TILE_TARGETS, 189).transpose(0, 2, 1)
+        src_dev = to_dev(np.ascontiguousarray(src_t), np.int32)
     return dict(n_tiles=n_tiles, tile_targets=to_dev(plan.tile_targets, np.int32),
-                tile_class=to_dev(plan.tile_class, np.int32),
-                src=to_dev(np.ascontiguousarray(src_t), np.int32))
+                tile_class=to_dev(plan.tile_class, np.int32), src=src_dev)
 
 
 def tf32_split(x: np.ndarray):

@@ -221,7 +221,66 @@ class FmmInstance:
         return self._device
 
 
-def setup(sources, targets, config: FmmConfig) -> FmmInstance:
+class LazyBuckets(dict):
+    """The reference's per-level ``TransferBuckets`` (``m2l_blas.py:214-258``),
+    built on first access: the device path needs only the target-stationary
+    plans, the level drop-in ``apply_level`` and the tests need the buckets."""
+
+    def __init__(self, source_tree, target_tree, levels):
+        super().__init__()
+        self._trees = (source_tree, target_tree)
+        self._levels = list(levels)
+
+    def __missing__(self, lvl):
+        if lvl not in self._levels:
+            raise KeyError(lvl)
+        b = m2l_blas.bucket_level(*self._trees, lvl)
+        self[lvl] = b
+        return b
+
+    def _fill(self):
+        for lvl in self._levels:
+            self[lvl]
+
+    def items(self):
+        self._fill()
+        return super().items()
+
+    def keys(self):
+        return list(self._levels)
+
+    def values(self):
+        self._fill()
+        return super().values()
+
+    def __iter__(self):
+        return iter(self._levels)
+
+    def __len__(self):
+        return len(self._levels)
+
+    def __contains__(self, lvl):
+        return lvl in self._levels
+
+
+def _device_build_available() -> bool:
+    import os
+    if os.environ.get("KIFMM_DEVICE_SETUP", "1") == "0":
+        return False
+    try:
+        import torch
+        from . import _native
+        return torch.cuda.is_available() and os.path.exists(_native.LIB_PATH)
+    except Exception:
+        return False
+
+
+def setup(sources, targets, config: FmmConfig, device_build=None) -> FmmInstance:
+    """Reference ``engine.setup`` (``engine.py:160``).  ``device_build``
+    (default: when a GPU and the library are present) builds the trees, the
+    near-field plan and the BLAS-M2L plans on the device (device_setup.py,
+    bit-identical to the host build); the reference's bucket lists are then
+    built lazily, on first access."""
     t0 = time.perf_counter()
     config.validate()
     src = np.ascontiguousarray(np.asarray(sources, dtype=np.float64).reshape(-1, 3))
@@ -229,8 +288,15 @@ def setup(sources, targets, config: FmmConfig) -> FmmInstance:
     if src.shape[0] < 1 or tgt.shape[0] < 1:
         raise ConfigError("both point sets must be nonempty")
     domain = Domain.from_points(np.vstack([src, tgt]))
-    stree = Octree(src, config.depth, domain)
-    ttree = Octree(tgt, config.depth, domain)
+    if device_build is None:
+        device_build = _device_build_available()
+    if device_build:
+        from . import device_setup
+        stree = device_setup.octree(src, config.depth, domain)
+        ttree = device_setup.octree(tgt, config.depth, domain)
+    else:
+        stree = Octree(src, config.depth, domain)
+        ttree = Octree(tgt, config.depth, domain)
     dt = config.dtype
     exp = ExpansionOperators(config.order_equiv, config.resolved_order_check(), dtype=dt,
                              alpha=config.alpha, cutoff=config.svd_cutoff,
@@ -243,17 +309,23 @@ def setup(sources, targets, config: FmmConfig) -> FmmInstance:
             rank_estimate=config.rank_estimate, oversamples=config.oversamples,
             seed=config.seed, dtype=dt, inner_scale=config.inner_scale,
             level_scale=1.0 / domain.box_side(config.depth))
-        for lvl in range(2, config.depth + 1):
-            b = m2l_blas.bucket_level(stree, ttree, lvl)
-            inst.buckets[lvl] = b
-            inst.blas_plans[lvl] = m2l_blas.level_plan_from_buckets(
-                b, ttree.level_keys(lvl).shape[0], child_index_codes(ttree.level_keys(lvl)))
+        if device_build:
+            inst.buckets = LazyBuckets(stree, ttree, range(2, config.depth + 1))
+            for lvl in range(2, config.depth + 1):
+                inst.blas_plans[lvl] = device_setup.blas_level_plan(stree, ttree, lvl)
+        else:
+            for lvl in range(2, config.depth + 1):
+                b = m2l_blas.bucket_level(stree, ttree, lvl)
+                inst.buckets[lvl] = b
+                inst.blas_plans[lvl] = m2l_blas.level_plan_from_buckets(
+                    b, ttree.level_keys(lvl).shape[0], child_index_codes(ttree.level_keys(lvl)))
     else:
         inst.fft_ops = m2l_fft.precompute_fft_operators(
             config.order_equiv, dtype=dt, inner_scale=config.inner_scale, workers=config.threads)
         for lvl in range(2, config.depth + 1):
             inst.halo_plans[lvl] = m2l_fft.build_halo_plan(stree, ttree, lvl)
-    inst.near = near_field_plan(stree, ttree)
+    inst.near = (device_setup.near_field_plan(stree, ttree) if device_build
+                 else near_field_plan(stree, ttree))
     inst.n_near_pairs = inst.near.n_pairs
     inst.setup_seconds = time.perf_counter() - t0
     return inst

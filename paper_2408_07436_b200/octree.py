@@ -264,6 +264,24 @@ class Octree:
         for lvl in range(depth - 1, -1, -1):
             self.levels[lvl] = np.unique(parent_codes(self.levels[lvl + 1]))
 
+    @classmethod
+    def from_arrays(cls, depth, domain, perm, sorted_points, leaf_starts, leaf_counts, levels):
+        """A tree from already-built arrays (device_setup.octree): points in
+        leaf-Morton order, the permutation, leaf runs and per-level codes."""
+        t = cls.__new__(cls)
+        t.depth = depth
+        t.domain = domain
+        t.perm = np.asarray(perm, dtype=np.int64)
+        sp = np.asarray(sorted_points, dtype=np.float64).reshape(-1, 3)
+        t.x = np.ascontiguousarray(sp[:, 0])
+        t.y = np.ascontiguousarray(sp[:, 1])
+        t.z = np.ascontiguousarray(sp[:, 2])
+        t.n_points = sp.shape[0]
+        t.leaf_starts = np.asarray(leaf_starts, dtype=np.int64)
+        t.leaf_counts = np.asarray(leaf_counts, dtype=np.int64)
+        t.levels = [np.asarray(l, dtype=np.uint64) for l in levels]
+        return t
+
     @property
     def leaves(self) -> np.ndarray:
         return self.levels[self.depth]

@@ -304,3 +304,46 @@ def test_evaluate_gradient(cuda, kw, tol_port, tol_direct):
     assert np.allclose(grad2[:, 0], grad, rtol=1e-6 if kw["precision"] == "f32" else 1e-12,
                        atol=1e-6 * np.abs(grad).max())
     assert np.allclose(grad2[:, 1], 2.0 * grad2[:, 0], rtol=1e-5, atol=1e-5 * np.abs(grad).max())
+
+
+# --------------------------------------------------------- device tree build
+@pytest.mark.parametrize("kind,depth", [("cube", 3), ("cube", 5), ("sphere", 6), ("two", 4)])
+def test_device_setup_matches_host(cuda, kind, depth):
+    """trees, near-field plan and BLAS-M2L plans built on
+    the device are bit-identical to the host build (octree.py,
+    engine.near_field_plan, m2l_blas.bucket_level + level_plan_from_buckets)."""
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(depth)
+    if kind == "sphere":
+        g = rng.standard_normal((60000, 3))
+        src = (g / np.linalg.norm(g, axis=1, keepdims=True) + 1.0) / 2.0
+        tgt = src
+    elif kind == "two":
+        src, tgt = rng.random((20000, 3)), rng.random((15000, 3)) * 0.5
+    else:
+        src = tgt = rng.random((30000, 3))
+    cfg = FmmConfig(depth=depth, order_equiv=4, backend="blas", precision="f32")
+    dev = setup(src, tgt, cfg, device_build=True)
+    host = setup(src, tgt, cfg, device_build=False)
+    for a, b in ((dev.source_tree, host.source_tree), (dev.target_tree, host.target_tree)):
+        assert np.array_equal(a.perm, b.perm)
+        for f in ("x", "y", "z", "leaf_starts", "leaf_counts"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
+        assert len(a.levels) == len(b.levels)
+        for la, lb in zip(a.levels, b.levels):
+            assert np.array_equal(la, lb)
+    assert np.array_equal(dev.near.offsets, host.near.offsets)
+    assert np.array_equal(dev.near.leaves, host.near.leaves)
+    assert dev.near.n_pairs == host.near.n_pairs
+    for lvl in host.blas_plans:
+        p, q = dev.blas_plans[lvl], host.blas_plans[lvl]
+        assert np.array_equal(p.tile_targets, q.tile_targets)
+        assert np.array_equal(p.tile_class, q.tile_class)
+        assert np.array_equal(p.src, q.src)
+        assert p.n_pairs == q.n_pairs
+        # the lazily built buckets equal the host's
+        bd, bh = dev.buckets[lvl], host.buckets[lvl]
+        for x, y in zip(bd.pairs, bh.pairs):
+            assert (x is None) == (y is None)
+            if x is not None:
+                assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
