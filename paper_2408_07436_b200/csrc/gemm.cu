@@ -7,6 +7,8 @@
 // accumulation and the L2L child scatter (rowmap).  The A loader can sum
 // `asum` column blocks (stride `astride`): that is how the partial
 // accumulators of the split M2L sweep are reduced, in a fixed order.
+#include <cstdlib>
+
 #include "common.cuh"
 
 using namespace kifmm;
@@ -142,6 +144,153 @@ int gemm(int64_t M, int64_t N, int64_t K, T alpha, const T* A, int64_t lda, int 
                             rowmap, accumulate, s);
 }
 
+// ---------------------------------------------------------------------------
+// float64 GEMM on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64), same
+// contract as gemm_kernel (split-sum A loader, colscale, alpha, accumulate,
+// row scatter).  CTA tile 128 x 64, 8 warps as 4 (M) x 2 (N), warp tile
+// 32 x 32 = 4 x 4 m8n8 fragments; 16-deep K stages, double-buffered: cp.async
+// straight to shared memory when A (asum == 1) and B rows are 16-byte
+// aligned, a register-staged loader otherwise.  Padded shared strides keep
+// the fragment loads conflict-free.
+constexpr int DBM = 128, DBN = 64, DBK = 16;
+constexpr int DAS = DBK + 4;    // A tile row stride (doubles)
+constexpr int DBS = DBN + 8;    // B tile row stride (doubles)
+
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) gemm_dmma_kernel(
+    int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
+    int asum, int64_t astride, const double* __restrict__ B, int64_t ldb,
+    const double* __restrict__ colscale, double* __restrict__ C, int64_t ldc,
+    const int32_t* __restrict__ rowmap, int accumulate, int async_a, int async_b) {
+  extern __shared__ __align__(16) double dg_smem[];
+  double (*As)[DBM * DAS] = reinterpret_cast<double (*)[DBM * DAS]>(dg_smem);
+  double (*Bs)[DBK * DBS] = reinterpret_cast<double (*)[DBK * DBS]>(dg_smem + 2 * DBM * DAS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int64_t m0 = (int64_t)blockIdx.y * DBM, n0 = (int64_t)blockIdx.x * DBN;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto stage = [&](int64_t k0, int buf) {
+    // A: 128 rows x 16 doubles = 8 chunks of 2 per row; thread -> (row, chunk)
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int e = tid + it * 256;
+      const int r = e >> 3, c = (e & 7) * 2;
+      const int64_t gm = m0 + r, gk = k0 + c;
+      double* dst = &As[buf][r * DAS + c];
+      if (async_a) {
+        const bool ok = gm < M && gk < K;         // K even: the pair is in or out together
+        cp_async16(dst, ok ? A + gm * lda + gk : A, ok);
+      } else {
+        double v0 = 0.0, v1 = 0.0;
+        if (gm < M) {
+          const double* p = A + gm * lda;
+          for (int q = 0; q < asum; ++q) {
+            if (gk < K) v0 += p[q * astride + gk];
+            if (gk + 1 < K) v1 += p[q * astride + gk + 1];
+          }
+        }
+        dst[0] = v0;
+        dst[1] = v1;
+      }
+    }
+    // B: 16 rows x 64 doubles = 32 chunks of 2 per row
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int e = tid + it * 256;
+      const int r = e >> 5, c = (e & 31) * 2;
+      const int64_t gk = k0 + r, gn = n0 + c;
+      double* dst = &Bs[buf][r * DBS + c];
+      if (async_b) {
+        const bool ok = gk < K && gn < N;         // N even
+        cp_async16(dst, ok ? B + gk * ldb + gn : B, ok);
+      } else {
+        dst[0] = (gk < K && gn < N) ? B[gk * ldb + gn] : 0.0;
+        dst[1] = (gk < K && gn + 1 < N) ? B[gk * ldb + gn + 1] : 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+
+  const int nk = (int)((K + DBK - 1) / DBK);
+  stage(0, 0);
+  const int arow = 32 * wm + (lane >> 2), acol = lane & 3;
+  const int bcol = 32 * wn + (lane >> 2), brow = lane & 3;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) {
+      stage((int64_t)(kt + 1) * DBK, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* a = &As[buf][arow * DAS + acol];
+    const double* b = &Bs[buf][brow * DBS + bcol];
+#pragma unroll
+    for (int ks = 0; ks < DBK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = a[i * 8 * DAS + ks];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = b[ks * DBS + j * 8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_884(acc[i][j], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gm = m0 + 32 * wm + 8 * i + (lane >> 2);
+    if (gm >= M) continue;
+    const int64_t row = rowmap ? (int64_t)rowmap[gm] : gm;
+    if (row < 0) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gn = n0 + 32 * wn + 8 * j + 2 * (lane & 3) + h;
+        if (gn >= N) continue;
+        double v = acc[i][j][h];
+        if (colscale) v *= colscale[gn];
+        v *= alpha;
+        double* dst = C + row * ldc + gn;
+        *dst = accumulate ? *dst + v : v;
+      }
+    }
+  }
+}
+
+int gemm_dmma(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+              int asum, int64_t astride, const double* B, int64_t ldb, const double* colscale,
+              double* C, int64_t ldc, const int32_t* rowmap, int accumulate, cudaStream_t s) {
+  const int async_a = asum == 1 && K % 2 == 0 && lda % 2 == 0 &&
+                      (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  const int async_b = N % 2 == 0 && ldb % 2 == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+  constexpr size_t kSmem = sizeof(double) * (2 * DBM * DAS + 2 * DBK * DBS);
+  set_max_smem((const void*)gemm_dmma_kernel, kSmem);
+  const int64_t max_rows = (int64_t)65535 * DBM;
+  for (int64_t r0 = 0; r0 < M; r0 += max_rows) {
+    const int64_t mm = M - r0 < max_rows ? M - r0 : max_rows;
+    dim3 grid(ceil_div(N, DBN), ceil_div(mm, DBM));
+    gemm_dmma_kernel<<<grid, 256, kSmem, s>>>(mm, N, K, alpha, A + r0 * lda, lda, asum, astride, B, ldb,
+                                          colscale, rowmap ? C : C + r0 * ldc, ldc,
+                                          rowmap ? rowmap + r0 : nullptr, accumulate, async_a,
+                                          async_b);
+  }
+  return launch_status();
+}
+
 template <typename T>
 __global__ void stack_kernel(const T* __restrict__ mult, const int32_t* __restrict__ child,
                              int64_t n_par, int64_t nrhs, int64_t ne, T* __restrict__ out) {
@@ -230,6 +379,15 @@ int kifmm_gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* 
                    int asum, int64_t astride, const double* B, int64_t ldb,
                    const double* colscale, double* C, int64_t ldc, const int32_t* rowmap,
                    int accumulate, void* s) {
+  // FP64 tensor cores for every tile-worthy shape (KIFMM_GEMM_DMMA=0: SIMT)
+  static int dmma = -1;
+  if (dmma < 0) {
+    const char* e = getenv("KIFMM_GEMM_DMMA");
+    dmma = e ? atoi(e) : 1;
+  }
+  if (dmma && M >= 256 && N >= 8 && K >= 4 && asum >= 1)
+    return gemm_dmma(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,
+                     accumulate, (cudaStream_t)s);
   return gemm<double>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,
                       accumulate, s);
 }

@@ -18,21 +18,22 @@ else:
 t0 = time.perf_counter(); inst = setup(pts, pts, FmmConfig(**kw)); ts = time.perf_counter() - t0
 dev = inst.device
 qd = torch.from_numpy(q).cuda()
+grad = "grad" in mode
 for _ in range(2):
-    dev.evaluate_graphed(qd, 1)
+    dev.evaluate_graphed(qd, 1, gradient=grad)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(5):
-    dev.evaluate_graphed(qd, 1)
+    dev.evaluate_graphed(qd, 1, gradient=grad)
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 5
 with profile_launches() as p:
-    dev.evaluate_device(qd, 1)
+    dev.evaluate_device(qd, 1, gradient=grad)
 agg = {}
 for name, tag, t in p.times():
     key = tag[:3] + ":" + name.replace("kifmm_", "")
     agg[key] = agg.get(key, 0) + t
-print(f"n={n} {kw} setup {ts:.1f}s evaluate {ms:.3f} ms -> {n/ms/1e3:.1f} Mpts/s")
+print(f"n={n} {kw} {mode} setup {ts:.1f}s evaluate {ms:.3f} ms -> {n/ms/1e3:.1f} Mpts/s")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:12]:
     print(f"   {k:40s} {v*1e3:9.1f} us")
