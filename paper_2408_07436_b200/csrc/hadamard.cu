@@ -11,6 +11,8 @@
 // registers for the whole sweep (64 complex MACs per gathered offset), so
 // the FP64/FP32 FMA pipe, not the loads, sets the pace.  phat is read and
 // written once.
+#include <cstdlib>
+
 #include "common.cuh"
 
 using namespace kifmm;
@@ -184,6 +186,11 @@ constexpr int UMAX = 600;      // source slots per tile; slots UMAX..UMAX+7 are 
 constexpr int QROWS = UMAX + 8;
 constexpr int FCH = 8;         // frequencies per CTA
 
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
 template <typename C> __device__ __forceinline__ C lds_c(unsigned a);
 template <> __device__ __forceinline__ double2 lds_c<double2>(unsigned a) {
   double2 v;
@@ -321,6 +328,138 @@ __global__ void __launch_bounds__(256, 1) hadamard_tiled_kernel(
   }
 }
 
+// float64 variant on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).  Per
+// (frequency, offset) the tile's block product is a real GEMM
+//   [Yre Yim] (256 x 16) += [Xre Xim] (256 x 16) . [[Kr^T, Ki^T], [-Ki^T, Kr^T]]
+// (k = 2 sigma + part, n = 2 tau + part).  An m8 fragment's 8 rows are the
+// 8 siblings of an octet (one per parity class: the A loads of a warp hit 16
+// distinct 16-byte units, see uslot); B fragments are read from the complex
+// khat in shared memory with the sign of -Ki applied per lane.  Staging,
+// plan and zero rows are those of hadamard_tiled_kernel.
+__global__ void __launch_bounds__(256, 1) hadamard_tiled_dmma_kernel(
+    const double2* __restrict__ khat, const double2* __restrict__ qhat,
+    const int64_t* __restrict__ tile_begin, const int64_t* __restrict__ src_off,
+    const int64_t* __restrict__ src, const int16_t* __restrict__ slots,
+    const int16_t* __restrict__ tcol, int64_t nf, int64_t nsc, int64_t ntc, int64_t nrhs,
+    int accumulate, double2* __restrict__ phat) {
+  using C = double2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* ks = reinterpret_cast<C*>(smem_raw);                        // [2][26][8 sigma][8 tau]
+  C* qs = ks + 2 * 26 * 64;                                      // [2][QROWS * 8]
+  int16_t* sl = reinterpret_cast<int16_t*>(qs + 2 * QROWS * 8);  // [26][TT]
+  int* ss = reinterpret_cast<int*>(sl + 26 * TT);                // [UMAX]
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int64_t t = blockIdx.x;
+  const int64_t f0 = (int64_t)blockIdx.y * FCH;
+  const int64_t r = blockIdx.z;
+  const int nfc = (int)min64(FCH, nf - f0);
+  const int64_t cb = tile_begin[t];
+  const int64_t so = src_off[t];
+  const int ns = (int)(src_off[t + 1] - so);
+
+  {
+    const int4* s4 = reinterpret_cast<const int4*>(slots + t * 26 * TT);
+    int4* d4 = reinterpret_cast<int4*>(sl);
+    for (int e = tid; e < 26 * TT * 2 / 16; e += 256) d4[e] = __ldg(&s4[e]);
+    for (int e = tid; e < ns; e += 256) ss[e] = (int)__ldg(&src[so + e]);
+    for (int e = tid; e < 2 * 64; e += 256)
+      qs[(e >> 6) * QROWS * 8 + UMAX * 8 + (e & 63)] = C{0.0, 0.0};
+  }
+  const int g8 = l >> 2, kq = l & 3;
+  const int c0 = 32 * w + 4 * g8;        // slot-table columns of this lane's 4 m-tile rows
+  int tgt[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tgt[i] = __ldg(&tcol[t * TT + c0 + i]);
+  const bool active = __any_sync(0xffffffffu, (tgt[0] >= 0) | (tgt[1] >= 0) | (tgt[2] >= 0) |
+                                                  (tgt[3] >= 0));
+  // B fragment coordinates: k = 4 ks + kq -> (sigma = 2 ks + (kq >> 1), pk = kq & 1);
+  // n = 8 jn + g8 -> (tau = 4 jn + (g8 >> 1), pn = g8 & 1)
+  const int pk = kq & 1, pn = g8 & 1;
+  const int comp = pk ^ pn;                              // 0: Re K, 1: Im K
+  const unsigned long long neg = (pk && !pn) ? 0x8000000000000000ull : 0ull;
+  __syncthreads();
+
+  auto stage = [&](int64_t f, int b) {
+    const C* kf = khat + f * (26 * 64);
+    C* kd = ks + b * 26 * 64;
+    for (int e = tid; e < 26 * 64; e += 256) {
+      const int o = e >> 6, tau = (e >> 3) & 7, sg = e & 7;
+      cp_async_c(kd + (o * 8 + sg) * 8 + tau, kf + e, true);
+    }
+    C* qd = qs + b * QROWS * 8;
+    const C* qf = qhat + f * nsc * 8 * nrhs + r;
+    for (int e = tid; e < ns * 8; e += 256) {
+      const int u = e >> 3, sg = e & 7;
+      const int sc = ss[u];
+      if (sc >= 0) cp_async_c(qd + u * 8 + (sg ^ (u & 7)), qf + ((int64_t)sc * 8 + sg) * nrhs, true);
+    }
+    cp_async_commit();
+  };
+
+  stage(f0, 0);
+  for (int i = 0; i < nfc; ++i) {
+    const int b = i & 1;
+    if (i + 1 < nfc) {
+      stage(f0 + i + 1, b ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (active) {
+      const double* q = reinterpret_cast<const double*>(qs + b * QROWS * 8);
+      const double* kb = reinterpret_cast<const double*>(ks + b * 26 * 64);
+      double acc[4][2][2];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int jn = 0; jn < 2; ++jn) acc[m][jn][0] = acc[m][jn][1] = 0.0;
+#pragma unroll 2
+      for (int o = 0; o < 26; ++o) {
+        const short4 s4 = *reinterpret_cast<const short4*>(sl + o * TT + c0);
+        const int su[4] = {s4.x, s4.y, s4.z, s4.w};
+        const int c = su[0] & 7;                         // source class, same for the 4 rows
+        const double* ko = kb + (o * 64) * 2;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int sga = 2 * kk + (kq >> 1);
+          const int aoff = 2 * (sga ^ c) + pk;
+          double af[4], bf[2];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) af[m] = q[su[m] * 16 + aoff];
+#pragma unroll
+          for (int jn = 0; jn < 2; ++jn) {
+            const int tau = 4 * jn + (g8 >> 1);
+            const double v = ko[(sga * 8 + tau) * 2 + comp];
+            bf[jn] = __longlong_as_double(__double_as_longlong(v) ^ (long long)neg);
+          }
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int jn = 0; jn < 2; ++jn) dmma_884(acc[m][jn], af[m], bf[jn]);
+        }
+      }
+      C* pf = phat + (f0 + i) * ntc * 8 * nrhs + r;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (tgt[m] < 0) continue;
+#pragma unroll
+        for (int jn = 0; jn < 2; ++jn) {
+          C* p = pf + ((cb + tgt[m]) * 8 + 4 * jn + kq) * nrhs;
+          C v{acc[m][jn][0], acc[m][jn][1]};
+          if (accumulate) {
+            const C old = *p;
+            v.x += old.x;
+            v.y += old.y;
+          }
+          *p = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <typename T>
 int hadamard_tiled(const T* khat, const T* qhat, const int64_t* tile_begin, const int64_t* src_off,
                    const int64_t* src, const int16_t* slots, const int16_t* tcol, int64_t n_tiles,
@@ -331,8 +470,23 @@ int hadamard_tiled(const T* khat, const T* qhat, const int64_t* tile_begin, cons
   if (n_tiles == 0 || nf == 0) return 0;
   const size_t smem = (2 * 26 * 64 + 2 * QROWS * 8) * sizeof(C) + 26 * TT * sizeof(int16_t) +
                       UMAX * sizeof(int);
-  set_max_smem((const void*)hadamard_tiled_kernel<T>, smem);
   dim3 grid((unsigned)n_tiles, ceil_div(nf, FCH), (unsigned)nrhs);
+  if constexpr (sizeof(T) == 8) {
+    static int dmma = -1;
+    if (dmma < 0) {
+      const char* e = getenv("KIFMM_HADAMARD_DMMA");
+      dmma = e ? atoi(e) : 1;
+    }
+    if (dmma) {
+      set_max_smem((const void*)hadamard_tiled_dmma_kernel, smem);
+      hadamard_tiled_dmma_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(
+          reinterpret_cast<const double2*>(khat), reinterpret_cast<const double2*>(qhat),
+          tile_begin, src_off, src, slots, tcol, nf, nsc, ntc, nrhs, accumulate,
+          reinterpret_cast<double2*>(phat));
+      return launch_status();
+    }
+  }
+  set_max_smem((const void*)hadamard_tiled_kernel<T>, smem);
   hadamard_tiled_kernel<T><<<grid, 256, smem, (cudaStream_t)stream>>>(
       reinterpret_cast<const C*>(khat), reinterpret_cast<const C*>(qhat), tile_begin, src_off, src,
       slots, tcol, nf, nsc, ntc, nrhs, accumulate, reinterpret_cast<C*>(phat));
