@@ -811,11 +811,18 @@ class DeviceFmm:
                 return out[0].cpu().numpy().copy(), out[1].cpu().numpy().copy()
             return out.cpu().numpy().copy()
         g, static_q, out = self.graph_for(R, gradient)
-        static_q.copy_(src)
+        # pinned host charges go over asynchronously, ordered before the replay
+        static_q.copy_(src, non_blocking=src.is_pinned())
         g.replay()
-        if gradient:
-            return out[0].cpu().numpy(), out[1].cpu().numpy()
-        return out.cpu().numpy()
+        outs = out if gradient else (out,)
+        # results land in fresh pinned buffers (the caller owns the arrays; the
+        # caching host allocator recycles a buffer only once it is released)
+        host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+        for h, o in zip(host, outs):
+            h.copy_(o, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        res = tuple(h.numpy() for h in host)
+        return res if gradient else res[0]
 
 
 # ---------------------------------------------------------------- shims
