@@ -128,6 +128,7 @@ struct TmaArgs {
   const int8_t* offsets;           // (316, 3)
   int64_t nrhs;
   int nsplit, jper;
+  int split_smem;                  // 1: A arrives raw (fp32), hi/lo formed in shared memory
   float* acc_out;
 };
 
@@ -146,7 +147,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
   const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
   uint64_t* empty = full + stages;
-  uint64_t* tfull = empty + stages;
+  uint64_t* ready = empty + stages;                      // A hi/lo formed (split_smem)
+  uint64_t* tfull = ready + stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -172,6 +174,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&ready[s], 128);
     }
     mbar_init(&tfull[0], 1);
     mbar_init(&tfull[1], 1);
@@ -210,11 +213,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
         const uint32_t bb = (uint32_t)(n_out * kc * 4);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                          smem_u32(&full[stage])),
-                     "r"(2 * a_bytes + 2 * bb)
+                     "r"((a.split_smem ? 1 : 2) * a_bytes + 2 * bb)
                      : "memory");
         const int c4 = sp * (int)a.nrhs + (int)r;
         tma_load_5d(sb, &tm_hi, c * KC, sz, sy, sx, c4, &full[stage]);
-        tma_load_5d(sb + a_bytes, &tm_lo, c * KC, sz, sy, sx, c4, &full[stage]);
+        if (!a.split_smem) tma_load_5d(sb + a_bytes, &tm_lo, c * KC, sz, sy, sx, c4, &full[stage]);
         const int64_t boff = (int64_t)t * n_out * kin + (int64_t)n_out * KC * c;
         bulk_copy(sb + 2 * a_bytes, a.bhi + boff, bb, &full[stage]);
         bulk_copy(sb + 2 * a_bytes + b_bytes, a.blo + boff, bb, &full[stage]);
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
         uint32_t acc_flag = 0;
         for (; st < vend * nchunks; ++st) {
           const int stage = st % stages;
-          mbar_wait(&full[stage], (st / stages) & 1, false);
+          mbar_wait(a.split_smem ? &ready[stage] : &full[stage], (st / stages) & 1, false);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const int c = st % nchunks;
           const int kc = min(KC, kin - c * KC);
@@ -260,12 +263,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
     }
     __syncwarp();
   } else {
-    // ------------------------------------- accumulator warps (2..5) + epilogue
+    // ------------------- accumulator warps (2..5): A hi/lo split, promotion
     const int sub = warp & 3;
     const int m = sub * 32 + lane;
     const uint32_t lane_base = (uint32_t)(sub * 32) << 16;
     const uint32_t acc_col = tmem + lane_base + 2u * (uint32_t)n_out;
-    for (int bi = 0; bi < nblocks; ++bi) {
+    const int ct = tid - 64;                               // 0..127 converter thread
+    auto promote = [&](int bi) {
       const int buf = bi & 1;
       mbar_wait(&tfull[buf], (bi >> 1) & 1, true);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -284,6 +288,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf]))
                    : "memory");
+    };
+    // A tile of a stage arrives raw (fp32, 128B-swizzled): form hi = tf32(A)
+    // in place and lo = tf32(A - hi) in the lo slot (element-wise, so the
+    // swizzled layout is kept), then release the stage to the MMA warp.
+    auto split_stage = [&](int st) {
+      const int stage = st % stages;
+      mbar_wait(&full[stage], (st / stages) & 1, false);
+      float4* hi4 = reinterpret_cast<float4*>(smem + stage * stage_bytes);
+      float4* lo4 = reinterpret_cast<float4*>(smem + stage * stage_bytes + a_bytes);
+#pragma unroll 4
+      for (int e = ct; e < (int)(a_bytes / 16); e += 128) {
+        float4 v = hi4[e], h, l;
+        float* pv = &v.x;
+        float* ph = &h.x;
+        float* pl = &l.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t hb, lb;
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(pv[q]));
+          ph[q] = __uint_as_float(hb);
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(pv[q] - ph[q]));
+          pl[q] = __uint_as_float(lb);
+        }
+        hi4[e] = h;
+        lo4[e] = l;
+      }
+      // generic-proxy writes -> visible to the tensor core (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&ready[stage]))
+                   : "memory");
+    };
+    int st = 0;
+    for (int bi = 0; bi <= nblocks; ++bi) {
+      if (a.split_smem && bi < nblocks) {
+        const int vend = min(nvec, (bi + 1) * FLUSH_V);
+        for (; st < vend * nchunks; ++st) split_stage(st);
+      }
+      if (bi >= 1) promote(bi - 1);
     }
     const int32_t tgt = a.tile_targets[slot * TMT + m];
     const int64_t ld = (int64_t)a.nsplit * n_out;
@@ -357,6 +399,10 @@ __global__ void dense_split_kernel(const float* __restrict__ qt, const int32_t* 
   const int64_t p = s / h3, cell = s - p * h3;
   const int64_t d = ((p * nrhs + r) * h3 + cell) * kin + k;
   const float v = qt[idx];
+  if (!lo) {                       // raw values; the sweep splits in shared memory
+    hi[d] = v;
+    return;
+  }
   uint32_t hb;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
   const float hf = __uint_as_float(hb);
@@ -391,9 +437,12 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
       n_tiles < 0 || nrhs < 1 || nsplit < 1 || nsplit > 189 || h < 1)
     return KIFMM_EARG;
   if (n_tiles == 0) return 0;
+  // qlo == NULL: qhi holds the raw fp32 values and the sweep forms hi/lo in
+  // shared memory (half the TMA traffic for the A operand)
+  const int split_smem = qlo == nullptr;
   CUtensorMap tm_hi, tm_lo;
   int st = make_map(&tm_hi, qhi, (int)kin, (int)h, 8 * nrhs);
-  if (!st) st = make_map(&tm_lo, qlo, (int)kin, (int)h, 8 * nrhs);
+  if (!st) st = make_map(&tm_lo, split_smem ? qhi : qlo, (int)kin, (int)h, 8 * nrhs);
   if (st) return st;
   const size_t stage_bytes = 2 * (size_t)TMT * KC * 4 + 2 * (size_t)n_out * KC * 4;
   static int max_stages = -1, ctas = -1;
@@ -410,7 +459,7 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
   int stages = (int)(((cps == 1 ? 222 * 1024 : 200 * 1024) / cps) / stage_bytes);
   if (stages > max_stages) stages = max_stages;
   if (stages < 2) return KIFMM_EARG;
-  const size_t smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  const size_t smem = 1024 + stages * stage_bytes + (3 * stages + 4) * 8 + 16;
   set_max_smem((const void*)m2l_sweep_tma_kernel, smem);
   TmaArgs a;
   a.bhi = bhi;
@@ -430,6 +479,7 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
   a.nsplit = (int)nsplit;
   a.jper = (int)((189 + nsplit - 1) / nsplit);
   a.acc_out = acc;
+  a.split_smem = split_smem;
   dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)nsplit);
   m2l_sweep_tma_kernel<<<grid, NTHREADS, smem, (cudaStream_t)stream>>>(tm_hi, tm_lo, a);
   return launch_status();

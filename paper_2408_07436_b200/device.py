@@ -291,6 +291,7 @@ class BlasDevice:
         # (3 TMEM accumulators of n_out <= 160 columns fit the 512-column TMEM;
         # above 256 columns the kernels run one CTA per SM)
         self.tc = bool(tensor_cores) and dt == np.float32 and -(-k // 16) * 16 <= 160
+        self.split_smem = os.environ.get("KIFMM_TMA_SPLIT", "host") == "smem"
         if self.tc:
             self.kin = -(-k // 8) * 8
             self.ko_pad = -(-k // 16) * 16
@@ -360,6 +361,11 @@ class BlasDevice:
         ld = nsplit * self.ko_pad
         la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
         hi, lo = dense
+        # KIFMM_TMA_SPLIT=smem: the dense array holds raw fp32 q~ and the sweep
+        # forms the TF32 hi/lo pair in shared memory (half the TMA bytes for A;
+        # measured slower on B200: the sweep is bound by shared-memory traffic,
+        # which the in-place split adds to)
+        lo = None if self.split_smem else lo
         launch("kifmm_dense_split_tf32", P(qt), P(plan["src_slot"]), n_s, nrhs, self.kin,
                plan["h"], P(hi), P(lo), stream_handle())
         launch("kifmm_m2l_sweep_tma_f32", P(hi), P(lo), P(self.Bhi), P(self.Blo), self.kin,
