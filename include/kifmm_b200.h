@@ -172,6 +172,16 @@ int kifmm_m2l_sweep_f64(const double* qt, const double* Dt, int64_t ki, int64_t 
                         const int32_t* tile_targets, const int32_t* tile_class,
                         const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
                         int64_t nrhs, int64_t nsplit, double* acc, void* stream);
+/* float64 sweep for sparse trees (empty boxes skipped, config 5): per tile
+ * only the vectors jlist[tile][0 .. jcount[tile]) that meet a source (int16,
+ * ascending), and per vector the 8-row groups with a source (gmask bits,
+ * uint16 over the tile's 16 groups); the others skip their DMMAs. */
+int kifmm_m2l_sweep_sparse_f64(const double* qt, const double* Dt, int64_t kin, int64_t ko_pad,
+                               const int32_t* tile_targets, const int32_t* tile_class,
+                               const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
+                               int64_t nrhs, int64_t nsplit, const uint16_t* gmask,
+                               const int16_t* jlist, const int32_t* jcount, double* acc,
+                               void* stream);
 
 /* Same sweep on the tcgen05 tensor cores for float32 (3xTF32): the caller
  * passes q~ split into TF32 hi/lo parts (kifmm_split_tf32) and the cores

@@ -50,6 +50,8 @@ SIGNATURES = {
     "kifmm_stack_children_f64": [_P, _P, _I, _I, _I, _P, _P],
     "kifmm_m2l_sweep_f32": [_P, _P, _I, _I, _P, _P, _P, _P, _I, _I, _I, _P, _P],
     "kifmm_m2l_sweep_f64": [_P, _P, _I, _I, _P, _P, _P, _P, _I, _I, _I, _P, _P],
+    "kifmm_m2l_sweep_sparse_f64": [_P, _P, _I, _I, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P,
+                                   _P],
     "kifmm_fft_forward_f32": [_P, _I, _I, _P, _I, _P, _I, _P, _P],
     "kifmm_fft_forward_f64": [_P, _I, _I, _P, _I, _P, _I, _P, _P],
     "kifmm_gather_rows_f32": [_P, _P, _I, _I, _P, _P],

@@ -205,36 +205,42 @@ int sweep(const T* qt, const T* Dt, int64_t kin, int64_t ko_pad, const int32_t* 
 // fp64 products and sums (only the summation order differs from SIMT).
 // Geometry (device.py blas_geometry): kin % 16 == 0; ko_pad = n_slabs * kob,
 // kob % 16 == 0, kob <= 160, n_slabs = ceil(ko_pad / 160).
-namespace dm {
-constexpr int BK = 16;          // k-chunk per pipeline stage
-constexpr int GS = BK + 4;      // Gs row stride (doubles): rows 8r..8r+3 -> distinct bank quarters
-constexpr int KOB_MAX = 160;
-}
-
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
 
-template <int NTW>
-__global__ void __launch_bounds__(256, NTW > 6 ? 1 : 2) m2l_sweep_dmma_kernel(
+template <int NTW, int BKT, int STG, int MINB>
+__global__ void __launch_bounds__(256, MINB) m2l_sweep_dmma_kernel(
     const double* __restrict__ qt, const double* __restrict__ Dt, int kin, int ko_pad,
     int nchunks, int n_slabs, int jper, const int32_t* __restrict__ tile_targets,
     const int32_t* __restrict__ tile_class, const int32_t* __restrict__ src,
-    const int32_t* __restrict__ class_tv, int64_t nrhs, int nsplit, double* __restrict__ acc_out) {
-  using namespace dm;
+    const int32_t* __restrict__ class_tv, int64_t nrhs, int nsplit,
+    const uint16_t* __restrict__ gmask, const int16_t* __restrict__ jlist,
+    const int32_t* __restrict__ jcount, double* __restrict__ acc_out) {
+  constexpr int BK = BKT;                             // k-chunk per pipeline stage
+  constexpr int GS = BK + 4;                          // row stride = 32 mod 128 bytes: conflict-free A
   constexpr int KOB = 16 * NTW;
   constexpr int DS = KOB + 8;                         // Ds row stride: rows k, k+1 in opposite bank halves
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* Gs = reinterpret_cast<double*>(smem_raw);   // [2][TMT][GS]
-  double* Ds = Gs + 2 * TMT * GS;                     // [2][BK][DS]
+  double* Gs = reinterpret_cast<double*>(smem_raw);   // [STG][TMT][GS]
+  double* Ds = Gs + STG * TMT * GS;                   // [STG][BK][DS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 3, wn = warp >> 2;
   const int64_t tile = blockIdx.x;
   const int64_t r = blockIdx.y;
   const int slab = blockIdx.z % n_slabs, split = blockIdx.z / n_slabs;
   const int c0 = slab * KOB;
-  const int j0 = split * jper, j1 = min(189, j0 + jper);
+  // Sparse trees: the tile's vectors with at least one source (jlist, in
+  // ascending order) are split over the CTAs of the tile, and per vector the
+  // 8-row groups without any source (gmask bit clear) skip their DMMAs.
+  const int cnt = jcount ? jcount[tile] : 189;
+  const int jp = jcount ? (cnt + nsplit - 1) / nsplit : jper;
+  const int j0 = split * jp, j1 = min(cnt, j0 + jp);
+  const int16_t* jl = jlist ? jlist + tile * 189 : nullptr;
+  const uint16_t* gm = gmask ? gmask + tile * 189 : nullptr;
+  auto vec_of = [&](int p) { return jl ? (int)jl[p] : p; };
+  __shared__ uint32_t stage_bits[STG];
   const int32_t* tsrc = src + tile * 189 * TMT;
   const int32_t* tv_list = class_tv + tile_class[tile] * 189;
 
@@ -244,68 +250,93 @@ __global__ void __launch_bounds__(256, NTW > 6 ? 1 : 2) m2l_sweep_dmma_kernel(
 #pragma unroll
     for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // Gather assignment: rows (tid >> 3) + 32 i, 16-byte chunk tid & 7.
-  const int grow = tid >> 3, gch = tid & 7;
-  int ids_cur[4], ids_next[4];
-  auto load_ids = [&](int j, int (&ids)[4]) {
+  // Gather assignment: 16-byte chunk tid % CPR of rows tid / CPR + RPP * i.
+  constexpr int CPR = BK / 2, RPP = 256 / CPR, NR = TMT / RPP;
+  const int grow = tid / CPR, gch = tid % CPR;
+  int ids_cur[NR], ids_next[NR];
+  auto load_ids = [&](int j, int (&ids)[NR]) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) ids[i] = j < j1 ? __ldg(&tsrc[j * TMT + grow + 32 * i]) : -1;
+    for (int i = 0; i < NR; ++i)
+      ids[i] = j < j1 ? __ldg(&tsrc[vec_of(j) * TMT + grow + RPP * i]) : -1;
   };
   const int nsteps = (j1 - j0) * nchunks;
   auto stage = [&](int st, int buf) {
-    const int j = j0 + st / nchunks, ch = st % nchunks;
+    const int p = j0 + st / nchunks, ch = st % nchunks;
+    const int j = vec_of(p);
     if (ch == 0) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) ids_cur[i] = ids_next[i];
-      load_ids(j + 1, ids_next);
+      for (int i = 0; i < NR; ++i) ids_cur[i] = ids_next[i];
+      load_ids(p + 1, ids_next);
     }
+    if (tid == 0) stage_bits[buf] = gm ? (uint32_t)gm[j] : 0xFFFFu;
     const int kk0 = ch * BK;
+    const bool kin_ok = kk0 + 2 * gch < kin;           // a partial last chunk reads zeros
     double* g = Gs + buf * TMT * GS;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NR; ++i) {
       const int s = ids_cur[i];
-      const double* gp = qt + ((int64_t)(s < 0 ? 0 : s) * nrhs + r) * kin + kk0 + 2 * gch;
-      cp_async16(g + (grow + 32 * i) * GS + 2 * gch, gp, s >= 0);
+      const bool ok = s >= 0 && kin_ok;
+      const double* gp = qt + ((int64_t)(ok ? s : 0) * nrhs + r) * kin + (ok ? kk0 + 2 * gch : 0);
+      cp_async16(g + (grow + RPP * i) * GS + 2 * gch, gp, ok);
     }
     const double* dsrc = Dt + ((int64_t)tv_list[j] * kin + kk0) * ko_pad + c0;
     double* d = Ds + buf * BK * DS;
     constexpr int DCH = BK * KOB / 2;
     for (int e = tid; e < DCH; e += 256) {
       const int row = e / (KOB / 2), v = e - row * (KOB / 2);
-      cp_async16(d + row * DS + 2 * v, dsrc + (int64_t)row * ko_pad + 2 * v, true);
+      const bool ok = kk0 + row < kin;
+      cp_async16(d + row * DS + 2 * v, ok ? dsrc + (int64_t)row * ko_pad + 2 * v : Dt, ok);
     }
     cp_async_commit();
   };
 
   load_ids(j0, ids_next);
-  if (nsteps > 0) stage(0, 0);
+  // STG-deep cp.async ring: stages st+1 .. st+STG-1 in flight while st computes
+  for (int q = 0; q < STG - 1; ++q) {
+    if (q < nsteps) stage(q, q);
+    else cp_async_commit();
+  }
   const int arow = 32 * wm + (lane >> 2), acol = lane & 3;
   const int bcol = wn * (KOB / 2) + (lane >> 2), brow = lane & 3;
   for (int st = 0; st < nsteps; ++st) {
-    const int buf = st & 1;
-    if (st + 1 < nsteps) {
-      stage(st + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    const int buf = st % STG;
+    cp_async_wait<STG - 2>();
     __syncthreads();
+    if (st + STG - 1 < nsteps) stage(st + STG - 1, (st + STG - 1) % STG);
+    else cp_async_commit();
     const double* g = Gs + buf * TMT * GS + arow * GS + acol;
     const double* d = Ds + buf * BK * DS + brow * DS + bcol;
+    const uint32_t mb = (stage_bits[buf] >> (4 * wm)) & 0xFu;   // warp-uniform
+    if (mb == 0xFu) {
 #pragma unroll
-    for (int ks = 0; ks < BK; ks += 4) {
-      double a[4], b[NTW];
+      for (int ks = 0; ks < BK; ks += 4) {
+        double a[4], b[NTW];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) a[mt] = g[mt * 8 * GS + ks];
+        for (int mt = 0; mt < 4; ++mt) a[mt] = g[mt * 8 * GS + ks];
 #pragma unroll
-      for (int nt = 0; nt < NTW; ++nt) b[nt] = d[ks * DS + nt * 8];
+        for (int nt = 0; nt < NTW; ++nt) b[nt] = d[ks * DS + nt * 8];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+        for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NTW; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
+          for (int nt = 0; nt < NTW; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
+      }
+    } else if (mb) {
+#pragma unroll 2
+      for (int ks = 0; ks < BK; ks += 4) {
+        double b[NTW];
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt) b[nt] = d[ks * DS + nt * 8];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          if (!((mb >> mt) & 1u)) continue;
+          const double a = g[mt * 8 * GS + ks];
+#pragma unroll
+          for (int nt = 0; nt < NTW; ++nt) dmma884(acc[mt][nt], a, b[nt]);
+        }
+      }
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
   const int64_t ld = (int64_t)nsplit * ko_pad;
 #pragma unroll
@@ -322,35 +353,53 @@ __global__ void __launch_bounds__(256, NTW > 6 ? 1 : 2) m2l_sweep_dmma_kernel(
 
 int sweep_dmma(const double* qt, const double* Dt, int64_t kin, int64_t ko_pad,
                const int32_t* tile_targets, const int32_t* tile_class, const int32_t* src,
-               const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, int64_t nsplit, double* acc,
+               const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, int64_t nsplit,
+               const uint16_t* gmask, const int16_t* jlist, const int32_t* jcount, double* acc,
                void* stream) {
-  using namespace dm;
-  if (kin < BK || kin % BK || ko_pad < 16 || n_tiles < 0 || nrhs < 1 || nsplit < 1 || nsplit > 189)
+  constexpr int KOB_MAX = 160;
+  if (kin < 16 || kin % 16 || ko_pad < 16 || n_tiles < 0 || nrhs < 1 || nsplit < 1 ||
+      nsplit > 189)
     return KIFMM_EARG;
   if (n_tiles == 0) return 0;
   const int n_slabs = (int)((ko_pad + KOB_MAX - 1) / KOB_MAX);
   if (ko_pad % n_slabs) return KIFMM_EARG;
   const int kob = (int)(ko_pad / n_slabs);
   if (kob % 16 || kob > KOB_MAX) return KIFMM_EARG;
-  const int nchunks = (int)(kin / BK);
   const int jper = (int)((189 + nsplit - 1) / nsplit);
-  const size_t smem = sizeof(double) * (2 * TMT * GS + 2 * BK * (kob + 8));
   dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)(n_slabs * nsplit));
   cudaStream_t s = (cudaStream_t)stream;
-  switch (kob / 16) {
-#define KIFMM_DMMA(NT_)                                                                          \
+  // Pipeline: 32-wide K chunks, 3 stages for large ranks (many stages per
+  // vector; latency-bound at 2 x 16); 16-wide double buffering for small k.
+  const bool wide = kin >= 64;
+  const int bk = wide ? 32 : 16;
+  const int nchunks = (int)((kin + bk - 1) / bk);
+  auto smem_of = [&](int st) {
+    return sizeof(double) * (size_t)st * (TMT * (bk + 4) + bk * (kob + 8));
+  };
+  const int stg = (wide && smem_of(3) <= 227 * 1024) ? 3 : 2;
+  const size_t smem = smem_of(stg);
+#define KIFMM_DMMA(NT_, BK_, STG_, MB_)                                                         \
+  {                                                                                              \
+    auto k_ = m2l_sweep_dmma_kernel<NT_, BK_, STG_, MB_>;                                        \
+    set_max_smem((const void*)k_, smem);                                                         \
+    k_<<<grid, 256, smem, s>>>(qt, Dt, (int)kin, (int)ko_pad, nchunks, n_slabs, jper,            \
+                               tile_targets, tile_class, src, class_tv, nrhs, (int)nsplit,       \
+                               gmask, jlist, jcount, acc);                                       \
+  }
+#define KIFMM_DMMA_NT(NT_)                                                                      \
   case NT_:                                                                                      \
-    set_max_smem((const void*)m2l_sweep_dmma_kernel<NT_>, smem);                                \
-    m2l_sweep_dmma_kernel<NT_><<<grid, 256, smem, s>>>(qt, Dt, (int)kin, (int)ko_pad, nchunks, \
-                                                       n_slabs, jper, tile_targets, tile_class, \
-                                                       src, class_tv, nrhs, (int)nsplit, acc);  \
+    if (wide && stg == 3) KIFMM_DMMA(NT_, 32, 3, 1)                                              \
+    else if (wide) KIFMM_DMMA(NT_, 32, 2, 1)                                                     \
+    else KIFMM_DMMA(NT_, 16, 2, (NT_ > 5 ? 1 : 2))                                               \
     break;
-    KIFMM_DMMA(1) KIFMM_DMMA(2) KIFMM_DMMA(3) KIFMM_DMMA(4) KIFMM_DMMA(5)
-    KIFMM_DMMA(6) KIFMM_DMMA(7) KIFMM_DMMA(8) KIFMM_DMMA(9) KIFMM_DMMA(10)
-#undef KIFMM_DMMA
+  switch (kob / 16) {
+    KIFMM_DMMA_NT(1) KIFMM_DMMA_NT(2) KIFMM_DMMA_NT(3) KIFMM_DMMA_NT(4) KIFMM_DMMA_NT(5)
+    KIFMM_DMMA_NT(6) KIFMM_DMMA_NT(7) KIFMM_DMMA_NT(8) KIFMM_DMMA_NT(9) KIFMM_DMMA_NT(10)
     default:
       return KIFMM_EARG;
   }
+#undef KIFMM_DMMA_NT
+#undef KIFMM_DMMA
   return launch_status();
 }
 
@@ -370,7 +419,17 @@ int kifmm_m2l_sweep_f64(const double* qt, const double* Dt, int64_t kin, int64_t
                         const int32_t* class_tv, int64_t n_tiles, int64_t nrhs, int64_t nsplit,
                         double* acc, void* s) {
   return sweep_dmma(qt, Dt, kin, ko_pad, tile_targets, tile_class, src, class_tv, n_tiles, nrhs,
-                    nsplit, acc, s);
+                    nsplit, nullptr, nullptr, nullptr, acc, s);
+}
+int kifmm_m2l_sweep_sparse_f64(const double* qt, const double* Dt, int64_t kin, int64_t ko_pad,
+                               const int32_t* tile_targets, const int32_t* tile_class,
+                               const int32_t* src, const int32_t* class_tv, int64_t n_tiles,
+                               int64_t nrhs, int64_t nsplit, const uint16_t* gmask,
+                               const int16_t* jlist, const int32_t* jcount, double* acc,
+                               void* s) {
+  if (!gmask || !jlist || !jcount) return KIFMM_EARG;
+  return sweep_dmma(qt, Dt, kin, ko_pad, tile_targets, tile_class, src, class_tv, n_tiles, nrhs,
+                    nsplit, gmask, jlist, jcount, acc, s);
 }
 
 }  // extern "C"

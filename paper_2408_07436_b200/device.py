@@ -213,14 +213,35 @@ def sweep_splits(n_tiles: int, n_slabs: int) -> int:
     return int(min(63, max(1, -(-4 * SM_COUNT // work))))
 
 
+def sparse_tile_lists(src: np.ndarray, n_tiles: int):
+    """Per tile: uint16 mask of its 8-row groups meeting a source through each
+    vector, the ascending list of vectors with any source (int16, -1 padded)
+    and its length (the sparse float64 sweep, csrc/m2l_blas.cu)."""
+    pres = (src.reshape(n_tiles, TILE_TARGETS // 8, 8, 189) >= 0).any(axis=2)   # (t, 16, 189)
+    gmask = (pres.astype(np.uint32) << np.arange(TILE_TARGETS // 8, dtype=np.uint32)[None, :, None]
+             ).sum(axis=1).astype(np.uint16)                                    # (t, 189)
+    nz = gmask != 0
+    order = np.argsort(~nz, axis=1, kind="stable")
+    jlist = np.where(np.take_along_axis(nz, order, axis=1), order, -1).astype(np.int16)
+    return gmask, jlist, nz.sum(axis=1).astype(np.int32)
+
+
 def upload_blas_plan(plan):
     n_tiles = plan.tile_class.shape[0]
     src_dev = getattr(plan, "src_dev", None)          # built on the device (device_setup)
     if src_dev is None:
         src_t = plan.src.reshape(n_tiles, TILE_TARGETS, 189).transpose(0, 2, 1)
         src_dev = to_dev(np.ascontiguousarray(src_t), np.int32)
-    return dict(n_tiles=n_tiles, tile_targets=to_dev(plan.tile_targets, np.int32),
-                tile_class=to_dev(plan.tile_class, np.int32), src=src_dev)
+    out = dict(n_tiles=n_tiles, tile_targets=to_dev(plan.tile_targets, np.int32),
+               tile_class=to_dev(plan.tile_class, np.int32), src=src_dev)
+    if n_tiles:
+        gmask, jlist, jcount = sparse_tile_lists(plan.src, n_tiles)
+        # the sparse sweep pays off when vectors or row groups go unused
+        full = int(jcount.sum()) == 189 * n_tiles and bool((gmask == 0xFFFF).all())
+        if not full:
+            out.update(gmask=to_dev(gmask.view(np.int16)), jlist=to_dev(jlist),
+                       jcount=to_dev(jcount))
+    return out
 
 
 def tf32_split(x: np.ndarray):
@@ -336,6 +357,11 @@ class BlasDevice:
                        self.kin, self.ko_pad, P(plan["tile_targets"]), P(plan["tile_class"]),
                        P(plan["src"]), P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc),
                        stream_handle())
+        elif plan["n_tiles"] and self.sfx == "f64" and "gmask" in plan:
+            launch("kifmm_m2l_sweep_sparse_f64", P(qt), P(self.Dt), self.kin, self.ko_pad,
+                   P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
+                   P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(plan["gmask"]),
+                   P(plan["jlist"]), P(plan["jcount"]), P(acc), stream_handle())
         elif plan["n_tiles"]:
             launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
                    P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
@@ -396,6 +422,11 @@ class BlasDevice:
                        self.kin, self.ko_pad, P(plan["tile_targets"]), P(plan["tile_class"]),
                        P(plan["src"]), P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc),
                        stream_handle())
+        elif plan["n_tiles"] and self.sfx == "f64" and "gmask" in plan:
+            launch("kifmm_m2l_sweep_sparse_f64", P(qt), P(self.Dt), self.kin, self.ko_pad,
+                   P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
+                   P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(plan["gmask"]),
+                   P(plan["jlist"]), P(plan["jcount"]), P(acc), stream_handle())
         elif plan["n_tiles"]:
             launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
                    P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),

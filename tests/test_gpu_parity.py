@@ -227,6 +227,25 @@ def test_separate_clouds_and_pruned_sphere(cuda):
     assert parity_report(got, want)["floored"] <= 1e-10
 
 
+def test_sparse_float64_sweep_on_a_surface(cuda):
+    """Config-5-like geometry (points on a sphere surface, empty boxes
+    skipped): the float64 sweep takes the sparse path (vector lists and
+    8-row-group masks) and matches the oracle."""
+    from oracle import port
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(9)
+    v = rng.standard_normal((30000, 3))
+    sph = (v / np.linalg.norm(v, axis=1)[:, None] + 1) / 2
+    qs = rng.standard_normal(30000)
+    inst = setup(sph, sph, FmmConfig(depth=5, order_equiv=5, backend="blas", precision="f64",
+                                     sigma_min=1e-12))
+    plans = inst.device.blas_plan_dev
+    assert any("gmask" in p for p in plans.values())
+    got = inst.evaluate(qs)
+    want = port.evaluate(inst, qs)[:, 0]
+    assert parity_report(got, want)["floored"] <= 1e-10
+
+
 @pytest.mark.parametrize("backend,precision", [("blas", "f32"), ("blas", "f64"), ("fft", "f64")])
 def test_partitioned_evaluate_matches_single_device(cuda, backend, precision):
     """Every device code path of the multi-GPU evaluate (owned ranges, rank

@@ -103,6 +103,26 @@ def test_hadamard_tiles_reproduce_halo(case):
                 assert np.array_equal(got[:, filled].T, hp.halo[b + tcol[filled]])
 
 
+def test_sparse_tile_lists_match_the_source_table(case):
+    """Host logic of the sparse float64 sweep: vector lists and 8-row-group
+    masks reproduce exactly where the BLAS plan's source table is populated."""
+    from paper_2408_07436_b200.device import sparse_tile_lists
+    name, g, inst = case
+    if inst.config.backend != "blas":
+        pytest.skip("blas only")
+    for lvl, plan in inst.blas_plans.items():
+        nt = plan.tile_class.shape[0]
+        gmask, jlist, jcount = sparse_tile_lists(plan.src, nt)
+        pres = (plan.src.reshape(nt, 16, 8, 189) >= 0).any(axis=2)
+        for t in range(nt):
+            bits = np.array([[(int(gmask[t, j]) >> k) & 1 for k in range(16)] for j in range(189)])
+            assert np.array_equal(bits.T.astype(bool), pres[t])
+            want = np.flatnonzero(pres[t].any(axis=0))
+            assert jcount[t] == want.shape[0]
+            assert np.array_equal(jlist[t, : jcount[t]], want)
+            assert (jlist[t, jcount[t]:] == -1).all()
+
+
 def test_config_validation_mirrors_reference():
     for bad in (dict(depth=1), dict(order_equiv=1), dict(order_equiv=6, order_check=5),
                 dict(backend="magic"), dict(backend="fft", order_equiv=6, order_check=8),
