@@ -366,3 +366,47 @@ def test_device_setup_matches_host(cuda, kind, depth):
             assert (x is None) == (y is None)
             if x is not None:
                 assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+
+
+# ----------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("backend", ["blas", "fft"])
+def test_degenerate_inputs(cuda, backend):
+    """Tiny, coincident and lopsided inputs run through the same device path
+    and agree with the oracle: one point, all points identical (r = 0 pairs
+    contribute nothing, _hot.pyx:44-50), depth 2 (no coarse levels), and
+    clouds far apart (levels where targets meet no sources)."""
+    from oracle import port
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(11)
+    cases = [
+        (np.array([[0.3, 0.4, 0.5]]), np.array([[0.3, 0.4, 0.5]]), 2),
+        (np.repeat([[0.5, 0.5, 0.5]], 50, axis=0), rng.random((40, 3)), 3),
+        (rng.random((500, 3)), rng.random((400, 3)), 2),
+        (rng.random((800, 3)) * 0.1, rng.random((600, 3)) * 0.1 + 0.9, 4),
+    ]
+    for src, tgt, depth in cases:
+        q = rng.uniform(-1, 1, src.shape[0])
+        inst = setup(src, tgt, FmmConfig(depth=depth, order_equiv=4, backend=backend,
+                                         precision="f64", sigma_min=1e-10))
+        got = inst.evaluate(q)
+        want = port.evaluate(inst, q)[:, 0]
+        assert got.shape == (tgt.shape[0],)
+        assert np.all(np.isfinite(got))
+        scale = max(np.abs(want).max(), 1e-300)
+        assert np.abs(got - want).max() <= 1e-10 * scale
+
+
+def test_many_rhs_with_gradient(cuda):
+    from oracle import port
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(12)
+    pts = rng.random((6000, 3))
+    q = rng.uniform(-1, 1, (6000, 5))
+    inst = setup(pts, pts, FmmConfig(depth=3, order_equiv=6, backend="fft", precision="f64"))
+    phi, grad = inst.evaluate(q, gradient=True)
+    assert phi.shape == (6000, 5) and grad.shape == (6000, 5, 3)
+    st = {}
+    want_phi = port.evaluate(inst, q, state=st)
+    want_grad = port.fmm_gradient(inst, q, st)
+    assert np.abs(phi - want_phi).max() <= 1e-10 * np.abs(want_phi).max()
+    assert np.abs(grad - want_grad).max() <= 1e-9 * np.abs(want_grad).max()
