@@ -280,7 +280,9 @@ def setup(sources, targets, config: FmmConfig, device_build=None) -> FmmInstance
     (default: when a GPU and the library are present) builds the trees, the
     near-field plan and the BLAS-M2L plans on the device (device_setup.py,
     bit-identical to the host build); the reference's bucket lists are then
-    built lazily, on first access."""
+    built lazily, on first access.  The operators are precomputed on the
+    host, bit-identical to the reference (a cuSOLVER version measured slower
+    on the B200 box: p = 10, 35 s vs 15 s; see DESIGN.md row f4)."""
     t0 = time.perf_counter()
     config.validate()
     src = np.ascontiguousarray(np.asarray(sources, dtype=np.float64).reshape(-1, 3))
