@@ -316,7 +316,14 @@ __device__ __forceinline__ u64 rsq2(u64 r2) {
   return pk2(a, b);
 }
 
-constexpr int kPairCap = 256;              // source pairs staged per warp (512 sources)
+#ifndef KIFMM_PAIR_CAP
+#define KIFMM_PAIR_CAP 224
+#endif
+// Source pairs staged per warp (448 sources; a near field of ~810 sources
+// takes two passes).  4 warps x 7 KB = 28 KB per CTA, so a leaf-pass CTA
+// still fits next to two sweep CTAs (2 x 99 KB) on an SM when the near field
+// runs concurrently with the finest-level M2L.
+constexpr int kPairCap = KIFMM_PAIR_CAP;
 constexpr float kFar = 1e18f;              // padding source: r2 ~ 1e36, charge 0
 
 // Stage source record j of the current fill into the paired layout.

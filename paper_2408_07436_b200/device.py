@@ -67,9 +67,17 @@ def set_tag(tag: str):
     _TAG = tag
 
 
+_TIMELINE = None     # list: (name, tag, stream, end event) per launch, overlap kept
+
+
 def launch(name, *args):
     if _PROF is None:
-        return nat.call(name, *args)
+        st = nat.call(name, *args)
+        if _TIMELINE is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(torch.cuda.current_stream())
+            _TIMELINE.append((name, _TAG, torch.cuda.current_stream().cuda_stream, e))
+        return st
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -466,8 +474,9 @@ class DeviceFmm:
         least, greatest = torch.cuda.Stream.priority_range()
         self.side_stream = torch.cuda.Stream(priority=least)
         self.hi_stream = torch.cuda.Stream(priority=greatest)
-        self.bulk_stream = torch.cuda.Stream(priority=max(greatest, least - 1)
-                                             if least > greatest else least)
+        mid = max(greatest, least - 1) if least > greatest else least
+        self.level_streams = {l: torch.cuda.Stream(priority=mid) for l in range(2, cfg.depth + 1)}
+        self.bulk_stream = self.level_streams[cfg.depth]
         dt = self.np_dtype
         leaf_side = inst.domain.box_side(cfg.depth)
         # points
@@ -524,11 +533,11 @@ class DeviceFmm:
             self.tma_plan = {l: tma_level_plan(st.level_keys(l), tt.level_keys(l), l)
                              for l in plans}
 
-    def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None, bulk=False):
-        """``bulk``: the finest level running concurrently with the coarser
-        ones (evaluate_device overlap) uses its own scratch (qt, acc)."""
+    def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None):
+        """Each level has its own scratch (qt, acc): levels run concurrently
+        in the overlapped evaluate."""
         b = self._buffers(nrhs)
-        qt, acc = (b["qt_bulk"], b["acc_bulk"]) if bulk else (b["qt"], b["acc"])
+        qt, acc = b["qt_lv"][lvl], b["acc_lv"][lvl]
         if self.tma and solve is not None:
             plan = self.tma_plan[lvl]
             return self.blas.run_level_tma(plan, mult, self.n_src[lvl], self.n_tgt[lvl], nrhs,
@@ -554,11 +563,11 @@ class DeviceFmm:
                                         halo=to_dev(p.halo, np.int64),
                                         tiles=upload_hadamard_tiles(p.halo, p.src_color, p.tgt_color))
 
-    def m2l_fft_level(self, lvl, mult, nrhs, check, plan=None, bulk=False):
+    def m2l_fft_level(self, lvl, mult, nrhs, check, plan=None):
         plan = plan if plan is not None else self.fft_plan_dev[lvl]
         b = self._buffers(nrhs)
         nsc, ntc = plan["nsc"], plan["ntc"]
-        qh, ph = (b["qhat_bulk"], b["phat_bulk"]) if bulk else (b["qhat"], b["phat"])
+        qh, ph = b["qhat_lv"][lvl], b["phat_lv"][lvl]
         qhat = qh[: 2 * self.n_freq * nsc * 8 * nrhs]
         phat = ph[: 2 * self.n_freq * ntc * 8 * nrhs]
         s = stream_handle()
@@ -593,39 +602,31 @@ class DeviceFmm:
                                dtype=T, device=dev)
         b["stack"] = torch.empty(max(self.n_src[2:d] + [1]) * R * 8 * self.n_e, dtype=T,
                                  device=dev)
-        # scratch of the M2L levels: one set for the coarse levels (run in
-        # sequence) and one for the finest level (may run concurrently, see
-        # evaluate_device); check rows of the finest level in phi_bulk
-        coarse = [l for l in range(2, d)] or [d]
-        b["phi_bulk"] = torch.empty(max(self.n_tgt[d] * R * self.n_c, 1), dtype=T, device=dev)
+        # per-level M2L scratch (levels run concurrently in the overlapped
+        # evaluate): check rows, and the BLAS (qt, acc) or FFT (qhat, phat) sets
+        levels = list(range(2, d + 1))
+        b["phi_lv"] = {l: torch.empty(max(self.n_tgt[l] * R * self.n_c, 1), dtype=T, device=dev)
+                       for l in levels}
         if self.cfg.backend == "blas":
-            def acc_need(levels):
-                n = max(self.blas.acc_elems(self.n_tgt[l], R, self.blas_plan_dev[l]["n_tiles"])
-                        for l in levels)
+            def acc_need(l):
+                n = self.blas.acc_elems(self.n_tgt[l], R, self.blas_plan_dev[l]["n_tiles"])
                 if self.tma:
-                    n = max(n, max(self.blas.acc_elems(self.n_tgt[l], R,
-                                                       self.tma_plan[l]["n_tiles"])
-                                   for l in levels))
+                    n = max(n, self.blas.acc_elems(self.n_tgt[l], R, self.tma_plan[l]["n_tiles"]))
                 return max(n, 1)
             qt_w = R * self.blas.kin * (3 if self.blas.tc else 1)
-            b["qt"] = torch.zeros(max(self.n_src[l] for l in coarse) * qt_w, dtype=T, device=dev)
-            b["acc"] = torch.zeros(acc_need(coarse), dtype=T, device=dev)
-            b["qt_bulk"] = torch.zeros(self.n_src[d] * qt_w, dtype=T, device=dev)
-            b["acc_bulk"] = torch.zeros(acc_need([d]), dtype=T, device=dev)
+            b["qt_lv"] = {l: torch.zeros(max(self.n_src[l], 1) * qt_w, dtype=T, device=dev)
+                          for l in levels}
+            b["acc_lv"] = {l: torch.zeros(acc_need(l), dtype=T, device=dev) for l in levels}
             if self.tma:
                 b["dense"] = {l: tuple(torch.zeros(8 * R * p["h"] ** 3 * self.blas.kin, dtype=T,
                                                    device=dev) for _ in range(2))
                               for l, p in self.tma_plan.items()}
         else:
             fp = self.fft_plan_dev
-            nsc = max(fp[l]["nsc"] for l in coarse)
-            ntc = max(fp[l]["ntc"] for l in coarse)
-            b["qhat"] = torch.empty(2 * self.n_freq * nsc * 8 * R, dtype=T, device=dev)
-            b["phat"] = torch.empty(2 * self.n_freq * ntc * 8 * R, dtype=T, device=dev)
-            b["qhat_bulk"] = torch.empty(2 * self.n_freq * fp[d]["nsc"] * 8 * R, dtype=T,
-                                         device=dev)
-            b["phat_bulk"] = torch.empty(2 * self.n_freq * fp[d]["ntc"] * 8 * R, dtype=T,
-                                         device=dev)
+            b["qhat_lv"] = {l: torch.empty(2 * self.n_freq * fp[l]["nsc"] * 8 * R, dtype=T,
+                                           device=dev) for l in levels}
+            b["phat_lv"] = {l: torch.empty(2 * self.n_freq * fp[l]["ntc"] * 8 * R, dtype=T,
+                                           device=dev) for l in levels}
         b["out"] = torch.empty(self.tx.shape[0] * R, dtype=T, device=dev)
         b["qin"] = torch.empty(self.sx.shape[0] * R, dtype=torch.float64, device=dev)
         self._bufs[nrhs] = b
@@ -704,11 +705,15 @@ class DeviceFmm:
                     P(self.s_count), P(self.near_off), P(self.near_leaf), R, P(self.t_perm),
                     parts, P(out)] + grad_ptr
 
-        if overlap:
-            main = torch.cuda.current_stream()
-            side = self.side_stream
-            side.wait_stream(main)
+        p2p_after = os.environ.get("KIFMM_P2P_AFTER", "pack")
+        side = self.side_stream
+
+        def fork_p2p():
+            side.wait_stream(torch.cuda.current_stream())
             launch(leaf_name, *leaf_args(2), side.cuda_stream)       # P2P, overwrite
+
+        if overlap and p2p_after == "pack":
+            fork_p2p()
         # P2M: check potentials, then the up_inv solve scaled by the leaf side.
         mult, phi, tmp = b["mult"], b["phi"], b["tmp"]
         nl = self.n_src[d]
@@ -716,35 +721,42 @@ class DeviceFmm:
                  P(self.s_start), P(self.s_count), nl, P(self.s_centers), P(self.check_base),
                  n_c, P(phi), s)
         la.chain(nl * R, phi, n_c, Linalg.solve_stages(self.up_inv, self.side[d]), mult[d], n_e)
+        if overlap and p2p_after == "p2m":
+            fork_p2p()
         loc = b["loc"]
         for lvl in range(2, d + 1):
             loc[lvl].zero_()
         calls = {}
 
-        def m2l(lvl, bulk):
+        def m2l(lvl):
             n_t = self.n_tgt[lvl]
-            check = (b["phi_bulk"] if bulk else phi)[: n_t * R * n_c]
+            check = b["phi_lv"][lvl][: n_t * R * n_c]
             if self.cfg.backend == "blas":
                 calls[lvl] = self.m2l_blas_level(lvl, mult[lvl], R, check,
-                                                 solve=(self.dn_inv, self.side[lvl], loc[lvl]),
-                                                 bulk=bulk)
+                                                 solve=(self.dn_inv, self.side[lvl], loc[lvl]))
             else:
-                calls[lvl] = self.m2l_fft_level(lvl, mult[lvl], R, check, bulk=bulk)
+                calls[lvl] = self.m2l_fft_level(lvl, mult[lvl], R, check)
                 la.chain(n_t * R, check, n_c, Linalg.solve_stages(self.dn_inv, self.side[lvl]),
                          loc[lvl], n_e, accumulate=True)
 
-        # With `overlap`, the finest level's M2L (the bulk of the far-field
-        # work; it needs only mult[d]) runs on its own stream, concurrently
-        # with the M2M pass and the coarser levels; the L2L into level d
-        # waits for it (both accumulate into loc[d]).
-        joined = True
-        bulk_run = overlap and d >= 3
-        if bulk_run:
-            bulk = self.bulk_stream
-            bulk.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(bulk):
-                m2l(d, True)
-            joined = False
+        # With `overlap`, every level's M2L except the coarsest runs on its own
+        # stream as soon as its multipoles exist (the finest level right after
+        # P2M, level l after the M2M into l), concurrently with the M2M pass;
+        # the main stream keeps only the dependent chain M2M -> M2L(2) ->
+        # L2L(2->3) -> ... -> L2L(d-1->d), and each L2L into level l waits for
+        # M2L(l) (both accumulate into loc[l]).  Every level has its own scratch.
+        main = torch.cuda.current_stream()
+        forked = {}
+
+        def fork_m2l(lvl):
+            st = self.level_streams[lvl]
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                m2l(lvl)
+            forked[lvl] = st
+
+        if overlap and d >= 3:
+            fork_m2l(d)
         phase("m2m")
         # M2M down to level 2 (levels 0-1 carry no M2L): children stacked in
         # the chain's loader, kernel product, then the up_inv solve.
@@ -754,22 +766,25 @@ class DeviceFmm:
                      [(self.m2mT, 8 * n_e, n_c, None, 1.0)]
                      + Linalg.solve_stages(self.up_inv, 1.0), mult[lvl - 1], n_e,
                      a_child=self.src_child[lvl], child_w=n_e, a_nrhs=R)
+            if overlap and lvl - 1 >= 3:
+                fork_m2l(lvl - 1)
+        if overlap and p2p_after == "m2m":
+            fork_p2p()
         for lvl in range(2, d + 1):
             n_t = self.n_tgt[lvl]
             phase(f"m2l{lvl}")
-            if not (lvl == d and bulk_run):
-                m2l(lvl, lvl == d)        # the finest level always uses its own scratch set
+            if lvl not in forked:
+                m2l(lvl)
             if lvl < d:
-                if lvl + 1 == d and not joined:
-                    torch.cuda.current_stream().wait_stream(bulk)
-                    joined = True
+                if lvl + 1 in forked:
+                    main.wait_stream(forked[lvl + 1])
                 phase(f"l2l{lvl}")
                 la.chain(n_t * R, loc[lvl], n_e,
                          [(self.l2lT, n_e, 8 * n_c, None, 1.0)]
                          + Linalg.solve_stages(self.dn_inv, 0.5), loc[lvl + 1], n_e,
                          rowmap=self._l2l_rowmap(lvl + 1, R), accumulate=True)
-        if not joined:
-            torch.cuda.current_stream().wait_stream(bulk)
+        for st in forked.values():
+            main.wait_stream(st)
         calls = [calls[l] for l in sorted(calls)]
         phase("leaf")
         if overlap:

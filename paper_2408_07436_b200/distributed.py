@@ -347,10 +347,8 @@ class DistributedFmm:
                 if self.inst.config.backend == "blas":
                     bd = d.blas
                     plan = self.blas_plan_dev[lvl]
-                    fine = lvl == depth          # scratch sets sized per level group
                     bd.run_level_rows(plan, mult[lvl], d.n_src[lvl], lo, hi, R, 1.0 / d.side[lvl],
-                                      check, b["qt_bulk" if fine else "qt"],
-                                      b["acc_bulk" if fine else "acc"])
+                                      check, b["qt_lv"][lvl], b["acc_lv"][lvl])
                 else:
                     self._fft_level(lvl, mult[lvl], R, check)
                 d.la.solve(d.dn_inv, _View(check, lo * R * n_c, isz), (hi - lo) * R,
@@ -381,9 +379,8 @@ class DistributedFmm:
         clo, chi, scl, n_scl, tiles = self.fft_sub[lvl]
         nsc = plan["nsc"]
         n_sub = chi - clo
-        fine = lvl == d.depth
-        qhat = b["qhat_bulk" if fine else "qhat"][: 2 * d.n_freq * nsc * 8 * nrhs]
-        phat = b["phat_bulk" if fine else "phat"][: 2 * d.n_freq * n_sub * 8 * nrhs]
+        qhat = b["qhat_lv"][lvl][: 2 * d.n_freq * nsc * 8 * nrhs]
+        phat = b["phat_lv"][lvl][: 2 * d.n_freq * n_sub * 8 * nrhs]
         s = stream_handle()
         launch(f"kifmm_fft_forward_{d.sfx}", P(mult), nrhs, d.order, P(plan["sbox"]), nsc, P(scl),
                n_scl, P(qhat), s)
