@@ -70,7 +70,11 @@ def set_tag(tag: str):
 _TIMELINE = None     # list: (name, tag, stream, end event) per launch, overlap kept
 
 
+LAUNCH_COUNT = [0]   # kernel launches through the C ABI (bench gpu_launches)
+
+
 def launch(name, *args):
+    LAUNCH_COUNT[0] += 1
     if _PROF is None:
         st = nat.call(name, *args)
         if _TIMELINE is not None:
