@@ -225,6 +225,16 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------------ ours
+def dram_traffic(key):
+    """DRAM bytes per launch of a kernel from the committed ncu capture
+    (profiles/r1/dram_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1", "dram_traffic.json")) as f:
+            return float(json.load(f)[key]["bytes"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def run_single(args):
     import torch
     from paper_2408_07436_b200 import FmmConfig, setup
@@ -290,11 +300,25 @@ def run_single(args):
         n_tiles = (dev.tma_plan if dev.tma else dev.blas_plan_dev)[lvl]["n_tiles"]
         execd = 3 * 2.0 * 128 * bd.kin * bd.ko_pad * 189 * n_tiles
         gather_bytes = 2 * 4.0 * bd.kin * per_level[lvl]["pairs"]
+        # shared-memory traffic model of the sweep (what bounds it): per
+        # (tile, vector) TMA writes of A hi/lo + core hi/lo, and the three
+        # MMAs' operand reads (A_lo.B_hi, A_hi.B_lo, A_hi.B_hi)
+        a_b, b_b = 2 * 4.0 * 128 * bd.kin, 2 * 4.0 * bd.ko_pad * bd.kin
+        smem_bytes = (a_b + b_b + 3 * (a_b + b_b) / 2) * 189 * n_tiles
+        clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+        smem_peak = 128.0 * 148 * clk_mhz * 1e6 / 1e9                    # GB/s
         rooflines["m2l_sweep_tc_f32"] = dict(
             bound="tensor",
             kernel=f"m2l_sweep_{'tma' if dev.tma else 'tc'}_f32 (level {lvl})",
             achieved=algo / (sweep_ms / 1e3) / 1e12, peak=peak_tc, unit="TFLOP/s",
-            frac=algo / (sweep_ms / 1e3) / 1e12 / peak_tc, traffic=None,
+            frac=algo / (sweep_ms / 1e3) / 1e12 / peak_tc,
+            traffic=dram_traffic("m2l_sweep_tma_f32_level5"),
+            smem_model=dict(bytes_per_launch=smem_bytes,
+                            achieved_gbs=smem_bytes / (sweep_ms / 1e3) / 1e9,
+                            peak_gbs=smem_peak,
+                            frac=smem_bytes / (sweep_ms / 1e3) / 1e9 / smem_peak,
+                            note="128 B/clk/SM shared-memory bandwidth; TMA writes + MMA "
+                                 "operand reads per (tile, vector)"),
             algorithmic=f"4 k sum_t m_t k_t = {algo:.4g} flop at level {lvl} (SURVEY 8d)",
             executed_tensor_tflops=execd / (sweep_ms / 1e3) / 1e12,
             gather_gbs=gather_bytes / (sweep_ms / 1e3) / 1e9,
@@ -313,7 +337,7 @@ def run_single(args):
     rooflines[leaf_key] = dict(
         bound="mufu", kernel=leaf_key, achieved=(inter + l2p) / (leaf_ms / 1e3) / 1e9,
         peak=peak_mufu, unit="Grsqrt/s", frac=(inter + l2p) / (leaf_ms / 1e3) / 1e9 / peak_mufu,
-        traffic=None,
+        traffic=dram_traffic("leaf_pass_f32"),
         algorithmic=f"{inter} P2P + {l2p:.0f} L2P kernel evaluations (one rsqrt each)",
         tflops_11_per_interaction=11.0 * inter / (leaf_ms / 1e3) / 1e12, fp32_peak=peak_f32,
         peak_source="kifmm_probe MUFU.RSQ measured in this run")
