@@ -129,6 +129,8 @@ struct TmaArgs {
   int64_t nrhs;
   int nsplit, jper;
   int split_smem;                  // 1: A arrives raw (fp32), hi/lo formed in shared memory
+  int mma2;                        // 1: two MMAs per k-step, A_hi x [B_hi | B_lo] (N = 2 n_out)
+  int nbuf;                        // TMEM accumulator buffers (2: MMA overlaps the promotion)
   float* acc_out;
 };
 
@@ -167,7 +169,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
   const int nsteps = nvec * nchunks;
   const int nblocks = (nvec + FLUSH_V - 1) / FLUSH_V;
   const int32_t* tv_list = a.class_tv + cls * 189;
-  const uint32_t need = 3u * (uint32_t)n_out;
+  // accumulator buffers of width dw (n_out, or 2 n_out in the 2-MMA form:
+  // [A_hi B_hi + A_lo B_hi | A_hi B_lo]) x 2 + the IEEE accumulator
+  const int dw = a.mma2 ? 2 * n_out : n_out;
+  const int nbuf = a.nbuf;
+  const uint32_t need = (uint32_t)(nbuf * dw) + (uint32_t)n_out;
   const uint32_t tmem_cols = need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
 
   if (tid == 0) {
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
         if (!a.split_smem) tma_load_5d(sb + a_bytes, &tm_lo, c * KC, sz, sy, sx, c4, &full[stage]);
         const int64_t boff = (int64_t)t * n_out * kin + (int64_t)n_out * KC * c;
         bulk_copy(sb + 2 * a_bytes, a.bhi + boff, bb, &full[stage]);
-        bulk_copy(sb + 2 * a_bytes + b_bytes, a.blo + boff, bb, &full[stage]);
+        bulk_copy(sb + 2 * a_bytes + bb, a.blo + boff, bb, &full[stage]);   // B_lo follows B_hi
       }
     }
     __syncwarp();
@@ -228,13 +234,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
     // ----------------------------------------------------------- MMA issue
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n_out >> 3) << 17) |
                            ((uint32_t)(TMT >> 4) << 24);
+    const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) |
+                            ((uint32_t)((2 * n_out) >> 3) << 17) | ((uint32_t)(TMT >> 4) << 24);
     if (lane == 0) {
       int st = 0;
       for (int bi = 0; bi < nblocks; ++bi) {
-        const int buf = bi & 1;
-        if (bi >= 2) mbar_wait(&tempty[buf], ((bi >> 1) - 1) & 1, false);
+        const int buf = bi % nbuf;
+        if (bi >= nbuf) mbar_wait(&tempty[buf], ((bi / nbuf) - 1) & 1, false);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t dcol = tmem + (uint32_t)(buf * n_out);
+        const uint32_t dcol = tmem + (uint32_t)(buf * dw);
         const int vend = min(nvec, (bi + 1) * FLUSH_V);
         uint32_t acc_flag = 0;
         for (; st < vend * nchunks; ++st) {
@@ -245,16 +253,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
           const int kc = min(KC, kin - c * KC);
           const uint32_t base = smem_u32(smem + stage * stage_bytes);
           const uint32_t a_hi = base, a_lo = base + a_bytes;
-          const uint32_t b_hi = base + 2 * a_bytes, b_lo = b_hi + b_bytes;
+          const uint32_t b_hi = base + 2 * a_bytes;
+          const uint32_t b_lo = b_hi + (uint32_t)(n_out * kc * 4);   // n-groups continue into B_lo
           const uint32_t sbo_b = (uint32_t)(kc / 4) * 128;
           for (int ks = 0; ks < kc / 8; ++ks) {
             const uint32_t ka = ks * 32;          // K offset inside the 128-byte swizzle row
             const uint32_t kb = ks * 256;         // two 128-byte core matrices along K
-            mma_tf32(dcol, desc_sw128(a_lo + ka), desc_nosw(b_hi + kb, 128, sbo_b), idesc,
-                     acc_flag);
-            acc_flag = 1;
-            mma_tf32(dcol, desc_sw128(a_hi + ka), desc_nosw(b_lo + kb, 128, sbo_b), idesc, 1);
-            mma_tf32(dcol, desc_sw128(a_hi + ka), desc_nosw(b_hi + kb, 128, sbo_b), idesc, 1);
+            if (a.mma2) {
+              // [D | D'] = A_hi . [B_hi | B_lo] (one read of A_hi), then D += A_lo . B_hi
+              mma_tf32(dcol, desc_sw128(a_hi + ka), desc_nosw(b_hi + kb, 128, sbo_b), idesc2,
+                       acc_flag);
+              acc_flag = 1;
+              mma_tf32(dcol, desc_sw128(a_lo + ka), desc_nosw(b_hi + kb, 128, sbo_b), idesc, 1);
+            } else {
+              mma_tf32(dcol, desc_sw128(a_lo + ka), desc_nosw(b_hi + kb, 128, sbo_b), idesc,
+                       acc_flag);
+              acc_flag = 1;
+              mma_tf32(dcol, desc_sw128(a_hi + ka), desc_nosw(b_lo + kb, 128, sbo_b), idesc, 1);
+              mma_tf32(dcol, desc_sw128(a_hi + ka), desc_nosw(b_hi + kb, 128, sbo_b), idesc, 1);
+            }
           }
           mma_commit(&empty[stage]);
         }
@@ -267,21 +284,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tma_kernel(
     const int sub = warp & 3;
     const int m = sub * 32 + lane;
     const uint32_t lane_base = (uint32_t)(sub * 32) << 16;
-    const uint32_t acc_col = tmem + lane_base + 2u * (uint32_t)n_out;
+    const uint32_t acc_col = tmem + lane_base + (uint32_t)(nbuf * dw);
     const int ct = tid - 64;                               // 0..127 converter thread
     auto promote = [&](int bi) {
-      const int buf = bi & 1;
-      mbar_wait(&tfull[buf], (bi >> 1) & 1, true);
+      const int buf = bi % nbuf;
+      mbar_wait(&tfull[buf], (bi / nbuf) & 1, true);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t bcol = tmem + lane_base + (uint32_t)(buf * n_out);
+      const uint32_t bcol = tmem + lane_base + (uint32_t)(buf * dw);
       for (int c0 = 0; c0 < n_out; c0 += 16) {
-        uint32_t v[16], s[16];
+        uint32_t v[16], w[16], s[16];
         tmem_ld16(bcol + c0, v);
+        if (a.mma2) tmem_ld16(bcol + n_out + c0, w);
         if (bi > 0) tmem_ld16(acc_col + c0, s);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          s[i] = bi > 0 ? __float_as_uint(__uint_as_float(s[i]) + __uint_as_float(v[i])) : v[i];
+        for (int i = 0; i < 16; ++i) {
+          float t = __uint_as_float(v[i]);
+          if (a.mma2) t += __uint_as_float(w[i]);
+          s[i] = __float_as_uint(bi > 0 ? __uint_as_float(s[i]) + t : t);
+        }
         tmem_st16(acc_col + c0, s);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -455,7 +476,20 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
   }
   // 3 * n_out accumulator columns > 256 take the whole 512-column TMEM:
   // one CTA per SM then, with the shared memory for deeper pipelining.
-  const int cps = 3 * n_out > 256 ? 1 : ctas;
+  static int mma2_env = -1;
+  if (mma2_env < 0) {
+    const char* g = getenv("KIFMM_TMA_MMA2");
+    mma2_env = g ? atoi(g) : 2;
+  }
+  // 2-MMA form (KIFMM_TMA_MMA2=2, default: single-buffered accumulator,
+  // 3 n_out TMEM columns, two CTAs/SM; =1: double-buffered, 5 n_out columns,
+  // one CTA/SM; =0: three MMAs per k-step) needs N = 2 n_out <= 256.
+  // Measured on B200 (config 2, level 5): =2 ~2% faster than =0, =1 ~50%
+  // slower (one CTA/SM).
+  const int mma2 = mma2_env && 2 * n_out <= 256 && 3 * n_out <= 256;
+  const int nbuf = mma2 && mma2_env == 2 ? 1 : 2;
+  const int cols = nbuf * (mma2 ? 2 : 1) * (int)n_out + (int)n_out;
+  const int cps = cols > 256 ? 1 : ctas;
   int stages = (int)(((cps == 1 ? 222 * 1024 : 200 * 1024) / cps) / stage_bytes);
   if (stages > max_stages) stages = max_stages;
   if (stages < 2) return KIFMM_EARG;
@@ -480,6 +514,8 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
   a.jper = (int)((189 + nsplit - 1) / nsplit);
   a.acc_out = acc;
   a.split_smem = split_smem;
+  a.mma2 = mma2;
+  a.nbuf = nbuf;
   dim3 grid((unsigned)n_tiles, (unsigned)nrhs, (unsigned)nsplit);
   m2l_sweep_tma_kernel<<<grid, NTHREADS, smem, (cudaStream_t)stream>>>(tm_hi, tm_lo, a);
   return launch_status();
