@@ -206,6 +206,34 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
                             const int8_t* offsets, int64_t nrhs, int64_t nsplit, float* acc,
                             void* stream);
 
+/* Tensor-memory variant (csrc/m2l_tmem.cu), persistent, one CTA per SM:
+ * the same tiles and dense sub-lattice array, but q (8*nrhs, h, h, h, kp)
+ * holds RAW fp32 q~ (kifmm_dense_split_tf32 with lo == NULL); each target
+ * row's source row is loaded into registers, split into TF32 hi/lo and
+ * stored into TMEM as the MMA's A operand.  bpair (316, 2*kp*kp) is
+ * [B_hi | B_lo] per vector, each packed [a/8][b/4][a%8][b%4] with one
+ * K chunk of width kp (device.py pack_tmem_cores).  class_tv (8, 189) may
+ * list each class's vectors in any order (device.py uses a locality order).
+ * Runs as clusters of 2 CTAs: pairs (n_pairs, 2) lists tile slots of the
+ * same class processed together (the cores are multicast to both); a class
+ * with an odd tile count repeats its last slot (device.py tile_pairs).
+ * Output: acc[(tgt*nrhs + r)*(nsplit*ostride) + split*ostride + c], c < kp.
+ * kp % 8 == 0, 8 <= kp <= 64, ostride >= kp, ostride % 4 == 0.  Replaces,
+ * with m2l_sweep_tma, the bucket loop of m2l_blas.py:296-318. */
+int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int64_t h,
+                             const int32_t* tile_targets, const int32_t* tile_ids, int64_t n_tiles,
+                             const int32_t* pairs, int64_t n_pairs, const int32_t* class_tv,
+                             const int8_t* offsets, int64_t nrhs, int64_t nsplit, int64_t ostride,
+                             float* acc, void* stream);
+
+/* nsplit for kifmm_m2l_sweep_tmem_f32 that balances the persistent CTA pairs. */
+int kifmm_m2l_sweep_tmem_splits(int64_t n_pairs, int64_t nrhs, int64_t* nsplit);
+
+/* Debug timeline: clock64 stamps of CTA 0 of the following tensor-memory
+ * sweeps with sub-lattice size h written into buf (12 x 1024 int64, device
+ * memory); NULL disables. */
+int kifmm_m2l_sweep_tmem_trace(long long* buf, int64_t h);
+
 /* q~ rows (n_boxes*nrhs, kin) -> TF32 hi/lo parts scattered into the dense
  * sub-lattice arrays at slot[box] = parity*h^3 + (ix*h + iy)*h + iz. */
 int kifmm_dense_split_tf32(const float* qt, const int32_t* slot, int64_t n_boxes, int64_t nrhs,

@@ -283,6 +283,35 @@ def pack_tc_cores(cores: np.ndarray, kin: int, n_out: int, kc_max: int = 32) -> 
     return np.ascontiguousarray(np.concatenate(blocks, axis=1))
 
 
+def pack_tmem_cores(hi: np.ndarray, lo: np.ndarray, kp: int) -> np.ndarray:
+    """(316, k, k) TF32 hi/lo cores -> (316, 2 kp kp): per vector [B_hi | B_lo],
+    each in the canonical K-major no-swizzle layout with one K chunk of width
+    kp, so the hi and lo halves continue each other along N (csrc/m2l_tmem.cu)."""
+    return np.ascontiguousarray(np.concatenate(
+        [pack_tc_cores(hi, kp, kp, kc_max=kp), pack_tc_cores(lo, kp, kp, kc_max=kp)], axis=1))
+
+
+def locality_transfer_table() -> np.ndarray:
+    """(8, 189) class vector lists (the vectors of class_transfer_table)
+    reordered for source-row reuse: grouped by the source sub-lattice, then
+    by the sub-lattice shift (x, y, z) with z fastest, so consecutive vectors
+    of the tensor-memory sweep read source blocks overlapping in 7 of 8 rows
+    (L1 hits).  The order only changes the summation order of the fp32
+    accumulator (promoted every 4 vectors)."""
+    from .octree import transfer_offsets
+    offs = transfer_offsets().astype(np.int64)
+    base = class_transfer_table()
+    rows = []
+    for cls in range(8):
+        par = np.array([(cls >> 2) & 1, (cls >> 1) & 1, cls & 1])
+        q = par[None, :] + offs[base[cls]]
+        sp = ((q[:, 0] & 1) << 2) | ((q[:, 1] & 1) << 1) | (q[:, 2] & 1)
+        sh = q >> 1
+        key = np.lexsort((sh[:, 2], sh[:, 1], sh[:, 0], sp))
+        rows.append(base[cls][key])
+    return np.stack(rows)
+
+
 def tma_level_plan(src_codes, tgt_codes, level):
     """Plan of the TMA-fed tcgen05 sweep (csrc/m2l_tma.cu) for one level:
     class tiles of 4 x 4 x 8 same-parity targets, the target row of every
@@ -303,8 +332,24 @@ def tma_level_plan(src_codes, tgt_codes, level):
     sp = ((sa[:, 0] & 1) << 2) | ((sa[:, 1] & 1) << 1) | (sa[:, 2] & 1)
     si = sa >> 1
     src_slot = sp * h ** 3 + (si[:, 0] * h + si[:, 1]) * h + si[:, 2]
+    pairs = tile_pairs(tile_ids, tx * ty * tz)
     return dict(h=h, n_tiles=int(tile_ids.shape[0]), tile_ids=to_dev(tile_ids, np.int32),
-                tile_targets=to_dev(tile_targets, np.int32), src_slot=to_dev(src_slot, np.int32))
+                tile_targets=to_dev(tile_targets, np.int32), src_slot=to_dev(src_slot, np.int32),
+                pairs=to_dev(pairs, np.int32), n_pairs=int(pairs.shape[0]))
+
+
+def tile_pairs(tile_ids: np.ndarray, per_class: int) -> np.ndarray:
+    """(n_pairs, 2) slots of same-class tiles processed by one CTA pair of the
+    tensor-memory sweep (consecutive slots of a class; an odd class repeats
+    its last slot, both CTAs then write the same rows)."""
+    cls = tile_ids // per_class
+    out = []
+    for c in np.unique(cls):
+        sl = np.flatnonzero(cls == c)
+        if sl.shape[0] % 2:
+            sl = np.append(sl, sl[-1])
+        out.append(sl.reshape(-1, 2))
+    return np.concatenate(out).astype(np.int32) if out else np.zeros((0, 2), np.int32)
 
 
 class BlasDevice:
@@ -340,6 +385,12 @@ class BlasDevice:
             self.class_tv = to_dev(class_transfer_table(), np.int32)
             from .octree import transfer_offsets
             self.offsets = to_dev(transfer_offsets(), np.int8)
+            # A operand in tensor memory (csrc/m2l_tmem.cu) for ranks <= 64;
+            # KIFMM_F32_SWEEP=tma keeps the shared-memory-staged TMA sweep
+            self.tmem = self.kin <= 64 and os.environ.get("KIFMM_F32_SWEEP", "tmem") == "tmem"
+            if self.tmem:
+                self.Bpair = to_dev(pack_tmem_cores(hi, lo, self.kin))
+                self.class_tv_local = to_dev(locality_transfer_table(), np.int32)
             return
         self.kin, self.ko_pad, self.n_slabs = blas_geometry(k, dt.itemsize)
         s_pad = np.zeros((self.n_e, self.kin), dtype=dt)
@@ -391,12 +442,41 @@ class BlasDevice:
                 astride=self.ko_pad)
         return 3
 
+    def tmem_splits(self, n_tiles, nrhs):
+        """Vector-range split of the persistent tensor-memory sweep (host-side
+        query of the library, not a kernel launch)."""
+        import ctypes
+        out = ctypes.c_int64(0)
+        nat.call("kifmm_m2l_sweep_tmem_splits", n_tiles, nrhs, ctypes.addressof(out))
+        return int(out.value)
+
     def run_level_tma(self, plan, mult, n_s, n_t, nrhs, level_scale, qt, dense, acc, solve):
-        """Engine path for float32: projection -> dense hi/lo sub-lattice
-        arrays -> TMA-fed tcgen05 sweep -> fused epilogue into the locals."""
+        """Engine path for float32: projection -> dense sub-lattice array ->
+        tcgen05 sweep (A in tensor memory, or TMA-staged hi/lo planes) ->
+        fused epilogue into the locals."""
         la = self.la
-        nsplit = sweep_splits(plan["n_tiles"], 1)
-        ld = nsplit * self.ko_pad
+        if self.tmem:
+            nsplit = self.tmem_splits(plan["n_pairs"], nrhs)
+            la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt,
+                    self.kin)
+            launch("kifmm_dense_split_tf32", P(qt), P(plan["src_slot"]), n_s, nrhs, self.kin,
+                   plan["h"], P(dense[0]), None, stream_handle())
+            launch("kifmm_m2l_sweep_tmem_f32", P(dense[0]), P(self.Bpair), self.kin, plan["h"],
+                   P(plan["tile_targets"]), P(plan["tile_ids"]), plan["n_tiles"],
+                   P(plan["pairs"]), plan["n_pairs"], P(self.class_tv_local), P(self.offsets),
+                   nrhs, nsplit, self.ko_pad, P(acc), stream_handle())
+        else:
+            nsplit = sweep_splits(plan["n_tiles"], 1)
+            self._run_tma(plan, mult, n_s, nrhs, qt, dense, acc, nsplit)
+        inv, side, loc = solve
+        la.chain(n_t * nrhs, acc, nsplit * self.ko_pad,
+                 [(self.UT, self.k, self.n_c, None, level_scale)]
+                 + Linalg.solve_stages(inv, side), loc, inv[2].shape[1], accumulate=True,
+                 asum=nsplit, astride=self.ko_pad)
+        return 4
+
+    def _run_tma(self, plan, mult, n_s, nrhs, qt, dense, acc, nsplit):
+        la = self.la
         la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
         hi, lo = dense
         # KIFMM_TMA_SPLIT=smem: the dense array holds raw fp32 q~ and the sweep
@@ -410,15 +490,12 @@ class BlasDevice:
                self.ko_pad, plan["h"], P(plan["tile_targets"]), P(plan["tile_ids"]),
                plan["n_tiles"], P(self.class_tv), P(self.offsets), nrhs, nsplit, P(acc),
                stream_handle())
-        inv, side, loc = solve
-        la.chain(n_t * nrhs, acc, ld,
-                 [(self.UT, self.k, self.n_c, None, level_scale)]
-                 + Linalg.solve_stages(inv, side), loc, inv[2].shape[1], accumulate=True,
-                 asum=nsplit, astride=self.ko_pad)
-        return 4
 
-    def acc_elems(self, n_t, nrhs, n_tiles):
-        return n_t * nrhs * sweep_splits(n_tiles, self.n_slabs) * self.ko_pad
+    def acc_elems(self, n_t, nrhs, n_tiles, tma=False, n_pairs=0):
+        ns = sweep_splits(n_tiles, self.n_slabs)
+        if tma and self.tmem:
+            ns = max(ns, self.tmem_splits(n_pairs, nrhs))
+        return n_t * nrhs * ns * self.ko_pad
 
     def run_level(self, plan, mult, n_s, n_t, nrhs, level_scale, check, qt, acc, solve=None):
         la = self.la
@@ -615,7 +692,8 @@ class DeviceFmm:
             def acc_need(l):
                 n = self.blas.acc_elems(self.n_tgt[l], R, self.blas_plan_dev[l]["n_tiles"])
                 if self.tma:
-                    n = max(n, self.blas.acc_elems(self.n_tgt[l], R, self.tma_plan[l]["n_tiles"]))
+                    n = max(n, self.blas.acc_elems(self.n_tgt[l], R, self.tma_plan[l]["n_tiles"],
+                                                   tma=True, n_pairs=self.tma_plan[l]["n_pairs"]))
                 return max(n, 1)
             qt_w = R * self.blas.kin * (3 if self.blas.tc else 1)
             b["qt_lv"] = {l: torch.zeros(max(self.n_src[l], 1) * qt_w, dtype=T, device=dev)

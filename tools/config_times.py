@@ -37,3 +37,6 @@ for name, tag, t in p.times():
 print(f"n={n} {kw} {mode} setup {ts:.1f}s evaluate {ms:.3f} ms -> {n/ms/1e3:.1f} Mpts/s")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:12]:
     print(f"   {k:40s} {v*1e3:9.1f} us")
+for name, tag, t in p.times():
+    if "m2l_sweep" in name:
+        print(f"   sweep {tag:10s} {name:32s} {t*1e3:9.1f} us")

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+C2="dict(depth=5, order_equiv=4, backend='blas', precision='f32', sigma_min=1e-6)"
+timeout 300 python tools/config_times.py 1000000 "$C2" > gpurun_out/c2_tmem.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$? >> gpurun_out/gpu_tests.log
