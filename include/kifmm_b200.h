@@ -214,9 +214,10 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
  * [B_hi | B_lo] per vector, each packed [a/8][b/4][a%8][b%4] with one
  * K chunk of width kp (device.py pack_tmem_cores).  class_tv (8, 189) may
  * list each class's vectors in any order (device.py uses a locality order).
- * Runs as clusters of 2 CTAs: pairs (n_pairs, 2) lists tile slots of the
- * same class processed together (the cores are multicast to both); a class
- * with an odd tile count repeats its last slot (device.py tile_pairs).
+ * Persistent, one CTA per SM; with KIFMM_TMEM_CLUSTER=2 it runs as clusters
+ * of 2 CTAs over pairs (n_pairs, 2) of same-class tile slots processed
+ * together (the cores multicast to both; an odd class repeats its last slot,
+ * device.py tile_pairs).
  * Output: acc[(tgt*nrhs + r)*(nsplit*ostride) + split*ostride + c], c < kp.
  * kp % 8 == 0, 8 <= kp <= 64, ostride >= kp, ostride % 4 == 0.  Replaces,
  * with m2l_sweep_tma, the bucket loop of m2l_blas.py:296-318. */
@@ -227,7 +228,7 @@ int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int
                              float* acc, void* stream);
 
 /* nsplit for kifmm_m2l_sweep_tmem_f32 that balances the persistent CTA pairs. */
-int kifmm_m2l_sweep_tmem_splits(int64_t n_pairs, int64_t nrhs, int64_t* nsplit);
+int kifmm_m2l_sweep_tmem_splits(int64_t n_tiles, int64_t n_pairs, int64_t nrhs, int64_t* nsplit);
 
 /* Debug timeline: clock64 stamps of CTA 0 of the following tensor-memory
  * sweeps with sub-lattice size h written into buf (12 x 1024 int64, device

@@ -81,7 +81,7 @@ SIGNATURES = {
     "kifmm_dense_split_tf32": [_P, _P, _I, _I, _I, _I, _P, _P, _P],
     "kifmm_m2l_sweep_tma_f32": [_P, _P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _P, _I, _I, _P, _P],
     "kifmm_m2l_sweep_tmem_f32": [_P, _P, _I, _I, _P, _P, _I, _P, _I, _P, _P, _I, _I, _I, _P, _P],
-    "kifmm_m2l_sweep_tmem_splits": [_I, _I, _P],
+    "kifmm_m2l_sweep_tmem_splits": [_I, _I, _I, _P],
     "kifmm_m2l_sweep_tmem_trace": [_P, _I],
     "kifmm_sm_target": [],
     "kifmm_probe": [_C, _I, _I, _I, _P, _P],

@@ -1,23 +1,25 @@
 // BLAS-M2L sweep on tcgen05 with the A operand in tensor memory (float32,
 // 3xTF32), persistent.
 //
-// Same contraction and numerics as m2l_tma.cu (3xTF32 products
-// A_hi.B_hi + A_lo.B_hi + A_hi.B_lo, TMEM accumulator promoted into an IEEE
-// fp32 accumulator every FLUSH_V vectors) over the same dense parity
-// sub-lattice array of raw q~ rows, Q[p*R + r][ix][iy][iz][KP], and the same
-// 4 x 4 x 8 same-parity target tiles (device.tma_level_plan).
+// Same contraction as m2l_tma.cu: per 4 x 4 x 8 same-parity target tile
+// (device.tma_level_plan) and transfer vector t, the 128 source rows of the
+// dense parity sub-lattice array of raw q~, Q[p*R + r][ix][iy][iz][KP], times
+// the dense core D_t, in 3xTF32 (A_hi.B_hi + A_lo.B_hi + A_hi.B_lo) with the
+// TMEM accumulator promoted into an IEEE fp32 accumulator every FLUSH_V
+// vectors.
 //
-// What changes is where A lives.  The TMA sweep stages every (tile, vector)
-// source block in shared memory as TF32 hi and lo planes: 2 x 128 x KP x 4
-// bytes written by TMA and read again by the MMA, which made it bound by
-// shared-memory bandwidth (128 B/clk/SM) and by L2->SM bytes.  Here every
-// loader thread owns one target row: it loads its source row for the vector
-// straight into registers (ld.global.nc, L1-allocating: consecutive vectors
-// of the locality-sorted order re-read 7/8 of the previous vector's rows),
-// splits it into TF32 hi/lo in registers and stores both into TMEM with
-// tcgen05.st (lane = row, column = K element).  The MMA reads A from TMEM;
-// only the packed cores B = [B_hi | B_lo] (one bulk copy per vector) pass
-// through shared memory.
+// What changes is where A lives and how often the cores travel.  The TMA
+// sweep staged every (tile, vector) source block in shared memory as TF32 hi
+// and lo planes (2 x 128 x KP x 4 bytes written by TMA and read again by the
+// MMA) plus the core pair, and was bound by shared-memory bandwidth.  Here:
+//  * the source block arrives raw by TMA (128-byte swizzle) and every loader
+//    thread reads its own row (conflict-free through the swizzle), splits it
+//    into TF32 hi/lo in registers and stores both into TMEM with tcgen05.st
+//    (lane = row, column = K element); the MMA reads A from TMEM, so only
+//    the core pair B = [B_hi | B_lo] is read from shared memory;
+//  * each CTA works on TWO same-class tiles at once (groups 0 and 1, one tile
+//    each): every core pair is loaded once per CTA and vector and read by
+//    both groups' MMAs, halving the core bytes per tile and vector.
 //
 // Per k-step (K = 8): D[:, 0:2KP] (+)= A_hi . [B_hi | B_lo]   (N = 2 KP)
 //                     D[:, 0:N2]  +=  A_lo . B_hi             (N2 = KP rounded up to 16;
@@ -25,12 +27,13 @@
 //   inside the B_lo half, which only adds the (tiny, correct) lo.lo term).
 // The promotion sums D[:, c] + D[:, KP + c] into the IEEE accumulator.
 //
-// Persistent: gridDim.x CTAs (one per SM) walk the work items (rhs, tile,
-// vector split) round-robin, keeping all pipelines running across items.
-// Roles (448 threads): warp 0 lane 0 bulk-copies the cores (NS stages);
-// warp 1 lane 0 issues tcgen05.mma.kind::tf32; warps 2..9 are two loader
-// groups (group g serves the vectors with global index = g mod 2 into TMEM
-// A buffer g); warps 10..13 promote and write the results.
+// Persistent: gridDim.x CTAs (one per SM) walk the work items (rhs, tile
+// pair, vector split) round-robin.  Roles (288 threads): warp 0 lane 0 loads
+// the stages (2 source blocks + 1 core pair per vector); warps 1..4 and 5..8
+// are the two groups: each loads, splits and stores its tile's source rows,
+// issues its own MMAs (one elected thread) into its own TMEM accumulator D_k,
+// promotes D_k into its registers every FLUSH_V vectors and writes the
+// tile's result rows at the end of an item.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -43,9 +46,9 @@ using namespace kifmm;
 namespace {
 
 constexpr int TMT = 128;
-constexpr int NG = 2;            // loader/MMA-issue groups, each with its own TMEM A and D
-constexpr int NTHREADS = 64 + 128 * NG + 128;
-constexpr int FLUSH_V = 4;
+constexpr int NG = 2;             // groups = tiles per CTA, each with its own TMEM A and D
+constexpr int NTHREADS = 32 + 128 * NG;
+constexpr int FLUSH_V = 8;        // vectors between promotions of a TMEM accumulator
 constexpr int BX = 4, BY = 4, BZ = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -122,39 +125,6 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* tm, in
 }
 // bulk copy into the same offset of every CTA in cta_mask (and complete_tx on
 // each one's barrier at the same offset)
-__device__ __forceinline__ void bulk_copy_mc(void* dst, const void* src, uint32_t bytes,
-                                             uint64_t* bar, uint16_t cta_mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(cta_mask)
-      : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_id_x() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t nclusters_x() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
   uint32_t b;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x));
@@ -167,10 +137,10 @@ struct TmemArgs {
   int h, tx, ty, tz;
   const int32_t* tile_targets;     // (n_tiles*128)
   const int32_t* tile_ids;         // (n_tiles)
-  const int32_t* pairs;            // (n_pairs, 2) tile slots of the same class per CTA pair
+  const int32_t* pairs;            // (n_pairs, 2) same-class tile slots handled by one CTA
   const int32_t* class_tv;         // (8, 189) vector order per target class
   const int8_t* offsets;           // (316, 3)
-  int n_tiles, n_pairs, nrhs, nsplit, jper, n_items, ns;
+  int n_pairs, nrhs, nsplit, jper, n_items, ns;
   int64_t ostride, ld;             // output: acc[(tgt*R + r)*ld + split*ostride + c]
   float* acc_out;
 };
@@ -185,38 +155,50 @@ constexpr int TRACE_N = 1024;
     if (trace_buf != nullptr && (i) < TRACE_N) trace_buf[(ev) * TRACE_N + (i)] = clock64(); \
   } while (0)
 
-// Work item it -> (r, tile slot, split); its vector range [j0, j1).
+// Work item it -> (r, tile pair, split): vectors [j0, j0 + nv) of the class
+// list.  A class with an odd tile count repeats its last slot in its last
+// pair: both groups then compute and write the same rows.
 struct Item {
-  int slot, r, split, j0, nv;
+  int pair, r, split, j0, nv;
 };
-// Items are (rhs, tile pair, split); CTA `rank` of the cluster takes tile
-// pairs[pair][rank] (a class with an odd tile count repeats its last tile:
-// both CTAs then compute and write the same rows).
-__device__ __forceinline__ Item item_of(const TmemArgs& a, int it, int rank) {
+__device__ __forceinline__ Item item_of(const TmemArgs& a, int it) {
   Item x;
   x.split = it % a.nsplit;
   const int rest = it / a.nsplit;
-  const int pr = rest % a.n_pairs;
-  x.slot = a.pairs[2 * pr + rank];
+  x.pair = rest % a.n_pairs;
   x.r = rest / a.n_pairs;
   x.j0 = x.split * a.jper;
   x.nv = max(0, min(189, x.j0 + a.jper) - x.j0);
   return x;
 }
 
-// Each vector's source block arrives in shared memory by TMA (raw fp32,
-// 128-byte swizzle, one 5-D box per 32 columns) together with its core pair
-// [B_hi | B_lo] (bulk copy); each loader thread reads its row from there
-// (conflict-free through the swizzle).
+struct TileGeom {
+  int cls, ix0, iy0, iz0, px, py, pz;
+};
+__device__ __forceinline__ TileGeom tile_geom(const TmemArgs& a, int slot) {
+  const int per_class = a.tx * a.ty * a.tz;
+  const int tile = a.tile_ids[slot];
+  TileGeom t;
+  t.cls = tile / per_class;
+  const int rem = tile - t.cls * per_class;
+  t.ix0 = (rem / (a.ty * a.tz)) * BX;
+  t.iy0 = ((rem / a.tz) % a.ty) * BY;
+  t.iz0 = (rem % a.tz) * BZ;
+  t.px = (t.cls >> 2) & 1;
+  t.py = (t.cls >> 1) & 1;
+  t.pz = t.cls & 1;
+  return t;
+}
+
 template <int KP>
 __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
     const __grid_constant__ CUtensorMap tm, const TmemArgs a) {
   constexpr int N1 = 2 * KP;
   constexpr int N2 = (KP + 15) / 16 * 16;
-  constexpr int NCH = (KP + 31) / 32;                                  // TMA boxes per vector
-  constexpr uint32_t ABYTES = NCH * TMT * 128u;
-  constexpr uint32_t BBYTES = 2u * KP * KP * 4u;
-  constexpr uint32_t SBYTES = (ABYTES + BBYTES + 1023u) / 1024u * 1024u;
+  constexpr int NCH = (KP + 31) / 32;                                  // TMA boxes per block
+  constexpr uint32_t ABYTES = NCH * TMT * 128u;                        // one source block
+  constexpr uint32_t BBYTES = 2u * KP * KP * 4u;                       // one core pair
+  constexpr uint32_t SBYTES = (NG * ABYTES + BBYTES + 1023u) / 1024u * 1024u;
   // TMEM per group k: D_k (N1 columns) then A_k = [hi | lo] (2 KP columns)
   constexpr int GCOLS = N1 + 2 * KP;
   constexpr int NEED = NG * GCOLS;
@@ -230,96 +212,79 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
       (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ns = a.ns;
-  // clusters of 2 CTAs: both walk the same items (tile pairs of one class),
-  // each loads its own source blocks and half of every core pair, which the
-  // bulk copy multicasts into both CTAs' stages
-  const int rank = (int)cluster_ctarank();
-  const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
-  constexpr uint32_t BHALF = BBYTES / 2;
   long long* const trace_buf = (blockIdx.x == 0 && g_trace_h == a.h) ? g_trace : nullptr;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * SBYTES);
-  uint64_t* empty = full + ns;
+  uint64_t* empty = full + ns;          // both groups' MMAs have read the stage
   uint64_t* done = empty + ns;          // [NG]: group k's MMAs of its last vector completed
-  uint64_t* tfull = done + NG;          // [NG]: D_k holds a finished block
-  uint64_t* tempty = tfull + NG;        // [NG]: D_k promoted
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NG);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + NG);
 
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);            // both CTAs' MMAs have read the stage
+      mbar_init(&empty[s], NG);
     }
-    for (int k = 0; k < NG; ++k) {
-      mbar_init(&done[k], 1);
-      mbar_init(&tfull[k], 1);
-      mbar_init(&tempty[k], 128);
-    }
+    for (int k = 0; k < NG; ++k) mbar_init(&done[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
   }
-  if (warp == 1) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  cluster_sync();                         // peer barriers initialised before any multicast
+  __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const int per_class = a.tx * a.ty * a.tz;
 
   if (warp == 0) {
-    // ------------------------------------------- producer: A boxes + cores
+    // ------------------- producer: both tiles' source blocks + the core pair
     if (lane == 0) {
       int g = 0;
-      for (int it = cid; it < a.n_items; it += ncl) {
-        const Item x = item_of(a, it, rank);
-        const int tile = a.tile_ids[x.slot];
-        const int cls = tile / per_class;
-        const int rem = tile - cls * per_class;
-        const int ix0 = (rem / (a.ty * a.tz)) * BX, iy0 = ((rem / a.tz) % a.ty) * BY,
-                  iz0 = (rem % a.tz) * BZ;
-        const int px = (cls >> 2) & 1, py = (cls >> 1) & 1, pz = cls & 1;
-        const int32_t* tv = a.class_tv + cls * 189 + x.j0;
+      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+        const Item x = item_of(a, it);
+        TileGeom tg[NG];
+#pragma unroll
+        for (int k = 0; k < NG; ++k) tg[k] = tile_geom(a, a.pairs[NG * x.pair + k]);
+        const int32_t* tv = a.class_tv + tg[0].cls * 189 + x.j0;
         for (int v = 0; v < x.nv; ++v, ++g) {
           const int s = g % ns;
           if (g >= ns) mbar_wait(&empty[s], ((g / ns) - 1) & 1, false);
           trace(4, g);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                            smem_u32(&full[s])),
-                       "r"(ABYTES + BBYTES)
+                       "r"(NG * ABYTES + BBYTES)
                        : "memory");
           const int t = tv[v];
           unsigned char* sb = smem + s * SBYTES;
           const int ox = a.offsets[3 * t], oy = a.offsets[3 * t + 1], oz = a.offsets[3 * t + 2];
-          const int qx = px + ox, qy = py + oy, qz = pz + oz;
-          const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
-          const int c4 = sp * a.nrhs + x.r;
 #pragma unroll
-          for (int c = 0; c < NCH; ++c)
-            tma_load_5d(sb + c * TMT * 128, &tm, c * 32, iz0 + (qz >> 1), iy0 + (qy >> 1),
-                        ix0 + (qx >> 1), c4, &full[s]);
-          bulk_copy_mc(sb + ABYTES + rank * BHALF,
-                       reinterpret_cast<const unsigned char*>(a.bpair + (int64_t)t * (2 * KP * KP)) +
-                           rank * BHALF,
-                       BHALF, &full[s], (uint16_t)0x3);
+          for (int k = 0; k < NG; ++k) {
+            const int qx = tg[k].px + ox, qy = tg[k].py + oy, qz = tg[k].pz + oz;
+            const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+              tma_load_5d(sb + k * ABYTES + c * TMT * 128, &tm, c * 32, tg[k].iz0 + (qz >> 1),
+                          tg[k].iy0 + (qy >> 1), tg[k].ix0 + (qx >> 1), sp * a.nrhs + x.r,
+                          &full[s]);
+          }
+          bulk_copy(sb + NG * ABYTES, a.bpair + (int64_t)t * (2 * KP * KP), BBYTES, &full[s]);
         }
       }
-      // drain: the peer's MMA commits into this CTA's empty barriers arrive
-      // asynchronously; wait for the last phase of every stage so no arrive
-      // can land after this CTA has exited
+      // drain: the MMA commits on the stages arrive asynchronously; wait for
+      // the last phase of every stage so none lands after this CTA exits
       for (int gg = g - ns < 0 ? 0 : g - ns; gg < g; ++gg)
         mbar_wait(&empty[gg % ns], (gg / ns) & 1, true);
     }
     __syncwarp();
-  } else if (warp >= 2 && warp < 2 + 4 * NG) {
-    // ------------------------- loader + MMA-issue groups (vectors g = k mod NG)
-    const int grp = (warp - 2) >> 2;
+  } else if (warp >= 1 && warp < 1 + 4 * NG) {
+    // --------------------- group k = tile k of the pair: load, issue, promote
+    const int grp = (warp - 1) >> 2;
     const int q4 = warp & 3;                       // TMEM lane quarter of this warp
     const int m = q4 * 32 + lane;                  // tile row = TMEM lane
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-    const bool issuer = (warp == 2 + 4 * grp) && lane == 0;
+    const bool issuer = (warp == 1 + 4 * grp) && lane == 0;
     const uint32_t dcol = tmem + (uint32_t)(grp * GCOLS);
     const uint32_t acol = dcol + N1;
     constexpr uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N1 >> 3) << 17) |
@@ -327,53 +292,50 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
     constexpr uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N2 >> 3) << 17) |
                                 ((uint32_t)(TMT >> 4) << 24);
     constexpr uint32_t SBO = (KP / 4) * 128;
+    float acc[KP];
     int nmine = 0;                                 // vectors this group has issued
-    int blk = 0;                                   // blocks this group has committed
     int g = 0;
-    for (int it = cid; it < a.n_items; it += ncl) {
-      const Item x = item_of(a, it, rank);
-      // this group's vectors of the item: v = v0, v0 + NG, ...
-      const int v0 = ((grp - g) % NG + NG) % NG;
-      int local = 0;                               // position inside the current block
-      for (int v = v0; v < x.nv; v += NG) {
-        const int gg = g + v;
-        const int s = gg % ns;
-        mbar_wait(&full[s], (gg / ns) & 1, false);
-        if (m == 0) trace(0, gg);
-        float4 cur[KP / 4];
-        const unsigned char* sb = smem + s * SBYTES + m * 128;
+    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+      const Item x = item_of(a, it);
 #pragma unroll
-        for (int i = 0; i < KP / 4; ++i)
-          cur[i] = *reinterpret_cast<const float4*>(sb + (i >> 3) * (TMT * 128) +
-                                                    (((i & 7) ^ (m & 7)) << 4));
-        // previous MMAs of this group done: A_k (and, at a block start, D_k) reusable
+      for (int c = 0; c < KP; ++c) acc[c] = 0.f;
+      for (int v = 0; v < x.nv; ++v, ++g) {
+        const int s = g % ns;
+        const int local = v % FLUSH_V;
+        mbar_wait(&full[s], (g / ns) & 1, false);
+        if (m == 0) trace(grp == 0 ? 0 : 5, g);
+        // this thread's source row -> TF32 hi (round-to-nearest-away on the bit
+        // pattern) and lo = x - hi (exact in fp32; enters the MMA truncated to
+        // TF32), in registers before waiting for the TMEM buffers
+        uint32_t hv[KP], lv[KP];
+        const unsigned char* sb = smem + s * SBYTES + grp * ABYTES + m * 128;
+#pragma unroll
+        for (int i = 0; i < KP / 4; ++i) {
+          const float4 c4 = *reinterpret_cast<const float4*>(sb + (i >> 3) * (TMT * 128) +
+                                                              (((i & 7) ^ (m & 7)) << 4));
+          const float f[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            hv[4 * i + j] = (__float_as_uint(f[j]) + 0x1000u) & 0xFFFFE000u;
+            lv[4 * i + j] = __float_as_uint(f[j] - __uint_as_float(hv[4 * i + j]));
+          }
+        }
+        // this group's previous MMAs done: A_k reusable (and D_k promoted below)
         if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);
-        if (local == 0 && blk > 0) mbar_wait(&tempty[grp], (blk - 1) & 1, false);
-        if (m == 0) trace(1, gg);
+        if (m == 0) trace(grp == 0 ? 1 : 6, g);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int c = 0; c < KP / 8; ++c) {
-          uint32_t hv[8], lv[8];
-          const float f[8] = {cur[2 * c].x,     cur[2 * c].y,     cur[2 * c].z,     cur[2 * c].w,
-                              cur[2 * c + 1].x, cur[2 * c + 1].y, cur[2 * c + 1].z, cur[2 * c + 1].w};
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            // hi = TF32 round-to-nearest-away on the bit pattern; lo = x - hi is
-            // exact in fp32 and enters the MMA truncated to TF32
-            hv[i] = (__float_as_uint(f[i]) + 0x1000u) & 0xFFFFE000u;
-            lv[i] = __float_as_uint(f[i] - __uint_as_float(hv[i]));
-          }
-          tmem_st8(acol + lane_base + c * 8, hv);
-          tmem_st8(acol + lane_base + KP + c * 8, lv);
+          tmem_st8(acol + lane_base + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&hv[c * 8]));
+          tmem_st8(acol + lane_base + KP + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&lv[c * 8]));
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
-        const bool last_of_block = (local == FLUSH_V - 1) || (v + NG >= x.nv);
         if (issuer) {
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          trace(3, gg);
-          const uint32_t bb = smem_u32(smem + s * SBYTES + ABYTES);
+          if (grp == 0) trace(3, g);
+          const uint32_t bb = smem_u32(smem + s * SBYTES + NG * ABYTES);
 #pragma unroll
           for (int ks = 0; ks < KP / 8; ++ks) {
             const uint64_t db = desc_nosw(bb + ks * 256, 128, SBO);
@@ -381,80 +343,41 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
             mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
           }
           mma_commit(&done[grp]);
-          mma_commit_mc(&empty[s], (uint16_t)0x3);
-          if (last_of_block) mma_commit(&tfull[grp]);
+          mma_commit(&empty[s]);
         }
         __syncwarp();
         ++nmine;
-        if (last_of_block) {
-          ++blk;
-          local = 0;
-        } else {
-          ++local;
-        }
-        if (m == 0) trace(2, gg);
-      }
-      g += x.nv;
-    }
-  } else if (warp >= 2 + 4 * NG) {
-    // --------------------------------- promotion of both groups' D, results
-    const int q4 = warp & 3;
-    const int m = q4 * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-    float acc[KP];
-    int cnt[NG];
-#pragma unroll
-    for (int k = 0; k < NG; ++k) cnt[k] = 0;
-    int g = 0;
-    for (int it = cid; it < a.n_items; it += ncl) {
-      const Item x = item_of(a, it, rank);
-#pragma unroll
-      for (int c = 0; c < KP; ++c) acc[c] = 0.f;
-      int nb[NG], nbmax = 0;
-#pragma unroll
-      for (int k = 0; k < NG; ++k) {
-        const int v0 = ((k - g) % NG + NG) % NG;
-        const int nk = x.nv > v0 ? (x.nv - v0 + NG - 1) / NG : 0;
-        nb[k] = (nk + FLUSH_V - 1) / FLUSH_V;
-        nbmax = max(nbmax, nb[k]);
-      }
-      for (int b = 0; b < nbmax; ++b) {
-#pragma unroll
-        for (int k = 0; k < NG; ++k) {
-          if (b >= nb[k]) continue;
-          mbar_wait(&tfull[k], cnt[k] & 1, true);
-          if (m == 0 && k == 0) trace(5, cnt[0]);
+        if (local == FLUSH_V - 1 || v == x.nv - 1) {
+          // promote D_k: wait for this block's last MMAs, add into registers;
+          // the next vector's MMA overwrites D_k only after the group barrier
+          mbar_wait(&done[grp], (nmine - 1) & 1, false);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t dcol = tmem + lane_base + (uint32_t)(k * GCOLS);
 #pragma unroll
           for (int c = 0; c < KP / 8; ++c) {
             uint32_t u[8], w[8];
-            tmem_ld8(dcol + c * 8, u);
-            tmem_ld8(dcol + KP + c * 8, w);
+            tmem_ld8(dcol + lane_base + c * 8, u);
+            tmem_ld8(dcol + lane_base + KP + c * 8, w);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               acc[c * 8 + i] += __uint_as_float(u[i]) + __uint_as_float(w[i]);
           }
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          mbar_arrive(&tempty[k]);
-          if (m == 0 && k == 0) trace(6, cnt[0]);
-          ++cnt[k];
         }
       }
-      const int32_t tgt = a.tile_targets[(int64_t)x.slot * TMT + m];
+      const int slot = a.pairs[NG * x.pair + grp];
+      const int32_t tgt = a.tile_targets[(int64_t)slot * TMT + m];
       if (tgt >= 0) {
         float* o = a.acc_out + ((int64_t)tgt * a.nrhs + x.r) * a.ld + (int64_t)x.split * a.ostride;
 #pragma unroll
         for (int c = 0; c < KP; c += 4)
           *reinterpret_cast<float4*>(o + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
       }
-      g += x.nv;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  cluster_sync();                         // no CTA leaves while its peer may still signal it
-  if (warp == 1) {
+  __syncthreads();
+  if (warp == 0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
@@ -508,38 +431,26 @@ int make_map(CUtensorMap* tm, const float* base, int kp, int h, int64_t planes) 
 template <int KP>
 int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   TmemArgs a = a0;
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  int st = make_map(&tm, a.q, KP, a.h, 8 * (int64_t)a.nrhs);
+  if (st) return st;
   static int ns_env = -1;
   if (ns_env < 0) {
     const char* e = getenv("KIFMM_TMEM_STAGES");
     ns_env = e ? atoi(e) : 4;
     if (ns_env < 2) ns_env = 2;
   }
-  CUtensorMap tm;
-  memset(&tm, 0, sizeof(tm));
-  int st = make_map(&tm, a.q, KP, a.h, 8 * (int64_t)a.nrhs);
-  if (st) return st;
-  const size_t sbytes = (((KP + 31) / 32) * TMT * 128 + 2ull * KP * KP * 4 + 1023) / 1024 * 1024;
+  const size_t sbytes =
+      ((size_t)NG * ((KP + 31) / 32) * TMT * 128 + 2ull * KP * KP * 4 + 1023) / 1024 * 1024;
   int ns = ns_env;
   while (ns > 2 && 1024 + ns * sbytes + 256 > 227 * 1024) --ns;
   a.ns = ns;
-  const size_t smem = 1024 + ns * sbytes + (2 * ns + 3 * NG) * 8 + 16;
-  const int ncl = a.n_items < sm_count() / 2 ? a.n_items : sm_count() / 2;
+  const size_t smem = 1024 + ns * sbytes + (2 * ns + NG) * 8 + 16;
+  const int grid = a.n_items < sm_count() ? a.n_items : sm_count();
   set_max_smem((const void*)m2l_sweep_tmem_kernel<KP>, smem);
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(2 * ncl, 1, 1);
-  cfg.blockDim = dim3(NTHREADS, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, m2l_sweep_tmem_kernel<KP>, tm, a);
-  return e == cudaSuccess ? launch_status() : (int)e;
+  m2l_sweep_tmem_kernel<KP><<<grid, NTHREADS, smem, stream>>>(tm, a);
+  return launch_status();
 }
 
 }  // namespace
@@ -556,23 +467,21 @@ int kifmm_m2l_sweep_tmem_trace(long long* buf, int64_t h) {
 }
 
 // Split of the 189-vector range (work items = R * n_pairs * nsplit) that
-// balances the persistent CTA pairs: the smallest nsplit whose item count is
-// within 4% of a whole number of waves (or the best found up to 16).
-int kifmm_m2l_sweep_tmem_splits(int64_t n_pairs, int64_t nrhs, int64_t* nsplit) {
-  if (n_pairs < 0 || nrhs < 1 || !nsplit) return KIFMM_EARG;
-  const int g = sm_count() / 2;           // CTA pairs
-  const int64_t n_tiles = n_pairs;
+// balances the persistent CTAs: the best whole-wave fill, discounted by the
+// per-item fixed cost (pipeline fill, result write).
+int kifmm_m2l_sweep_tmem_splits(int64_t n_tiles, int64_t n_pairs, int64_t nrhs,
+                                int64_t* nsplit) {
+  if (n_tiles < 0 || n_pairs < 0 || nrhs < 1 || !nsplit) return KIFMM_EARG;
+  const int g = sm_count();
   int best = 1;
   double best_eff = 0;
   for (int s = 1; s <= 16; ++s) {
     const int jper = (189 + s - 1) / s;
     if ((s - 1) * jper >= 189) continue;           // would leave an empty piece
-    const int nsp = s;
-    const double items = (double)n_tiles * nrhs * nsp;
+    const double items = (double)n_pairs * nrhs * s;
     const double waves = items / g;
     const double eff = waves / ((int64_t)(waves + 0.999999));
-    // per-item fixed cost (first loads, result write) ~ 1/4 of a vector block
-    const double cost = eff / (1.0 + 0.02 * nsp);
+    const double cost = eff / (1.0 + 0.02 * s);
     if (cost > best_eff * 1.001) {
       best_eff = cost;
       best = s;
@@ -604,7 +513,6 @@ int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int
   a.n_pairs = (int)n_pairs;
   a.class_tv = class_tv;
   a.offsets = offsets;
-  a.n_tiles = (int)n_tiles;
   a.nrhs = (int)nrhs;
   a.nsplit = (int)nsplit;
   a.jper = (int)((189 + nsplit - 1) / nsplit);

@@ -442,12 +442,12 @@ class BlasDevice:
                 astride=self.ko_pad)
         return 3
 
-    def tmem_splits(self, n_tiles, nrhs):
+    def tmem_splits(self, n_tiles, n_pairs, nrhs):
         """Vector-range split of the persistent tensor-memory sweep (host-side
         query of the library, not a kernel launch)."""
         import ctypes
         out = ctypes.c_int64(0)
-        nat.call("kifmm_m2l_sweep_tmem_splits", n_tiles, nrhs, ctypes.addressof(out))
+        nat.call("kifmm_m2l_sweep_tmem_splits", n_tiles, n_pairs, nrhs, ctypes.addressof(out))
         return int(out.value)
 
     def run_level_tma(self, plan, mult, n_s, n_t, nrhs, level_scale, qt, dense, acc, solve):
@@ -456,7 +456,7 @@ class BlasDevice:
         fused epilogue into the locals."""
         la = self.la
         if self.tmem:
-            nsplit = self.tmem_splits(plan["n_pairs"], nrhs)
+            nsplit = self.tmem_splits(plan["n_tiles"], plan["n_pairs"], nrhs)
             la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt,
                     self.kin)
             launch("kifmm_dense_split_tf32", P(qt), P(plan["src_slot"]), n_s, nrhs, self.kin,
@@ -494,7 +494,7 @@ class BlasDevice:
     def acc_elems(self, n_t, nrhs, n_tiles, tma=False, n_pairs=0):
         ns = sweep_splits(n_tiles, self.n_slabs)
         if tma and self.tmem:
-            ns = max(ns, self.tmem_splits(n_pairs, nrhs))
+            ns = max(ns, self.tmem_splits(n_tiles, n_pairs, nrhs))
         return n_t * nrhs * ns * self.ko_pad
 
     def run_level(self, plan, mult, n_s, n_t, nrhs, level_scale, check, qt, acc, solve=None):
@@ -899,8 +899,18 @@ class DeviceFmm:
                     self.evaluate_device(static_q, nrhs, gradient=gradient)
             torch.cuda.current_stream().wait_stream(side)
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                out = self.evaluate_device(static_q, nrhs, gradient=gradient)
+            # no garbage collection during the capture: a collected graph of
+            # another instance would be destroyed mid-capture (not permitted,
+            # invalidates this capture)
+            import gc
+            was_enabled = gc.isenabled()
+            gc.disable()
+            try:
+                with torch.cuda.graph(g):
+                    out = self.evaluate_device(static_q, nrhs, gradient=gradient)
+            finally:
+                if was_enabled:
+                    gc.enable()
             self._graphs[key] = (g, static_q, out)
         return self._graphs[key]
 
