@@ -298,30 +298,50 @@ def run_single(args):
         # three MMAs per fp32 product
         peak_tc = peaks["bf16_tflops"] / 2.0 / 3.0
         n_tiles = (dev.tma_plan if dev.tma else dev.blas_plan_dev)[lvl]["n_tiles"]
-        execd = 3 * 2.0 * 128 * bd.kin * bd.ko_pad * 189 * n_tiles
-        gather_bytes = 2 * 4.0 * bd.kin * per_level[lvl]["pairs"]
-        # shared-memory traffic model of the sweep (what bounds it): per
-        # (tile, vector) TMA writes of A hi/lo + core hi/lo, and the three
-        # MMAs' operand reads (A_lo.B_hi, A_hi.B_lo, A_hi.B_hi)
-        a_b, b_b = 2 * 4.0 * 128 * bd.kin, 2 * 4.0 * bd.ko_pad * bd.kin
-        smem_bytes = (a_b + b_b + 3 * (a_b + b_b) / 2) * 189 * n_tiles
         clk_mhz = clk.summary().get("sm_mhz") or 1965.0
         smem_peak = 128.0 * 148 * clk_mhz * 1e6 / 1e9                    # GB/s
+        tmem = dev.tma and bd.tmem
+        kp = bd.kin
+        if tmem:
+            # tensor-memory sweep (csrc/m2l_tmem.cu): per (tile, vector) one MMA
+            # of N = 2 kp (A_hi . [B_hi | B_lo]) and one of N = kp rounded to 16
+            # (A_lo . B_hi), K = kp, M = 128; A from TMEM
+            n2 = -(-kp // 16) * 16
+            execd = 2.0 * 128 * (2 * kp + n2) * kp * 189 * n_tiles
+            # shared-memory traffic per (tile, vector): TMA write of the raw
+            # source block (128-byte rows, 32-column boxes), the loaders' read
+            # of it, half a core pair write (2 tiles per CTA share it), the
+            # MMAs' reads of the core pair
+            a_b = 128.0 * 128 * (-(-kp // 32))
+            smem_bytes = (a_b + 128.0 * kp * 4 + 2.0 * kp * kp * 4 / 2
+                          + (2 * kp + n2) * kp * 4.0) * 189 * n_tiles
+            kname = "m2l_sweep_tmem_f32"
+            note = ("128 B/clk/SM shared-memory bandwidth; TMA source-block write + loader read, "
+                    "half a core-pair write, MMA core reads per (tile, vector); A reaches the "
+                    "tensor core from TMEM")
+        else:
+            execd = 3 * 2.0 * 128 * bd.kin * bd.ko_pad * 189 * n_tiles
+            # per (tile, vector) TMA writes of A hi/lo + core hi/lo, and the
+            # three MMAs' operand reads (A_lo.B_hi, A_hi.B_lo, A_hi.B_hi)
+            a_b, b_b = 2 * 4.0 * 128 * bd.kin, 2 * 4.0 * bd.ko_pad * bd.kin
+            smem_bytes = (a_b + b_b + 3 * (a_b + b_b) / 2) * 189 * n_tiles
+            kname = f"m2l_sweep_{'tma' if dev.tma else 'tc'}_f32"
+            note = "128 B/clk/SM shared-memory bandwidth; TMA writes + MMA operand reads per (tile, vector)"
+        gather_bytes = 4.0 * bd.kin * per_level[lvl]["pairs"]
         rooflines["m2l_sweep_tc_f32"] = dict(
             bound="tensor",
-            kernel=f"m2l_sweep_{'tma' if dev.tma else 'tc'}_f32 (level {lvl})",
+            kernel=f"{kname} (level {lvl})",
             achieved=algo / (sweep_ms / 1e3) / 1e12, peak=peak_tc, unit="TFLOP/s",
             frac=algo / (sweep_ms / 1e3) / 1e12 / peak_tc,
-            traffic=dram_traffic("m2l_sweep_tma_f32_level5"),
+            traffic=dram_traffic(f"{kname}_level5"),
             smem_model=dict(bytes_per_launch=smem_bytes,
                             achieved_gbs=smem_bytes / (sweep_ms / 1e3) / 1e9,
                             peak_gbs=smem_peak,
                             frac=smem_bytes / (sweep_ms / 1e3) / 1e9 / smem_peak,
-                            note="128 B/clk/SM shared-memory bandwidth; TMA writes + MMA "
-                                 "operand reads per (tile, vector)"),
+                            note=note),
             algorithmic=f"4 k sum_t m_t k_t = {algo:.4g} flop at level {lvl} (SURVEY 8d)",
             executed_tensor_tflops=execd / (sweep_ms / 1e3) / 1e12,
-            gather_gbs=gather_bytes / (sweep_ms / 1e3) / 1e9,
+            source_row_gbs=gather_bytes / (sweep_ms / 1e3) / 1e9,
             peak_source="MEASURED_PEAKS.json bf16_tflops / 2 (TF32) / 3 (3xTF32)")
     else:
         rooflines["m2l_sweep"] = dict(

@@ -8,10 +8,23 @@ KEYS = ["Duration", "Grid Size", "Block Size", "Registers Per Thread", "Dynamic 
         "Compute (SM) Throughput", "Mem Busy", "Max Bandwidth"]
 
 
-def main(path):
+def main(path, launch=None):
+    """Summary of one launch of the report: `launch` = ncu ID, default the
+    longest launch."""
     det = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(det)))
     hdr = rows[0]
+    idi = hdr.index("ID")
+    if launch is None:
+        durs = {}
+        for r in rows[1:]:
+            if r[hdr.index("Metric Name")] == "Duration":
+                v = float(r[hdr.index("Metric Value")].replace(",", ""))
+                durs[r[idi]] = v * (1e3 if r[hdr.index("Metric Unit")] == "ms" else 1.0)
+        launch = max(durs, key=durs.get) if durs else "0"
+    launch = str(launch)
+    print("launch ID:", launch)
+    rows = [hdr] + [r for r in rows[1:] if r[idi] == launch]
     ni, vi, ui = hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     kn = hdr.index("Kernel Name")
     print("kernel:", rows[1][kn][:90])
@@ -22,7 +35,8 @@ def main(path):
             print(f"  {r[ni]:38s} {r[vi]:>14s} {r[ui]}")
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
-    names, units, vals = rr[0], rr[1], rr[2]
+    names, units = rr[0], rr[1]
+    vals = next(r for r in rr[2:] if r[names.index("ID")] == launch)
     want = {}
     for i, n in enumerate(names):
         if n.startswith("smsp__average_warp_latency_issue_stalled_") or n.startswith("smsp__average_warps_issue_stalled_"):
@@ -47,4 +61,4 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
