@@ -12,7 +12,8 @@ import ctypes
 import os
 
 LIB_NAME = "libkifmm_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("KIFMM_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)     # KIFMM_LIB: variant builds (tools)
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int64

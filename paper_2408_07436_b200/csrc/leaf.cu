@@ -24,15 +24,6 @@ using namespace kifmm;
 
 namespace {
 
-inline bool getenv_flag(const char* name) {
-  static int cached = -1;
-  if (cached < 0) {
-    const char* v = std::getenv(name);
-    cached = (v && *v && *v != '0') ? 1 : 0;
-  }
-  return cached == 1;
-}
-
 template <typename T> struct vec4;
 template <> struct vec4<float> { using v = float4; };
 template <> struct vec4<double> { using v = double4; };
@@ -316,68 +307,51 @@ __device__ __forceinline__ u64 rsq2(u64 r2) {
   return pk2(a, b);
 }
 
-#ifndef KIFMM_PAIR_CAP
-#define KIFMM_PAIR_CAP 224
+#ifndef KIFMM_LEAF_MINB
+#define KIFMM_LEAF_MINB 7      // leaf-pass CTAs per SM the register budget is sized for
 #endif
-// Source pairs staged per warp (448 sources; a near field of ~810 sources
-// takes two passes).  4 warps x 7 KB = 28 KB per CTA, so a leaf-pass CTA
-// still fits next to two sweep CTAs (2 x 99 KB) on an SM when the near field
-// runs concurrently with the finest-level M2L.
-constexpr int kPairCap = KIFMM_PAIR_CAP;
-constexpr float kFar = 1e18f;              // padding source: r2 ~ 1e36, charge 0
+#ifndef KIFMM_SRC_CAP
+#define KIFMM_SRC_CAP 448
+#endif
+// Source records staged per warp (448 sources; a near field of ~810 sources
+// takes two passes): 4 warps x 7 KB = 28 KB per CTA.
+constexpr int kSrcCap = KIFMM_SRC_CAP;
 
-// Stage source record j of the current fill into the paired layout.
-__device__ __forceinline__ void stage_pair(float* buf, int j, const float4* src) {
-  float* rec = buf + (j >> 1) * 8 + (j & 1);
-  const float* g = reinterpret_cast<const float*>(src);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(rec + 2 * c);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(g + c));
-  }
+__device__ __forceinline__ void fma2_acc(u64& acc, u64 a, u64 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
 }
-
-// Sum over pairs [0, np); pairs below `gpairs` may hold coincident points.
-// Two accumulators alternate so consecutive pairs do not serialise on one
-// FFMA2 dependency chain.
-template <bool TWO>
-__device__ __forceinline__ void pair_sum(const float* buf, int np, int gpairs, u64 X, u64 Y,
-                                         u64 Z, float x0, float y0, float z0, u64& acc) {
-  const float4* b4 = reinterpret_cast<const float4*>(buf);
+// Sum over AoS source records s = start, start + stride, ... < ns of the
+// lane's two targets (X, Y, Z packed pairs) against each source; records
+// below `guard_n` may coincide with a target (r2 = 0 -> no contribution).
+// One 16-byte shared load per source feeds two interactions; two
+// accumulators alternate so consecutive sources do not serialise on one
+// FFMA2 chain.
+__device__ __forceinline__ void quad_sum(const float4* buf, int ns, int guard_n, int start,
+                                         int stride, u64 X, u64 Y, u64 Z, u64& acc) {
   u64 acc2 = pk2(0.f, 0.f);
-  auto body = [&](int p, u64& a_, auto guard) {
+  auto body = [&](int j, u64& a_, auto guard) {
     constexpr bool G = decltype(guard)::value;
-    const float4 a = b4[2 * p], b = b4[2 * p + 1];   // (xA xB yA yB), (zA zB qA qB)
-    if (TWO) {
-      // targets (lane, lane+32) against source A, then source B
-      u64 dx = sub2(X, pk2(a.x, a.x)), dy = sub2(Y, pk2(a.z, a.z)), dz = sub2(Z, pk2(b.x, b.x));
-      u64 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
-      a_ = fma2(rsq2<G>(r2), pk2(b.z, b.z), a_);
-      dx = sub2(X, pk2(a.y, a.y)); dy = sub2(Y, pk2(a.w, a.w)); dz = sub2(Z, pk2(b.y, b.y));
-      r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
-      a_ = fma2(rsq2<G>(r2), pk2(b.w, b.w), a_);
-    } else {
-      // this lane's target against sources (A, B)
-      const u64 dx = sub2(pk2(x0, x0), pk2(a.x, a.y));
-      const u64 dy = sub2(pk2(y0, y0), pk2(a.z, a.w));
-      const u64 dz = sub2(pk2(z0, z0), pk2(b.x, b.y));
-      const u64 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
-      a_ = fma2(rsq2<G>(r2), pk2(b.z, b.w), a_);
-    }
+    const float4 s = buf[j];                         // (x, y, z, q)
+    const u64 dx = sub2(X, pk2(s.x, s.x));
+    const u64 dy = sub2(Y, pk2(s.y, s.y));
+    const u64 dz = sub2(Z, pk2(s.z, s.z));
+    const u64 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+    fma2_acc(a_, rsq2<G>(r2), pk2(s.w, s.w));
   };
-  int p = 0;
-  for (; p < gpairs; ++p) body(p, acc, std::true_type{});
-#pragma unroll 2
-  for (; p + 1 < np; p += 2) {
-    body(p, acc, std::false_type{});
-    body(p + 1, acc2, std::false_type{});
+  int j = start;
+  for (; j < guard_n && j < ns; j += stride) body(j, acc, std::true_type{});
+  for (; j + 3 * stride < ns; j += 4 * stride) {
+    body(j, acc, std::false_type{});
+    body(j + stride, acc2, std::false_type{});
+    body(j + 2 * stride, acc, std::false_type{});
+    body(j + 3 * stride, acc2, std::false_type{});
   }
-  if (p < np) body(p, acc, std::false_type{});
+  for (; j < ns; j += stride) body(j, acc, std::false_type{});
   const float2 u = up2(acc), v = up2(acc2);
   acc = pk2(u.x + v.x, u.y + v.y);
 }
 
-__global__ void __launch_bounds__(32 * kWarps) leaf_pass_x2_kernel(
+__global__ void __launch_bounds__(32 * kWarps, KIFMM_LEAF_MINB) leaf_pass_x2_kernel(
     const float* __restrict__ tx, const float* __restrict__ ty, const float* __restrict__ tz,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
     const double* __restrict__ centers, const double* __restrict__ base, int64_t ne,
@@ -385,10 +359,10 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_x2_kernel(
     const int32_t* __restrict__ sstart, const int32_t* __restrict__ scount,
     const int32_t* __restrict__ near_off, const int32_t* __restrict__ near_leaf, int64_t nrhs,
     const int64_t* __restrict__ perm, int parts, float* __restrict__ out) {
-  constexpr int kCap = 2 * kPairCap;
-  __shared__ __align__(16) float sbuf[kWarps][kPairCap * 8];
+  constexpr int kCap = kSrcCap;
+  __shared__ __align__(16) float4 sbuf[kWarps][kCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* buf = sbuf[w];
+  float4* buf = sbuf[w];
   const int64_t b = (int64_t)blockIdx.x * kWarps + w;
   if (b >= n_tleaves) return;
   const int64_t t0 = tstart[b];
@@ -403,20 +377,22 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_x2_kernel(
     seg_start = sstart[sl];
     seg_cnt = scount[sl];
   }
-  // pad slot m (odd fills): far away, zero charge
-  auto pad = [&](int m) {
-    if ((m & 1) && lane == 0) {
-      float* rec = buf + (m >> 1) * 8 + 1;
-      rec[0] = kFar; rec[2] = kFar; rec[4] = kFar; rec[6] = 0.f;
-    }
-  };
-  for (int tb = 0; tb < tc; tb += 64) {
-    const bool two = tc - tb > 32;                 // warp-uniform
-    const bool live0 = tb + lane < tc, live1 = tb + 32 + lane < tc;
-    const int64_t i0 = t0 + tb + lane, i1 = i0 + 32;
-    const float x0 = live0 ? tx[i0] : 0.f, y0 = live0 ? ty[i0] : 0.f, z0 = live0 ? tz[i0] : 0.f;
-    const float x1 = live1 ? tx[i1] : 0.f, y1 = live1 ? ty[i1] : 0.f, z1 = live1 ? tz[i1] : 0.f;
-    const u64 X = pk2(x0, x1), Y = pk2(y0, y1), Z = pk2(z0, z1);
+  // Passes of up to 32 targets, two per lane (the halves of the packed FP32
+  // pairs).  A pass of n targets uses R = next power of two >= n/2 lanes per
+  // source subset and f = 32 / R subsets: lane l serves targets l % R and
+  // l % R + R over the sources j = l / R (mod f); the f partial sums are
+  // combined with shuffles.  (A leaf of 30 targets: 16 lanes x 2 targets x
+  // half the sources each; of 37: one such pass and a 5-target pass at an
+  // 8-way source split.)
+  for (int tb = 0; tb < tc; tb += 32) {
+    const int n = min(32, tc - tb);
+    const int h = (n + 1) >> 1;
+    const int R = h <= 1 ? 1 : 1 << (32 - __clz(h - 1));
+    const int f = 32 / R, sub = lane / R;
+    const int ti = lane % R;
+    const bool live0 = ti < n, live1 = ti + R < n;
+    const int64_t ia = t0 + tb + (live0 ? ti : 0), ib = t0 + tb + (live1 ? ti + R : 0);
+    const u64 X = pk2(tx[ia], tx[ib]), Y = pk2(ty[ia], ty[ib]), Z = pk2(tz[ia], tz[ib]);
     for (int64_t r = 0; r < nrhs; ++r) {
       u64 far = pk2(0.f, 0.f), near = pk2(0.f, 0.f);
       // L2P: downward equivalent densities of the leaf -> its targets.
@@ -426,16 +402,12 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_x2_kernel(
         __syncwarp();
         for (int k = lane; k < m; k += 32) {
           const int64_t e = e0 + k;
-          float* rec = buf + (k >> 1) * 8 + (k & 1);
-          rec[0] = real_traits<float>::from_d(exact_add(cx, base[e * 3]));
-          rec[2] = real_traits<float>::from_d(exact_add(cy, base[e * 3 + 1]));
-          rec[4] = real_traits<float>::from_d(exact_add(cz, base[e * 3 + 2]));
-          rec[6] = loc[e];
+          buf[k] = make_float4(real_traits<float>::from_d(exact_add(cx, base[e * 3])),
+                               real_traits<float>::from_d(exact_add(cy, base[e * 3 + 1])),
+                               real_traits<float>::from_d(exact_add(cz, base[e * 3 + 2])), loc[e]);
         }
-        pad(m);
         __syncwarp();
-        if (two) pair_sum<true>(buf, (m + 1) >> 1, 0, X, Y, Z, x0, y0, z0, far);
-        else pair_sum<false>(buf, (m + 1) >> 1, 0, X, Y, Z, x0, y0, z0, far);
+        quad_sum(buf, m, 0, sub, f, X, Y, Z, far);
       }
       // P2P: own leaf first, then neighbours in Morton order.
       if (parts & 2) {
@@ -445,24 +417,21 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_x2_kernel(
         auto flush = [&]() {
           cp_async_commit();
           cp_async_wait<0>();
-          pad(fill);
           __syncwarp();
           const int g = min(guarded, fill);
-          const int np = (fill + 1) >> 1, gp = (g + 1) >> 1;
-          if (two) pair_sum<true>(buf, np, gp, X, Y, Z, x0, y0, z0, near);
-          else pair_sum<false>(buf, np, gp, X, Y, Z, x0, y0, z0, near);
+          quad_sum(buf, fill, g, sub, f, X, Y, Z, near);
           guarded -= g;
           fill = 0;
           __syncwarp();
         };
         __syncwarp();
-        for (int n = 0; n < n1 - n0; ++n) {
-          const int64_t j0 = __shfl_sync(0xffffffffu, seg_start, n & 31);
-          const int jc = __shfl_sync(0xffffffffu, seg_cnt, n & 31);
+        for (int nn = 0; nn < n1 - n0; ++nn) {
+          const int64_t j0 = __shfl_sync(0xffffffffu, seg_start, nn & 31);
+          const int jc = __shfl_sync(0xffffffffu, seg_cnt, nn & 31);
           for (int jb = 0; jb < jc;) {
             if (fill == kCap) flush();
             const int m = min(jc - jb, kCap - fill);
-            for (int k = lane; k < m; k += 32) stage_pair(buf, fill + k, srow + j0 + jb + k);
+            for (int k = lane; k < m; k += 32) cp_async16_ca(buf + fill + k, srow + j0 + jb + k, true);
             fill += m;
             jb += m;
           }
@@ -471,17 +440,27 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_x2_kernel(
       }
       const float c = real_traits<float>::inv4pi();
       const float2 fv = up2(far), nv = up2(near);
-      // single mode: (x, y) halves are two partial sums of the same target;
-      // two mode: they are the two targets.
-      const float v0 = two ? fv.x * c + nv.x * c : (fv.x + fv.y) * c + (nv.x + nv.y) * c;
-      if (live0) {
-        float* o = out + (perm ? perm[i0] : i0) * nrhs + r;
-        *o = (parts & 4) ? *o + v0 : v0;
+      float fa = fv.x, fb = fv.y, na = nv.x, nb = nv.y;
+      // combine the f source subsets of each target
+      for (int off = R; off < 32; off <<= 1) {
+        fa += __shfl_xor_sync(0xffffffffu, fa, off);
+        fb += __shfl_xor_sync(0xffffffffu, fb, off);
+        na += __shfl_xor_sync(0xffffffffu, na, off);
+        nb += __shfl_xor_sync(0xffffffffu, nb, off);
       }
-      if (two && live1) {
-        float* o = out + (perm ? perm[i1] : i1) * nrhs + r;
-        const float v1 = fv.y * c + nv.y * c;
-        *o = (parts & 4) ? *o + v1 : v1;
+      if (sub == 0) {
+        if (live0) {
+          const int64_t i = t0 + tb + ti;
+          float* o = out + (perm ? perm[i] : i) * nrhs + r;
+          const float v = fa * c + na * c;
+          *o = (parts & 4) ? *o + v : v;
+        }
+        if (live1) {
+          const int64_t i = t0 + tb + ti + R;
+          float* o = out + (perm ? perm[i] : i) * nrhs + r;
+          const float v = fb * c + nb * c;
+          *o = (parts & 4) ? *o + v : v;
+        }
       }
     }
   }
@@ -519,7 +498,7 @@ int leaf_pass(const T* tx, const T* ty, const T* tz, const int32_t* ts, const in
   if (ntl == 0) return 0;
   const auto* s4 = reinterpret_cast<const typename vec4<T>::v*>(src4);
   if constexpr (sizeof(T) == 4) {
-    if (!grad && !getenv_flag("KIFMM_LEAF_SCALAR")) {
+    if (!grad) {
       leaf_pass_x2_kernel<<<ceil_div(ntl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
           tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local, s4, ns, ss, sc, no, nlf, nrhs,
           perm, parts, out);
