@@ -29,8 +29,8 @@ __global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t 
   constexpr int TM = BM * BN / (NT * TN);        // rows per thread: 4 (BM=64), 2, 1
   constexpr int AE = BM * BK / NT;               // A elements loaded per thread
   constexpr int BE = BK * BN / NT;               // B elements loaded per thread (4)
-  __shared__ T As[BK][BM + 4];
-  __shared__ T Bs[BK][BN + 4];
+  __shared__ __align__(16) T As[BK][BM + 4];
+  __shared__ __align__(16) T Bs[BK][BN + 4];
   const int tid = threadIdx.x;
   const int tn = tid % (BN / TN), tm = tid / (BN / TN);
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
@@ -79,11 +79,13 @@ __global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t 
     if (k0 + BK < K) load(k0 + BK);              // overlap the next tile's loads
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
+      // vector shared loads: the TM rows and TN columns of a thread are
+      // contiguous (one 16-byte load each for float; TM may be 1 or 2)
       T a[TM], b[TN];
 #pragma unroll
       for (int i = 0; i < TM; ++i) a[i] = As[kk][tm * TM + i];
 #pragma unroll
-      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tn + j * (BN / TN)];
+      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tn * TN + j];
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t 
     if (row < 0) continue;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int64_t gn = n0 + tn + j * (BN / TN);
+      const int64_t gn = n0 + tn * TN + j;
       if (gn >= N) continue;
       T v = acc[i][j];
       if (colscale) v *= colscale[gn];
@@ -142,6 +144,147 @@ int gemm(int64_t M, int64_t N, int64_t K, T alpha, const T* A, int64_t lda, int 
                               rowmap, accumulate, s);
   return launch_gemm<T, 16>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc,
                             rowmap, accumulate, s);
+}
+
+// ---------------------------------------------------------------------------
+// float32 tall-skinny GEMM, the throughput form used for >= 4k-row operator
+// applications: CTA tile 128 x 64, 256 threads of 8 x 4 outputs, 16-deep K
+// stages double-buffered in shared memory.  A rows and B rows arrive by
+// 16-byte cp.async when aligned (one instruction per 16 bytes, no register
+// staging); the split-sum A loader (asum > 1) and unaligned shapes go through
+// registers.  Same contract (colscale, alpha, accumulate, row scatter) as
+// gemm_kernel.  The per-thread 8 A values are broadcast loads (a warp spans
+// two row groups), the 4 B values one 16-byte load.
+constexpr int SBM = 128, SBN = 64, SBK = 16;
+constexpr int SAS = SBK + 4;      // A tile row stride (floats): 16-byte rows, rows on distinct banks
+constexpr int SBS = SBN + 4;      // B tile row stride
+
+__global__ void __launch_bounds__(256) gemm_ts_kernel(
+    int64_t M, int64_t N, int64_t K, float alpha, const float* __restrict__ A, int64_t lda,
+    int asum, int64_t astride, const float* __restrict__ B, int64_t ldb,
+    const float* __restrict__ colscale, float* __restrict__ C, int64_t ldc,
+    const int32_t* __restrict__ rowmap, int accumulate, int async_a, int async_b) {
+  __shared__ __align__(16) float As[2][SBM * SAS];
+  __shared__ __align__(16) float Bs[2][SBK * SBS];
+  const int tid = threadIdx.x;
+  const int tn = tid & 15, tm = tid >> 4;         // 16 column groups of 4, 16 row groups of 8
+  const int64_t m0 = (int64_t)blockIdx.y * SBM, n0 = (int64_t)blockIdx.x * SBN;
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  auto stage = [&](int64_t k0, int buf) {
+    // A: 128 rows x 4 chunks of 4 floats
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int e = tid + it * 256;
+      const int r = e >> 2, c = (e & 3) * 4;
+      const int64_t gm = m0 + r, gk = k0 + c;
+      float* dst = &As[buf][r * SAS + c];
+      if (async_a) {
+        const bool ok = gm < M && gk < K;         // K % 4 == 0: the chunk is in or out
+        cp_async16(dst, ok ? A + gm * lda + gk : A, ok);
+      } else {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (gm < M) {
+          const float* p = A + gm * lda;
+          for (int q = 0; q < asum; ++q)
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+              if (gk + h < K) v[h] += p[q * astride + gk + h];
+        }
+        *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+      }
+    }
+    // B: 16 rows x 16 chunks of 4 floats
+    {
+      const int e = tid;
+      const int r = e >> 4, c = (e & 15) * 4;
+      const int64_t gk = k0 + r, gn = n0 + c;
+      float* dst = &Bs[buf][r * SBS + c];
+      if (async_b) {
+        const bool ok = gk < K && gn < N;         // N % 4 == 0
+        cp_async16(dst, ok ? B + gk * ldb + gn : B, ok);
+      } else {
+        float v[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) v[h] = (gk < K && gn + h < N) ? B[gk * ldb + gn + h] : 0.f;
+        *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+      }
+    }
+    cp_async_commit();
+  };
+
+  const int nk = (int)((K + SBK - 1) / SBK);
+  stage(0, 0);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) {
+      stage((int64_t)(kt + 1) * SBK, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const float* a = &As[buf][(tm * 8) * SAS];
+    const float* b = &Bs[buf][tn * 4];
+#pragma unroll
+    for (int kk = 0; kk < SBK; ++kk) {
+      const float4 bv = *reinterpret_cast<const float4*>(b + kk * SBS);
+      float av[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) av[i] = a[i * SAS + kk];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        acc[i][0] = fmaf(av[i], bv.x, acc[i][0]);
+        acc[i][1] = fmaf(av[i], bv.y, acc[i][1]);
+        acc[i][2] = fmaf(av[i], bv.z, acc[i][2]);
+        acc[i][3] = fmaf(av[i], bv.w, acc[i][3]);
+      }
+    }
+    __syncthreads();
+  }
+  float cs[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t gn = n0 + tn * 4 + j;
+    cs[j] = (colscale && gn < N ? colscale[gn] : 1.f) * alpha;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t gm = m0 + tm * 8 + i;
+    if (gm >= M) continue;
+    const int64_t row = rowmap ? (int64_t)rowmap[gm] : gm;
+    if (row < 0) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gn = n0 + tn * 4 + j;
+      if (gn >= N) continue;
+      const float v = acc[i][j] * cs[j];
+      float* dst = C + row * ldc + gn;
+      *dst = accumulate ? *dst + v : v;
+    }
+  }
+}
+
+int gemm_ts(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda, int asum,
+            int64_t astride, const float* B, int64_t ldb, const float* colscale, float* C,
+            int64_t ldc, const int32_t* rowmap, int accumulate, cudaStream_t s) {
+  const int async_a = asum == 1 && K % 4 == 0 && lda % 4 == 0 &&
+                      (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  const int async_b = N % 4 == 0 && ldb % 4 == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+  const int64_t max_rows = (int64_t)65535 * SBM;
+  for (int64_t r0 = 0; r0 < M; r0 += max_rows) {
+    const int64_t mm = M - r0 < max_rows ? M - r0 : max_rows;
+    dim3 grid(ceil_div(N, SBN), ceil_div(mm, SBM));
+    gemm_ts_kernel<<<grid, 256, 0, s>>>(mm, N, K, alpha, A + r0 * lda, lda, asum, astride, B, ldb,
+                                       colscale, rowmap ? C : C + r0 * ldc, ldc,
+                                       rowmap ? rowmap + r0 : nullptr, accumulate, async_a,
+                                       async_b);
+  }
+  return launch_status();
 }
 
 // ---------------------------------------------------------------------------
@@ -372,6 +515,17 @@ int kifmm_scatter_rows_f64(const double* src, const int32_t* rows, int64_t n_row
 int kifmm_gemm_f32(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
                    int asum, int64_t astride, const float* B, int64_t ldb, const float* colscale,
                    float* C, int64_t ldc, const int32_t* rowmap, int accumulate, void* s) {
+  if (M < 0 || N < 0 || K < 0 || asum < 1) return KIFMM_EARG;
+  if (M == 0 || N == 0) return 0;
+  // tall shapes: the 128-row cp.async kernel (KIFMM_GEMM_TS=0: the SIMT tiles)
+  static int ts = -1;
+  if (ts < 0) {
+    const char* e = getenv("KIFMM_GEMM_TS");
+    ts = e ? atoi(e) : 1;
+  }
+  if (ts && M * ((N + SBN - 1) / SBN) >= 128 * 148)
+    return gemm_ts(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,
+                   accumulate, (cudaStream_t)s);
   return gemm<float>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,
                      accumulate, s);
 }
