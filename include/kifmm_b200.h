@@ -214,11 +214,11 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
  * [B_hi | B_lo] per vector, each packed [a/8][b/4][a%8][b%4] with one
  * K chunk of width kp (device.py pack_tmem_cores).  class_tv (8, 189) may
  * list each class's vectors in any order (device.py uses a locality order).
- * Persistent, one CTA per SM; with KIFMM_TMEM_CLUSTER=2 it runs as clusters
- * of 2 CTAs over pairs (n_pairs, 2) of same-class tile slots processed
- * together (the cores multicast to both; an odd class repeats its last slot,
- * device.py tile_pairs).
- * Output: acc[(tgt*nrhs + r)*(nsplit*ostride) + split*ostride + c], c < kp.
+ * Persistent, one CTA per SM over (rhs, tile, vector split) items; two
+ * loader/MMA groups per CTA take alternate vectors and write their partial
+ * sums to their own slots (pairs / n_pairs are accepted for ABI stability).
+ * Output: acc[(tgt*nrhs + r)*(2*nsplit*ostride) + (2*split + g)*ostride + c],
+ * g in {0, 1}, c < kp: the caller sums the 2*nsplit slots.
  * kp % 8 == 0, 8 <= kp <= 64, ostride >= kp, ostride % 4 == 0.  Replaces,
  * with m2l_sweep_tma, the bucket loop of m2l_blas.py:296-318. */
 int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int64_t h,

@@ -8,18 +8,15 @@
 // TMEM accumulator promoted into an IEEE fp32 accumulator every FLUSH_V
 // vectors.
 //
-// What changes is where A lives and how often the cores travel.  The TMA
-// sweep staged every (tile, vector) source block in shared memory as TF32 hi
-// and lo planes (2 x 128 x KP x 4 bytes written by TMA and read again by the
-// MMA) plus the core pair, and was bound by shared-memory bandwidth.  Here:
-//  * the source block arrives raw by TMA (128-byte swizzle) and every loader
-//    thread reads its own row (conflict-free through the swizzle), splits it
-//    into TF32 hi/lo in registers and stores both into TMEM with tcgen05.st
-//    (lane = row, column = K element); the MMA reads A from TMEM, so only
-//    the core pair B = [B_hi | B_lo] is read from shared memory;
-//  * each CTA works on TWO same-class tiles at once (groups 0 and 1, one tile
-//    each): every core pair is loaded once per CTA and vector and read by
-//    both groups' MMAs, halving the core bytes per tile and vector.
+// What changes is where A lives.  The TMA sweep staged every (tile, vector)
+// source block in shared memory as TF32 hi and lo planes (2 x 128 x KP x 4
+// bytes written by TMA and read again by the MMA) plus the core pair, and
+// was bound by shared-memory bandwidth.  Here the source block arrives raw by
+// TMA (columns 0..31 in a 128-byte-swizzled box, the remaining KP - 32 in an
+// exact-width box) and every loader thread reads its own row, splits it into
+// TF32 hi/lo in registers and stores both into TMEM with tcgen05.st (lane =
+// row, column = K element); the MMA reads A from TMEM, so only the core pair
+// B = [B_hi | B_lo] is read from shared memory.
 //
 // Per k-step (K = 8): D[:, 0:2KP] (+)= A_hi . [B_hi | B_lo]   (N = 2 KP)
 //                     D[:, 0:N2]  +=  A_lo . B_hi             (N2 = KP rounded up to 16;
@@ -27,13 +24,16 @@
 //   inside the B_lo half, which only adds the (tiny, correct) lo.lo term).
 // The promotion sums D[:, c] + D[:, KP + c] into the IEEE accumulator.
 //
-// Persistent: gridDim.x CTAs (one per SM) walk the work items (rhs, tile
-// pair, vector split) round-robin.  Roles (288 threads): warp 0 lane 0 loads
-// the stages (2 source blocks + 1 core pair per vector); warps 1..4 and 5..8
-// are the two groups: each loads, splits and stores its tile's source rows,
-// issues its own MMAs (one elected thread) into its own TMEM accumulator D_k,
-// promotes D_k into its registers every FLUSH_V vectors and writes the
-// tile's result rows at the end of an item.
+// Persistent: gridDim.x CTAs (one per SM) walk the work items (rhs, tile,
+// vector split) round-robin through a ring of NS stages (source block + core
+// pair, 53 KB at KP = 56).  Roles (288 threads): warp 0 lane 0 loads the
+// stages; warps 1..4 and 5..8 are two groups taking alternate vectors: each
+// loads, splits and stores its source rows into its own TMEM A buffer,
+// issues its own MMAs (one elected thread) into its own TMEM accumulator,
+// promotes it into registers every FLUSH_V of its vectors and writes its
+// partial result to its own output slot (2 * split + group).  Groups never
+// share a TMEM accumulator, so no MMA ordering between issuing threads is
+// needed.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -46,7 +46,7 @@ using namespace kifmm;
 namespace {
 
 constexpr int TMT = 128;
-constexpr int NG = 2;             // groups = tiles per CTA, each with its own TMEM A and D
+constexpr int NG = 2;             // groups per CTA (alternate vectors), each with its own TMEM A and D
 constexpr int NTHREADS = 32 + 128 * NG;
 constexpr int FLUSH_V = 8;        // vectors between promotions of a TMEM accumulator
 constexpr int BX = 4, BY = 4, BZ = 8;
@@ -140,7 +140,7 @@ struct TmemArgs {
   const int32_t* pairs;            // (n_pairs, 2) same-class tile slots handled by one CTA
   const int32_t* class_tv;         // (8, 189) vector order per target class
   const int8_t* offsets;           // (316, 3)
-  int n_pairs, nrhs, nsplit, jper, n_items, ns;
+  int n_tiles, n_pairs, nrhs, nsplit, jper, n_items, ns;
   int64_t ostride, ld;             // output: acc[(tgt*R + r)*ld + split*ostride + c]
   float* acc_out;
 };
@@ -155,18 +155,17 @@ constexpr int TRACE_N = 1024;
     if (trace_buf != nullptr && (i) < TRACE_N) trace_buf[(ev) * TRACE_N + (i)] = clock64(); \
   } while (0)
 
-// Work item it -> (r, tile pair, split): vectors [j0, j0 + nv) of the class
-// list.  A class with an odd tile count repeats its last slot in its last
-// pair: both groups then compute and write the same rows.
+// Work item it -> (r, tile slot, split): vectors [j0, j0 + nv) of the
+// class list.
 struct Item {
-  int pair, r, split, j0, nv;
+  int slot, r, split, j0, nv;
 };
 __device__ __forceinline__ Item item_of(const TmemArgs& a, int it) {
   Item x;
   x.split = it % a.nsplit;
   const int rest = it / a.nsplit;
-  x.pair = rest % a.n_pairs;
-  x.r = rest / a.n_pairs;
+  x.slot = rest % a.n_tiles;
+  x.r = rest / a.n_tiles;
   x.j0 = x.split * a.jper;
   x.nv = max(0, min(189, x.j0 + a.jper) - x.j0);
   return x;
@@ -192,13 +191,18 @@ __device__ __forceinline__ TileGeom tile_geom(const TmemArgs& a, int slot) {
 
 template <int KP>
 __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
-    const __grid_constant__ CUtensorMap tm, const TmemArgs a) {
+    const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm2,
+    const TmemArgs a) {
   constexpr int N1 = 2 * KP;
   constexpr int N2 = (KP + 15) / 16 * 16;
-  constexpr int NCH = (KP + 31) / 32;                                  // TMA boxes per block
-  constexpr uint32_t ABYTES = NCH * TMT * 128u;                        // one source block
+  // source block: columns [0, 32) in a 128-byte-swizzled box, the rest
+  // (KP - 32 columns) in a second box, swizzled when it is 32 wide and
+  // linear (rows of (KP - 32) * 4 bytes, exact width) otherwise
+  constexpr int W1 = KP > 32 ? KP - 32 : 0;
+  constexpr bool SW1 = W1 == 32;
+  constexpr uint32_t ABYTES = TMT * 128u + TMT * W1 * 4u;              // one source block
   constexpr uint32_t BBYTES = 2u * KP * KP * 4u;                       // one core pair
-  constexpr uint32_t SBYTES = (NG * ABYTES + BBYTES + 1023u) / 1024u * 1024u;
+  constexpr uint32_t SBYTES = (ABYTES + BBYTES + 1023u) / 1024u * 1024u;
   // TMEM per group k: D_k (N1 columns) then A_k = [hi | lo] (2 KP columns)
   constexpr int GCOLS = N1 + 2 * KP;
   constexpr int NEED = NG * GCOLS;
@@ -214,18 +218,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
   const int ns = a.ns;
   long long* const trace_buf = (blockIdx.x == 0 && g_trace_h == a.h) ? g_trace : nullptr;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * SBYTES);
-  uint64_t* empty = full + ns;          // both groups' MMAs have read the stage
+  uint64_t* empty = full + ns;          // the consuming group's MMAs have read the stage
   uint64_t* done = empty + ns;          // [NG]: group k's MMAs of its last vector completed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + NG);
 
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NG);
+      mbar_init(&empty[s], 1);
     }
     for (int k = 0; k < NG; ++k) mbar_init(&done[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+    if (W1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2)) : "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -239,37 +244,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------- producer: both tiles' source blocks + the core pair
+    // ------------------------------ producer: source block + core pair
     if (lane == 0) {
       int g = 0;
       for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
         const Item x = item_of(a, it);
-        TileGeom tg[NG];
-#pragma unroll
-        for (int k = 0; k < NG; ++k) tg[k] = tile_geom(a, a.pairs[NG * x.pair + k]);
-        const int32_t* tv = a.class_tv + tg[0].cls * 189 + x.j0;
+        const TileGeom tg = tile_geom(a, x.slot);
+        const int32_t* tv = a.class_tv + tg.cls * 189 + x.j0;
         for (int v = 0; v < x.nv; ++v, ++g) {
           const int s = g % ns;
           if (g >= ns) mbar_wait(&empty[s], ((g / ns) - 1) & 1, false);
           trace(4, g);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                            smem_u32(&full[s])),
-                       "r"(NG * ABYTES + BBYTES)
+                       "r"(ABYTES + BBYTES)
                        : "memory");
           const int t = tv[v];
           unsigned char* sb = smem + s * SBYTES;
           const int ox = a.offsets[3 * t], oy = a.offsets[3 * t + 1], oz = a.offsets[3 * t + 2];
-#pragma unroll
-          for (int k = 0; k < NG; ++k) {
-            const int qx = tg[k].px + ox, qy = tg[k].py + oy, qz = tg[k].pz + oz;
-            const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
-#pragma unroll
-            for (int c = 0; c < NCH; ++c)
-              tma_load_5d(sb + k * ABYTES + c * TMT * 128, &tm, c * 32, tg[k].iz0 + (qz >> 1),
-                          tg[k].iy0 + (qy >> 1), tg[k].ix0 + (qx >> 1), sp * a.nrhs + x.r,
-                          &full[s]);
-          }
-          bulk_copy(sb + NG * ABYTES, a.bpair + (int64_t)t * (2 * KP * KP), BBYTES, &full[s]);
+          const int qx = tg.px + ox, qy = tg.py + oy, qz = tg.pz + oz;
+          const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
+          const int cz = tg.iz0 + (qz >> 1), cy = tg.iy0 + (qy >> 1), cx = tg.ix0 + (qx >> 1);
+          tma_load_5d(sb, &tm, 0, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
+          if (W1) tma_load_5d(sb + TMT * 128, &tm2, 32, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
+          bulk_copy(sb + ABYTES, a.bpair + (int64_t)t * (2 * KP * KP), BBYTES, &full[s]);
         }
       }
       // drain: the MMA commits on the stages arrive asynchronously; wait for
@@ -279,7 +277,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
     }
     __syncwarp();
   } else if (warp >= 1 && warp < 1 + 4 * NG) {
-    // --------------------- group k = tile k of the pair: load, issue, promote
+    // ------- group k: the vectors v = k (mod 2) of each item; load, issue,
+    // promote into its own TMEM accumulator and registers, write its partial
+    // result to split slot 2 * split + k
     const int grp = (warp - 1) >> 2;
     const int q4 = warp & 3;                       // TMEM lane quarter of this warp
     const int m = q4 * 32 + lane;                  // tile row = TMEM lane
@@ -299,20 +299,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
       const Item x = item_of(a, it);
 #pragma unroll
       for (int c = 0; c < KP; ++c) acc[c] = 0.f;
-      for (int v = 0; v < x.nv; ++v, ++g) {
-        const int s = g % ns;
-        const int local = v % FLUSH_V;
-        mbar_wait(&full[s], (g / ns) & 1, false);
-        if (m == 0) trace(grp == 0 ? 0 : 5, g);
+      int local = 0;                               // position in the group's current block
+      for (int v = grp; v < x.nv; v += NG) {
+        const int gg = g + v;
+        const int s = gg % ns;
+        mbar_wait(&full[s], (gg / ns) & 1, false);
+        if (m == 0) trace(grp == 0 ? 0 : 5, gg);
         // this thread's source row -> TF32 hi (round-to-nearest-away on the bit
         // pattern) and lo = x - hi (exact in fp32; enters the MMA truncated to
         // TF32), in registers before waiting for the TMEM buffers
         uint32_t hv[KP], lv[KP];
-        const unsigned char* sb = smem + s * SBYTES + grp * ABYTES + m * 128;
+        const unsigned char* sb = smem + s * SBYTES;
 #pragma unroll
         for (int i = 0; i < KP / 4; ++i) {
-          const float4 c4 = *reinterpret_cast<const float4*>(sb + (i >> 3) * (TMT * 128) +
-                                                              (((i & 7) ^ (m & 7)) << 4));
+          const unsigned char* src;
+          if (i < 8)
+            src = sb + m * 128 + (((i & 7) ^ (m & 7)) << 4);
+          else if (SW1)
+            src = sb + TMT * 128 + m * 128 + (((i & 7) ^ (m & 7)) << 4);
+          else
+            src = sb + TMT * 128 + m * (W1 * 4) + (i - 8) * 16;
+          const float4 c4 = *reinterpret_cast<const float4*>(src);
           const float f[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -322,7 +329,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
         }
         // this group's previous MMAs done: A_k reusable (and D_k promoted below)
         if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);
-        if (m == 0) trace(grp == 0 ? 1 : 6, g);
+        if (m == 0) trace(grp == 0 ? 1 : 6, gg);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int c = 0; c < KP / 8; ++c) {
@@ -334,8 +341,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
         asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
         if (issuer) {
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (grp == 0) trace(3, g);
-          const uint32_t bb = smem_u32(smem + s * SBYTES + NG * ABYTES);
+          if (grp == 0) trace(3, gg);
+          const uint32_t bb = smem_u32(smem + s * SBYTES + ABYTES);
 #pragma unroll
           for (int ks = 0; ks < KP / 8; ++ks) {
             const uint64_t db = desc_nosw(bb + ks * 256, 128, SBO);
@@ -347,7 +354,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
         }
         __syncwarp();
         ++nmine;
-        if (local == FLUSH_V - 1 || v == x.nv - 1) {
+        const bool last_of_block = local == FLUSH_V - 1 || v + NG >= x.nv;
+        local = last_of_block ? 0 : local + 1;
+        if (last_of_block) {
           // promote D_k: wait for this block's last MMAs, add into registers;
           // the next vector's MMA overwrites D_k only after the group barrier
           mbar_wait(&done[grp], (nmine - 1) & 1, false);
@@ -365,14 +374,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         }
       }
-      const int slot = a.pairs[NG * x.pair + grp];
-      const int32_t tgt = a.tile_targets[(int64_t)slot * TMT + m];
+      const int32_t tgt = a.tile_targets[(int64_t)x.slot * TMT + m];
       if (tgt >= 0) {
-        float* o = a.acc_out + ((int64_t)tgt * a.nrhs + x.r) * a.ld + (int64_t)x.split * a.ostride;
+        float* o = a.acc_out + ((int64_t)tgt * a.nrhs + x.r) * a.ld +
+                   (int64_t)(NG * x.split + grp) * a.ostride;
 #pragma unroll
         for (int c = 0; c < KP; c += 4)
           *reinterpret_cast<float4*>(o + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
       }
+      g += x.nv;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -412,18 +422,21 @@ EncodeFn encoder() {
 }
 
 // 5-D map over the dense sub-lattice array (k, iz, iy, ix, p*R + r); boxes of
-// 32 k x (8, 4, 4) boxes x 1 plane, 128-byte swizzle, out-of-range -> zeros.
-int make_map(CUtensorMap* tm, const float* base, int kp, int h, int64_t planes) {
+// `width` k x (8, 4, 4) boxes x 1 plane, 128-byte swizzle or linear rows,
+// out-of-range -> zeros.
+int make_map(CUtensorMap* tm, const float* base, int kp, int h, int64_t planes, int width,
+             bool swizzle) {
   EncodeFn enc = encoder();
   if (!enc) return KIFMM_EARG;
   cuuint64_t dims[5] = {(cuuint64_t)kp, (cuuint64_t)h, (cuuint64_t)h, (cuuint64_t)h,
                         (cuuint64_t)planes};
   const cuuint64_t row = (cuuint64_t)kp * 4;
   cuuint64_t strides[4] = {row, row * h, row * h * h, row * h * h * h};
-  cuuint32_t box[5] = {32, BZ, BY, BX, 1};
+  cuuint32_t box[5] = {(cuuint32_t)width, BZ, BY, BX, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult res = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS ? 0 : KIFMM_EARG;
 }
@@ -431,25 +444,28 @@ int make_map(CUtensorMap* tm, const float* base, int kp, int h, int64_t planes) 
 template <int KP>
 int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   TmemArgs a = a0;
-  CUtensorMap tm;
+  constexpr int W1 = KP > 32 ? KP - 32 : 0;
+  CUtensorMap tm, tm2;
   memset(&tm, 0, sizeof(tm));
-  int st = make_map(&tm, a.q, KP, a.h, 8 * (int64_t)a.nrhs);
+  memset(&tm2, 0, sizeof(tm2));
+  int st = make_map(&tm, a.q, KP, a.h, 8 * (int64_t)a.nrhs, 32, true);
+  if (!st && W1) st = make_map(&tm2, a.q, KP, a.h, 8 * (int64_t)a.nrhs, W1, W1 == 32);
   if (st) return st;
   static int ns_env = -1;
   if (ns_env < 0) {
     const char* e = getenv("KIFMM_TMEM_STAGES");
-    ns_env = e ? atoi(e) : 4;
+    ns_env = e ? atoi(e) : 4;             // config 2 on B200: 4 ~ 3 stages (281-288 us), 2: 362 us
     if (ns_env < 2) ns_env = 2;
   }
-  const size_t sbytes =
-      ((size_t)NG * ((KP + 31) / 32) * TMT * 128 + 2ull * KP * KP * 4 + 1023) / 1024 * 1024;
+  const size_t sbytes = ((size_t)TMT * 128 + (size_t)TMT * W1 * 4 + 2ull * KP * KP * 4 + 1023) /
+                        1024 * 1024;
   int ns = ns_env;
   while (ns > 2 && 1024 + ns * sbytes + 256 > 227 * 1024) --ns;
   a.ns = ns;
   const size_t smem = 1024 + ns * sbytes + (2 * ns + NG) * 8 + 16;
   const int grid = a.n_items < sm_count() ? a.n_items : sm_count();
   set_max_smem((const void*)m2l_sweep_tmem_kernel<KP>, smem);
-  m2l_sweep_tmem_kernel<KP><<<grid, NTHREADS, smem, stream>>>(tm, a);
+  m2l_sweep_tmem_kernel<KP><<<grid, NTHREADS, smem, stream>>>(tm, tm2, a);
   return launch_status();
 }
 
@@ -466,7 +482,7 @@ int kifmm_m2l_sweep_tmem_trace(long long* buf, int64_t h) {
   return e == cudaSuccess ? 0 : (int)e;
 }
 
-// Split of the 189-vector range (work items = R * n_pairs * nsplit) that
+// Split of the 189-vector range (work items = R * n_tiles * nsplit) that
 // balances the persistent CTAs: the best whole-wave fill, discounted by the
 // per-item fixed cost (pipeline fill, result write).
 int kifmm_m2l_sweep_tmem_splits(int64_t n_tiles, int64_t n_pairs, int64_t nrhs,
@@ -478,7 +494,7 @@ int kifmm_m2l_sweep_tmem_splits(int64_t n_tiles, int64_t n_pairs, int64_t nrhs,
   for (int s = 1; s <= 16; ++s) {
     const int jper = (189 + s - 1) / s;
     if ((s - 1) * jper >= 189) continue;           // would leave an empty piece
-    const double items = (double)n_pairs * nrhs * s;
+    const double items = (double)n_tiles * nrhs * s;
     const double waves = items / g;
     const double eff = waves / ((int64_t)(waves + 0.999999));
     const double cost = eff / (1.0 + 0.02 * s);
@@ -516,9 +532,10 @@ int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int
   a.nrhs = (int)nrhs;
   a.nsplit = (int)nsplit;
   a.jper = (int)((189 + nsplit - 1) / nsplit);
-  a.n_items = (int)(nrhs * n_pairs * nsplit);
+  a.n_tiles = (int)n_tiles;
+  a.n_items = (int)(nrhs * n_tiles * nsplit);
   a.ostride = ostride;
-  a.ld = nsplit * ostride;
+  a.ld = NG * nsplit * ostride;             // each group writes its own slot per split
   a.acc_out = acc;
   a.ns = 2;
   cudaStream_t s = (cudaStream_t)stream;
