@@ -327,16 +327,24 @@ __device__ __forceinline__ void fma2_acc(u64& acc, u64 a, u64 b) {
 // accumulators alternate so consecutive sources do not serialise on one
 // FFMA2 chain.
 __device__ __forceinline__ void quad_sum(const float4* buf, int ns, int guard_n, int start,
-                                         int stride, u64 X, u64 Y, u64 Z, u64& acc) {
-  u64 acc2 = pk2(0.f, 0.f);
-  auto body = [&](int j, u64& a_, auto guard) {
+                                         int stride, u64 X64, u64 Y64, u64 Z64, u64& acc64) {
+  // float2 intrinsics (FADD2/FMUL2/FFMA2): the compiler keeps the packed
+  // accumulators in place (no register moves per interaction)
+  const float2 X = up2(X64), Y = up2(Y64), Z = up2(Z64);
+  float2 acc = up2(acc64), acc2 = make_float2(0.f, 0.f);
+  auto body = [&](int j, float2& a_, auto guard) {
     constexpr bool G = decltype(guard)::value;
     const float4 s = buf[j];                         // (x, y, z, q)
-    const u64 dx = sub2(X, pk2(s.x, s.x));
-    const u64 dy = sub2(Y, pk2(s.y, s.y));
-    const u64 dz = sub2(Z, pk2(s.z, s.z));
-    const u64 r2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
-    fma2_acc(a_, rsq2<G>(r2), pk2(s.w, s.w));
+    const float2 dx = __fadd2_rn(X, make_float2(-s.x, -s.x));
+    const float2 dy = __fadd2_rn(Y, make_float2(-s.y, -s.y));
+    const float2 dz = __fadd2_rn(Z, make_float2(-s.z, -s.z));
+    const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+    float w0 = real_traits<float>::rsq(r2.x), w1 = real_traits<float>::rsq(r2.y);
+    if (G) {
+      w0 = r2.x > 0.f ? w0 : 0.f;
+      w1 = r2.y > 0.f ? w1 : 0.f;
+    }
+    a_ = __ffma2_rn(make_float2(w0, w1), make_float2(s.w, s.w), a_);
   };
   int j = start;
   for (; j < guard_n && j < ns; j += stride) body(j, acc, std::true_type{});
@@ -347,8 +355,7 @@ __device__ __forceinline__ void quad_sum(const float4* buf, int ns, int guard_n,
     body(j + 3 * stride, acc2, std::false_type{});
   }
   for (; j < ns; j += stride) body(j, acc, std::false_type{});
-  const float2 u = up2(acc), v = up2(acc2);
-  acc = pk2(u.x + v.x, u.y + v.y);
+  acc64 = pk2(acc.x + acc2.x, acc.y + acc2.y);
 }
 
 __global__ void __launch_bounds__(32 * kWarps, KIFMM_LEAF_MINB) leaf_pass_x2_kernel(

@@ -48,7 +48,10 @@ namespace {
 constexpr int TMT = 128;
 constexpr int NG = 2;             // groups per CTA (alternate vectors), each with its own TMEM A and D
 constexpr int NTHREADS = 32 + 128 * NG;
-constexpr int FLUSH_V = 8;        // vectors between promotions of a TMEM accumulator
+#ifndef KIFMM_TMEM_FLUSH
+#define KIFMM_TMEM_FLUSH 8
+#endif
+constexpr int FLUSH_V = KIFMM_TMEM_FLUSH;   // vectors between promotions of a TMEM accumulator
 constexpr int BX = 4, BY = 4, BZ = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
