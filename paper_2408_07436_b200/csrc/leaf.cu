@@ -473,6 +473,68 @@ __global__ void __launch_bounds__(32 * kWarps, KIFMM_LEAF_MINB) leaf_pass_x2_ker
   }
 }
 
+// L2P only (the final pass of the overlapped evaluate, after the P2P ran
+// early): the same packed-FP32 target mapping as leaf_pass_x2_kernel without
+// the near-field machinery, 8 warps per CTA and 0.9 KB of shared memory per
+// warp, so many leaves are in flight at once (the pass is latency-bound:
+// ~56 interactions per target).
+constexpr int kL2pWarps = 8;
+__global__ void __launch_bounds__(32 * kL2pWarps) l2p_x2_kernel(
+    const float* __restrict__ tx, const float* __restrict__ ty, const float* __restrict__ tz,
+    const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
+    const double* __restrict__ centers, const double* __restrict__ base, int ne,
+    const float* __restrict__ local, int64_t nrhs, const int64_t* __restrict__ perm,
+    int accumulate, float* __restrict__ out) {
+  extern __shared__ __align__(16) float4 l2p_buf[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float4* buf = l2p_buf + w * ne;
+  const int64_t b = (int64_t)blockIdx.x * kL2pWarps + w;
+  if (b >= n_tleaves) return;
+  const int64_t t0 = tstart[b];
+  const int tc = tcount[b];
+  const double cx = centers[b * 3], cy = centers[b * 3 + 1], cz = centers[b * 3 + 2];
+  for (int tb = 0; tb < tc; tb += 32) {
+    const int n = min(32, tc - tb);
+    const int h = (n + 1) >> 1;
+    const int R = h <= 1 ? 1 : 1 << (32 - __clz(h - 1));
+    const int f = 32 / R, sub = lane / R;
+    const int ti = lane % R;
+    const bool live0 = ti < n, live1 = ti + R < n;
+    const int64_t ia = t0 + tb + (live0 ? ti : 0), ib = t0 + tb + (live1 ? ti + R : 0);
+    const u64 X = pk2(tx[ia], tx[ib]), Y = pk2(ty[ia], ty[ib]), Z = pk2(tz[ia], tz[ib]);
+    for (int64_t r = 0; r < nrhs; ++r) {
+      const float* loc = local + (b * nrhs + r) * ne;
+      __syncwarp();
+      for (int k = lane; k < ne; k += 32)
+        buf[k] = make_float4(real_traits<float>::from_d(exact_add(cx, base[k * 3])),
+                             real_traits<float>::from_d(exact_add(cy, base[k * 3 + 1])),
+                             real_traits<float>::from_d(exact_add(cz, base[k * 3 + 2])), loc[k]);
+      __syncwarp();
+      u64 acc = pk2(0.f, 0.f);
+      quad_sum(buf, ne, 0, sub, f, X, Y, Z, acc);
+      const float2 av = up2(acc);
+      float fa = av.x, fb = av.y;
+      for (int off = R; off < 32; off <<= 1) {
+        fa += __shfl_xor_sync(0xffffffffu, fa, off);
+        fb += __shfl_xor_sync(0xffffffffu, fb, off);
+      }
+      const float c = real_traits<float>::inv4pi();
+      if (sub == 0) {
+        if (live0) {
+          const int64_t i = t0 + tb + ti;
+          float* o = out + (perm ? perm[i] : i) * nrhs + r;
+          *o = accumulate ? *o + fa * c : fa * c;
+        }
+        if (live1) {
+          const int64_t i = t0 + tb + ti + R;
+          float* o = out + (perm ? perm[i] : i) * nrhs + r;
+          *o = accumulate ? *o + fb * c : fb * c;
+        }
+      }
+    }
+  }
+}
+
 // AoS source records for the leaf pass: out[r*ns + j] = (x_j, y_j, z_j, q[j*nrhs + r]).
 template <typename T>
 __global__ void pack_sources_kernel(const T* __restrict__ sx, const T* __restrict__ sy,
@@ -505,6 +567,13 @@ int leaf_pass(const T* tx, const T* ty, const T* tz, const int32_t* ts, const in
   if (ntl == 0) return 0;
   const auto* s4 = reinterpret_cast<const typename vec4<T>::v*>(src4);
   if constexpr (sizeof(T) == 4) {
+    if (!grad && !(parts & 2) && ne <= 256) {
+      const size_t smem = (size_t)kL2pWarps * ne * sizeof(float4);
+      l2p_x2_kernel<<<ceil_div(ntl, kL2pWarps), 32 * kL2pWarps, smem, (cudaStream_t)stream>>>(
+          tx, ty, tz, ts, tcnt, ntl, centers, base, (int)ne, local, nrhs, perm, (parts & 4) != 0,
+          out);
+      return launch_status();
+    }
     if (!grad) {
       leaf_pass_x2_kernel<<<ceil_div(ntl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
           tx, ty, tz, ts, tcnt, ntl, centers, base, ne, local, s4, ns, ss, sc, no, nlf, nrhs,
