@@ -28,16 +28,15 @@ torch.cuda.synchronize()
 nat.call("kifmm_m2l_sweep_tmem_trace", None, 0)
 t = buf.cpu().numpy().reshape(12, 1024).astype(np.float64)
 t0 = t[t > 0].min()
-names = ["have_A", "buf_free", "issued", "mma_issue", "stage_free", "promo_start", "promo_end", "x7", "x8", "x9", "x10", "x11"]
-n = int((t[3] > 0).sum())
-print("vectors traced", n)
+names = {0: "g0_have_A", 1: "g0_buf_free", 3: "g0_issue", 4: "stage_free", 5: "g1_have_A", 6: "g1_buf_free"}
 rel = np.where(t > 0, t - t0, np.nan)
-for g in list(range(0, 24)) + list(range(n - 8, n)):
-    print(g, " ".join(f"{names[e]}={rel[e][g]:9.0f}" for e in (0, 1, 3, 2, 4)))
-for bc in range(0, 8):
-    print("block", bc, f"start={rel[5][bc]:9.0f} end={rel[6][bc]:9.0f}")
-d = np.diff(rel[3][:n])
-d = np.diff(rel[3][:n])
-print("mma issue interval: median %.0f mean %.0f clk" % (np.nanmedian(d), np.nanmean(d)))
-print("have_A -> buf_free median %.0f; buf_free -> mma_issue median %.0f; mma_issue -> issued %.0f" % (
-    np.nanmedian(rel[1][:n] - rel[0][:n]), np.nanmedian(rel[3][:n] - rel[1][:n]), np.nanmedian(rel[2][:n] - rel[3][:n])))
+n = int(np.nanmax(np.where(t[4] > 0, np.arange(1024), -1))) + 1
+print("vectors traced", n)
+for g in list(range(0, 20)) + list(range(n - 6, n)):
+    print(g, " ".join(f"{names[e]}={rel[e][g]:9.0f}" for e in (4, 0, 1, 3, 5, 6)))
+iss = rel[3][:n]
+iss = iss[~np.isnan(iss)]
+print("group-0 issue interval: median %.0f clk (2 vectors per interval)" % np.median(np.diff(iss)))
+a0, f0 = rel[0][:n], rel[1][:n]
+print("g0 have_A -> buf_free median %.0f; buf_free -> issue median %.0f; stage_free -> have_A median %.0f" % (
+    np.nanmedian(f0 - a0), np.nanmedian(rel[3][:n] - f0), np.nanmedian(a0 - rel[4][:n])))
