@@ -535,6 +535,64 @@ __global__ void __launch_bounds__(32 * kL2pWarps) l2p_x2_kernel(
   }
 }
 
+// float32 P2M check potentials on packed FP32: every lane evaluates two
+// check points (c, c + 32) of its leaf against the leaf's sources, staged
+// once per warp (one 16-byte shared load feeds two interactions).
+__global__ void __launch_bounds__(32 * kWarps) p2m_check_x2_kernel(
+    const float* __restrict__ sx, const float* __restrict__ sy, const float* __restrict__ sz,
+    const float* __restrict__ q, int64_t nrhs, const int32_t* __restrict__ leaf_start,
+    const int32_t* __restrict__ leaf_count, int64_t n_leaves, const double* __restrict__ centers,
+    const double* __restrict__ base, int64_t nc, float* __restrict__ phi) {
+  __shared__ __align__(16) float4 buf[kWarps][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t leaf = (int64_t)blockIdx.x * kWarps + w;
+  if (leaf >= n_leaves) return;
+  const int64_t s0 = leaf_start[leaf];
+  const int cnt = leaf_count[leaf];
+  const double cx = centers[leaf * 3], cy = centers[leaf * 3 + 1], cz = centers[leaf * 3 + 2];
+  for (int64_t c0 = 0; c0 < nc; c0 += 64) {
+    const int64_t ca = c0 + lane, cb = c0 + 32 + lane;
+    auto pt = [&](int64_t c, double o, int d) {
+      return c < nc ? real_traits<float>::from_d(exact_add(o, base[c * 3 + d])) : 0.f;
+    };
+    const float2 X = make_float2(pt(ca, cx, 0), pt(cb, cx, 0));
+    const float2 Y = make_float2(pt(ca, cy, 1), pt(cb, cy, 1));
+    const float2 Z = make_float2(pt(ca, cz, 2), pt(cb, cz, 2));
+    for (int64_t r = 0; r < nrhs; ++r) {
+      float2 acc = make_float2(0.f, 0.f), acc2 = make_float2(0.f, 0.f);
+      for (int j0 = 0; j0 < cnt; j0 += 64) {
+        const int m = min(64, cnt - j0);
+        __syncwarp();
+        for (int k = lane; k < m; k += 32) {
+          const int64_t j = s0 + j0 + k;
+          buf[w][k] = make_float4(sx[j], sy[j], sz[j], q[j * nrhs + r]);
+        }
+        __syncwarp();
+        auto body = [&](int k, float2& a_) {
+          const float4 v = buf[w][k];
+          const float2 dx = __fadd2_rn(X, make_float2(-v.x, -v.x));
+          const float2 dy = __fadd2_rn(Y, make_float2(-v.y, -v.y));
+          const float2 dz = __fadd2_rn(Z, make_float2(-v.z, -v.z));
+          const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+          float w0 = real_traits<float>::rsq(r2.x), w1 = real_traits<float>::rsq(r2.y);
+          w0 = r2.x > 0.f ? w0 : 0.f;
+          w1 = r2.y > 0.f ? w1 : 0.f;
+          a_ = __ffma2_rn(make_float2(w0, w1), make_float2(v.w, v.w), a_);
+        };
+        int k = 0;
+        for (; k + 1 < m; k += 2) {
+          body(k, acc);
+          body(k + 1, acc2);
+        }
+        if (k < m) body(k, acc);
+      }
+      const float c = real_traits<float>::inv4pi();
+      if (ca < nc) phi[(leaf * nrhs + r) * nc + ca] = (acc.x + acc2.x) * c;
+      if (cb < nc) phi[(leaf * nrhs + r) * nc + cb] = (acc.y + acc2.y) * c;
+    }
+  }
+}
+
 // AoS source records for the leaf pass: out[r*ns + j] = (x_j, y_j, z_j, q[j*nrhs + r]).
 template <typename T>
 __global__ void pack_sources_kernel(const T* __restrict__ sx, const T* __restrict__ sy,
@@ -552,6 +610,11 @@ int p2m_check(const T* sx, const T* sy, const T* sz, const T* q, int64_t nrhs, c
               T* phi, void* stream) {
   if (nl < 0 || nc < 1 || nrhs < 1) return KIFMM_EARG;
   if (nl == 0) return 0;
+  if constexpr (sizeof(T) == 4) {
+    p2m_check_x2_kernel<<<ceil_div(nl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
+        sx, sy, sz, q, nrhs, ls, lc, nl, centers, base, nc, phi);
+    return launch_status();
+  }
   p2m_check_kernel<T><<<ceil_div(nl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
       sx, sy, sz, q, nrhs, ls, lc, nl, centers, base, nc, phi);
   return launch_status();

@@ -338,6 +338,20 @@ def tma_level_plan(src_codes, tgt_codes, level):
                 pairs=to_dev(pairs, np.int32), n_pairs=int(pairs.shape[0]))
 
 
+def dense_rowmap(plan, nrhs):
+    """Row map of the projection GEMM into the dense sub-lattice array: row
+    (box b, rhs r) -> ((p * R + r) * h^3 + cell), p, cell from src_slot[b]."""
+    key = ("dense_rowmap", nrhs)
+    if key not in plan:
+        h3 = plan["h"] ** 3
+        slot = plan["src_slot"].long()
+        p, cell = slot // h3, slot % h3
+        r = torch.arange(nrhs, device=slot.device)
+        rm = (p[:, None] * nrhs + r[None, :]) * h3 + cell[:, None]
+        plan[key] = rm.reshape(-1).to(torch.int32).contiguous()
+    return plan[key]
+
+
 def tile_pairs(tile_ids: np.ndarray, per_class: int) -> np.ndarray:
     """(n_pairs, 2) slots of same-class tiles processed by one CTA pair of the
     tensor-memory sweep (consecutive slots of a class; an odd class repeats
@@ -459,10 +473,10 @@ class BlasDevice:
             # the tensor-memory sweep writes two partial slots per vector split
             # (its two vector-interleaved groups); the epilogue sums them all
             nsplit = self.tmem_splits(plan["n_tiles"], plan["n_pairs"], nrhs)
-            la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt,
-                    self.kin)
-            launch("kifmm_dense_split_tf32", P(qt), P(plan["src_slot"]), n_s, nrhs, self.kin,
-                   plan["h"], P(dense[0]), None, stream_handle())
+            # projection q~ = M S written straight into the dense parity
+            # sub-lattice array (row map (box, rhs) -> plane p*R + r, cell)
+            la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin,
+                    dense[0], self.kin, rowmap=dense_rowmap(plan, nrhs))
             launch("kifmm_m2l_sweep_tmem_f32", P(dense[0]), P(self.Bpair), self.kin, plan["h"],
                    P(plan["tile_targets"]), P(plan["tile_ids"]), plan["n_tiles"],
                    P(plan["pairs"]), plan["n_pairs"], P(self.class_tv_local), P(self.offsets),
