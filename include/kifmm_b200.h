@@ -215,10 +215,10 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
  * K chunk of width kp (device.py pack_tmem_cores).  class_tv (8, 189) may
  * list each class's vectors in any order (device.py uses a locality order).
  * Persistent, one CTA per SM over (rhs, tile, vector split) items; two
- * loader/MMA groups per CTA take alternate vectors and write their partial
- * sums to their own slots (pairs / n_pairs are accepted for ABI stability).
- * Output: acc[(tgt*nrhs + r)*(2*nsplit*ostride) + (2*split + g)*ostride + c],
- * g in {0, 1}, c < kp: the caller sums the 2*nsplit slots.
+ * loader/MMA groups per CTA take alternate vectors (pairs / n_pairs are
+ * accepted for ABI stability).
+ * Output: acc[(tgt*nrhs + r)*(nsplit*ostride) + split*ostride + c], c < kp:
+ * the caller sums the nsplit slots.
  * kp % 8 == 0, 8 <= kp <= 64, ostride >= kp, ostride % 4 == 0.  Replaces,
  * with m2l_sweep_tma, the bucket loop of m2l_blas.py:296-318. */
 int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int64_t h,

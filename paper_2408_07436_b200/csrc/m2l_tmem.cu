@@ -30,10 +30,10 @@
 // stages; warps 1..4 and 5..8 are two groups taking alternate vectors: each
 // loads, splits and stores its source rows into its own TMEM A buffer,
 // issues its own MMAs (one elected thread) into its own TMEM accumulator,
-// promotes it into registers every FLUSH_V of its vectors and writes its
-// partial result to its own output slot (2 * split + group).  Groups never
-// share a TMEM accumulator, so no MMA ordering between issuing threads is
-// needed.
+// promotes it into registers every FLUSH_V of its vectors; at the end of an
+// item the two partial sums are combined through shared memory and group 0
+// writes the result.  Groups never share a TMEM accumulator, so no MMA
+// ordering between issuing threads is needed.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * SBYTES);
   uint64_t* empty = full + ns;          // the consuming group's MMAs have read the stage
   uint64_t* done = empty + ns;          // [NG]: group k's MMAs of its last vector completed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + NG);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + NG);   // + 16 B, then 4 KB reduction buffer
 
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
@@ -377,10 +377,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         }
       }
+      // combine the two groups' partial sums in shared memory, 8 columns at
+      // a time, and let group 0 write the item's result (one output slot per
+      // vector split)
+      float4* red = reinterpret_cast<float4*>(tmem_slot + 4);     // 128 x 8 floats
+#pragma unroll
+      for (int c = 0; c < KP; c += 8) {
+        if (grp == 1) {
+          red[2 * m] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+          red[2 * m + 1] = make_float4(acc[c + 4], acc[c + 5], acc[c + 6], acc[c + 7]);
+        }
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (grp == 0) {
+          const float4 u = red[2 * m], w = red[2 * m + 1];
+          acc[c] += u.x;
+          acc[c + 1] += u.y;
+          acc[c + 2] += u.z;
+          acc[c + 3] += u.w;
+          acc[c + 4] += w.x;
+          acc[c + 5] += w.y;
+          acc[c + 6] += w.z;
+          acc[c + 7] += w.w;
+        }
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+      }
       const int32_t tgt = a.tile_targets[(int64_t)x.slot * TMT + m];
-      if (tgt >= 0) {
-        float* o = a.acc_out + ((int64_t)tgt * a.nrhs + x.r) * a.ld +
-                   (int64_t)(NG * x.split + grp) * a.ostride;
+      if (grp == 0 && tgt >= 0) {
+        float* o = a.acc_out + ((int64_t)tgt * a.nrhs + x.r) * a.ld + (int64_t)x.split * a.ostride;
 #pragma unroll
         for (int c = 0; c < KP; c += 4)
           *reinterpret_cast<float4*>(o + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
@@ -463,9 +486,9 @@ int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   const size_t sbytes = ((size_t)TMT * 128 + (size_t)TMT * W1 * 4 + 2ull * KP * KP * 4 + 1023) /
                         1024 * 1024;
   int ns = ns_env;
-  while (ns > 2 && 1024 + ns * sbytes + 256 > 227 * 1024) --ns;
+  while (ns > 2 && 1024 + ns * sbytes + 256 + 4096 > 227 * 1024) --ns;
   a.ns = ns;
-  const size_t smem = 1024 + ns * sbytes + (2 * ns + NG) * 8 + 16;
+  const size_t smem = 1024 + ns * sbytes + (2 * ns + NG) * 8 + 16 + 4096;
   const int grid = a.n_items < sm_count() ? a.n_items : sm_count();
   set_max_smem((const void*)m2l_sweep_tmem_kernel<KP>, smem);
   m2l_sweep_tmem_kernel<KP><<<grid, NTHREADS, smem, stream>>>(tm, tm2, a);
@@ -538,7 +561,7 @@ int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int
   a.n_tiles = (int)n_tiles;
   a.n_items = (int)(nrhs * n_tiles * nsplit);
   a.ostride = ostride;
-  a.ld = NG * nsplit * ostride;             // each group writes its own slot per split
+  a.ld = nsplit * ostride;
   a.acc_out = acc;
   a.ns = 2;
   cudaStream_t s = (cudaStream_t)stream;

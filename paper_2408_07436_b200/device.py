@@ -470,8 +470,6 @@ class BlasDevice:
         fused epilogue into the locals."""
         la = self.la
         if self.tmem:
-            # the tensor-memory sweep writes two partial slots per vector split
-            # (its two vector-interleaved groups); the epilogue sums them all
             nsplit = self.tmem_splits(plan["n_tiles"], plan["n_pairs"], nrhs)
             # projection q~ = M S written straight into the dense parity
             # sub-lattice array (row map (box, rhs) -> plane p*R + r, cell)
@@ -481,7 +479,6 @@ class BlasDevice:
                    P(plan["tile_targets"]), P(plan["tile_ids"]), plan["n_tiles"],
                    P(plan["pairs"]), plan["n_pairs"], P(self.class_tv_local), P(self.offsets),
                    nrhs, nsplit, self.ko_pad, P(acc), stream_handle())
-            nsplit *= 2
         else:
             nsplit = sweep_splits(plan["n_tiles"], 1)
             self._run_tma(plan, mult, n_s, nrhs, qt, dense, acc, nsplit)
@@ -511,7 +508,7 @@ class BlasDevice:
     def acc_elems(self, n_t, nrhs, n_tiles, tma=False, n_pairs=0):
         ns = sweep_splits(n_tiles, self.n_slabs)
         if tma and self.tmem:
-            ns = max(ns, 2 * self.tmem_splits(n_tiles, n_pairs, nrhs))
+            ns = max(ns, self.tmem_splits(n_tiles, n_pairs, nrhs))
         return n_t * nrhs * ns * self.ko_pad
 
     def run_level(self, plan, mult, n_s, n_t, nrhs, level_scale, check, qt, acc, solve=None):
