@@ -265,6 +265,13 @@ int kifmm_scatter_rows_f32(const float* src, const int32_t* rows, int64_t n_rows
                            float* dst, void* stream);
 int kifmm_scatter_rows_f64(const double* src, const int32_t* rows, int64_t n_rows, int64_t width,
                            double* dst, void* stream);
+/* dst[rows[i]*width + e] += src[i*width + e] (rows[i] < 0: skipped): the L2L
+ * child check potentials added to the M2L check potentials of a level before
+ * the one down_inv solve (engine.py:355,370 merged). */
+int kifmm_scatter_add_rows_f32(const float* src, const int32_t* rows, int64_t n_rows,
+                               int64_t width, float* dst, void* stream);
+int kifmm_scatter_add_rows_f64(const double* src, const int32_t* rows, int64_t n_rows,
+                               int64_t width, double* dst, void* stream);
 
 /* FFT-M2L inverse (m2l_fft.py:252-261): for each target box b, take the
  * spectrum phat[f, tgt_slot[b], r], inverse real 3-D DFT, read the

@@ -84,6 +84,8 @@ SIGNATURES = {
     "kifmm_m2l_sweep_tmem_f32": [_P, _P, _I, _I, _P, _P, _I, _P, _I, _P, _P, _I, _I, _I, _P, _P],
     "kifmm_m2l_sweep_tmem_splits": [_I, _I, _I, _P],
     "kifmm_m2l_sweep_tmem_trace": [_P, _I],
+    "kifmm_scatter_add_rows_f32": [_P, _P, _I, _I, _P, _P],
+    "kifmm_scatter_add_rows_f64": [_P, _P, _I, _I, _P, _P],
     "kifmm_sm_target": [],
     "kifmm_probe": [_C, _I, _I, _I, _P, _P],
 }

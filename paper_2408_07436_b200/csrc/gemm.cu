@@ -477,8 +477,13 @@ __global__ void rows_kernel(const T* __restrict__ src, const int32_t* __restrict
   if (idx >= n_rows * width) return;
   const int64_t i = idx / width, e = idx - i * width;
   const int64_t g = rows[i];
-  if (scatter) dst[g * width + e] = src[idx];
-  else dst[idx] = src[g * width + e];
+  if (scatter == 2) {                      // scatter-add; rows < 0 are skipped
+    if (g >= 0) dst[g * width + e] += src[idx];
+  } else if (scatter) {
+    dst[g * width + e] = src[idx];
+  } else {
+    dst[idx] = src[g * width + e];
+  }
 }
 
 template <typename T>
@@ -510,6 +515,15 @@ int kifmm_scatter_rows_f32(const float* src, const int32_t* rows, int64_t n_rows
 int kifmm_scatter_rows_f64(const double* src, const int32_t* rows, int64_t n_rows, int64_t width,
                            double* dst, void* s) {
   return rows_op<double>(src, rows, n_rows, width, dst, 1, s);
+}
+
+int kifmm_scatter_add_rows_f32(const float* src, const int32_t* rows, int64_t n_rows,
+                               int64_t width, float* dst, void* s) {
+  return rows_op<float>(src, rows, n_rows, width, dst, 2, s);
+}
+int kifmm_scatter_add_rows_f64(const double* src, const int32_t* rows, int64_t n_rows,
+                               int64_t width, double* dst, void* s) {
+  return rows_op<double>(src, rows, n_rows, width, dst, 2, s);
 }
 
 int kifmm_gemm_f32(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,

@@ -464,7 +464,8 @@ class BlasDevice:
         nat.call("kifmm_m2l_sweep_tmem_splits", n_tiles, n_pairs, nrhs, ctypes.addressof(out))
         return int(out.value)
 
-    def run_level_tma(self, plan, mult, n_s, n_t, nrhs, level_scale, qt, dense, acc, solve):
+    def run_level_tma(self, plan, mult, n_s, n_t, nrhs, level_scale, qt, dense, acc, solve,
+                      check=None):
         """Engine path for float32: projection -> dense sub-lattice array ->
         tcgen05 sweep (A in tensor memory, or TMA-staged hi/lo planes) ->
         fused epilogue into the locals."""
@@ -482,6 +483,12 @@ class BlasDevice:
         else:
             nsplit = sweep_splits(plan["n_tiles"], 1)
             self._run_tma(plan, mult, n_s, nrhs, qt, dense, acc, nsplit)
+        if solve is None:
+            # check potentials only (the caller applies the solve, merged
+            # with the L2L contribution of the level)
+            la.gemm(n_t * nrhs, self.n_c, self.k, level_scale, acc, nsplit * self.ko_pad,
+                    self.UT, self.n_c, check, self.n_c, asum=nsplit, astride=self.ko_pad)
+            return 3
         inv, side, loc = solve
         la.chain(n_t * nrhs, acc, nsplit * self.ko_pad,
                  [(self.UT, self.k, self.n_c, None, level_scale)]
@@ -633,10 +640,11 @@ class DeviceFmm:
         in the overlapped evaluate."""
         b = self._buffers(nrhs)
         qt, acc = b["qt_lv"][lvl], b["acc_lv"][lvl]
-        if self.tma and solve is not None:
+        if self.tma:
             plan = self.tma_plan[lvl]
             return self.blas.run_level_tma(plan, mult, self.n_src[lvl], self.n_tgt[lvl], nrhs,
-                                           1.0 / self.side[lvl], qt, b["dense"][lvl], acc, solve)
+                                           1.0 / self.side[lvl], qt, b["dense"][lvl], acc, solve,
+                                           check=check)
         return self.blas.run_level(self.blas_plan_dev[lvl], mult, self.n_src[lvl],
                                    self.n_tgt[lvl], nrhs, 1.0 / self.side[lvl], check, qt, acc,
                                    solve=solve)
@@ -820,20 +828,26 @@ class DeviceFmm:
         if overlap and p2p_after == "p2m":
             fork_p2p()
         loc = b["loc"]
-        for lvl in range(2, d + 1):
-            loc[lvl].zero_()
         calls = {}
-
+        # Each level's M2L leaves its check potentials (x 1/side) in
+        # phi_lv[l]; the L2L from the parent level adds its child check
+        # potentials (x 0.5/side) into the same rows; one down_inv solve
+        # (x side) then overwrites the locals.  The solve is linear, so this
+        # equals the reference's two solves accumulated into the locals
+        # (engine.py:355, 370) and saves one solve per level.
         def m2l(lvl):
             n_t = self.n_tgt[lvl]
             check = b["phi_lv"][lvl][: n_t * R * n_c]
             if self.cfg.backend == "blas":
-                calls[lvl] = self.m2l_blas_level(lvl, mult[lvl], R, check,
-                                                 solve=(self.dn_inv, self.side[lvl], loc[lvl]))
+                calls[lvl] = self.m2l_blas_level(lvl, mult[lvl], R, check)
             else:
                 calls[lvl] = self.m2l_fft_level(lvl, mult[lvl], R, check)
-                la.chain(n_t * R, check, n_c, Linalg.solve_stages(self.dn_inv, self.side[lvl]),
-                         loc[lvl], n_e, accumulate=True)
+
+        def solve_level(lvl):
+            n_t = self.n_tgt[lvl]
+            check = b["phi_lv"][lvl][: n_t * R * n_c]
+            la.chain(n_t * R, check, n_c, Linalg.solve_stages(self.dn_inv, self.side[lvl]),
+                     loc[lvl], n_e)
 
         # With `overlap`, every level's M2L except the coarsest runs on its own
         # stream as soon as its multipoles exist (the finest level right after
@@ -869,16 +883,28 @@ class DeviceFmm:
         for lvl in range(2, d + 1):
             n_t = self.n_tgt[lvl]
             phase(f"m2l{lvl}")
-            if lvl not in forked:
+            if lvl not in forked and lvl not in calls:
                 m2l(lvl)
+            if lvl == 2:
+                solve_level(2)
             if lvl < d:
+                # the level's M2L check potentials must exist before the L2L
+                # adds to them
                 if lvl + 1 in forked:
                     main.wait_stream(forked[lvl + 1])
+                else:
+                    phase(f"m2l{lvl + 1}")
+                    m2l(lvl + 1)
                 phase(f"l2l{lvl}")
-                la.chain(n_t * R, loc[lvl], n_e,
-                         [(self.l2lT, n_e, 8 * n_c, None, 1.0)]
-                         + Linalg.solve_stages(self.dn_inv, 0.5), loc[lvl + 1], n_e,
-                         rowmap=self._l2l_rowmap(lvl + 1, R), accumulate=True)
+                # child check potentials (parent row x 8 children x n_c) into
+                # scratch, then added to the level's M2L check rows
+                check_c = b["phi_lv"][lvl + 1][: self.n_tgt[lvl + 1] * R * n_c]
+                l2l_tmp = la.scratch(3, n_t * R * 8 * n_c, self.T, check_c.device)
+                la.gemm(n_t * R, 8 * n_c, n_e, 0.5 / self.side[lvl + 1], loc[lvl], n_e,
+                        self.l2lT, 8 * n_c, l2l_tmp, 8 * n_c)
+                launch(f"kifmm_scatter_add_rows_{sfx}", P(l2l_tmp),
+                       P(self._l2l_rowmap(lvl + 1, R)), n_t * R * 8, n_c, P(check_c), s)
+                solve_level(lvl + 1)
         for st in forked.values():
             main.wait_stream(st)
         calls = [calls[l] for l in sorted(calls)]
