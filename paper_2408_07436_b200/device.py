@@ -484,10 +484,11 @@ class BlasDevice:
             nsplit = sweep_splits(plan["n_tiles"], 1)
             self._run_tma(plan, mult, n_s, nrhs, qt, dense, acc, nsplit)
         if solve is None:
-            # check potentials only (the caller applies the solve, merged
-            # with the L2L contribution of the level)
-            la.gemm(n_t * nrhs, self.n_c, self.k, level_scale, acc, nsplit * self.ko_pad,
-                    self.UT, self.n_c, check, self.n_c, asum=nsplit, astride=self.ko_pad)
+            # t = check . U_dn in one product (acc . (U^T U_dn)); the caller
+            # adds the L2L part and applies the rest of the solve
+            r = self.UTU.shape[1]
+            la.gemm(n_t * nrhs, r, self.k, level_scale, acc, nsplit * self.ko_pad,
+                    self.UTU, r, check, r, asum=nsplit, astride=self.ko_pad)
             return 3
         inv, side, loc = solve
         la.chain(n_t * nrhs, acc, nsplit * self.ko_pad,
@@ -608,6 +609,18 @@ class DeviceFmm:
         self.r_up, self.r_dn = exp.up_inv.rank, exp.down_inv.rank
         self.m2mT = to_dev(np.ascontiguousarray(exp.m2m_kernels.T), dt)
         self.l2lT = to_dev(np.ascontiguousarray(exp.l2l_kernels.T), dt)
+        # Folded down-solve operators of the engine's downward pass (float64
+        # products, cast once): t = check . U_dn carries each level's M2L and
+        # L2L contributions, locals = t . diag(inv) V_dn^T x side.
+        u_dn = np.asarray(exp.down_inv.u, dtype=np.float64)               # (n_c, r)
+        self.r_fold = u_dn.shape[1]
+        self.dn_vv = to_dev(np.asarray(exp.down_inv.inv_vals, np.float64)[:, None]
+                            * np.asarray(exp.down_inv.v, np.float64).T, dt)  # (r, n_e)
+        l2l = np.asarray(exp.l2l_kernels, dtype=np.float64).T                  # (n_e, 8 n_c)
+        n_e_, n_c_ = l2l.shape[0], u_dn.shape[0]
+        self.l2lU = to_dev(np.ascontiguousarray(
+            (l2l.reshape(n_e_, 8, n_c_) @ u_dn).reshape(n_e_, 8 * self.r_fold)), dt)
+        self.dn_u = to_dev(u_dn, dt)
         # tree levels
         self.n_src = [st.level_keys(l).shape[0] for l in range(cfg.depth + 1)]
         self.n_tgt = [tt.level_keys(l).shape[0] for l in range(cfg.depth + 1)]
@@ -627,6 +640,10 @@ class DeviceFmm:
     def _init_blas(self, ops, plans):
         import os
         self.blas = BlasDevice(ops, self.np_dtype, self.la)
+        # M2L expansion folded with the down-solve's first factor: U^T U_dn
+        self.blas.UTU = to_dev(np.asarray(ops.u, np.float64).T
+                               @ np.asarray(self.inst.expansions.down_inv.u, np.float64),
+                               self.np_dtype)
         self.blas_plan_dev = {l: upload_blas_plan(p) for l, p in plans.items()}
         # float32 engine path: TMA-fed sweep on dense sub-lattice arrays
         self.tma = self.blas.tc and os.environ.get("KIFMM_SWEEP", "tma") == "tma"
@@ -710,6 +727,8 @@ class DeviceFmm:
         levels = list(range(2, d + 1))
         b["phi_lv"] = {l: torch.empty(max(self.n_tgt[l] * R * self.n_c, 1), dtype=T, device=dev)
                        for l in levels}
+        b["t_lv"] = {l: torch.empty(max(self.n_tgt[l] * R * self.r_fold, 1), dtype=T, device=dev)
+                     for l in levels}
         if self.cfg.backend == "blas":
             def acc_need(l):
                 n = self.blas.acc_elems(self.n_tgt[l], R, self.blas_plan_dev[l]["n_tiles"])
@@ -835,19 +854,27 @@ class DeviceFmm:
         # (x side) then overwrites the locals.  The solve is linear, so this
         # equals the reference's two solves accumulated into the locals
         # (engine.py:355, 370) and saves one solve per level.
+        rf = self.r_fold
+
         def m2l(lvl):
+            # t_l = check_l . U_dn (rank rf) from the level's M2L
             n_t = self.n_tgt[lvl]
+            t_l = b["t_lv"][lvl][: n_t * R * rf]
+            if self.cfg.backend == "blas" and self.tma:
+                calls[lvl] = self.m2l_blas_level(lvl, mult[lvl], R, t_l)
+                return
             check = b["phi_lv"][lvl][: n_t * R * n_c]
             if self.cfg.backend == "blas":
                 calls[lvl] = self.m2l_blas_level(lvl, mult[lvl], R, check)
             else:
                 calls[lvl] = self.m2l_fft_level(lvl, mult[lvl], R, check)
+            la.gemm(n_t * R, rf, n_c, 1.0, check, n_c, self.dn_u, rf, t_l, rf)
 
         def solve_level(lvl):
+            # locals = t_l . diag(inv) V_dn^T x side (overwrite)
             n_t = self.n_tgt[lvl]
-            check = b["phi_lv"][lvl][: n_t * R * n_c]
-            la.chain(n_t * R, check, n_c, Linalg.solve_stages(self.dn_inv, self.side[lvl]),
-                     loc[lvl], n_e)
+            t_l = b["t_lv"][lvl][: n_t * R * rf]
+            la.gemm(n_t * R, n_e, rf, self.side[lvl], t_l, rf, self.dn_vv, n_e, loc[lvl], n_e)
 
         # With `overlap`, every level's M2L except the coarsest runs on its own
         # stream as soon as its multipoles exist (the finest level right after
@@ -898,12 +925,14 @@ class DeviceFmm:
                 phase(f"l2l{lvl}")
                 # child check potentials (parent row x 8 children x n_c) into
                 # scratch, then added to the level's M2L check rows
-                check_c = b["phi_lv"][lvl + 1][: self.n_tgt[lvl + 1] * R * n_c]
-                l2l_tmp = la.scratch(3, n_t * R * 8 * n_c, self.T, check_c.device)
-                la.gemm(n_t * R, 8 * n_c, n_e, 0.5 / self.side[lvl + 1], loc[lvl], n_e,
-                        self.l2lT, 8 * n_c, l2l_tmp, 8 * n_c)
+                # child parts of t (parent row x 8 children x rf) into scratch,
+                # then added to the level's M2L part
+                t_c = b["t_lv"][lvl + 1][: self.n_tgt[lvl + 1] * R * rf]
+                l2l_tmp = la.scratch(3, n_t * R * 8 * rf, self.T, t_c.device)
+                la.gemm(n_t * R, 8 * rf, n_e, 0.5 / self.side[lvl + 1], loc[lvl], n_e,
+                        self.l2lU, 8 * rf, l2l_tmp, 8 * rf)
                 launch(f"kifmm_scatter_add_rows_{sfx}", P(l2l_tmp),
-                       P(self._l2l_rowmap(lvl + 1, R)), n_t * R * 8, n_c, P(check_c), s)
+                       P(self._l2l_rowmap(lvl + 1, R)), n_t * R * 8, rf, P(t_c), s)
                 solve_level(lvl + 1)
         for st in forked.values():
             main.wait_stream(st)
