@@ -193,7 +193,11 @@ __device__ __forceinline__ TileGeom tile_geom(const TmemArgs& a, int slot) {
 }
 
 template <int KP>
+#ifdef KIFMM_TMEM_MAXNREG
+__global__ void __maxnreg__(KIFMM_TMEM_MAXNREG) m2l_sweep_tmem_kernel(
+#else
 __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
+#endif
     const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm2,
     const TmemArgs a) {
   constexpr int N1 = 2 * KP;
