@@ -410,3 +410,55 @@ def test_many_rhs_with_gradient(cuda):
     want_grad = port.fmm_gradient(inst, q, st)
     assert np.abs(phi - want_phi).max() <= 1e-10 * np.abs(want_phi).max()
     assert np.abs(grad - want_grad).max() <= 1e-9 * np.abs(want_grad).max()
+
+
+# ------------------------------------------- tensor-memory sweep (csrc/m2l_tmem.cu)
+@pytest.mark.parametrize("n,depth,order,nrhs,clustered", [
+    (20000, 3, 4, 1, False), (60000, 4, 4, 2, False), (30000, 4, 3, 1, True)])
+def test_tmem_sweep_matches_tma_sweep_and_reference(cuda, monkeypatch, n, depth, order, nrhs,
+                                                    clustered):
+    """The float32 engine sweep with the A operand in tensor memory (ranks
+    <= 64) against the TMA-staged sweep on the same instance inputs, and
+    against the reference; uniform and clustered (pruned boxes) clouds, 1 and
+    2 right-hand sides; re-evaluation is bitwise deterministic."""
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(21)
+    pts = rng.random((n, 3))
+    if clustered:
+        pts = pts ** 3
+    q = rng.random((n, nrhs)) if nrhs > 1 else rng.random(n)
+    kw = dict(depth=depth, order_equiv=order, backend="blas", precision="f32", sigma_min=1e-6)
+    res = {}
+    for sweep in ("tma", "tmem"):
+        monkeypatch.setenv("KIFMM_F32_SWEEP", sweep)
+        inst = setup(pts, pts, FmmConfig(**kw))
+        assert inst.device.blas.tmem == (sweep == "tmem")
+        res[sweep] = np.asarray(inst.evaluate(q), dtype=np.float64)
+        if sweep == "tmem":
+            again = np.asarray(inst.evaluate(q), dtype=np.float64)
+            assert np.array_equal(res[sweep], again)
+    rel = np.abs(res["tmem"] - res["tma"]) / np.abs(res["tma"])
+    assert rel.max() <= TOL["f32"], rel.max()
+    if nrhs == 1:
+        want, _ = _reference_run(pts, q, kw)
+        assert parity_report(res["tmem"], want)["max_rel"] <= TOL["f32"]
+
+
+def test_scatter_add_rows(cuda):
+    """kifmm_scatter_add_rows_f32: dst[rows[i]] += src[i]; rows < 0 skipped
+    (the L2L child rows of absent children)."""
+    import torch
+    from paper_2408_07436_b200 import _native as nat
+    rng = np.random.default_rng(3)
+    src = rng.random((10, 7)).astype(np.float32)
+    rows = np.array([4, -1, 0, 9, 2, -1, 5, 1, 8, 3], dtype=np.int32)
+    dst = rng.random((10, 7)).astype(np.float32)
+    want = dst.copy()
+    for i, r in enumerate(rows):
+        if r >= 0:
+            want[r] += src[i]
+    s_d, r_d, d_d = (torch.from_numpy(a).cuda() for a in (src, rows, dst))
+    nat.call("kifmm_scatter_add_rows_f32", s_d.data_ptr(), r_d.data_ptr(), 10, 7, d_d.data_ptr(),
+             torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_d.cpu().numpy(), want)

@@ -141,3 +141,36 @@ def test_setup_rejects_empty_clouds():
         setup(np.empty((0, 3)), pts, FmmConfig(depth=2, order_equiv=3))
     with pytest.raises(ConfigError):
         setup(pts, np.empty((0, 3)), FmmConfig(depth=2, order_equiv=3))
+
+
+def test_locality_vector_order_is_a_permutation():
+    """The tensor-memory sweep's class vector order (device.py
+    locality_transfer_table) lists exactly each class's 189 admissible
+    vectors, grouped by source sub-lattice."""
+    from paper_2408_07436_b200.device import locality_transfer_table
+    from paper_2408_07436_b200.octree import class_transfer_table, transfer_offsets
+    loc, base = locality_transfer_table(), class_transfer_table()
+    offs = transfer_offsets()
+    for cls in range(8):
+        assert sorted(loc[cls].tolist()) == sorted(base[cls].tolist())
+        par = np.array([(cls >> 2) & 1, (cls >> 1) & 1, cls & 1])
+        q = par[None, :] + offs[loc[cls]]
+        sp = ((q[:, 0] & 1) << 2) | ((q[:, 1] & 1) << 1) | (q[:, 2] & 1)
+        assert np.all(np.diff(sp) >= 0)
+
+
+def test_tmem_core_packing_layout():
+    """pack_tmem_cores: per vector [B_hi | B_lo], each K-major [n/8][k/4][n%8][k%4]."""
+    from paper_2408_07436_b200.device import pack_tmem_cores
+    rng = np.random.default_rng(0)
+    kp = 16
+    hi = rng.random((3, 13, 13)).astype(np.float32)
+    lo = rng.random((3, 13, 13)).astype(np.float32)
+    out = pack_tmem_cores(hi, lo, kp)
+    assert out.shape == (3, 2 * kp * kp)
+    for t in range(3):
+        for half, src in ((0, hi), (1, lo)):
+            blk = out[t, half * kp * kp:(half + 1) * kp * kp].reshape(kp // 8, kp // 4, 8, 4)
+            dense = blk.transpose(0, 2, 1, 3).reshape(kp, kp)
+            assert np.array_equal(dense[:13, :13], src[t])
+            assert not dense[13:].any() and not dense[:, 13:].any()
