@@ -493,7 +493,15 @@ int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   while (ns > 2 && 1024 + ns * sbytes + 256 + 4096 > 227 * 1024) --ns;
   a.ns = ns;
   const size_t smem = 1024 + ns * sbytes + (2 * ns + NG) * 8 + 16 + 4096;
-  const int grid = a.n_items < sm_count() ? a.n_items : sm_count();
+  // persistent CTAs: one per SM, or KIFMM_TMEM_GRID (fewer leaves SMs to the
+  // concurrent small kernels of the other streams)
+  static int grid_env = -1;
+  if (grid_env < 0) {
+    const char* e = getenv("KIFMM_TMEM_GRID");
+    grid_env = e ? atoi(e) : 0;
+  }
+  const int g_max = grid_env > 0 && grid_env < sm_count() ? grid_env : sm_count();
+  const int grid = a.n_items < g_max ? a.n_items : g_max;
   set_max_smem((const void*)m2l_sweep_tmem_kernel<KP>, smem);
   m2l_sweep_tmem_kernel<KP><<<grid, NTHREADS, smem, stream>>>(tm, tm2, a);
   return launch_status();
