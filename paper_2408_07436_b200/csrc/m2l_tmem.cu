@@ -48,6 +48,9 @@ namespace {
 constexpr int TMT = 128;
 constexpr int NG = 2;             // groups per CTA (alternate vectors), each with its own TMEM A and D
 constexpr int NTHREADS = 32 + 128 * NG;
+#ifndef KIFMM_TMEM_STW
+#define KIFMM_TMEM_STW 8           // widest tcgen05.st piece (8 / 16 / 32 columns)
+#endif
 #ifndef KIFMM_TMEM_FLUSH
 #define KIFMM_TMEM_FLUSH 8
 #endif
@@ -103,6 +106,46 @@ __device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t (&v)[8]) 
       "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
 }
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16};" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+// A = [hi | lo] rows of this warp's 32 lanes: columns [0, KP) from hv and
+// [KP, 2 KP) from lv, hi and lo pieces interleaved, pieces of up to
+// KIFMM_TMEM_STW columns (x32 / x16 / x8 tcgen05.st)
+template <int KP>
+__device__ __forceinline__ void tmem_st_a(uint32_t addr, const uint32_t (&hv)[KP],
+                                          const uint32_t (&lv)[KP]) {
+  constexpr int C32 = KIFMM_TMEM_STW >= 32 ? KP / 32 * 32 : 0;
+  constexpr int C16 = KIFMM_TMEM_STW >= 16 ? C32 + (KP - C32) / 16 * 16 : C32;
+#pragma unroll
+  for (int c = 0; c < C32; c += 32) {
+    tmem_st32(addr + c, &hv[c]);
+    tmem_st32(addr + KP + c, &lv[c]);
+  }
+#pragma unroll
+  for (int c = C32; c < C16; c += 16) {
+    tmem_st16(addr + c, &hv[c]);
+    tmem_st16(addr + KP + c, &lv[c]);
+  }
+#pragma unroll
+  for (int c = C16; c < KP; c += 8) {
+    tmem_st8(addr + c, *reinterpret_cast<const uint32_t(*)[8]>(&hv[c]));
+    tmem_st8(addr + KP + c, *reinterpret_cast<const uint32_t(*)[8]>(&lv[c]));
+  }
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
@@ -125,13 +168,6 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* tm, in
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
       "r"(smem_u32(bar))
       : "memory");
-}
-// bulk copy into the same offset of every CTA in cta_mask (and complete_tx on
-// each one's barrier at the same offset)
-__device__ __forceinline__ uint32_t tf32_rna(float x) {
-  uint32_t b;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x));
-  return b;
 }
 
 struct TmemArgs {
@@ -338,11 +374,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
         if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);
         if (m == 0) trace(grp == 0 ? 1 : 6, gg);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#if KIFMM_TMEM_STW > 8
+        tmem_st_a<KP>(acol + lane_base, hv, lv);
+#else
 #pragma unroll
         for (int c = 0; c < KP / 8; ++c) {
           tmem_st8(acol + lane_base + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&hv[c * 8]));
           tmem_st8(acol + lane_base + KP + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&lv[c * 8]));
         }
+#endif
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
@@ -411,6 +451,380 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
 #pragma unroll
         for (int c = 0; c < KP; c += 4)
           *reinterpret_cast<float4*>(o + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+      }
+      g += x.nv;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Brick-fed variant.  For a target tile (4 x 4 x 8 same-parity targets) the
+// 189 vectors of the class list (device.locality_transfer_table order) fall
+// into runs of equal source sub-lattice sp and x shift, and within a run
+// every vector's 128 source rows are a (y, z)-shifted window of the same
+// 4 x 6 x 10 "brick" of source rows (shift (qy >> 1, qz >> 1) in {-1,0,1}^2).
+// The brick (240 rows, 53 KB at KP = 56) is loaded by ONE TMA box per run
+// (~8 vectors) and every vector gathers its A rows from it with shared loads;
+// only the core pair (25 KB, one bulk copy) streams per vector.
+//
+// Measured (tools/trace_brick.py, config 2 level 5): correct, but ~1320
+// cycles per vector against ~1150 for the stage-ring kernel above, so it is
+// not the default (see use_brick).  What the traces showed: the per-vector
+// chain of a group - MMA completion (~1000 cycles for 620 cycles of tensor
+// work), tcgen05.st of the next A (~550), hand-over and issue (~500) - is the
+// same in both kernels and bounds both; an mbarrier wait in a thread that
+// has MMAs in flight costs ~350 cycles, hence one issuer warp per group here
+// and the core-pair wait done by the loader warps.
+//
+// Brick rows are KP * 4 bytes apart (linear, no swizzle: one box, fewest
+// rows); the two-way bank conflict of rows i and i + 4 in an 8-lane LDS.128
+// phase is removed by reading each chunk pair in swapped order on lanes
+// with bit 2 set.  Two brick buffers (the next run's brick is prefetched
+// while the current run is swept), nsb core-pair stages.  Roles as in the
+// kernel above: warp 0 lane 0 loads bricks (one run ahead) and core pairs;
+// groups 0 / 1 take alternate vectors; every consumer warp releases a brick
+// after its last gather from it (8 arrivals).
+constexpr int BRX = BX, BRY = BY + 2, BRZ = BZ + 2;
+constexpr int BROWS = BRX * BRY * BRZ;                   // 240
+
+__host__ __device__ constexpr uint32_t brick_bytes(int kp) {
+  return ((uint32_t)BROWS * kp * 4u + 1023u) / 1024u * 1024u;
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
+#ifndef KIFMM_BRICK_BCHUNK
+#define KIFMM_BRICK_BCHUNK 1      // bulk copies per core pair (BBYTES / chunk must stay a multiple of 16)
+#endif
+#ifndef KIFMM_BRICK_PF
+#define KIFMM_BRICK_PF 0          // L2 prefetch distance of the core pairs, in vectors (0: off)
+#endif
+#ifndef KIFMM_BRICK_ROT
+#define KIFMM_BRICK_ROT 1
+#endif
+// Walk position v of item it -> vector index: every item starts its walk at
+// a different point of the class list (all CTAs walking the same list in
+// lock step would read the same core pair from L2 at the same time).
+__device__ __forceinline__ int vrot(const Item& x, int it, int v) {
+  if (!KIFMM_BRICK_ROT || x.nv == 0) return v;
+  const int r = (int)(((unsigned)it * 2654435761u) >> 8) % x.nv;
+  const int w = v + r;
+  return w >= x.nv ? w - x.nv : w;
+}
+
+struct BrickMaps {
+  CUtensorMap m[1];
+};
+
+constexpr int NTHREADS_B = NTHREADS + 32 * NG;   // + one MMA issuer warp per group
+
+template <int KP>
+__global__ void __launch_bounds__(NTHREADS_B, 1) m2l_sweep_brick_kernel(
+    const __grid_constant__ BrickMaps maps, const TmemArgs a) {
+  constexpr int N1 = 2 * KP;
+  constexpr int N2 = (KP + 15) / 16 * 16;
+  constexpr uint32_t BRB = brick_bytes(KP);
+  constexpr uint32_t BBYTES = 2u * KP * KP * 4u;
+  constexpr int GCOLS = N1 + 2 * KP;
+  constexpr int NEED = NG * GCOLS;
+  constexpr uint32_t TMEM_COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128
+                                 : NEED <= 256 ? 256 : 512;
+  static_assert(NEED <= 512, "TMEM budget");
+  static_assert(KP % 8 == 0 && N1 <= 256, "shape");
+
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nsb = a.ns;
+  long long* const trace_buf = (blockIdx.x == 0 && g_trace_h == a.h) ? g_trace : nullptr;
+  unsigned char* bstage = smem + 2 * BRB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bstage + nsb * BBYTES);   // core pair landed
+  uint64_t* empty = full + nsb;         // the MMAs reading the core pair completed
+  uint64_t* bfull = empty + nsb;        // [2] brick landed
+  uint64_t* bempty = bfull + 2;         // [2] every consumer warp done gathering from the brick
+  uint64_t* done = bempty + 2;          // [NG]
+  uint64_t* ready = done + NG;          // [NG] the group's four warps stored their A rows
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + NG);
+  float4* red = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 15) &
+                                          ~uintptr_t(15));            // 128 x 8 floats
+  uint16_t* code = reinterpret_cast<uint16_t*>(red + 2 * TMT);       // [8 * 189]: sp | brick row shift << 3
+
+  for (int i = tid; i < 8 * 189; i += NTHREADS_B) {
+    const int cls = i / 189;
+    const int t = a.class_tv[i];
+    const int qx = ((cls >> 2) & 1) + a.offsets[3 * t], qy = ((cls >> 1) & 1) + a.offsets[3 * t + 1],
+              qz = (cls & 1) + a.offsets[3 * t + 2];
+    const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
+    const int sh = ((qy >> 1) + 1) * BRZ + ((qz >> 1) + 1);
+    code[i] = (uint16_t)(sp | (((qx >> 1) + 1) << 3) | (sh << 5));
+  }
+  if (tid == 0) {
+    for (int s = 0; s < nsb; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bfull[b], 1);
+      mbar_init(&bempty[b], 4 * NG);
+    }
+    for (int k = 0; k < NG; ++k) {
+      mbar_init(&done[k], 1);
+      mbar_init(&ready[k], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[0])) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // brick cursor: the next run to load (item it_b, first vector vb)
+      int it_b = blockIdx.x, vb = 0, kb = 0;
+      auto skip_empty = [&]() {
+        while (it_b < a.n_items && item_of(a, it_b).nv == 0) it_b += gridDim.x;
+      };
+      skip_empty();
+      auto issue_brick = [&]() {
+        const Item x = item_of(a, it_b);
+        const TileGeom tg = tile_geom(a, x.slot);
+        const uint16_t* cv = code + tg.cls * 189 + x.j0;
+        const int key = cv[vrot(x, it_b, vb)] & 31;
+        const int sp = key & 7, sx = key >> 3;
+        const int b = kb & 1;
+        if (kb >= 2) mbar_wait(&bempty[b], ((kb >> 1) - 1) & 1, false);
+        trace(8, kb);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         smem_u32(&bfull[b])),
+                     "r"((uint32_t)BROWS * KP * 4u)
+                     : "memory");
+        tma_load_5d(smem + b * BRB, &maps.m[0], 0, tg.iz0 - 1, tg.iy0 - 1, tg.ix0 - 1 + sx,
+                    sp * a.nrhs + x.r, &bfull[b]);
+        ++kb;
+        while (vb < x.nv && (cv[vrot(x, it_b, vb)] & 31) == key) ++vb;
+        if (vb == x.nv) {
+          vb = 0;
+          it_b += gridDim.x;
+          skip_empty();
+        }
+      };
+      int g = 0, run = -1;
+      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+        const Item x = item_of(a, it);
+        const TileGeom tg = tile_geom(a, x.slot);
+        const uint16_t* cv = code + tg.cls * 189 + x.j0;
+        const int32_t* tv = a.class_tv + tg.cls * 189 + x.j0;
+        int prev_sp = -1;
+        for (int v = 0; v < x.nv; ++v, ++g) {
+          trace(9, g);
+          const int sp = cv[vrot(x, it, v)] & 31;
+          if (sp != prev_sp) {
+            ++run;
+            prev_sp = sp;
+          }
+          while (kb <= run) issue_brick();                  // this run's brick (normally issued already)
+          if (kb == run + 1 && it_b < a.n_items &&          // look one run ahead when its buffer is free
+              (kb < 2 || mbar_test(&bempty[kb & 1], ((kb >> 1) - 1) & 1)))
+            issue_brick();
+          const int s = g % nsb;
+          if (g >= nsb) mbar_wait(&empty[s], ((g / nsb) - 1) & 1, false);
+          trace(4, g);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                           smem_u32(&full[s])),
+                       "r"(BBYTES)
+                       : "memory");
+#pragma unroll
+          for (int c = 0; c < KIFMM_BRICK_BCHUNK; ++c)
+            bulk_copy(bstage + s * BBYTES + c * (BBYTES / KIFMM_BRICK_BCHUNK),
+                      reinterpret_cast<const unsigned char*>(a.bpair + (int64_t)tv[vrot(x, it, v)] * (2 * KP * KP)) +
+                          c * (BBYTES / KIFMM_BRICK_BCHUNK),
+                      BBYTES / KIFMM_BRICK_BCHUNK, &full[s]);
+          if (KIFMM_BRICK_PF > 0 && v + KIFMM_BRICK_PF < x.nv)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             a.bpair + (int64_t)tv[vrot(x, it, v + KIFMM_BRICK_PF)] * (2 * KP * KP)),
+                         "r"(BBYTES)
+                         : "memory");
+          trace(2, g);
+        }
+      }
+      for (int gg = g - nsb < 0 ? 0 : g - nsb; gg < g; ++gg)
+        mbar_wait(&empty[gg % nsb], (gg / nsb) & 1, true);
+    }
+    __syncwarp();
+  } else if (warp >= 1 && warp < 1 + 4 * NG) {
+    const int grp = (warp - 1) >> 2;
+    const int q4 = warp & 3;
+    const int m = q4 * 32 + lane;
+    const int mrow = ((m >> 5) * BRY + ((m >> 3) & 3)) * BRZ + (m & 7);   // slab row at shift (., -1, -1)
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const uint32_t dcol = tmem + (uint32_t)(grp * GCOLS);
+    const uint32_t acol = dcol + N1;
+    float acc[KP];
+    int nmine = 0;
+    int g = 0, run = -1;
+    auto release = [&](int r) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bempty[r & 1]);
+    };
+    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+      const Item x = item_of(a, it);
+      const TileGeom tg = tile_geom(a, x.slot);
+      const uint16_t* cv = code + tg.cls * 189 + x.j0;
+#pragma unroll
+      for (int c = 0; c < KP; ++c) acc[c] = 0.f;
+      int local = 0;
+      int prev_sp = -1;
+      for (int v = 0; v < x.nv; ++v) {
+        const int cd = cv[vrot(x, it, v)];
+        if ((cd & 31) != prev_sp) {
+          if (prev_sp >= 0) release(run);
+          ++run;
+          prev_sp = cd & 31;
+        }
+        if ((v % NG) != grp) continue;
+        const int gg = g + v;
+        mbar_wait(&bfull[run & 1], (run >> 1) & 1, false);
+        const int br = mrow + (cd >> 5);
+        const unsigned char* bb = smem + (run & 1) * BRB;
+        uint32_t hv[KP], lv[KP];
+        // rows are 4 * KP bytes apart (KP = 56: 56 words), so lanes i and i + 4
+        // of an 8-lane LDS.128 phase share banks: lanes with bit 2 set read
+        // the two chunks of every chunk pair in swapped order
+        const bool swp = (lane >> 2) & 1;
+        const unsigned char* rowp = bb + br * (KP * 4);
+#pragma unroll
+        for (int i = 0; i < KP / 4; i += 2) {
+          const float4 p0 = *reinterpret_cast<const float4*>(rowp + ((i + (swp ? 1 : 0)) << 4));
+          const float4 p1 = *reinterpret_cast<const float4*>(rowp + ((i + (swp ? 0 : 1)) << 4));
+          const float4 c0 = swp ? p1 : p0, c1 = swp ? p0 : p1;
+          const float f[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            hv[4 * i + j] = (__float_as_uint(f[j]) + 0x1000u) & 0xFFFFE000u;
+            lv[4 * i + j] = __float_as_uint(f[j] - __uint_as_float(hv[4 * i + j]));
+          }
+        }
+        if (m == 0) trace(grp == 0 ? 0 : 5, gg);
+        if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);
+        if (m == 0) trace(grp == 0 ? 1 : 6, gg);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tmem_st_a<KP>(acol + lane_base, hv, lv);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (grp == 0 && lane == 0 && q4 == 1) trace(10, gg);
+        if (grp == 0 && lane == 0 && q4 == 0) trace(11, gg);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        // hand over to the group's issuer warp: the core pair has landed too
+        // (waited here, so the issuing thread never waits on an mbarrier)
+        mbar_wait(&full[gg % nsb], (gg / nsb) & 1, false);
+        asm volatile("bar.arrive %0, %1;" ::"r"(4 + grp), "n"(160) : "memory");
+        ++nmine;
+        const bool last_of_block = local == FLUSH_V - 1 || v + NG >= x.nv;
+        local = last_of_block ? 0 : local + 1;
+        if (last_of_block) {
+          mbar_wait(&done[grp], (nmine - 1) & 1, false);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < KP / 8; ++c) {
+            uint32_t u[8], w[8];
+            tmem_ld8(dcol + lane_base + c * 8, u);
+            tmem_ld8(dcol + lane_base + KP + c * 8, w);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              acc[c * 8 + i] += __uint_as_float(u[i]) + __uint_as_float(w[i]);
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        }
+      }
+      if (prev_sp >= 0) release(run);
+#pragma unroll
+      for (int c = 0; c < KP; c += 8) {
+        if (grp == 1) {
+          red[2 * m] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+          red[2 * m + 1] = make_float4(acc[c + 4], acc[c + 5], acc[c + 6], acc[c + 7]);
+        }
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (grp == 0) {
+          const float4 u = red[2 * m], w = red[2 * m + 1];
+          acc[c] += u.x;
+          acc[c + 1] += u.y;
+          acc[c + 2] += u.z;
+          acc[c + 3] += u.w;
+          acc[c + 4] += w.x;
+          acc[c + 5] += w.y;
+          acc[c + 6] += w.z;
+          acc[c + 7] += w.w;
+        }
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+      }
+      const int32_t tgt = a.tile_targets[(int64_t)x.slot * TMT + m];
+      if (grp == 0 && tgt >= 0) {
+        float* o = a.acc_out + ((int64_t)tgt * a.nrhs + x.r) * a.ld + (int64_t)x.split * a.ostride;
+#pragma unroll
+        for (int c = 0; c < KP; c += 4)
+          *reinterpret_cast<float4*>(o + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+      }
+      g += x.nv;
+    }
+  }
+  if (warp >= 1 + 4 * NG) {
+    // ---------------- MMA issuer of group grp (its own thread: an mbarrier
+    // wait behind in-flight MMAs of the issuing thread costs ~350 cycles, so
+    // the two groups' issue streams run on two threads)
+    const int grp = warp - (1 + 4 * NG);
+    constexpr uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N1 >> 3) << 17) |
+                                ((uint32_t)(TMT >> 4) << 24);
+    constexpr uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N2 >> 3) << 17) |
+                                ((uint32_t)(TMT >> 4) << 24);
+    constexpr uint32_t SBO = (KP / 4) * 128;
+    const uint32_t dcol = tmem + (uint32_t)(grp * GCOLS);
+    const uint32_t acol = dcol + N1;
+    int g = 0;
+    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+      const Item x = item_of(a, it);
+      int loc = 0;
+      for (int v = grp; v < x.nv; v += NG) {
+        const int gg = g + v;
+        const int s = gg % nsb;
+        asm volatile("bar.sync %0, %1;" ::"r"(4 + grp), "n"(160) : "memory");
+        if (lane == 0) {
+          if (grp == 0) trace(3, gg);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t bp = smem_u32(bstage + s * BBYTES);
+#pragma unroll
+          for (int ks = 0; ks < KP / 8; ++ks) {
+            const uint64_t db = desc_nosw(bp + ks * 256, 128, SBO);
+            mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, loc | ks);
+            mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
+          }
+          mma_commit(&done[grp]);
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
+        loc = (loc == FLUSH_V - 1 || v + NG >= x.nv) ? 0 : loc + 1;
       }
       g += x.nv;
     }
@@ -507,6 +921,59 @@ int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   return launch_status();
 }
 
+// shared memory of the brick kernel with nsb core-pair stages
+constexpr size_t brick_smem(int kp, int nsb) {
+  return 1024 + 2 * (size_t)brick_bytes(kp) + (size_t)nsb * 2 * kp * kp * 4 + (2 * nsb + 4 + 2 * NG) * 8 +
+         16 + 16 + 2 * TMT * 16 + 8 * 189 * 2;
+}
+
+template <int KP>
+int launch_brick(const TmemArgs& a0, cudaStream_t stream) {
+  TmemArgs a = a0;
+  BrickMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  {
+    EncodeFn enc = encoder();
+    if (!enc) return KIFMM_EARG;
+    cuuint64_t dims[5] = {(cuuint64_t)KP, (cuuint64_t)a.h, (cuuint64_t)a.h, (cuuint64_t)a.h,
+                          8 * (cuuint64_t)a.nrhs};
+    const cuuint64_t row = (cuuint64_t)KP * 4;
+    cuuint64_t strides[4] = {row, row * a.h, row * a.h * a.h, row * a.h * a.h * a.h};
+    cuuint32_t box[5] = {(cuuint32_t)KP, BRZ, BRY, BRX, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    if (enc(&maps.m[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(a.q), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return KIFMM_EARG;
+  }
+  int nsb = 2;
+  while (nsb < 6 && brick_smem(KP, nsb + 1) <= 227 * 1024) ++nsb;
+  a.ns = nsb;
+  const size_t smem = brick_smem(KP, nsb);
+  static int grid_env = -1;
+  if (grid_env < 0) {
+    const char* e = getenv("KIFMM_TMEM_GRID");
+    grid_env = e ? atoi(e) : 0;
+  }
+  const int g_max = grid_env > 0 && grid_env < sm_count() ? grid_env : sm_count();
+  const int grid = a.n_items < g_max ? a.n_items : g_max;
+  set_max_smem((const void*)m2l_sweep_brick_kernel<KP>, smem);
+  m2l_sweep_brick_kernel<KP><<<grid, NTHREADS_B, smem, stream>>>(maps, a);
+  return launch_status();
+}
+
+// KIFMM_TMEM_BRICK=1 selects the brick-fed kernel (when two bricks and two
+// core-pair stages fit in shared memory, KP <= 56).  Off by default: on
+// config 2 it sweeps level 5 in 360-370 us against 280-285 us for the
+// stage-ring kernel (tools/trace_brick.py: ~1320 cycles per vector; the chain
+// MMA completion -> tcgen05.st of the next A -> hand-over -> issue of each
+// group is not shortened by the smaller ingress).  Read per call so tests can
+// switch it.
+bool use_brick(int kp) {
+  const char* e = getenv("KIFMM_TMEM_BRICK");
+  return e && atoi(e) != 0 && brick_smem(kp, 2) <= 227 * 1024;
+}
+
 }  // namespace
 
 extern "C" {
@@ -577,6 +1044,15 @@ int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int
   a.acc_out = acc;
   a.ns = 2;
   cudaStream_t s = (cudaStream_t)stream;
+  if (use_brick((int)kp)) switch (kp) {
+      case 8: return launch_brick<8>(a, s);
+      case 16: return launch_brick<16>(a, s);
+      case 24: return launch_brick<24>(a, s);
+      case 32: return launch_brick<32>(a, s);
+      case 40: return launch_brick<40>(a, s);
+      case 48: return launch_brick<48>(a, s);
+      case 56: return launch_brick<56>(a, s);
+    }
   switch (kp) {
     case 8: return launch_tmem<8>(a, s);
     case 16: return launch_tmem<16>(a, s);

@@ -418,7 +418,8 @@ def test_many_rhs_with_gradient(cuda):
 def test_tmem_sweep_matches_tma_sweep_and_reference(cuda, monkeypatch, n, depth, order, nrhs,
                                                     clustered):
     """The float32 engine sweep with the A operand in tensor memory (ranks
-    <= 64) against the TMA-staged sweep on the same instance inputs, and
+    <= 64; stage-ring and brick-fed kernels) against the TMA-staged sweep on
+    the same instance inputs, and
     against the reference; uniform and clustered (pruned boxes) clouds, 1 and
     2 right-hand sides; re-evaluation is bitwise deterministic."""
     from paper_2408_07436_b200 import FmmConfig, setup
@@ -429,16 +430,18 @@ def test_tmem_sweep_matches_tma_sweep_and_reference(cuda, monkeypatch, n, depth,
     q = rng.random((n, nrhs)) if nrhs > 1 else rng.random(n)
     kw = dict(depth=depth, order_equiv=order, backend="blas", precision="f32", sigma_min=1e-6)
     res = {}
-    for sweep in ("tma", "tmem"):
-        monkeypatch.setenv("KIFMM_F32_SWEEP", sweep)
+    for sweep in ("tma", "tmem", "brick"):      # brick: the brick-fed variant (KIFMM_TMEM_BRICK=1)
+        monkeypatch.setenv("KIFMM_F32_SWEEP", "tma" if sweep == "tma" else "tmem")
+        monkeypatch.setenv("KIFMM_TMEM_BRICK", "1" if sweep == "brick" else "0")
         inst = setup(pts, pts, FmmConfig(**kw))
-        assert inst.device.blas.tmem == (sweep == "tmem")
+        assert inst.device.blas.tmem == (sweep != "tma")
         res[sweep] = np.asarray(inst.evaluate(q), dtype=np.float64)
-        if sweep == "tmem":
+        if sweep != "tma":
             again = np.asarray(inst.evaluate(q), dtype=np.float64)
             assert np.array_equal(res[sweep], again)
-    rel = np.abs(res["tmem"] - res["tma"]) / np.abs(res["tma"])
-    assert rel.max() <= TOL["f32"], rel.max()
+    for sweep in ("tmem", "brick"):
+        rel = np.abs(res[sweep] - res["tma"]) / np.abs(res["tma"])
+        assert rel.max() <= TOL["f32"], (sweep, rel.max())
     if nrhs == 1:
         want, _ = _reference_run(pts, q, kw)
         assert parity_report(res["tmem"], want)["max_rel"] <= TOL["f32"]

@@ -74,6 +74,7 @@ int main() {
   struct C { int ns, stage, chunk; } cs[] = {
       {3, 57344, 28672}, {4, 49152, 24576}, {6, 32768, 16384}, {8, 24576, 12288},
       {3, 57344, 4096},  {12, 16384, 16384}, {2, 57344, 28672}, {6, 32768, 32768},
+      {4, 25088, 25088}, {4, 25088, 6272}, {2, 25088, 25088}, {8, 25088, 25088},
   };
   for (auto c : cs) {
     const int iters = 2000;
