@@ -353,22 +353,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
         // TF32), in registers before waiting for the TMEM buffers
         uint32_t hv[KP], lv[KP];
         const unsigned char* sb = smem + s * SBYTES;
-#pragma unroll
-        for (int i = 0; i < KP / 4; ++i) {
-          const unsigned char* src;
-          if (i < 8)
-            src = sb + m * 128 + (((i & 7) ^ (m & 7)) << 4);
-          else if (SW1)
-            src = sb + TMT * 128 + m * 128 + (((i & 7) ^ (m & 7)) << 4);
-          else
-            src = sb + TMT * 128 + m * (W1 * 4) + (i - 8) * 16;
-          const float4 c4 = *reinterpret_cast<const float4*>(src);
+        auto split4 = [&](int i, const float4& c4) {
           const float f[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             hv[4 * i + j] = (__float_as_uint(f[j]) + 0x1000u) & 0xFFFFE000u;
             lv[4 * i + j] = __float_as_uint(f[j] - __uint_as_float(hv[4 * i + j]));
           }
+        };
+#pragma unroll
+        for (int i = 0; i < (KP < 32 ? KP / 4 : 8); ++i)
+          split4(i, *reinterpret_cast<const float4*>(sb + m * 128 + (((i & 7) ^ (m & 7)) << 4)));
+        if (SW1) {
+#pragma unroll
+          for (int i = 8; i < KP / 4; ++i)
+            split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * 128 +
+                                                       (((i & 7) ^ (m & 7)) << 4)));
+        } else {
+          // linear second box: rows W1 * 4 bytes apart (the 2-way bank conflict
+          // of rows i, i + 4 costs less than swapping chunk pairs: 284 vs 303 us)
+#pragma unroll
+          for (int i = 8; i < KP / 4; ++i)
+            split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * (W1 * 4) + (i - 8) * 16));
         }
         // this group's previous MMAs done: A_k reusable (and D_k promoted below)
         if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);

@@ -892,7 +892,11 @@ class DeviceFmm:
                 m2l(lvl)
             forked[lvl] = st
 
-        if overlap and d >= 3:
+        # KIFMM_FINE_M2L_AT: fork the finest level's M2L right after P2M
+        # ("p2m") or after the M2M pass ("m2m": the persistent sweep then
+        # cannot hold the SMs the latency-bound M2M chain needs)
+        fine_at = os.environ.get("KIFMM_FINE_M2L_AT", "p2m")
+        if overlap and d >= 3 and fine_at == "p2m":
             fork_m2l(d)
         phase("m2m")
         # M2M down to level 2 (levels 0-1 carry no M2L): children stacked in
@@ -905,6 +909,8 @@ class DeviceFmm:
                      a_child=self.src_child[lvl], child_w=n_e, a_nrhs=R)
             if overlap and lvl - 1 >= 3:
                 fork_m2l(lvl - 1)
+        if overlap and d >= 3 and fine_at == "m2m":
+            fork_m2l(d)
         if overlap and p2p_after == "m2m":
             fork_p2p()
         for lvl in range(2, d + 1):

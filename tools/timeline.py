@@ -36,7 +36,10 @@ t0 = g[0].time_range.start
 end = max(e.time_range.end for e in g)
 print(f"evaluates found {len(groups)}; last spans {end - t0:.1f} us, {len(g)} kernels")
 for e in g:
-    nm = e.name.split("(")[0].split("<")[0][-40:]
+    nm = e.name
+    for pre in ("void ", "(anonymous namespace)::", "kifmm::"):
+        nm = nm.replace(pre, "")
+    nm = nm.split("(")[0].split("<")[0][-40:]
     s = e.time_range.start - t0
     print(f"{s:8.1f} {s + e.time_range.elapsed_us():8.1f} {e.time_range.elapsed_us():7.1f}  "
           f"st{getattr(e, 'device_resource_id', -1):>4}  {nm}")
