@@ -63,6 +63,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
+#ifdef KIFMM_MBAR_DEBUG
+__device__ unsigned g_mbar_dbg_n = 0;
+__device__ unsigned g_mbar_dbg[256];
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, bool sleep) {
   const uint32_t a = smem_u32(bar);
   uint32_t done = 0, spins = 0;
@@ -75,7 +79,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, bool s
         : "memory");
     if (done) break;
     if (sleep) __nanosleep(64);
+#ifdef KIFMM_MBAR_DEBUG
+    if (++spins > (1u << 22)) {            // debug build: record the stuck wait and give up
+      const unsigned i = atomicAdd(&g_mbar_dbg_n, 1u);
+      if (i < 64) {
+        g_mbar_dbg[4 * i] = blockIdx.x;
+        g_mbar_dbg[4 * i + 1] = threadIdx.x;
+        g_mbar_dbg[4 * i + 2] = a;
+        g_mbar_dbg[4 * i + 3] = parity;
+      }
+      break;
+    }
+#else
     if (++spins > (1u << 27)) __trap();    // watchdog: a lost arrive faults, never hangs
+#endif
   }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -460,6 +477,293 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
       }
       g += x.nv;
     }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined variant (KIFMM_TMEM_PIPE=1, opt-in): ONE TMEM accumulator and
+// three A buffers instead of an (accumulator, A) pair per group.  The traces
+// of the kernel above show each group's serial chain per vector - wait for
+// its previous MMAs, tcgen05.st of the next A, hand-over, issue - as the
+// bound; with A triple-buffered a loader group stores vector v while the
+// MMAs of v - 1 and v - 2 run, and only the tensor pipe (620 cycles per
+// vector at KP = 56) and the TMEM stores (~550) remain as per-vector costs.
+//
+// Roles (320 threads): warp 0 lane 0 loads stages (unchanged); warps 1-4
+// and 5-8 are loader groups taking alternate vectors (A buffer v % 3);
+// warp 9 lane 0 issues every MMA into the single accumulator D, in vector
+// order, after the vector's loader group signalled ready[v % 3] (the group
+// waited for the stage itself, so the issuer waits on one barrier per
+// vector); blocks of FLUSH_V consecutive vectors of an item accumulate in
+// D, the issuer commits dfull at a block end and waits dfree before the
+// next block's first MMA; blocks are promoted into registers by the groups
+// alternately (block kb by group kb % 2), which combine at the item end.
+//
+// Measured (tools/trace_tmem.py, config 2 level 5): the loaders now run
+// ahead, but the single issue stream advances only every ~1550 cycles per
+// vector (one accumulator, every MMA dependent on the previous vector's),
+// against ~1150 for two interleaved accumulators: 350-375 us vs 280-285 us.
+// An mbarrier hand-over to the issuer was worse still (~1700 cycles), hence
+// the named barriers.
+constexpr int NTHREADS_P = NTHREADS + 32;
+constexpr int NA = 3;
+
+template <int KP>
+__global__ void __launch_bounds__(NTHREADS_P, 1) m2l_sweep_pipe_kernel(
+    const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm2,
+    const TmemArgs a) {
+  constexpr int N1 = 2 * KP;
+  constexpr int N2 = (KP + 15) / 16 * 16;
+  constexpr int W1 = KP > 32 ? KP - 32 : 0;
+  constexpr bool SW1 = W1 == 32;
+  constexpr uint32_t ABYTES = TMT * 128u + TMT * W1 * 4u;
+  constexpr uint32_t BBYTES = 2u * KP * KP * 4u;
+  constexpr uint32_t SBYTES = (ABYTES + BBYTES + 1023u) / 1024u * 1024u;
+  constexpr int NEED = N1 + NA * 2 * KP;
+  constexpr uint32_t TMEM_COLS = NEED <= 256 ? 256 : 512;
+  static_assert(NEED <= 512, "TMEM budget");
+  static_assert(KP % 8 == 0 && N1 <= 256, "shape");
+
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ns = a.ns;
+  long long* const trace_buf = (blockIdx.x == 0 && g_trace_h == a.h) ? g_trace : nullptr;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * SBYTES);
+  uint64_t* empty = full + ns;
+  uint64_t* afree = empty + ns;         // [NA] the MMAs reading A buffer i completed
+  uint64_t* ready = afree + NA;         // [NA] A buffer i stored by its 4 loader warps
+  // [2] by block parity: one barrier per promoting group, so no waiter
+  // ever runs two phases ahead of a barrier (parity aliasing)
+  uint64_t* dfull = ready + NA;         // block kb's last MMAs completed (dfull[kb & 1])
+  uint64_t* dfree = dfull + 2;          // block kb promoted by its 4 warps (dfree[kb & 1])
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dfree + 2);
+  float4* red = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 15) &
+                                          ~uintptr_t(15));
+
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(&afree[i], 1);
+      mbar_init(&ready[i], 4);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&dfull[b], 1);
+      mbar_init(&dfree[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+    if (W1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2)) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t dcol = tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0;
+      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+        const Item x = item_of(a, it);
+        const TileGeom tg = tile_geom(a, x.slot);
+        const int32_t* tv = a.class_tv + tg.cls * 189 + x.j0;
+        for (int v = 0; v < x.nv; ++v, ++g) {
+          const int s = g % ns;
+          if (g >= ns) mbar_wait(&empty[s], ((g / ns) - 1) & 1, false);
+          trace(4, g);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                           smem_u32(&full[s])),
+                       "r"(ABYTES + BBYTES)
+                       : "memory");
+          const int t = tv[v];
+          unsigned char* sb = smem + s * SBYTES;
+          const int ox = a.offsets[3 * t], oy = a.offsets[3 * t + 1], oz = a.offsets[3 * t + 2];
+          const int qx = tg.px + ox, qy = tg.py + oy, qz = tg.pz + oz;
+          const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
+          const int cz = tg.iz0 + (qz >> 1), cy = tg.iy0 + (qy >> 1), cx = tg.ix0 + (qx >> 1);
+          tma_load_5d(sb, &tm, 0, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
+          if (W1) tma_load_5d(sb + TMT * 128, &tm2, 32, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
+          bulk_copy(sb + ABYTES, a.bpair + (int64_t)t * (2 * KP * KP), BBYTES, &full[s]);
+        }
+      }
+      for (int gg = g - ns < 0 ? 0 : g - ns; gg < g; ++gg)
+        mbar_wait(&empty[gg % ns], (gg / ns) & 1, true);
+    }
+    __syncwarp();
+  } else if (warp >= 1 && warp < 1 + 4 * NG) {
+    const int grp = (warp - 1) >> 2;
+    const int q4 = warp & 3;
+    const int m = q4 * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    float acc[KP];
+    int g = 0, kb = 0;                     // global vector / block counters
+    auto promote = [&](int blk) {
+      mbar_wait(&dfull[blk & 1], (blk >> 1) & 1, false);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < KP / 8; ++c) {
+        uint32_t u[8], w[8];
+        tmem_ld8(dcol + lane_base + c * 8, u);
+        tmem_ld8(dcol + lane_base + KP + c * 8, w);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[c * 8 + i] += __uint_as_float(u[i]) + __uint_as_float(w[i]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dfree[blk & 1]);
+    };
+    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+      const Item x = item_of(a, it);
+#pragma unroll
+      for (int c = 0; c < KP; ++c) acc[c] = 0.f;
+      for (int v = 0; v < x.nv; ++v) {
+        const int gg = g + v;
+        if (v % NG == grp) {
+          const int s = gg % ns;
+          const int ab = gg % NA;
+          mbar_wait(&full[s], (gg / ns) & 1, false);
+          if (m == 0) trace(grp == 0 ? 0 : 5, gg);
+          uint32_t hv[KP], lv[KP];
+          const unsigned char* sb = smem + s * SBYTES;
+          auto split4 = [&](int i, const float4& c4) {
+            const float f[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              hv[4 * i + j] = (__float_as_uint(f[j]) + 0x1000u) & 0xFFFFE000u;
+              lv[4 * i + j] = __float_as_uint(f[j] - __uint_as_float(hv[4 * i + j]));
+            }
+          };
+#pragma unroll
+          for (int i = 0; i < (KP < 32 ? KP / 4 : 8); ++i)
+            split4(i, *reinterpret_cast<const float4*>(sb + m * 128 + (((i & 7) ^ (m & 7)) << 4)));
+#pragma unroll
+          for (int i = 8; i < KP / 4; ++i) {
+            if (SW1)
+              split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * 128 +
+                                                         (((i & 7) ^ (m & 7)) << 4)));
+            else
+              split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * (W1 * 4) + (i - 8) * 16));
+          }
+          // A buffer ab free: the MMAs of vector gg - NA completed
+          if (gg >= NA) mbar_wait(&afree[ab], ((gg / NA) - 1) & 1, false);
+          if (m == 0) trace(grp == 0 ? 1 : 6, gg);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t acol = tmem + N1 + ab * (2 * KP);
+#pragma unroll
+          for (int c = 0; c < KP / 8; ++c) {
+            tmem_st8(acol + lane_base + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&hv[c * 8]));
+            tmem_st8(acol + lane_base + KP + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&lv[c * 8]));
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          // hand-over on a named barrier (4 loader warps + the issuer warp):
+          // an mbarrier wait in the MMA-issuing thread stalls behind its
+          // in-flight MMAs, a bar.sync does not
+          asm volatile("bar.arrive %0, %1;" ::"r"(4 + ab), "n"(160) : "memory");
+        }
+        // block boundary: block kb ended at v - 1 -> its promoter (group kb % 2)
+        if (v > 0 && v % FLUSH_V == 0) {
+          if ((kb & 1) == grp) promote(kb);
+          ++kb;
+        }
+      }
+      if (x.nv > 0) {
+        if ((kb & 1) == grp) promote(kb);
+        ++kb;
+      }
+#pragma unroll
+      for (int c = 0; c < KP; c += 8) {
+        if (grp == 1) {
+          red[2 * m] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+          red[2 * m + 1] = make_float4(acc[c + 4], acc[c + 5], acc[c + 6], acc[c + 7]);
+        }
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (grp == 0) {
+          const float4 u = red[2 * m], w = red[2 * m + 1];
+          acc[c] += u.x;
+          acc[c + 1] += u.y;
+          acc[c + 2] += u.z;
+          acc[c + 3] += u.w;
+          acc[c + 4] += w.x;
+          acc[c + 5] += w.y;
+          acc[c + 6] += w.z;
+          acc[c + 7] += w.w;
+        }
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+      }
+      const int32_t tgt = a.tile_targets[(int64_t)x.slot * TMT + m];
+      if (grp == 0 && tgt >= 0) {
+        float* o = a.acc_out + ((int64_t)tgt * a.nrhs + x.r) * a.ld + (int64_t)x.split * a.ostride;
+#pragma unroll
+        for (int c = 0; c < KP; c += 4)
+          *reinterpret_cast<float4*>(o + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+      }
+      g += x.nv;
+    }
+  } else if (warp == 1 + 4 * NG) {
+    // ------------------------------ MMA issuer (lane 0; the warp joins the barriers)
+    constexpr uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N1 >> 3) << 17) |
+                                ((uint32_t)(TMT >> 4) << 24);
+    constexpr uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N2 >> 3) << 17) |
+                                ((uint32_t)(TMT >> 4) << 24);
+    constexpr uint32_t SBO = (KP / 4) * 128;
+    int g = 0, kb = 0;
+    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+      const Item x = item_of(a, it);
+      for (int v = 0; v < x.nv; ++v) {
+        const int gg = g + v;
+        const int s = gg % ns;
+        const int ab = gg % NA;
+        const bool first = v % FLUSH_V == 0;
+        const bool last = v % FLUSH_V == FLUSH_V - 1 || v == x.nv - 1;
+        if (first && kb > 0 && lane == 0)
+          mbar_wait(&dfree[(kb - 1) & 1], ((kb - 1) >> 1) & 1, false);   // D promoted
+        asm volatile("bar.sync %0, %1;" ::"r"(4 + ab), "n"(160) : "memory");
+        if (lane == 0) {
+          if (trace_buf) trace(3, gg);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t acol = tmem + N1 + ab * (2 * KP);
+          const uint32_t bp = smem_u32(smem + s * SBYTES + ABYTES);
+#pragma unroll
+          for (int ks = 0; ks < KP / 8; ++ks) {
+            const uint64_t db = desc_nosw(bp + ks * 256, 128, SBO);
+            mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, (first ? 0 : 1) | ks);
+            mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
+          }
+          mma_commit(&afree[ab]);
+          mma_commit(&empty[s]);
+          if (last) mma_commit(&dfull[kb & 1]);
+        }
+        __syncwarp();
+        if (last) ++kb;
+      }
+      g += x.nv;
+    }
+    if (lane == 0) {
+      for (int gg = g - NA < 0 ? 0 : g - NA; gg < g; ++gg)
+        mbar_wait(&afree[gg % NA], (gg / NA) & 1, true);
+      // wait for the final promotion so no MMA-side arrive targets this CTA
+      // after exit
+      if (kb > 0) mbar_wait(&dfree[(kb - 1) & 1], ((kb - 1) >> 1) & 1, true);
+    }
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -927,6 +1231,42 @@ int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   return launch_status();
 }
 
+template <int KP>
+int launch_pipe(const TmemArgs& a0, cudaStream_t stream) {
+  TmemArgs a = a0;
+  constexpr int W1 = KP > 32 ? KP - 32 : 0;
+  CUtensorMap tm, tm2;
+  memset(&tm, 0, sizeof(tm));
+  memset(&tm2, 0, sizeof(tm2));
+  int st = make_map(&tm, a.q, KP, a.h, 8 * (int64_t)a.nrhs, 32, true);
+  if (!st && W1) st = make_map(&tm2, a.q, KP, a.h, 8 * (int64_t)a.nrhs, W1, W1 == 32);
+  if (st) return st;
+  static int ns_env = -1;
+  if (ns_env < 0) {
+    const char* e = getenv("KIFMM_TMEM_STAGES");
+    ns_env = e ? atoi(e) : 4;             // config 2 on B200: 4 ~ 3 stages (281-288 us), 2: 362 us
+    if (ns_env < 2) ns_env = 2;
+  }
+  const size_t sbytes = ((size_t)TMT * 128 + (size_t)TMT * W1 * 4 + 2ull * KP * KP * 4 + 1023) /
+                        1024 * 1024;
+  int ns = ns_env;
+  while (ns > 2 && 1024 + ns * sbytes + 256 + 4096 > 227 * 1024) --ns;
+  a.ns = ns;
+  const size_t smem = 1024 + ns * sbytes + (2 * ns + 2 * NA + 4) * 8 + 32 + 4096;
+  // persistent CTAs: one per SM, or KIFMM_TMEM_GRID (fewer leaves SMs to the
+  // concurrent small kernels of the other streams)
+  static int grid_env = -1;
+  if (grid_env < 0) {
+    const char* e = getenv("KIFMM_TMEM_GRID");
+    grid_env = e ? atoi(e) : 0;
+  }
+  const int g_max = grid_env > 0 && grid_env < sm_count() ? grid_env : sm_count();
+  const int grid = a.n_items < g_max ? a.n_items : g_max;
+  set_max_smem((const void*)m2l_sweep_pipe_kernel<KP>, smem);
+  m2l_sweep_pipe_kernel<KP><<<grid, NTHREADS_P, smem, stream>>>(tm, tm2, a);
+  return launch_status();
+}
+
 // shared memory of the brick kernel with nsb core-pair stages
 constexpr size_t brick_smem(int kp, int nsb) {
   return 1024 + 2 * (size_t)brick_bytes(kp) + (size_t)nsb * 2 * kp * kp * 4 + (2 * nsb + 4 + 2 * NG) * 8 +
@@ -983,6 +1323,13 @@ bool use_brick(int kp) {
 }  // namespace
 
 extern "C" {
+
+#ifdef KIFMM_MBAR_DEBUG
+int kifmm_mbar_debug_read(unsigned* host) {
+  cudaMemcpyFromSymbol(host, g_mbar_dbg_n, sizeof(unsigned));
+  return (int)cudaMemcpyFromSymbol(host + 1, g_mbar_dbg, sizeof(g_mbar_dbg));
+}
+#endif
 
 // Debug: record the timeline of CTA 0 of the following sweeps into buf
 // (12 x 1024 int64 clock64 stamps; events documented at trace()); null stops.
@@ -1058,6 +1405,19 @@ int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int
       case 40: return launch_brick<40>(a, s);
       case 48: return launch_brick<48>(a, s);
       case 56: return launch_brick<56>(a, s);
+    }
+  // KIFMM_TMEM_PIPE=1: the pipelined kernel (opt-in; 350-375 us against
+  // 280-285 us for the two-accumulator kernel on config 2 level 5)
+  const char* pe = getenv("KIFMM_TMEM_PIPE");
+  if (pe && atoi(pe) != 0) switch (kp) {
+      case 8: return launch_pipe<8>(a, s);
+      case 16: return launch_pipe<16>(a, s);
+      case 24: return launch_pipe<24>(a, s);
+      case 32: return launch_pipe<32>(a, s);
+      case 40: return launch_pipe<40>(a, s);
+      case 48: return launch_pipe<48>(a, s);
+      case 56: return launch_pipe<56>(a, s);
+      case 64: return launch_pipe<64>(a, s);
     }
   switch (kp) {
     case 8: return launch_tmem<8>(a, s);

@@ -430,16 +430,18 @@ def test_tmem_sweep_matches_tma_sweep_and_reference(cuda, monkeypatch, n, depth,
     q = rng.random((n, nrhs)) if nrhs > 1 else rng.random(n)
     kw = dict(depth=depth, order_equiv=order, backend="blas", precision="f32", sigma_min=1e-6)
     res = {}
-    for sweep in ("tma", "tmem", "brick"):      # brick: the brick-fed variant (KIFMM_TMEM_BRICK=1)
+    # brick / pipe: the opt-in variants (KIFMM_TMEM_BRICK=1 / KIFMM_TMEM_PIPE=1)
+    for sweep in ("tma", "tmem", "brick", "pipe"):
         monkeypatch.setenv("KIFMM_F32_SWEEP", "tma" if sweep == "tma" else "tmem")
         monkeypatch.setenv("KIFMM_TMEM_BRICK", "1" if sweep == "brick" else "0")
+        monkeypatch.setenv("KIFMM_TMEM_PIPE", "1" if sweep == "pipe" else "0")
         inst = setup(pts, pts, FmmConfig(**kw))
         assert inst.device.blas.tmem == (sweep != "tma")
         res[sweep] = np.asarray(inst.evaluate(q), dtype=np.float64)
         if sweep != "tma":
             again = np.asarray(inst.evaluate(q), dtype=np.float64)
             assert np.array_equal(res[sweep], again)
-    for sweep in ("tmem", "brick"):
+    for sweep in ("tmem", "brick", "pipe"):
         rel = np.abs(res[sweep] - res["tma"]) / np.abs(res["tma"])
         assert rel.max() <= TOL["f32"], (sweep, rel.max())
     if nrhs == 1:
