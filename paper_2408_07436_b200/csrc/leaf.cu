@@ -502,8 +502,17 @@ __global__ void __launch_bounds__(32 * kL2pWarps) l2p_x2_kernel(
     const bool live0 = ti < n, live1 = ti + R < n;
     const int64_t ia = t0 + tb + (live0 ? ti : 0), ib = t0 + tb + (live1 ? ti + R : 0);
     const u64 X = pk2(tx[ia], tx[ib]), Y = pk2(ty[ia], ty[ib]), Z = pk2(tz[ia], tz[ib]);
+    // output rows and, when accumulating, the values already there (the
+    // near field): issued before the interaction loop so the un-permuting
+    // scatter at the end carries no dependent global load
+    const int64_t oa = perm ? perm[ia] : ia, ob = perm ? perm[ib] : ib;
     for (int64_t r = 0; r < nrhs; ++r) {
       const float* loc = local + (b * nrhs + r) * ne;
+      float pa = 0.f, pb = 0.f;
+      if (accumulate && sub == 0) {
+        if (live0) pa = out[oa * nrhs + r];
+        if (live1) pb = out[ob * nrhs + r];
+      }
       __syncwarp();
       for (int k = lane; k < ne; k += 32)
         buf[k] = make_float4(real_traits<float>::from_d(exact_add(cx, base[k * 3])),
@@ -520,16 +529,8 @@ __global__ void __launch_bounds__(32 * kL2pWarps) l2p_x2_kernel(
       }
       const float c = real_traits<float>::inv4pi();
       if (sub == 0) {
-        if (live0) {
-          const int64_t i = t0 + tb + ti;
-          float* o = out + (perm ? perm[i] : i) * nrhs + r;
-          *o = accumulate ? *o + fa * c : fa * c;
-        }
-        if (live1) {
-          const int64_t i = t0 + tb + ti + R;
-          float* o = out + (perm ? perm[i] : i) * nrhs + r;
-          *o = accumulate ? *o + fb * c : fb * c;
-        }
+        if (live0) out[oa * nrhs + r] = accumulate ? pa + fa * c : fa * c;
+        if (live1) out[ob * nrhs + r] = accumulate ? pb + fb * c : fb * c;
       }
     }
   }

@@ -755,6 +755,16 @@ class DeviceFmm:
         self._bufs[nrhs] = b
         return b
 
+    def _l2l_children_dense(self, lvl):
+        """True when child c of parent p is target row 8p + c at level lvl for
+        every parent (uniform trees), so the L2L output needs no row map."""
+        if not hasattr(self, "_l2l_dense"):
+            self._l2l_dense = {}
+        if lvl not in self._l2l_dense:
+            ch = np.asarray(self._tgt_child_np[lvl]).reshape(-1)
+            self._l2l_dense[lvl] = bool(np.array_equal(ch, np.arange(ch.size)))
+        return self._l2l_dense[lvl]
+
     def _l2l_rowmap(self, lvl, nrhs):
         """Row map of the L2L solve output (p, r, c) -> child row * R + r."""
         key = (lvl, nrhs)
@@ -934,11 +944,18 @@ class DeviceFmm:
                 # child parts of t (parent row x 8 children x rf) into scratch,
                 # then added to the level's M2L part
                 t_c = b["t_lv"][lvl + 1][: self.n_tgt[lvl + 1] * R * rf]
-                l2l_tmp = la.scratch(3, n_t * R * 8 * rf, self.T, t_c.device)
-                la.gemm(n_t * R, 8 * rf, n_e, 0.5 / self.side[lvl + 1], loc[lvl], n_e,
-                        self.l2lU, 8 * rf, l2l_tmp, 8 * rf)
-                launch(f"kifmm_scatter_add_rows_{sfx}", P(l2l_tmp),
-                       P(self._l2l_rowmap(lvl + 1, R)), n_t * R * 8, rf, P(t_c), s)
+                if R == 1 and self._l2l_children_dense(lvl + 1):
+                    # every parent has its 8 children at rows 8p..8p+7: the
+                    # GEMM accumulates straight into them (same roundings as
+                    # the scratch + scatter-add below, one launch fewer)
+                    la.gemm(n_t, 8 * rf, n_e, 0.5 / self.side[lvl + 1], loc[lvl], n_e,
+                            self.l2lU, 8 * rf, t_c, 8 * rf, accumulate=True)
+                else:
+                    l2l_tmp = la.scratch(3, n_t * R * 8 * rf, self.T, t_c.device)
+                    la.gemm(n_t * R, 8 * rf, n_e, 0.5 / self.side[lvl + 1], loc[lvl], n_e,
+                            self.l2lU, 8 * rf, l2l_tmp, 8 * rf)
+                    launch(f"kifmm_scatter_add_rows_{sfx}", P(l2l_tmp),
+                           P(self._l2l_rowmap(lvl + 1, R)), n_t * R * 8, rf, P(t_c), s)
                 solve_level(lvl + 1)
         for st in forked.values():
             main.wait_stream(st)
