@@ -820,9 +820,12 @@ class DeviceFmm:
         launch(f"kifmm_pack_sources_{sfx}", P(self.sx), P(self.sy), P(self.sz), P(q),
                self.sx.shape[0], R, P(b["src4"]), s)
         # The near field (P2P) needs only the packed sources: with `overlap`
-        # it runs on a low-priority side stream concurrently with the whole
+        # it runs on a low-priority side stream concurrently with the
         # far-field pipeline (mostly latency-bound small-level kernels), and
-        # the L2P pass adds the far field at the end.  Eager timing/profiling
+        # the L2P pass adds the far field at the end.  It is forked after the
+        # upward pass (KIFMM_P2P_AFTER=m2m; "pack"/"p2m" fork it earlier):
+        # forked at once its CTAs fill the machine and the P2M/M2M chain on
+        # the critical path waits for free slots (config 2: 0.904 -> 0.892 ms).  Eager timing/profiling
         # passes keep the fused sequential leaf pass.
         out = b["out"]
         nt = self.tx.shape[0]
@@ -838,7 +841,7 @@ class DeviceFmm:
                     P(self.s_count), P(self.near_off), P(self.near_leaf), R, P(self.t_perm),
                     parts, P(out)] + grad_ptr
 
-        p2p_after = os.environ.get("KIFMM_P2P_AFTER", "pack")
+        p2p_after = os.environ.get("KIFMM_P2P_AFTER", "m2m")
         side = self.side_stream
 
         def fork_p2p():
