@@ -282,13 +282,39 @@ int kifmm_fft_inverse_f64(const double* phat, int64_t nrhs, int64_t order,
                           const int32_t* slot_box, int64_t ntc, double level_scale, double* check,
                           void* stream);
 
+/* Mutual near field, sources == targets (same tree), float32, potential.
+ * Replaces _hot.p2p_blocked (_hot.pyx:91-138) on the gather plan of
+ * engine.py:224-256 when the two clouds are one point set: each unordered
+ * pair of adjacent leaves (A < B, Morton order) is evaluated once, one
+ * rsqrt feeding both directions; the leaf's own block is direct (r2 == 0
+ * -> 0).  Results go to partial-sum slots (no atomics, deterministic):
+ *   P[r*pstride + base[B] + s*n_B + t], s = 0: B's row sums, s = 1..nlow_B:
+ *   the column sums of B's s-th lower neighbour (its entry s of B's near list);
+ * near_dst[e] = base[B] + s*n_B for the entry e = (A, B > A) of A's near
+ * list.  guard != 0: also guard the cross-leaf pairs against r2 == 0. */
+int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, const int32_t* leaf_start,
+                         const int32_t* leaf_count, int64_t n_leaves, const float* src4,
+                         int64_t npts, const int32_t* near_off, const int32_t* near_leaf,
+                         const int32_t* near_dst, const int32_t* base, int64_t nrhs,
+                         int64_t pstride, int guard, float* P, void* stream);
+/* Final pass of the mutual near field: out[perm[i]*nrhs + r] = L2P(i)
+ * (engine.py:377-389) + sum_{s=0..nlow_b} P[r*pstride + base[b] + s*n_b + t]
+ * (slot order), the un-permute of engine.py:399-404. */
+int kifmm_l2p_mutual_f32(const float* tx, const float* ty, const float* tz, const int32_t* tleaf_start,
+                         const int32_t* tleaf_count, int64_t n_tleaves, const double* centers,
+                         const double* base_e, int64_t ne, const float* local, int64_t nrhs,
+                         const int64_t* perm, const int32_t* base, const int32_t* nlow,
+                         int64_t pstride, const float* P, float* out, void* stream);
+
 /* Leaf pass: fused L2P + P2P + un-permute (engine.py:377-404).  For target
  * leaf b and target i in it:
  *   out[perm[i]*nrhs + r] = sum_e K(t_i, center_b + base_e) local[(b*nrhs+r)*ne + e]
  *                         + sum_{near source leaves s of b, in order} sum_{j in s} K(t_i, s_j) q[j]
  * near_off (n_leaves+1) / near_leaf: source-leaf CSR (own leaf first, then
  * neighbours by Morton code, engine.py:231-240).  parts: bit 0 = L2P term,
- * bit 1 = P2P term, bit 2 = accumulate into out instead of overwriting;
+ * bit 1 = P2P term, bit 2 = accumulate into out instead of overwriting,
+ * bit 3 = guard every near-field record against r2 == 0 (not only the own
+ * leaf's: set when float32 rounding merges points of different leaves);
  * perm NULL -> tree order. */
 int kifmm_leaf_pass_f32(const float* tx, const float* ty, const float* tz, const int32_t* tleaf_start,
                         const int32_t* tleaf_count, int64_t n_tleaves, const double* centers,

@@ -15,6 +15,7 @@
 // Surface points are formed from a float64 leaf centre and float64 unit
 // offsets with an exact add and one rounding, which reproduces the host's
 // per-leaf surface arrays (engine.py:149-156) bit for bit.
+#include <climits>
 #include <cstdlib>
 #include <type_traits>
 
@@ -198,7 +199,9 @@ __global__ void __launch_bounds__(32 * kWarps) leaf_pass_kernel(
       if (parts & 2) {
         const V* srow = src4 + r * ns;
         int fill = 0;
-        int guarded = n1 > n0 ? scount[near_leaf[n0]] : 0;
+        // bit 3 of parts: every record may coincide with a target (float32
+        // rounding merged points of different leaves, checked at setup)
+        int guarded = (parts & 8) ? INT_MAX : n1 > n0 ? scount[near_leaf[n0]] : 0;
         auto flush = [&]() {
           cp_async_commit();
           cp_async_wait<0>();
@@ -420,7 +423,7 @@ __global__ void __launch_bounds__(32 * kWarps, KIFMM_LEAF_MINB) leaf_pass_x2_ker
       if (parts & 2) {
         const float4* srow = src4 + r * ns;
         int fill = 0;
-        int guarded = __shfl_sync(0xffffffffu, seg_cnt, 0);
+        int guarded = (parts & 8) ? INT_MAX : __shfl_sync(0xffffffffu, seg_cnt, 0);
         auto flush = [&]() {
           cp_async_commit();
           cp_async_wait<0>();
@@ -627,7 +630,7 @@ int leaf_pass(const T* tx, const T* ty, const T* tz, const int32_t* ts, const in
               const T* src4, int64_t ns, const int32_t* ss, const int32_t* sc, const int32_t* no,
               const int32_t* nlf, int64_t nrhs, const int64_t* perm, int parts, T* out,
               T* grad, void* stream) {
-  if (ntl < 0 || ne < 1 || nrhs < 1 || parts < 1 || parts > 7 || ns < 0) return KIFMM_EARG;
+  if (ntl < 0 || ne < 1 || nrhs < 1 || parts < 1 || parts > 15 || ns < 0) return KIFMM_EARG;
   if (ntl == 0) return 0;
   const auto* s4 = reinterpret_cast<const typename vec4<T>::v*>(src4);
   if constexpr (sizeof(T) == 4) {

@@ -56,6 +56,13 @@ constexpr int NTHREADS = 32 + 128 * NG;
 #endif
 constexpr int FLUSH_V = KIFMM_TMEM_FLUSH;   // vectors between promotions of a TMEM accumulator
 constexpr int BX = 4, BY = 4, BZ = 8;
+#ifndef KIFMM_TMEM_TAIL_LINEAR
+#define KIFMM_TMEM_TAIL_LINEAR 0
+#endif
+// 1: columns 32..KP of the source block in ONE linear box (2-way bank
+// conflicts on the loader reads); 0: 16- and 8-column boxes with the 64- and
+// 32-byte swizzles (conflict-free, one more TMA per stage)
+constexpr bool TAIL_LINEAR = KIFMM_TMEM_TAIL_LINEAR != 0;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -252,7 +259,7 @@ __global__ void __maxnreg__(KIFMM_TMEM_MAXNREG) m2l_sweep_tmem_kernel(
 __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
 #endif
     const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm2,
-    const TmemArgs a) {
+    const __grid_constant__ CUtensorMap tm3, const TmemArgs a) {
   constexpr int N1 = 2 * KP;
   constexpr int N2 = (KP + 15) / 16 * 16;
   // source block: columns [0, 32) in a 128-byte-swizzled box, the rest
@@ -260,6 +267,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
   // linear (rows of (KP - 32) * 4 bytes, exact width) otherwise
   constexpr int W1 = KP > 32 ? KP - 32 : 0;
   constexpr bool SW1 = W1 == 32;
+  // narrower remainders: a 16-column box with the 64-byte swizzle and/or an
+  // 8-column box with the 32-byte swizzle, so every loader read of the block
+  // is bank-conflict-free (a linear 24-column box costs 2-way conflicts)
+  constexpr int W16 = (!SW1 && !TAIL_LINEAR && W1 >= 16) ? 16 : 0;
+  constexpr int W8 = (!SW1 && !TAIL_LINEAR && W1 % 16 == 8) ? 8 : 0;
+  static_assert(SW1 || TAIL_LINEAR || W1 == W16 + W8, "remainder boxes");
+  constexpr uint32_t OFF8 = TMT * 128u + TMT * W16 * 4u;               // 8-column box
   constexpr uint32_t ABYTES = TMT * 128u + TMT * W1 * 4u;              // one source block
   constexpr uint32_t BBYTES = 2u * KP * KP * 4u;                       // one core pair
   constexpr uint32_t SBYTES = (ABYTES + BBYTES + 1023u) / 1024u * 1024u;
@@ -290,7 +304,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
     for (int k = 0; k < NG; ++k) mbar_init(&done[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
-    if (W1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2)) : "memory");
+    if (SW1 || W16 || (TAIL_LINEAR && W1)) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2)) : "memory");
+    if (W8) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm3)) : "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -326,7 +341,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
           const int cz = tg.iz0 + (qz >> 1), cy = tg.iy0 + (qy >> 1), cx = tg.ix0 + (qx >> 1);
           tma_load_5d(sb, &tm, 0, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
-          if (W1) tma_load_5d(sb + TMT * 128, &tm2, 32, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
+          if (SW1 || W16 || (TAIL_LINEAR && W1)) tma_load_5d(sb + TMT * 128, &tm2, 32, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
+          if (W8) tma_load_5d(sb + OFF8, &tm3, 32 + W16, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
           bulk_copy(sb + ABYTES, a.bpair + (int64_t)t * (2 * KP * KP), BBYTES, &full[s]);
         }
       }
@@ -386,12 +402,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           for (int i = 8; i < KP / 4; ++i)
             split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * 128 +
                                                        (((i & 7) ^ (m & 7)) << 4)));
-        } else {
-          // linear second box: rows W1 * 4 bytes apart (the 2-way bank conflict
-          // of rows i, i + 4 costs less than swapping chunk pairs: 284 vs 303 us)
+        } else if (TAIL_LINEAR) {
 #pragma unroll
           for (int i = 8; i < KP / 4; ++i)
             split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * (W1 * 4) + (i - 8) * 16));
+        } else {
+          // 64-byte swizzle: 16-byte chunk c of row m at m * 64 + (c ^ (m >> 1 & 3)) * 16
+#pragma unroll
+          for (int i = 8; i < 8 + W16 / 4; ++i)
+            split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * 64 +
+                                                       (((i - 8) ^ ((m >> 1) & 3)) << 4)));
+          // 32-byte swizzle: chunk c of row m at m * 32 + (c ^ (m >> 2 & 1)) * 16
+#pragma unroll
+          for (int i = 8 + W16 / 4; i < KP / 4; ++i)
+            split4(i, *reinterpret_cast<const float4*>(sb + OFF8 + m * 32 +
+                                                       (((i - 8 - W16 / 4) ^ ((m >> 2) & 1)) << 4)));
         }
         // this group's previous MMAs done: A_k reusable (and D_k promoted below)
         if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);
@@ -485,677 +510,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
   }
 }
 
-// ---------------------------------------------------------------------------
-// Pipelined variant (KIFMM_TMEM_PIPE=1, opt-in): ONE TMEM accumulator and
-// three A buffers instead of an (accumulator, A) pair per group.  The traces
-// of the kernel above show each group's serial chain per vector - wait for
-// its previous MMAs, tcgen05.st of the next A, hand-over, issue - as the
-// bound; with A triple-buffered a loader group stores vector v while the
-// MMAs of v - 1 and v - 2 run, and only the tensor pipe (620 cycles per
-// vector at KP = 56) and the TMEM stores (~550) remain as per-vector costs.
-//
-// Roles (320 threads): warp 0 lane 0 loads stages (unchanged); warps 1-4
-// and 5-8 are loader groups taking alternate vectors (A buffer v % 3);
-// warp 9 lane 0 issues every MMA into the single accumulator D, in vector
-// order, after the vector's loader group signalled ready[v % 3] (the group
-// waited for the stage itself, so the issuer waits on one barrier per
-// vector); blocks of FLUSH_V consecutive vectors of an item accumulate in
-// D, the issuer commits dfull at a block end and waits dfree before the
-// next block's first MMA; blocks are promoted into registers by the groups
-// alternately (block kb by group kb % 2), which combine at the item end.
-//
-// Measured (tools/trace_tmem.py, config 2 level 5): the loaders now run
-// ahead, but the single issue stream advances only every ~1550 cycles per
-// vector (one accumulator, every MMA dependent on the previous vector's),
-// against ~1150 for two interleaved accumulators: 350-375 us vs 280-285 us.
-// An mbarrier hand-over to the issuer was worse still (~1700 cycles), hence
-// the named barriers.
-constexpr int NTHREADS_P = NTHREADS + 32;
-constexpr int NA = 3;
-
-template <int KP>
-__global__ void __launch_bounds__(NTHREADS_P, 1) m2l_sweep_pipe_kernel(
-    const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm2,
-    const TmemArgs a) {
-  constexpr int N1 = 2 * KP;
-  constexpr int N2 = (KP + 15) / 16 * 16;
-  constexpr int W1 = KP > 32 ? KP - 32 : 0;
-  constexpr bool SW1 = W1 == 32;
-  constexpr uint32_t ABYTES = TMT * 128u + TMT * W1 * 4u;
-  constexpr uint32_t BBYTES = 2u * KP * KP * 4u;
-  constexpr uint32_t SBYTES = (ABYTES + BBYTES + 1023u) / 1024u * 1024u;
-  constexpr int NEED = N1 + NA * 2 * KP;
-  constexpr uint32_t TMEM_COLS = NEED <= 256 ? 256 : 512;
-  static_assert(NEED <= 512, "TMEM budget");
-  static_assert(KP % 8 == 0 && N1 <= 256, "shape");
-
-  extern __shared__ __align__(1024) unsigned char smem_dyn[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ns = a.ns;
-  long long* const trace_buf = (blockIdx.x == 0 && g_trace_h == a.h) ? g_trace : nullptr;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * SBYTES);
-  uint64_t* empty = full + ns;
-  uint64_t* afree = empty + ns;         // [NA] the MMAs reading A buffer i completed
-  uint64_t* ready = afree + NA;         // [NA] A buffer i stored by its 4 loader warps
-  // [2] by block parity: one barrier per promoting group, so no waiter
-  // ever runs two phases ahead of a barrier (parity aliasing)
-  uint64_t* dfull = ready + NA;         // block kb's last MMAs completed (dfull[kb & 1])
-  uint64_t* dfree = dfull + 2;          // block kb promoted by its 4 warps (dfree[kb & 1])
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dfree + 2);
-  float4* red = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 15) &
-                                          ~uintptr_t(15));
-
-  if (tid == 0) {
-    for (int s = 0; s < ns; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int i = 0; i < NA; ++i) {
-      mbar_init(&afree[i], 1);
-      mbar_init(&ready[i], 4);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&dfull[b], 1);
-      mbar_init(&dfree[b], 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
-    if (W1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2)) : "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t dcol = tmem;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int g = 0;
-      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
-        const Item x = item_of(a, it);
-        const TileGeom tg = tile_geom(a, x.slot);
-        const int32_t* tv = a.class_tv + tg.cls * 189 + x.j0;
-        for (int v = 0; v < x.nv; ++v, ++g) {
-          const int s = g % ns;
-          if (g >= ns) mbar_wait(&empty[s], ((g / ns) - 1) & 1, false);
-          trace(4, g);
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                           smem_u32(&full[s])),
-                       "r"(ABYTES + BBYTES)
-                       : "memory");
-          const int t = tv[v];
-          unsigned char* sb = smem + s * SBYTES;
-          const int ox = a.offsets[3 * t], oy = a.offsets[3 * t + 1], oz = a.offsets[3 * t + 2];
-          const int qx = tg.px + ox, qy = tg.py + oy, qz = tg.pz + oz;
-          const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
-          const int cz = tg.iz0 + (qz >> 1), cy = tg.iy0 + (qy >> 1), cx = tg.ix0 + (qx >> 1);
-          tma_load_5d(sb, &tm, 0, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
-          if (W1) tma_load_5d(sb + TMT * 128, &tm2, 32, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
-          bulk_copy(sb + ABYTES, a.bpair + (int64_t)t * (2 * KP * KP), BBYTES, &full[s]);
-        }
-      }
-      for (int gg = g - ns < 0 ? 0 : g - ns; gg < g; ++gg)
-        mbar_wait(&empty[gg % ns], (gg / ns) & 1, true);
-    }
-    __syncwarp();
-  } else if (warp >= 1 && warp < 1 + 4 * NG) {
-    const int grp = (warp - 1) >> 2;
-    const int q4 = warp & 3;
-    const int m = q4 * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-    float acc[KP];
-    int g = 0, kb = 0;                     // global vector / block counters
-    auto promote = [&](int blk) {
-      mbar_wait(&dfull[blk & 1], (blk >> 1) & 1, false);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-      for (int c = 0; c < KP / 8; ++c) {
-        uint32_t u[8], w[8];
-        tmem_ld8(dcol + lane_base + c * 8, u);
-        tmem_ld8(dcol + lane_base + KP + c * 8, w);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[c * 8 + i] += __uint_as_float(u[i]) + __uint_as_float(w[i]);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&dfree[blk & 1]);
-    };
-    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
-      const Item x = item_of(a, it);
-#pragma unroll
-      for (int c = 0; c < KP; ++c) acc[c] = 0.f;
-      for (int v = 0; v < x.nv; ++v) {
-        const int gg = g + v;
-        if (v % NG == grp) {
-          const int s = gg % ns;
-          const int ab = gg % NA;
-          mbar_wait(&full[s], (gg / ns) & 1, false);
-          if (m == 0) trace(grp == 0 ? 0 : 5, gg);
-          uint32_t hv[KP], lv[KP];
-          const unsigned char* sb = smem + s * SBYTES;
-          auto split4 = [&](int i, const float4& c4) {
-            const float f[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              hv[4 * i + j] = (__float_as_uint(f[j]) + 0x1000u) & 0xFFFFE000u;
-              lv[4 * i + j] = __float_as_uint(f[j] - __uint_as_float(hv[4 * i + j]));
-            }
-          };
-#pragma unroll
-          for (int i = 0; i < (KP < 32 ? KP / 4 : 8); ++i)
-            split4(i, *reinterpret_cast<const float4*>(sb + m * 128 + (((i & 7) ^ (m & 7)) << 4)));
-#pragma unroll
-          for (int i = 8; i < KP / 4; ++i) {
-            if (SW1)
-              split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * 128 +
-                                                         (((i & 7) ^ (m & 7)) << 4)));
-            else
-              split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * (W1 * 4) + (i - 8) * 16));
-          }
-          // A buffer ab free: the MMAs of vector gg - NA completed
-          if (gg >= NA) mbar_wait(&afree[ab], ((gg / NA) - 1) & 1, false);
-          if (m == 0) trace(grp == 0 ? 1 : 6, gg);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t acol = tmem + N1 + ab * (2 * KP);
-#pragma unroll
-          for (int c = 0; c < KP / 8; ++c) {
-            tmem_st8(acol + lane_base + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&hv[c * 8]));
-            tmem_st8(acol + lane_base + KP + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&lv[c * 8]));
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          // hand-over on a named barrier (4 loader warps + the issuer warp):
-          // an mbarrier wait in the MMA-issuing thread stalls behind its
-          // in-flight MMAs, a bar.sync does not
-          asm volatile("bar.arrive %0, %1;" ::"r"(4 + ab), "n"(160) : "memory");
-        }
-        // block boundary: block kb ended at v - 1 -> its promoter (group kb % 2)
-        if (v > 0 && v % FLUSH_V == 0) {
-          if ((kb & 1) == grp) promote(kb);
-          ++kb;
-        }
-      }
-      if (x.nv > 0) {
-        if ((kb & 1) == grp) promote(kb);
-        ++kb;
-      }
-#pragma unroll
-      for (int c = 0; c < KP; c += 8) {
-        if (grp == 1) {
-          red[2 * m] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-          red[2 * m + 1] = make_float4(acc[c + 4], acc[c + 5], acc[c + 6], acc[c + 7]);
-        }
-        asm volatile("bar.sync 3, 256;" ::: "memory");
-        if (grp == 0) {
-          const float4 u = red[2 * m], w = red[2 * m + 1];
-          acc[c] += u.x;
-          acc[c + 1] += u.y;
-          acc[c + 2] += u.z;
-          acc[c + 3] += u.w;
-          acc[c + 4] += w.x;
-          acc[c + 5] += w.y;
-          acc[c + 6] += w.z;
-          acc[c + 7] += w.w;
-        }
-        asm volatile("bar.sync 3, 256;" ::: "memory");
-      }
-      const int32_t tgt = a.tile_targets[(int64_t)x.slot * TMT + m];
-      if (grp == 0 && tgt >= 0) {
-        float* o = a.acc_out + ((int64_t)tgt * a.nrhs + x.r) * a.ld + (int64_t)x.split * a.ostride;
-#pragma unroll
-        for (int c = 0; c < KP; c += 4)
-          *reinterpret_cast<float4*>(o + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-      }
-      g += x.nv;
-    }
-  } else if (warp == 1 + 4 * NG) {
-    // ------------------------------ MMA issuer (lane 0; the warp joins the barriers)
-    constexpr uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N1 >> 3) << 17) |
-                                ((uint32_t)(TMT >> 4) << 24);
-    constexpr uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N2 >> 3) << 17) |
-                                ((uint32_t)(TMT >> 4) << 24);
-    constexpr uint32_t SBO = (KP / 4) * 128;
-    int g = 0, kb = 0;
-    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
-      const Item x = item_of(a, it);
-      for (int v = 0; v < x.nv; ++v) {
-        const int gg = g + v;
-        const int s = gg % ns;
-        const int ab = gg % NA;
-        const bool first = v % FLUSH_V == 0;
-        const bool last = v % FLUSH_V == FLUSH_V - 1 || v == x.nv - 1;
-        if (first && kb > 0 && lane == 0)
-          mbar_wait(&dfree[(kb - 1) & 1], ((kb - 1) >> 1) & 1, false);   // D promoted
-        asm volatile("bar.sync %0, %1;" ::"r"(4 + ab), "n"(160) : "memory");
-        if (lane == 0) {
-          if (trace_buf) trace(3, gg);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t acol = tmem + N1 + ab * (2 * KP);
-          const uint32_t bp = smem_u32(smem + s * SBYTES + ABYTES);
-#pragma unroll
-          for (int ks = 0; ks < KP / 8; ++ks) {
-            const uint64_t db = desc_nosw(bp + ks * 256, 128, SBO);
-            mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, (first ? 0 : 1) | ks);
-            mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
-          }
-          mma_commit(&afree[ab]);
-          mma_commit(&empty[s]);
-          if (last) mma_commit(&dfull[kb & 1]);
-        }
-        __syncwarp();
-        if (last) ++kb;
-      }
-      g += x.nv;
-    }
-    if (lane == 0) {
-      for (int gg = g - NA < 0 ? 0 : g - NA; gg < g; ++gg)
-        mbar_wait(&afree[gg % NA], (gg / NA) & 1, true);
-      // wait for the final promotion so no MMA-side arrive targets this CTA
-      // after exit
-      if (kb > 0) mbar_wait(&dfree[(kb - 1) & 1], ((kb - 1) >> 1) & 1, true);
-    }
-    __syncwarp();
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Brick-fed variant.  For a target tile (4 x 4 x 8 same-parity targets) the
-// 189 vectors of the class list (device.locality_transfer_table order) fall
-// into runs of equal source sub-lattice sp and x shift, and within a run
-// every vector's 128 source rows are a (y, z)-shifted window of the same
-// 4 x 6 x 10 "brick" of source rows (shift (qy >> 1, qz >> 1) in {-1,0,1}^2).
-// The brick (240 rows, 53 KB at KP = 56) is loaded by ONE TMA box per run
-// (~8 vectors) and every vector gathers its A rows from it with shared loads;
-// only the core pair (25 KB, one bulk copy) streams per vector.
-//
-// Measured (tools/trace_brick.py, config 2 level 5): correct, but ~1320
-// cycles per vector against ~1150 for the stage-ring kernel above, so it is
-// not the default (see use_brick).  What the traces showed: the per-vector
-// chain of a group - MMA completion (~1000 cycles for 620 cycles of tensor
-// work), tcgen05.st of the next A (~550), hand-over and issue (~500) - is the
-// same in both kernels and bounds both; an mbarrier wait in a thread that
-// has MMAs in flight costs ~350 cycles, hence one issuer warp per group here
-// and the core-pair wait done by the loader warps.
-//
-// Brick rows are KP * 4 bytes apart (linear, no swizzle: one box, fewest
-// rows); the two-way bank conflict of rows i and i + 4 in an 8-lane LDS.128
-// phase is removed by reading each chunk pair in swapped order on lanes
-// with bit 2 set.  Two brick buffers (the next run's brick is prefetched
-// while the current run is swept), nsb core-pair stages.  Roles as in the
-// kernel above: warp 0 lane 0 loads bricks (one run ahead) and core pairs;
-// groups 0 / 1 take alternate vectors; every consumer warp releases a brick
-// after its last gather from it (8 arrivals).
-constexpr int BRX = BX, BRY = BY + 2, BRZ = BZ + 2;
-constexpr int BROWS = BRX * BRY * BRZ;                   // 240
-
-__host__ __device__ constexpr uint32_t brick_bytes(int kp) {
-  return ((uint32_t)BROWS * kp * 4u + 1023u) / 1024u * 1024u;
-}
-
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  asm volatile(
-      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(done)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return done != 0;
-}
-
-#ifndef KIFMM_BRICK_BCHUNK
-#define KIFMM_BRICK_BCHUNK 1      // bulk copies per core pair (BBYTES / chunk must stay a multiple of 16)
-#endif
-#ifndef KIFMM_BRICK_PF
-#define KIFMM_BRICK_PF 0          // L2 prefetch distance of the core pairs, in vectors (0: off)
-#endif
-#ifndef KIFMM_BRICK_ROT
-#define KIFMM_BRICK_ROT 1
-#endif
-// Walk position v of item it -> vector index: every item starts its walk at
-// a different point of the class list (all CTAs walking the same list in
-// lock step would read the same core pair from L2 at the same time).
-__device__ __forceinline__ int vrot(const Item& x, int it, int v) {
-  if (!KIFMM_BRICK_ROT || x.nv == 0) return v;
-  const int r = (int)(((unsigned)it * 2654435761u) >> 8) % x.nv;
-  const int w = v + r;
-  return w >= x.nv ? w - x.nv : w;
-}
-
-struct BrickMaps {
-  CUtensorMap m[1];
-};
-
-constexpr int NTHREADS_B = NTHREADS + 32 * NG;   // + one MMA issuer warp per group
-
-template <int KP>
-__global__ void __launch_bounds__(NTHREADS_B, 1) m2l_sweep_brick_kernel(
-    const __grid_constant__ BrickMaps maps, const TmemArgs a) {
-  constexpr int N1 = 2 * KP;
-  constexpr int N2 = (KP + 15) / 16 * 16;
-  constexpr uint32_t BRB = brick_bytes(KP);
-  constexpr uint32_t BBYTES = 2u * KP * KP * 4u;
-  constexpr int GCOLS = N1 + 2 * KP;
-  constexpr int NEED = NG * GCOLS;
-  constexpr uint32_t TMEM_COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128
-                                 : NEED <= 256 ? 256 : 512;
-  static_assert(NEED <= 512, "TMEM budget");
-  static_assert(KP % 8 == 0 && N1 <= 256, "shape");
-
-  extern __shared__ __align__(1024) unsigned char smem_dyn[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nsb = a.ns;
-  long long* const trace_buf = (blockIdx.x == 0 && g_trace_h == a.h) ? g_trace : nullptr;
-  unsigned char* bstage = smem + 2 * BRB;
-  uint64_t* full = reinterpret_cast<uint64_t*>(bstage + nsb * BBYTES);   // core pair landed
-  uint64_t* empty = full + nsb;         // the MMAs reading the core pair completed
-  uint64_t* bfull = empty + nsb;        // [2] brick landed
-  uint64_t* bempty = bfull + 2;         // [2] every consumer warp done gathering from the brick
-  uint64_t* done = bempty + 2;          // [NG]
-  uint64_t* ready = done + NG;          // [NG] the group's four warps stored their A rows
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + NG);
-  float4* red = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 15) &
-                                          ~uintptr_t(15));            // 128 x 8 floats
-  uint16_t* code = reinterpret_cast<uint16_t*>(red + 2 * TMT);       // [8 * 189]: sp | brick row shift << 3
-
-  for (int i = tid; i < 8 * 189; i += NTHREADS_B) {
-    const int cls = i / 189;
-    const int t = a.class_tv[i];
-    const int qx = ((cls >> 2) & 1) + a.offsets[3 * t], qy = ((cls >> 1) & 1) + a.offsets[3 * t + 1],
-              qz = (cls & 1) + a.offsets[3 * t + 2];
-    const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
-    const int sh = ((qy >> 1) + 1) * BRZ + ((qz >> 1) + 1);
-    code[i] = (uint16_t)(sp | (((qx >> 1) + 1) << 3) | (sh << 5));
-  }
-  if (tid == 0) {
-    for (int s = 0; s < nsb; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bfull[b], 1);
-      mbar_init(&bempty[b], 4 * NG);
-    }
-    for (int k = 0; k < NG; ++k) {
-      mbar_init(&done[k], 1);
-      mbar_init(&ready[k], 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[0])) : "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // brick cursor: the next run to load (item it_b, first vector vb)
-      int it_b = blockIdx.x, vb = 0, kb = 0;
-      auto skip_empty = [&]() {
-        while (it_b < a.n_items && item_of(a, it_b).nv == 0) it_b += gridDim.x;
-      };
-      skip_empty();
-      auto issue_brick = [&]() {
-        const Item x = item_of(a, it_b);
-        const TileGeom tg = tile_geom(a, x.slot);
-        const uint16_t* cv = code + tg.cls * 189 + x.j0;
-        const int key = cv[vrot(x, it_b, vb)] & 31;
-        const int sp = key & 7, sx = key >> 3;
-        const int b = kb & 1;
-        if (kb >= 2) mbar_wait(&bempty[b], ((kb >> 1) - 1) & 1, false);
-        trace(8, kb);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                         smem_u32(&bfull[b])),
-                     "r"((uint32_t)BROWS * KP * 4u)
-                     : "memory");
-        tma_load_5d(smem + b * BRB, &maps.m[0], 0, tg.iz0 - 1, tg.iy0 - 1, tg.ix0 - 1 + sx,
-                    sp * a.nrhs + x.r, &bfull[b]);
-        ++kb;
-        while (vb < x.nv && (cv[vrot(x, it_b, vb)] & 31) == key) ++vb;
-        if (vb == x.nv) {
-          vb = 0;
-          it_b += gridDim.x;
-          skip_empty();
-        }
-      };
-      int g = 0, run = -1;
-      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
-        const Item x = item_of(a, it);
-        const TileGeom tg = tile_geom(a, x.slot);
-        const uint16_t* cv = code + tg.cls * 189 + x.j0;
-        const int32_t* tv = a.class_tv + tg.cls * 189 + x.j0;
-        int prev_sp = -1;
-        for (int v = 0; v < x.nv; ++v, ++g) {
-          trace(9, g);
-          const int sp = cv[vrot(x, it, v)] & 31;
-          if (sp != prev_sp) {
-            ++run;
-            prev_sp = sp;
-          }
-          while (kb <= run) issue_brick();                  // this run's brick (normally issued already)
-          if (kb == run + 1 && it_b < a.n_items &&          // look one run ahead when its buffer is free
-              (kb < 2 || mbar_test(&bempty[kb & 1], ((kb >> 1) - 1) & 1)))
-            issue_brick();
-          const int s = g % nsb;
-          if (g >= nsb) mbar_wait(&empty[s], ((g / nsb) - 1) & 1, false);
-          trace(4, g);
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                           smem_u32(&full[s])),
-                       "r"(BBYTES)
-                       : "memory");
-#pragma unroll
-          for (int c = 0; c < KIFMM_BRICK_BCHUNK; ++c)
-            bulk_copy(bstage + s * BBYTES + c * (BBYTES / KIFMM_BRICK_BCHUNK),
-                      reinterpret_cast<const unsigned char*>(a.bpair + (int64_t)tv[vrot(x, it, v)] * (2 * KP * KP)) +
-                          c * (BBYTES / KIFMM_BRICK_BCHUNK),
-                      BBYTES / KIFMM_BRICK_BCHUNK, &full[s]);
-          if (KIFMM_BRICK_PF > 0 && v + KIFMM_BRICK_PF < x.nv)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                             a.bpair + (int64_t)tv[vrot(x, it, v + KIFMM_BRICK_PF)] * (2 * KP * KP)),
-                         "r"(BBYTES)
-                         : "memory");
-          trace(2, g);
-        }
-      }
-      for (int gg = g - nsb < 0 ? 0 : g - nsb; gg < g; ++gg)
-        mbar_wait(&empty[gg % nsb], (gg / nsb) & 1, true);
-    }
-    __syncwarp();
-  } else if (warp >= 1 && warp < 1 + 4 * NG) {
-    const int grp = (warp - 1) >> 2;
-    const int q4 = warp & 3;
-    const int m = q4 * 32 + lane;
-    const int mrow = ((m >> 5) * BRY + ((m >> 3) & 3)) * BRZ + (m & 7);   // slab row at shift (., -1, -1)
-    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-    const uint32_t dcol = tmem + (uint32_t)(grp * GCOLS);
-    const uint32_t acol = dcol + N1;
-    float acc[KP];
-    int nmine = 0;
-    int g = 0, run = -1;
-    auto release = [&](int r) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bempty[r & 1]);
-    };
-    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
-      const Item x = item_of(a, it);
-      const TileGeom tg = tile_geom(a, x.slot);
-      const uint16_t* cv = code + tg.cls * 189 + x.j0;
-#pragma unroll
-      for (int c = 0; c < KP; ++c) acc[c] = 0.f;
-      int local = 0;
-      int prev_sp = -1;
-      for (int v = 0; v < x.nv; ++v) {
-        const int cd = cv[vrot(x, it, v)];
-        if ((cd & 31) != prev_sp) {
-          if (prev_sp >= 0) release(run);
-          ++run;
-          prev_sp = cd & 31;
-        }
-        if ((v % NG) != grp) continue;
-        const int gg = g + v;
-        mbar_wait(&bfull[run & 1], (run >> 1) & 1, false);
-        const int br = mrow + (cd >> 5);
-        const unsigned char* bb = smem + (run & 1) * BRB;
-        uint32_t hv[KP], lv[KP];
-        // rows are 4 * KP bytes apart (KP = 56: 56 words), so lanes i and i + 4
-        // of an 8-lane LDS.128 phase share banks: lanes with bit 2 set read
-        // the two chunks of every chunk pair in swapped order
-        const bool swp = (lane >> 2) & 1;
-        const unsigned char* rowp = bb + br * (KP * 4);
-#pragma unroll
-        for (int i = 0; i < KP / 4; i += 2) {
-          const float4 p0 = *reinterpret_cast<const float4*>(rowp + ((i + (swp ? 1 : 0)) << 4));
-          const float4 p1 = *reinterpret_cast<const float4*>(rowp + ((i + (swp ? 0 : 1)) << 4));
-          const float4 c0 = swp ? p1 : p0, c1 = swp ? p0 : p1;
-          const float f[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            hv[4 * i + j] = (__float_as_uint(f[j]) + 0x1000u) & 0xFFFFE000u;
-            lv[4 * i + j] = __float_as_uint(f[j] - __uint_as_float(hv[4 * i + j]));
-          }
-        }
-        if (m == 0) trace(grp == 0 ? 0 : 5, gg);
-        if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);
-        if (m == 0) trace(grp == 0 ? 1 : 6, gg);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        tmem_st_a<KP>(acol + lane_base, hv, lv);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        if (grp == 0 && lane == 0 && q4 == 1) trace(10, gg);
-        if (grp == 0 && lane == 0 && q4 == 0) trace(11, gg);
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        // hand over to the group's issuer warp: the core pair has landed too
-        // (waited here, so the issuing thread never waits on an mbarrier)
-        mbar_wait(&full[gg % nsb], (gg / nsb) & 1, false);
-        asm volatile("bar.arrive %0, %1;" ::"r"(4 + grp), "n"(160) : "memory");
-        ++nmine;
-        const bool last_of_block = local == FLUSH_V - 1 || v + NG >= x.nv;
-        local = last_of_block ? 0 : local + 1;
-        if (last_of_block) {
-          mbar_wait(&done[grp], (nmine - 1) & 1, false);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-          for (int c = 0; c < KP / 8; ++c) {
-            uint32_t u[8], w[8];
-            tmem_ld8(dcol + lane_base + c * 8, u);
-            tmem_ld8(dcol + lane_base + KP + c * 8, w);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              acc[c * 8 + i] += __uint_as_float(u[i]) + __uint_as_float(w[i]);
-          }
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        }
-      }
-      if (prev_sp >= 0) release(run);
-#pragma unroll
-      for (int c = 0; c < KP; c += 8) {
-        if (grp == 1) {
-          red[2 * m] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-          red[2 * m + 1] = make_float4(acc[c + 4], acc[c + 5], acc[c + 6], acc[c + 7]);
-        }
-        asm volatile("bar.sync 3, 256;" ::: "memory");
-        if (grp == 0) {
-          const float4 u = red[2 * m], w = red[2 * m + 1];
-          acc[c] += u.x;
-          acc[c + 1] += u.y;
-          acc[c + 2] += u.z;
-          acc[c + 3] += u.w;
-          acc[c + 4] += w.x;
-          acc[c + 5] += w.y;
-          acc[c + 6] += w.z;
-          acc[c + 7] += w.w;
-        }
-        asm volatile("bar.sync 3, 256;" ::: "memory");
-      }
-      const int32_t tgt = a.tile_targets[(int64_t)x.slot * TMT + m];
-      if (grp == 0 && tgt >= 0) {
-        float* o = a.acc_out + ((int64_t)tgt * a.nrhs + x.r) * a.ld + (int64_t)x.split * a.ostride;
-#pragma unroll
-        for (int c = 0; c < KP; c += 4)
-          *reinterpret_cast<float4*>(o + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-      }
-      g += x.nv;
-    }
-  }
-  if (warp >= 1 + 4 * NG) {
-    // ---------------- MMA issuer of group grp (its own thread: an mbarrier
-    // wait behind in-flight MMAs of the issuing thread costs ~350 cycles, so
-    // the two groups' issue streams run on two threads)
-    const int grp = warp - (1 + 4 * NG);
-    constexpr uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N1 >> 3) << 17) |
-                                ((uint32_t)(TMT >> 4) << 24);
-    constexpr uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N2 >> 3) << 17) |
-                                ((uint32_t)(TMT >> 4) << 24);
-    constexpr uint32_t SBO = (KP / 4) * 128;
-    const uint32_t dcol = tmem + (uint32_t)(grp * GCOLS);
-    const uint32_t acol = dcol + N1;
-    int g = 0;
-    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
-      const Item x = item_of(a, it);
-      int loc = 0;
-      for (int v = grp; v < x.nv; v += NG) {
-        const int gg = g + v;
-        const int s = gg % nsb;
-        asm volatile("bar.sync %0, %1;" ::"r"(4 + grp), "n"(160) : "memory");
-        if (lane == 0) {
-          if (grp == 0) trace(3, gg);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t bp = smem_u32(bstage + s * BBYTES);
-#pragma unroll
-          for (int ks = 0; ks < KP / 8; ++ks) {
-            const uint64_t db = desc_nosw(bp + ks * 256, 128, SBO);
-            mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, loc | ks);
-            mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
-          }
-          mma_commit(&done[grp]);
-          mma_commit(&empty[s]);
-        }
-        __syncwarp();
-        loc = (loc == FLUSH_V - 1 || v + NG >= x.nv) ? 0 : loc + 1;
-      }
-      g += x.nv;
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
-  }
-}
-
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sm_count() { return device_sm_count(); }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1176,10 +531,10 @@ EncodeFn encoder() {
 }
 
 // 5-D map over the dense sub-lattice array (k, iz, iy, ix, p*R + r); boxes of
-// `width` k x (8, 4, 4) boxes x 1 plane, 128-byte swizzle or linear rows,
-// out-of-range -> zeros.
+// `width` k x (8, 4, 4) boxes x 1 plane with the given swizzle (the row of the
+// box, width * 4 bytes, equals the swizzle span), out-of-range -> zeros.
 int make_map(CUtensorMap* tm, const float* base, int kp, int h, int64_t planes, int width,
-             bool swizzle) {
+             CUtensorMapSwizzle swizzle) {
   EncodeFn enc = encoder();
   if (!enc) return KIFMM_EARG;
   cuuint64_t dims[5] = {(cuuint64_t)kp, (cuuint64_t)h, (cuuint64_t)h, (cuuint64_t)h,
@@ -1190,7 +545,7 @@ int make_map(CUtensorMap* tm, const float* base, int kp, int h, int64_t planes, 
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult res = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides,
                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     swizzle,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS ? 0 : KIFMM_EARG;
 }
@@ -1199,11 +554,19 @@ template <int KP>
 int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   TmemArgs a = a0;
   constexpr int W1 = KP > 32 ? KP - 32 : 0;
-  CUtensorMap tm, tm2;
+  constexpr int W16 = (W1 != 32 && !TAIL_LINEAR && W1 >= 16) ? 16 : 0;
+  constexpr int W8 = (W1 != 32 && !TAIL_LINEAR && W1 % 16 == 8) ? 8 : 0;
+  CUtensorMap tm, tm2, tm3;
   memset(&tm, 0, sizeof(tm));
   memset(&tm2, 0, sizeof(tm2));
-  int st = make_map(&tm, a.q, KP, a.h, 8 * (int64_t)a.nrhs, 32, true);
-  if (!st && W1) st = make_map(&tm2, a.q, KP, a.h, 8 * (int64_t)a.nrhs, W1, W1 == 32);
+  memset(&tm3, 0, sizeof(tm3));
+  const int64_t planes = 8 * (int64_t)a.nrhs;
+  int st = make_map(&tm, a.q, KP, a.h, planes, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!st && W1 == 32) st = make_map(&tm2, a.q, KP, a.h, planes, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!st && TAIL_LINEAR && W1 && W1 != 32)
+    st = make_map(&tm2, a.q, KP, a.h, planes, W1, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (!st && W16) st = make_map(&tm2, a.q, KP, a.h, planes, 16, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (!st && W8) st = make_map(&tm3, a.q, KP, a.h, planes, 8, CU_TENSOR_MAP_SWIZZLE_32B);
   if (st) return st;
   static int ns_env = -1;
   if (ns_env < 0) {
@@ -1227,97 +590,8 @@ int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   const int g_max = grid_env > 0 && grid_env < sm_count() ? grid_env : sm_count();
   const int grid = a.n_items < g_max ? a.n_items : g_max;
   set_max_smem((const void*)m2l_sweep_tmem_kernel<KP>, smem);
-  m2l_sweep_tmem_kernel<KP><<<grid, NTHREADS, smem, stream>>>(tm, tm2, a);
+  m2l_sweep_tmem_kernel<KP><<<grid, NTHREADS, smem, stream>>>(tm, tm2, tm3, a);
   return launch_status();
-}
-
-template <int KP>
-int launch_pipe(const TmemArgs& a0, cudaStream_t stream) {
-  TmemArgs a = a0;
-  constexpr int W1 = KP > 32 ? KP - 32 : 0;
-  CUtensorMap tm, tm2;
-  memset(&tm, 0, sizeof(tm));
-  memset(&tm2, 0, sizeof(tm2));
-  int st = make_map(&tm, a.q, KP, a.h, 8 * (int64_t)a.nrhs, 32, true);
-  if (!st && W1) st = make_map(&tm2, a.q, KP, a.h, 8 * (int64_t)a.nrhs, W1, W1 == 32);
-  if (st) return st;
-  static int ns_env = -1;
-  if (ns_env < 0) {
-    const char* e = getenv("KIFMM_TMEM_STAGES");
-    ns_env = e ? atoi(e) : 4;             // config 2 on B200: 4 ~ 3 stages (281-288 us), 2: 362 us
-    if (ns_env < 2) ns_env = 2;
-  }
-  const size_t sbytes = ((size_t)TMT * 128 + (size_t)TMT * W1 * 4 + 2ull * KP * KP * 4 + 1023) /
-                        1024 * 1024;
-  int ns = ns_env;
-  while (ns > 2 && 1024 + ns * sbytes + 256 + 4096 > 227 * 1024) --ns;
-  a.ns = ns;
-  const size_t smem = 1024 + ns * sbytes + (2 * ns + 2 * NA + 4) * 8 + 32 + 4096;
-  // persistent CTAs: one per SM, or KIFMM_TMEM_GRID (fewer leaves SMs to the
-  // concurrent small kernels of the other streams)
-  static int grid_env = -1;
-  if (grid_env < 0) {
-    const char* e = getenv("KIFMM_TMEM_GRID");
-    grid_env = e ? atoi(e) : 0;
-  }
-  const int g_max = grid_env > 0 && grid_env < sm_count() ? grid_env : sm_count();
-  const int grid = a.n_items < g_max ? a.n_items : g_max;
-  set_max_smem((const void*)m2l_sweep_pipe_kernel<KP>, smem);
-  m2l_sweep_pipe_kernel<KP><<<grid, NTHREADS_P, smem, stream>>>(tm, tm2, a);
-  return launch_status();
-}
-
-// shared memory of the brick kernel with nsb core-pair stages
-constexpr size_t brick_smem(int kp, int nsb) {
-  return 1024 + 2 * (size_t)brick_bytes(kp) + (size_t)nsb * 2 * kp * kp * 4 + (2 * nsb + 4 + 2 * NG) * 8 +
-         16 + 16 + 2 * TMT * 16 + 8 * 189 * 2;
-}
-
-template <int KP>
-int launch_brick(const TmemArgs& a0, cudaStream_t stream) {
-  TmemArgs a = a0;
-  BrickMaps maps;
-  memset(&maps, 0, sizeof(maps));
-  {
-    EncodeFn enc = encoder();
-    if (!enc) return KIFMM_EARG;
-    cuuint64_t dims[5] = {(cuuint64_t)KP, (cuuint64_t)a.h, (cuuint64_t)a.h, (cuuint64_t)a.h,
-                          8 * (cuuint64_t)a.nrhs};
-    const cuuint64_t row = (cuuint64_t)KP * 4;
-    cuuint64_t strides[4] = {row, row * a.h, row * a.h * a.h, row * a.h * a.h * a.h};
-    cuuint32_t box[5] = {(cuuint32_t)KP, BRZ, BRY, BRX, 1};
-    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    if (enc(&maps.m[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(a.q), dims, strides,
-            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return KIFMM_EARG;
-  }
-  int nsb = 2;
-  while (nsb < 6 && brick_smem(KP, nsb + 1) <= 227 * 1024) ++nsb;
-  a.ns = nsb;
-  const size_t smem = brick_smem(KP, nsb);
-  static int grid_env = -1;
-  if (grid_env < 0) {
-    const char* e = getenv("KIFMM_TMEM_GRID");
-    grid_env = e ? atoi(e) : 0;
-  }
-  const int g_max = grid_env > 0 && grid_env < sm_count() ? grid_env : sm_count();
-  const int grid = a.n_items < g_max ? a.n_items : g_max;
-  set_max_smem((const void*)m2l_sweep_brick_kernel<KP>, smem);
-  m2l_sweep_brick_kernel<KP><<<grid, NTHREADS_B, smem, stream>>>(maps, a);
-  return launch_status();
-}
-
-// KIFMM_TMEM_BRICK=1 selects the brick-fed kernel (when two bricks and two
-// core-pair stages fit in shared memory, KP <= 56).  Off by default: on
-// config 2 it sweeps level 5 in 360-370 us against 280-285 us for the
-// stage-ring kernel (tools/trace_brick.py: ~1320 cycles per vector; the chain
-// MMA completion -> tcgen05.st of the next A -> hand-over -> issue of each
-// group is not shortened by the smaller ingress).  Read per call so tests can
-// switch it.
-bool use_brick(int kp) {
-  const char* e = getenv("KIFMM_TMEM_BRICK");
-  return e && atoi(e) != 0 && brick_smem(kp, 2) <= 227 * 1024;
 }
 
 }  // namespace
@@ -1397,28 +671,6 @@ int kifmm_m2l_sweep_tmem_f32(const float* q, const float* bpair, int64_t kp, int
   a.acc_out = acc;
   a.ns = 2;
   cudaStream_t s = (cudaStream_t)stream;
-  if (use_brick((int)kp)) switch (kp) {
-      case 8: return launch_brick<8>(a, s);
-      case 16: return launch_brick<16>(a, s);
-      case 24: return launch_brick<24>(a, s);
-      case 32: return launch_brick<32>(a, s);
-      case 40: return launch_brick<40>(a, s);
-      case 48: return launch_brick<48>(a, s);
-      case 56: return launch_brick<56>(a, s);
-    }
-  // KIFMM_TMEM_PIPE=1: the pipelined kernel (opt-in; 350-375 us against
-  // 280-285 us for the two-accumulator kernel on config 2 level 5)
-  const char* pe = getenv("KIFMM_TMEM_PIPE");
-  if (pe && atoi(pe) != 0) switch (kp) {
-      case 8: return launch_pipe<8>(a, s);
-      case 16: return launch_pipe<16>(a, s);
-      case 24: return launch_pipe<24>(a, s);
-      case 32: return launch_pipe<32>(a, s);
-      case 40: return launch_pipe<40>(a, s);
-      case 48: return launch_pipe<48>(a, s);
-      case 56: return launch_pipe<56>(a, s);
-      case 64: return launch_pipe<64>(a, s);
-    }
   switch (kp) {
     case 8: return launch_tmem<8>(a, s);
     case 16: return launch_tmem<16>(a, s);

@@ -27,6 +27,7 @@ import torch
 from . import _native as nat
 from .engine import child_table, leaf_centers, leaf_surface_base
 from .m2l_blas import TILE_TARGETS, dense_cores, level_plan_from_buckets
+from .nearfield import f32_cross_leaf_coincident, mutual_slots
 from .octree import class_transfer_table
 
 _NP2T = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
@@ -187,12 +188,17 @@ class Linalg:
 
     def scratch(self, slot, n, T, dev):
         """Grow-only scratch buffers (allocated outside graph capture on the
-        eager warm-up pass, reused afterwards)."""
+        eager warm-up pass, reused afterwards).  A buffer that is outgrown is
+        retired, never freed: CUDA graphs captured earlier (another n_rhs)
+        keep its raw pointer and must not replay into recycled memory."""
         if not hasattr(self, "_scratch"):
             self._scratch = {}
-        slot = (torch.cuda.current_stream().cuda_stream, slot)   # per stream: levels overlap
+            self._retired = []
+        slot = (torch.cuda.current_stream().cuda_stream, slot, T)   # per stream: levels overlap
         t = self._scratch.get(slot)
-        if t is None or t.numel() < n or t.dtype != T:
+        if t is None or t.numel() < n:
+            if t is not None:
+                self._retired.append(t)
             t = torch.empty(n, dtype=T, device=dev)
             self._scratch[slot] = t
         return t
@@ -600,6 +606,19 @@ class DeviceFmm:
             raise ValueError("a leaf's near field spans more than 32 leaves (leaf pass limit)")
         self.near_off = to_dev(inst.near.offsets, np.int32)
         self.near_leaf = to_dev(inst.near.leaves, np.int32)
+        # float32 rounding can merge points of different leaves: then every
+        # near-field pair is guarded against r2 == 0 (reference _hot.pyx:44-50)
+        self.p2p_guard = self.sfx == "f32" and f32_cross_leaf_coincident(tt, st)
+        # sources == targets (one point set): the mutual near field evaluates
+        # each pair of adjacent leaves once (csrc/p2p_mutual.cu); float32
+        # potential path (KIFMM_P2P=direct keeps the per-target-leaf pass)
+        self.mutual = None
+        if (self.sfx == "f32" and getattr(inst, "self_interaction", False)
+                and os.environ.get("KIFMM_P2P", "mutual") == "mutual"
+                and np.array_equal(st.perm, tt.perm)):
+            ms = mutual_slots(inst.near.offsets, inst.near.leaves, st.leaf_counts)
+            self.mutual = dict(base=to_dev(ms.base), nlow=to_dev(ms.nlow),
+                               dst=to_dev(ms.near_dst), total=ms.total)
         # unit-box operators
         def inv_parts(inv):
             return (to_dev(inv.u, dt), to_dev(inv.inv_vals, dt),
@@ -751,6 +770,8 @@ class DeviceFmm:
             b["phat_lv"] = {l: torch.empty(2 * self.n_freq * fp[l]["ntc"] * 8 * R, dtype=T,
                                            device=dev) for l in levels}
         b["out"] = torch.empty(self.tx.shape[0] * R, dtype=T, device=dev)
+        if self.mutual is not None:
+            b["pmut"] = torch.empty(max(self.mutual["total"], 1) * R, dtype=T, device=dev)
         b["qin"] = torch.empty(self.sx.shape[0] * R, dtype=torch.float64, device=dev)
         self._bufs[nrhs] = b
         return b
@@ -834,19 +855,44 @@ class DeviceFmm:
         grad_ptr = [P(b["grad"])] if gradient else []
         leaf_name = f"kifmm_leaf_pass_grad_{sfx}" if gradient else f"kifmm_leaf_pass_{sfx}"
 
+        guard_bit = 8 if self.p2p_guard else 0
+
         def leaf_args(parts):
             return [P(self.tx), P(self.ty), P(self.tz), P(self.t_start), P(self.t_count),
                     self.n_tgt[d], P(self.t_centers), P(self.equiv_base), n_e,
                     P(b["loc"][d]), P(b["src4"]), self.sx.shape[0], P(self.s_start),
                     P(self.s_count), P(self.near_off), P(self.near_leaf), R, P(self.t_perm),
-                    parts, P(out)] + grad_ptr
+                    parts | guard_bit, P(out)] + grad_ptr
+
+        mut = self.mutual if not gradient else None
+
+        def p2p_pass(stream):
+            if mut is not None:
+                # mutual near field into the partial-sum slots
+                launch("kifmm_p2p_mutual_f32", P(self.tx), P(self.ty), P(self.tz),
+                       P(self.t_start), P(self.t_count), self.n_tgt[d], P(b["src4"]),
+                       self.sx.shape[0], P(self.near_off), P(self.near_leaf), P(mut["dst"]),
+                       P(mut["base"]), R, mut["total"], int(self.p2p_guard), P(b["pmut"]),
+                       stream)
+            else:
+                launch(leaf_name, *leaf_args(2), stream)             # P2P, overwrite
+
+        def l2p_final(stream):
+            if mut is not None:
+                # L2P + the near-field slots, un-permuted
+                launch("kifmm_l2p_mutual_f32", P(self.tx), P(self.ty), P(self.tz),
+                       P(self.t_start), P(self.t_count), self.n_tgt[d], P(self.t_centers),
+                       P(self.equiv_base), n_e, P(b["loc"][d]), R, P(self.t_perm),
+                       P(mut["base"]), P(mut["nlow"]), mut["total"], P(b["pmut"]), P(out), stream)
+            else:
+                launch(leaf_name, *leaf_args(1 | 4), stream)         # L2P, accumulate
 
         p2p_after = os.environ.get("KIFMM_P2P_AFTER", "m2m")
         side = self.side_stream
 
         def fork_p2p():
             side.wait_stream(torch.cuda.current_stream())
-            launch(leaf_name, *leaf_args(2), side.cuda_stream)       # P2P, overwrite
+            p2p_pass(side.cuda_stream)
 
         if overlap and p2p_after == "pack":
             fork_p2p()
@@ -966,7 +1012,12 @@ class DeviceFmm:
         phase("leaf")
         if overlap:
             main.wait_stream(side)
-            launch(leaf_name, *leaf_args(1 | 4), s)                  # L2P, accumulate
+            l2p_final(s)
+        elif mut is not None:
+            phase("p2p")
+            p2p_pass(s)
+            phase("l2p")
+            l2p_final(s)
         else:
             launch(leaf_name, *leaf_args(3), s)                      # fused L2P + P2P
         phase("end")
@@ -1028,7 +1079,8 @@ class DeviceFmm:
             key = "p2p" if n0 == "leaf" else ("m2l" if n0.startswith("m2l") else
                                                "l2l" if n0.startswith("l2l") else n0)
             t[key] += dt_s
-        t["leaf_fused"] = 1.0      # l2p is fused into the p2p leaf pass
+        # without a separate l2p phase, L2P is fused into the leaf pass
+        t["leaf_fused"] = 0.0 if any(n == "l2p" for n, _ in ev) else 1.0
         return t
 
     def evaluate_host(self, q_host: np.ndarray, timings=False, gradient=False):

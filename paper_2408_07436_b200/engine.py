@@ -196,6 +196,8 @@ class FmmInstance:
     n_near_pairs: int = 0
     _last_charges: np.ndarray | None = None
     _device: object = None
+    # sources and targets are one point set (the mutual near field applies)
+    self_interaction: bool = False
     # per-operator CUDA-event timings (operator_timings) cost an eager,
     # un-graphed evaluate; off by default
     profile: bool = False
@@ -305,6 +307,7 @@ def setup(sources, targets, config: FmmConfig, device_build=None) -> FmmInstance
                              inner_scale=config.inner_scale, outer_scale=config.outer_scale)
     inst = FmmInstance(config=config, domain=domain, source_tree=stree, target_tree=ttree,
                        expansions=exp)
+    inst.self_interaction = bool(src.shape == tgt.shape and np.array_equal(src, tgt))
     if config.backend == "blas":
         inst.blas_ops = m2l_blas.precompute(
             config.order_equiv, config.resolved_order_check(), sigma_min=config.sigma_min,

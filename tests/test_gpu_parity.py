@@ -204,6 +204,26 @@ def test_evaluate_is_deterministic_and_linear(cuda):
     assert np.abs(multi[:, 0] - a).max() <= 1e-12 * np.abs(a).max()
 
 
+@pytest.mark.parametrize("n,kw", [
+    (1_000_000, dict(depth=5, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6)),
+    (20_000, dict(depth=4, order_equiv=4, backend="blas", precision="f64", sigma_min=1e-10)),
+])
+def test_graph_replay_after_rhs_change(cuda, n, kw):
+    """Graphs captured for one n_rhs must stay valid after another n_rhs grew
+    the shared scratch buffers (R=1 -> R=3 -> R=1 bitwise)."""
+    from paper_2408_07436_b200 import FmmConfig, setup
+    from conftest import uniform_points
+    pts = uniform_points(n, seed=8)
+    inst = setup(pts, pts, FmmConfig(**kw))
+    rng = np.random.default_rng(9)
+    q = rng.random(n)
+    a = inst.evaluate(q)
+    three = inst.evaluate(np.stack([q, 2 * q, rng.random(n)], axis=1))
+    b = inst.evaluate(q)
+    assert np.array_equal(a, b)
+    assert np.abs(three[:, 0] - a).max() <= 1e-5 * np.abs(a).max()
+
+
 def test_separate_clouds_and_pruned_sphere(cuda):
     from oracle import port
     from paper_2408_07436_b200 import FmmConfig, setup
@@ -413,37 +433,39 @@ def test_many_rhs_with_gradient(cuda):
 
 
 # ------------------------------------------- tensor-memory sweep (csrc/m2l_tmem.cu)
-@pytest.mark.parametrize("n,depth,order,nrhs,clustered", [
-    (20000, 3, 4, 1, False), (60000, 4, 4, 2, False), (30000, 4, 3, 1, True)])
+@pytest.mark.parametrize("n,depth,order,nrhs,clustered,rank", [
+    (20000, 3, 4, 1, False, None), (60000, 4, 4, 2, False, None), (30000, 4, 3, 1, True, None),
+    (20000, 3, 4, 1, False, 36), (20000, 3, 4, 1, False, 44), (20000, 3, 5, 1, False, 60)])
 def test_tmem_sweep_matches_tma_sweep_and_reference(cuda, monkeypatch, n, depth, order, nrhs,
-                                                    clustered):
+                                                    clustered, rank):
     """The float32 engine sweep with the A operand in tensor memory (ranks
-    <= 64; stage-ring and brick-fed kernels) against the TMA-staged sweep on
-    the same instance inputs, and
+    <= 64) against the TMA-staged sweep on the same instance inputs, and
     against the reference; uniform and clustered (pruned boxes) clouds, 1 and
-    2 right-hand sides; re-evaluation is bitwise deterministic."""
+    2 right-hand sides; re-evaluation is bitwise deterministic.  The forced
+    ranks cover every source-block box split: k = 51 (KP 56: 32-column box
+    with the 128-byte swizzle + 16 (64-byte) + 8 (32-byte)), 36 (KP 40: + 8),
+    44 (KP 48: + 16), 60 (KP 64: two 128-byte boxes)."""
     from paper_2408_07436_b200 import FmmConfig, setup
     rng = np.random.default_rng(21)
     pts = rng.random((n, 3))
     if clustered:
         pts = pts ** 3
     q = rng.random((n, nrhs)) if nrhs > 1 else rng.random(n)
-    kw = dict(depth=depth, order_equiv=order, backend="blas", precision="f32", sigma_min=1e-6)
+    kw = dict(depth=depth, order_equiv=order, backend="blas", precision="f32", sigma_min=1e-6,
+              rank_estimate=rank)
     res = {}
-    # brick / pipe: the opt-in variants (KIFMM_TMEM_BRICK=1 / KIFMM_TMEM_PIPE=1)
-    for sweep in ("tma", "tmem", "brick", "pipe"):
-        monkeypatch.setenv("KIFMM_F32_SWEEP", "tma" if sweep == "tma" else "tmem")
-        monkeypatch.setenv("KIFMM_TMEM_BRICK", "1" if sweep == "brick" else "0")
-        monkeypatch.setenv("KIFMM_TMEM_PIPE", "1" if sweep == "pipe" else "0")
+    for sweep in ("tma", "tmem"):
+        monkeypatch.setenv("KIFMM_F32_SWEEP", sweep)
         inst = setup(pts, pts, FmmConfig(**kw))
         assert inst.device.blas.tmem == (sweep != "tma")
+        if rank is not None:
+            assert inst.blas_ops.k == rank
         res[sweep] = np.asarray(inst.evaluate(q), dtype=np.float64)
         if sweep != "tma":
             again = np.asarray(inst.evaluate(q), dtype=np.float64)
             assert np.array_equal(res[sweep], again)
-    for sweep in ("tmem", "brick", "pipe"):
-        rel = np.abs(res[sweep] - res["tma"]) / np.abs(res["tma"])
-        assert rel.max() <= TOL["f32"], (sweep, rel.max())
+    rel = np.abs(res["tmem"] - res["tma"]) / np.abs(res["tma"])
+    assert rel.max() <= TOL["f32"], rel.max()
     if nrhs == 1:
         want, _ = _reference_run(pts, q, kw)
         assert parity_report(res["tmem"], want)["max_rel"] <= TOL["f32"]
@@ -467,3 +489,43 @@ def test_scatter_add_rows(cuda):
              torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert np.array_equal(d_d.cpu().numpy(), want)
+
+
+# ------------------------------------------- mutual near field (csrc/p2p_mutual.cu)
+@pytest.mark.parametrize("n,depth,nrhs,clustered,merge", [
+    (60000, 4, 1, False, False), (60000, 4, 2, False, False), (40000, 4, 1, True, False),
+    (20000, 3, 1, False, True)])
+def test_mutual_near_field(cuda, monkeypatch, n, depth, nrhs, clustered, merge):
+    """sources == targets: each pair of adjacent leaves evaluated once into
+    partial-sum slots, against the per-target-leaf pass and the reference;
+    uniform and clustered clouds (leaves over 32 points: several target
+    passes; over 256 upper columns: several staging fills), 2 right-hand
+    sides, and (merge) a pair of points of different leaves that float32
+    rounding merges (the guarded variant; r2 == 0 contributes 0)."""
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(31)
+    pts = rng.random((n, 3))
+    if clustered:
+        pts = pts ** 3
+    if merge:
+        pts[:2] = [[0.5 - 1e-12, 0.3, 0.3], [0.5 + 1e-12, 0.3, 0.3]]
+    q = rng.random((n, nrhs)) if nrhs > 1 else rng.random(n)
+    kw = dict(depth=depth, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6)
+    res = {}
+    for mode in ("direct", "mutual"):
+        monkeypatch.setenv("KIFMM_P2P", mode)
+        inst = setup(pts, pts, FmmConfig(**kw))
+        dev = inst.device
+        assert (dev.mutual is not None) == (mode == "mutual")
+        assert dev.p2p_guard == merge
+        res[mode] = np.asarray(inst.evaluate(q), dtype=np.float64)
+        assert np.all(np.isfinite(res[mode]))
+        if mode == "mutual":
+            assert np.array_equal(res[mode], inst.evaluate(q))        # deterministic
+            inst.profile = True                                        # eager (un-graphed) path
+            assert np.abs(inst.evaluate(q) - res[mode]).max() <= 1e-6 * np.abs(res[mode]).max()
+    rel = np.abs(res["mutual"] - res["direct"]) / np.abs(res["direct"])
+    assert rel.max() <= TOL["f32"], rel.max()
+    if nrhs == 1:
+        want, _ = _reference_run(pts, q, kw)
+        assert parity_report(res["mutual"], want)["max_rel"] <= TOL["f32"]
