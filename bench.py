@@ -136,6 +136,20 @@ def m2l_flops(inst):
     return apply_f, apply_f + solve_f, per_level
 
 
+def near_field_counts(inst):
+    """P2P work: interactions the reference evaluates (each ordered target /
+    near-source pair) and, for sources == targets, the rsqrt the mutual pass
+    executes (own-leaf blocks + each adjacent leaf pair once)."""
+    near, t = inst.near, inst.target_tree
+    n = t.leaf_counts.astype(np.int64)
+    owner = np.repeat(np.arange(n.shape[0]), np.diff(near.offsets))
+    up = near.leaves > owner
+    self_pairs = int((n * n).sum())
+    upper_pairs = int((n[owner[up]] * inst.source_tree.leaf_counts[near.leaves[up]]).sum())
+    return dict(interactions=int(inst.n_near_pairs), self_pairs=self_pairs,
+                upper_pairs=upper_pairs, rsqrt_executed=self_pairs + upper_pairs)
+
+
 def measured_peaks():
     """Driver-written MEASURED_PEAKS.json, else the profiling guide's fallback."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -351,16 +365,35 @@ def run_single(args):
             algorithmic=f"4 k sum_t m_t k_t = {algo:.4g} flop at level {lvl}",
             peak_source="kifmm_probe FFMA measured in this run")
     inter = inst.n_near_pairs
-    leaf_key = [k for k in per_kernel if k.startswith("leaf_pass")][0]
-    leaf_ms = per_kernel[leaf_key]
     l2p = float(inst.target_tree.n_points) * inst.expansions.n_equiv
-    rooflines[leaf_key] = dict(
-        bound="mufu", kernel=leaf_key, achieved=(inter + l2p) / (leaf_ms / 1e3) / 1e9,
-        peak=peak_mufu, unit="Grsqrt/s", frac=(inter + l2p) / (leaf_ms / 1e3) / 1e9 / peak_mufu,
-        traffic=dram_traffic("leaf_pass_f32"),
-        algorithmic=f"{inter} P2P + {l2p:.0f} L2P kernel evaluations (one rsqrt each)",
-        tflops_11_per_interaction=11.0 * inter / (leaf_ms / 1e3) / 1e12, fp32_peak=peak_f32,
-        peak_source="kifmm_probe MUFU.RSQ measured in this run")
+    nf = near_field_counts(inst)
+    if "p2p_mutual_f32" in per_kernel:
+        # mutual near field: every adjacent leaf pair once (one rsqrt, both
+        # directions) + the own-leaf blocks; L2P runs in l2p_mutual_f32
+        leaf_key = "p2p_mutual_f32"
+        leaf_ms = per_kernel[leaf_key]
+        execd = nf["rsqrt_executed"]
+        rooflines[leaf_key] = dict(
+            bound="mufu", kernel=leaf_key, achieved=execd / (leaf_ms / 1e3) / 1e9,
+            peak=peak_mufu, unit="Grsqrt/s", frac=execd / (leaf_ms / 1e3) / 1e9 / peak_mufu,
+            traffic=dram_traffic("p2p_mutual_f32"),
+            algorithmic=f"{inter} P2P interactions served by {execd} executed rsqrt "
+                        f"({nf['self_pairs']} own-leaf + {nf['upper_pairs']} mutual pairs)",
+            interactions_per_s=inter / (leaf_ms / 1e3),
+            rsqrt_executed=execd, interactions=inter,
+            tflops_11_per_interaction=11.0 * inter / (leaf_ms / 1e3) / 1e12, fp32_peak=peak_f32,
+            peak_source="kifmm_probe MUFU.RSQ measured in this run")
+    else:
+        leaf_key = [k for k in per_kernel if k.startswith("leaf_pass")][0]
+        leaf_ms = per_kernel[leaf_key]
+        rooflines[leaf_key] = dict(
+            bound="mufu", kernel=leaf_key, achieved=(inter + l2p) / (leaf_ms / 1e3) / 1e9,
+            peak=peak_mufu, unit="Grsqrt/s", frac=(inter + l2p) / (leaf_ms / 1e3) / 1e9 / peak_mufu,
+            traffic=dram_traffic("leaf_pass_f32"),
+            algorithmic=f"{inter} P2P + {l2p:.0f} L2P kernel evaluations (one rsqrt each)",
+            rsqrt_executed=inter + l2p, interactions=inter,
+            tflops_11_per_interaction=11.0 * inter / (leaf_ms / 1e3) / 1e12, fp32_peak=peak_f32,
+            peak_source="kifmm_probe MUFU.RSQ measured in this run")
     roof = rooflines["m2l_sweep_tc_f32" if bd.tc else "m2l_sweep"] if "sweep" in dom[0] \
         else rooflines[leaf_key]
 

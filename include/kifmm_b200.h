@@ -290,12 +290,15 @@ int kifmm_fft_inverse_f64(const double* phat, int64_t nrhs, int64_t order,
  * -> 0).  Results go to partial-sum slots (no atomics, deterministic):
  *   P[r*pstride + base[B] + s*n_B + t], s = 0: B's row sums, s = 1..nlow_B:
  *   the column sums of B's s-th lower neighbour (its entry s of B's near list);
- * near_dst[e] = base[B] + s*n_B for the entry e = (A, B > A) of A's near
- * list.  guard != 0: also guard the cross-leaf pairs against r2 == 0. */
-int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, const int32_t* leaf_start,
-                         const int32_t* leaf_count, int64_t n_leaves, const float* src4,
-                         int64_t npts, const int32_t* near_off, const int32_t* near_leaf,
-                         const int32_t* near_dst, const int32_t* base, int64_t nrhs,
+ * near_pack[e] = (start, count, dst, leaf) of entry e of a near list (the
+ * CSR near_off): the entry leaf's first point and point count, and dst =
+ * base[B] + s*n_B for an upper entry (A, B > A), base[A] for the own entry
+ * (entry 0).  order (n_leaves, or NULL): the leaves in launch order
+ * (heaviest first balances the uneven per-leaf work).  guard != 0: also
+ * guard the cross-leaf pairs against r2 == 0. */
+int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, int64_t n_leaves,
+                         const float* src4, int64_t npts, const int32_t* near_off,
+                         const int32_t* near_pack, const int32_t* order, int64_t nrhs,
                          int64_t pstride, int guard, float* P, void* stream);
 /* Final pass of the mutual near field: out[perm[i]*nrhs + r] = L2P(i)
  * (engine.py:377-389) + sum_{s=0..nlow_b} P[r*pstride + base[b] + s*n_b + t]

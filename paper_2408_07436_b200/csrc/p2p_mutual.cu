@@ -45,8 +45,16 @@ using namespace kifmm;
 
 namespace {
 
-constexpr int kMW = 4;              // warps per CTA (one target leaf per warp)
-constexpr int kMCols = 256;         // upper columns staged per fill (x2 entries: the chunk twice)
+#ifndef KIFMM_MUT_WARPS
+#define KIFMM_MUT_WARPS 2
+#endif
+// warps per CTA (one target leaf per warp): single-warp CTAs release their
+// resources as soon as their leaf is done (the work per leaf varies with its
+// count of upper neighbours, 0..26)
+constexpr int kMW = KIFMM_MUT_WARPS;
+#ifndef KIFMM_MUT_MINB
+#define KIFMM_MUT_MINB (20 / KIFMM_MUT_WARPS)   // CTAs per SM the register budget is sized for
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ float4 pad_col() {
@@ -89,8 +97,13 @@ __device__ __forceinline__ void mutual_rounds(const float4* buf, const int32_t* 
                                               float2 QA, float2& phi, float* __restrict__ Pr,
                                               bool rmw) {
   for (int c0 = 0; c0 < m; c0 += 32) {
-    const int k = c0 / R + grp;
+    const int k = c0 / R + grp;                    // R is a compile-time power of two
     const float4* p = buf + 2 * R * k + ti;
+    const int col = k * R + ti;
+    // a later target pass of the same leaf adds to the column sums of the
+    // earlier ones: fetch them before the chain of steps
+    float* o = Pr + (col < m ? dst[col] : 0);
+    const float old = (rmw && col < m) ? __ldcg(o) : 0.f;
     float2 psi = make_float2(0.f, 0.f);
     float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -115,128 +128,156 @@ __device__ __forceinline__ void mutual_rounds(const float4* buf, const int32_t* 
       }
     }
     phi = __fadd2_rn(phi, acc2);
-    const int col = k * R + ti;
-    if (col < m) {
-      float* o = Pr + dst[col];
-      const float v = psi.x + psi.y;
-      *o = rmw ? __ldcg(o) + v : v;
-    }
+    if (col < m) *o = old + (psi.x + psi.y);
   }
 }
 
+// Per-warp shared memory: two column buffers (fills of kFC columns, staged
+// twice: 2 kFC records) with their destinations, the own-leaf records and
+// the upper-segment table of the current leaf.
+constexpr int kFC = 128;
+constexpr int kSelf = 64;
+struct WarpSmem {
+  float4 col[2][2 * kFC];
+  int32_t dst[2][kFC];
+  float4 self[kSelf];
+  int2 seg[32];           // (source row - first column, dst - first column) of upper segment e
+  int32_t incl[32];       // inclusive end column of segment e (0-size for non-upper entries)
+};
+
 template <bool GUARD>
-__global__ void __launch_bounds__(32 * kMW) p2p_mutual_kernel(
+__global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
     const float* __restrict__ tx, const float* __restrict__ ty, const float* __restrict__ tz,
-    const int32_t* __restrict__ lstart, const int32_t* __restrict__ lcount, int64_t n_leaves,
-    const float4* __restrict__ src4, int64_t npts, const int32_t* __restrict__ near_off,
-    const int32_t* __restrict__ near_leaf, const int32_t* __restrict__ near_dst,
-    const int32_t* __restrict__ base, int64_t nrhs, int64_t pstride, float* __restrict__ P) {
-  __shared__ __align__(16) float4 sbuf[kMW][2 * kMCols];
-  __shared__ int32_t sdst[kMW][kMCols];
+    int64_t n_leaves, const float4* __restrict__ src4, int64_t npts,
+    const int32_t* __restrict__ near_off, const int4* __restrict__ near_pack,
+    const int32_t* __restrict__ order, int64_t nrhs, int64_t pstride, float* __restrict__ P) {
+  __shared__ WarpSmem sm_all[kMW];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float4* buf = sbuf[w];
-  int32_t* dsts = sdst[w];
-  const int64_t a = (int64_t)blockIdx.x * kMW + w;
-  if (a >= n_leaves) return;
-  const int64_t t0 = lstart[a];
-  const int tc = lcount[a];
-  const int n0 = near_off[a], n1 = near_off[a + 1];
-  // near entries by lane (<= 27): upper neighbours are the entries whose leaf
-  // row is above a (own leaf first, then neighbours ascending)
-  int seg_start = 0, seg_cnt = 0, seg_dst = 0;
-  bool upper = false;
-  if (lane < n1 - n0) {
-    const int sl = near_leaf[n0 + lane];
-    seg_start = lstart[sl];
-    seg_cnt = lcount[sl];
-    seg_dst = near_dst[n0 + lane];
-    upper = sl > a;
+  WarpSmem& sm = sm_all[w];
+  // one leaf per warp, heaviest first (order: leaves by descending work)
+  const int64_t slot = (int64_t)blockIdx.x * kMW + w;
+  if (slot >= n_leaves) return;
+  const int64_t a = order ? order[slot] : slot;
+  // near entries of the first leaf: (start, count, dst, leaf); entry 0 is the
+  // leaf itself, its dst field holds the leaf's slot base
+  int4 ent = make_int4(0, 0, 0, -1);
+  int nent = 0;
+  {
+    const int n0 = near_off[a];
+    nent = near_off[a + 1] - n0;
+    if (lane < nent) ent = near_pack[n0 + lane];
   }
-  const unsigned umask = __ballot_sync(kFull, upper);
-  const int32_t own_base = base[a];
-  for (int64_t r = 0; r < nrhs; ++r) {
-    const float4* srow = src4 + r * npts;
-    float* Pr = P + r * pstride;
-    for (int tb = 0; tb < tc; tb += 32) {
-      const int n = min(32, tc - tb);
-      const int h = (n + 1) >> 1;
-      const int R = h <= 1 ? 1 : 1 << (32 - __clz(h - 1));
-      const int f = 32 / R, grp = lane / R, ti = lane % R;
-      const bool live0 = ti < n, live1 = ti + R < n;
-      const int64_t ia = t0 + tb + (live0 ? ti : 0), ib = t0 + tb + (live1 ? ti + R : 0);
-      const float2 X = make_float2(tx[ia], tx[ib]), Y = make_float2(ty[ia], ty[ib]),
-                   Z = make_float2(tz[ia], tz[ib]);
-      const float2 QA = make_float2(live0 ? srow[ia].w : 0.f, live1 ? srow[ib].w : 0.f);
-      float2 phi = make_float2(0.f, 0.f);
-      // ---- own block (direct, guarded), in pieces of 2 kMCols records
-      for (int j0 = 0; j0 < tc; j0 += 2 * kMCols) {
-        const int m = min(2 * kMCols, tc - j0);
-        __syncwarp();
-        for (int k = lane; k < m; k += 32) cp_async16(buf + k, srow + t0 + j0 + k, true);
+  {
+    const int t0 = __shfl_sync(kFull, ent.x, 0), tc = __shfl_sync(kFull, ent.y, 0);
+    const int32_t own_base = __shfl_sync(kFull, ent.z, 0);
+    // upper segments: exclusive prefix of their sizes over the entries
+    const int ucnt = (lane > 0 && lane < nent && ent.w > a) ? ent.y : 0;
+    int incl = ucnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int ncols = __shfl_sync(kFull, incl, 31);
+    const int excl = incl - ucnt;
+    __syncwarp();
+    sm.seg[lane] = make_int2(ent.x - excl, ent.z - excl);
+    sm.incl[lane] = incl;
+    __syncwarp();
+    for (int64_t r = 0; r < nrhs; ++r) {
+      const float4* srow = src4 + r * npts;
+      float* Pr = P + r * pstride;
+      for (int tb = 0; tb < tc; tb += 32) {
+        const int n = min(32, tc - tb);
+        const int h = (n + 1) >> 1;
+        const int lr = h <= 1 ? 0 : 32 - __clz(h - 1);       // R = 2^lr
+        const int R = 1 << lr;
+        const int grp = lane >> lr, ti = lane & (R - 1), f = 32 >> lr;
+        const bool live0 = ti < n, live1 = ti + R < n;
+        const int64_t ia = t0 + tb + (live0 ? ti : 0), ib = t0 + tb + (live1 ? ti + R : 0);
+        // stage one fill of columns [k kFC, ...) into buffer k & 1: each
+        // column twice (2R-record chunks), padded to whole 32-column rounds
+        auto stage = [&](int k) {
+          float4* cb = sm.col[k & 1];
+          int32_t* db = sm.dst[k & 1];
+          const int c0 = k * kFC, m = min(kFC, ncols - c0), mp = (m + 31) & ~31;
+          for (int cc = lane; cc < mp; cc += 32) {
+            const int e2 = ((cc >> lr) << (lr + 1)) + (cc & (R - 1));
+            if (cc < m) {
+              const int c = c0 + cc;
+              int e = 0;
+#pragma unroll
+              for (int st = 16; st > 0; st >>= 1)
+                if (sm.incl[e + st - 1] <= c) e += st;
+              const int2 sg = sm.seg[e];
+              cp_async16(cb + e2, srow + sg.x + c, true);
+              cp_async16(cb + e2 + R, srow + sg.x + c, true);
+              db[cc] = sg.y + c;
+            } else {
+              cb[e2] = pad_col();
+              cb[e2 + R] = pad_col();
+            }
+          }
+          cp_async_commit();
+        };
+        const int nfill = (ncols + kFC - 1) / kFC;
+        // own leaf (first kSelf records) and the first fill in flight together
+        const int ms = min(kSelf, tc);
+        for (int k = lane; k < ms; k += 32) cp_async16(sm.self + k, srow + t0 + k, true);
         cp_async_commit();
-        cp_async_wait<0>();
+        if (nfill) stage(0);
+        const float2 X = make_float2(tx[ia], tx[ib]), Y = make_float2(ty[ia], ty[ib]),
+                     Z = make_float2(tz[ia], tz[ib]);
+        const float2 QA = make_float2(live0 ? srow[ia].w : 0.f, live1 ? srow[ib].w : 0.f);
+        float2 phi = make_float2(0.f, 0.f);
+        // ---- own block (direct, guarded)
+        if (nfill) cp_async_wait<1>();
+        else cp_async_wait<0>();
         __syncwarp();
-        self_sum(buf, m, grp, f, X, Y, Z, phi);
-      }
-      // ---- upper blocks: columns of all upper neighbours, kMCols per fill
-      int fill = 0;
-      auto process = [&](int m) {
-        // pad to whole rounds of 32 columns
-        const int mp = (m + 31) & ~31;
-        for (int c = m + lane; c < mp; c += 32) {
-          const int k = c / R, pos = c % R;
-          buf[2 * R * k + pos] = pad_col();
-          buf[2 * R * k + R + pos] = pad_col();
+        self_sum(sm.self, ms, grp, f, X, Y, Z, phi);
+        for (int j0 = kSelf; j0 < tc; j0 += kSelf) {           // large leaves: more pieces
+          const int m = min(kSelf, tc - j0);
+          __syncwarp();
+          for (int k = lane; k < m; k += 32) cp_async16(sm.self + k, srow + t0 + j0 + k, true);
+          cp_async_commit();
+          cp_async_wait<0>();                                  // (also completes fill 0)
+          __syncwarp();
+          self_sum(sm.self, m, grp, f, X, Y, Z, phi);
         }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncwarp();
+        // ---- upper blocks: double-buffered fills
         const bool rmw = tb > 0;
-        switch (R) {
-          case 1: mutual_rounds<1, GUARD>(buf, dsts, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
-          case 2: mutual_rounds<2, GUARD>(buf, dsts, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
-          case 4: mutual_rounds<4, GUARD>(buf, dsts, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
-          case 8: mutual_rounds<8, GUARD>(buf, dsts, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
-          default: mutual_rounds<16, GUARD>(buf, dsts, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
+        for (int k = 0; k < nfill; ++k) {
+          if (k + 1 < nfill) {
+            stage(k + 1);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+          __syncwarp();
+          const float4* cb = sm.col[k & 1];
+          const int32_t* db = sm.dst[k & 1];
+          const int m = min(kFC, ncols - k * kFC);
+          switch (lr) {
+            case 0: mutual_rounds<1, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
+            case 1: mutual_rounds<2, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
+            case 2: mutual_rounds<4, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
+            case 3: mutual_rounds<8, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
+            default: mutual_rounds<16, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
+          }
+          __syncwarp();
+        }
+        // ---- row sums of the pass: combine the f groups, slot 0
+        float pa = phi.x, pb = phi.y;
+        for (int off = R; off < 32; off <<= 1) {
+          pa += __shfl_xor_sync(kFull, pa, off);
+          pb += __shfl_xor_sync(kFull, pb, off);
+        }
+        if (grp == 0) {
+          if (live0) Pr[own_base + tb + ti] = pa;
+          if (live1) Pr[own_base + tb + ti + R] = pb;
         }
         __syncwarp();
-      };
-      __syncwarp();
-      unsigned um = umask;
-      while (um) {
-        const int nn = __ffs(um) - 1;
-        um &= um - 1;
-        const int64_t j0 = __shfl_sync(kFull, seg_start, nn);
-        const int jc = __shfl_sync(kFull, seg_cnt, nn);
-        const int32_t d0 = __shfl_sync(kFull, seg_dst, nn);
-        for (int jb = 0; jb < jc;) {
-          if (fill == kMCols) {
-            process(fill);
-            fill = 0;
-          }
-          const int m = min(jc - jb, kMCols - fill);
-          for (int k = lane; k < m; k += 32) {
-            const int c = fill + k, ck = c / R, pos = c % R;
-            cp_async16(buf + 2 * R * ck + pos, srow + j0 + jb + k, true);
-            cp_async16(buf + 2 * R * ck + R + pos, srow + j0 + jb + k, true);
-            dsts[c] = d0 + jb + k;
-          }
-          fill += m;
-          jb += m;
-        }
       }
-      if (fill) process(fill);
-      // ---- row sums of the pass: combine the f groups, slot 0
-      float pa = phi.x, pb = phi.y;
-      for (int off = R; off < 32; off <<= 1) {
-        pa += __shfl_xor_sync(kFull, pa, off);
-        pb += __shfl_xor_sync(kFull, pb, off);
-      }
-      if (grp == 0) {
-        if (live0) Pr[own_base + tb + ti] = pa;
-        if (live1) Pr[own_base + tb + ti + R] = pb;
-      }
-      __syncwarp();
     }
   }
 }
@@ -274,12 +315,13 @@ __global__ void __launch_bounds__(32 * kLW) l2p_mutual_kernel(
     const int64_t oa = perm ? perm[ia] : ia, ob = perm ? perm[ib] : ib;
     for (int64_t r = 0; r < nrhs; ++r) {
       const float* loc = local + (b * nrhs + r) * ne;
-      // near field: the target's slots, in slot order (issued before the
-      // interaction loop; independent loads)
+      // near field: the target's slots, spread over the f lane groups (group
+      // g adds slots g, g + f, ...; the groups are combined below with the
+      // far field); loads issued before the interaction loop
       float na = 0.f, nb = 0.f;
-      if (sub == 0) {
+      {
         const float* Pr = P + r * pstride + pb0 + tb + ti;
-        for (int s = 0; s < slots; ++s) {
+        for (int s = sub; s < slots; s += f) {
           if (live0) na += __ldg(Pr + (int64_t)s * tc);
           if (live1) nb += __ldg(Pr + (int64_t)s * tc + R);
         }
@@ -321,6 +363,8 @@ __global__ void __launch_bounds__(32 * kLW) l2p_mutual_kernel(
       for (int off = R; off < 32; off <<= 1) {
         fa += __shfl_xor_sync(kFull, fa, off);
         fb += __shfl_xor_sync(kFull, fb, off);
+        na += __shfl_xor_sync(kFull, na, off);
+        nb += __shfl_xor_sync(kFull, nb, off);
       }
       const float c = real_traits<float>::inv4pi();
       if (sub == 0) {
@@ -339,22 +383,21 @@ extern "C" {
 // targets, tree order.  src4: (nrhs, npts) records (x, y, z, q); near_dst[e]
 // = base_B + slot * n_B for an upper entry e of leaf A's near list (B > A),
 // unused otherwise; P: nrhs planes of pstride floats.
-int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, const int32_t* lstart,
-                         const int32_t* lcount, int64_t n_leaves, const float* src4, int64_t npts,
-                         const int32_t* near_off, const int32_t* near_leaf,
-                         const int32_t* near_dst, const int32_t* base, int64_t nrhs,
+int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, int64_t n_leaves,
+                         const float* src4, int64_t npts, const int32_t* near_off,
+                         const int32_t* near_pack, const int32_t* order, int64_t nrhs,
                          int64_t pstride, int guard, float* P, void* stream) {
   if (n_leaves < 0 || npts < 0 || nrhs < 1 || pstride < npts) return KIFMM_EARG;
   if (n_leaves == 0) return 0;
   const auto* s4 = reinterpret_cast<const float4*>(src4);
+  const auto* pk = reinterpret_cast<const int4*>(near_pack);
+  const unsigned grid = ceil_div(n_leaves, kMW);
   if (guard)
-    p2p_mutual_kernel<true><<<ceil_div(n_leaves, kMW), 32 * kMW, 0, (cudaStream_t)stream>>>(
-        tx, ty, tz, lstart, lcount, n_leaves, s4, npts, near_off, near_leaf, near_dst, base, nrhs,
-        pstride, P);
+    p2p_mutual_kernel<true><<<grid, 32 * kMW, 0, (cudaStream_t)stream>>>(
+        tx, ty, tz, n_leaves, s4, npts, near_off, pk, order, nrhs, pstride, P);
   else
-    p2p_mutual_kernel<false><<<ceil_div(n_leaves, kMW), 32 * kMW, 0, (cudaStream_t)stream>>>(
-        tx, ty, tz, lstart, lcount, n_leaves, s4, npts, near_off, near_leaf, near_dst, base, nrhs,
-        pstride, P);
+    p2p_mutual_kernel<false><<<grid, 32 * kMW, 0, (cudaStream_t)stream>>>(
+        tx, ty, tz, n_leaves, s4, npts, near_off, pk, order, nrhs, pstride, P);
   return launch_status();
 }
 

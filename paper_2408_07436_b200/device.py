@@ -27,7 +27,7 @@ import torch
 from . import _native as nat
 from .engine import child_table, leaf_centers, leaf_surface_base
 from .m2l_blas import TILE_TARGETS, dense_cores, level_plan_from_buckets
-from .nearfield import f32_cross_leaf_coincident, mutual_slots
+from .nearfield import f32_cross_leaf_coincident, mutual_order, mutual_slots
 from .octree import class_transfer_table
 
 _NP2T = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
@@ -617,8 +617,11 @@ class DeviceFmm:
                 and os.environ.get("KIFMM_P2P", "mutual") == "mutual"
                 and np.array_equal(st.perm, tt.perm)):
             ms = mutual_slots(inst.near.offsets, inst.near.leaves, st.leaf_counts)
-            self.mutual = dict(base=to_dev(ms.base), nlow=to_dev(ms.nlow),
-                               dst=to_dev(ms.near_dst), total=ms.total)
+            self.mutual = dict(base=to_dev(ms.base), nlow=to_dev(ms.nlow), total=ms.total,
+                               pack=to_dev(ms.pack(inst.near.offsets, inst.near.leaves,
+                                                   st.leaf_starts, st.leaf_counts)),
+                               order=to_dev(mutual_order(inst.near.offsets, inst.near.leaves,
+                                                         st.leaf_counts)))
         # unit-box operators
         def inv_parts(inv):
             return (to_dev(inv.u, dt), to_dev(inv.inv_vals, dt),
@@ -652,6 +655,7 @@ class DeviceFmm:
         else:
             self._init_fft(inst.fft_ops, inst.halo_plans)
         self._bufs = {}
+        self._marks = None
         self.last_timings = {}
         self.last_m2l_calls = []
 
@@ -826,6 +830,15 @@ class DeviceFmm:
         n_e, n_c = self.n_e, self.n_c
         la, sfx = self.la, self.sfx
         ev = [] if timings else None
+        # operator intervals recorded inside a captured graph (external
+        # events: re-recorded by every replay; graph_timings reads them)
+        marks = self._marks
+
+        def mark(key):
+            if marks is not None:
+                e = torch.cuda.Event(enable_timing=True, external=True)
+                e.record(torch.cuda.current_stream())
+                marks.setdefault(key, []).append(e)
 
         def phase(name):
             set_tag(name)
@@ -835,6 +848,7 @@ class DeviceFmm:
                 ev.append((name, e))
 
         phase("p2m")
+        mark("p2m")
         q = b["q"]
         launch(f"kifmm_gather_charges_{sfx}", P(q_dev), P(self.s_perm), self.sx.shape[0], R,
                P(q), s)
@@ -870,9 +884,9 @@ class DeviceFmm:
             if mut is not None:
                 # mutual near field into the partial-sum slots
                 launch("kifmm_p2p_mutual_f32", P(self.tx), P(self.ty), P(self.tz),
-                       P(self.t_start), P(self.t_count), self.n_tgt[d], P(b["src4"]),
-                       self.sx.shape[0], P(self.near_off), P(self.near_leaf), P(mut["dst"]),
-                       P(mut["base"]), R, mut["total"], int(self.p2p_guard), P(b["pmut"]),
+                       self.n_tgt[d], P(b["src4"]), self.sx.shape[0], P(self.near_off),
+                       P(mut["pack"]), P(mut["order"]), R, mut["total"], int(self.p2p_guard),
+                       P(b["pmut"]),
                        stream)
             else:
                 launch(leaf_name, *leaf_args(2), stream)             # P2P, overwrite
@@ -892,7 +906,10 @@ class DeviceFmm:
 
         def fork_p2p():
             side.wait_stream(torch.cuda.current_stream())
-            p2p_pass(side.cuda_stream)
+            with torch.cuda.stream(side):
+                mark("p2p")
+                p2p_pass(side.cuda_stream)
+                mark("p2p")
 
         if overlap and p2p_after == "pack":
             fork_p2p()
@@ -903,6 +920,7 @@ class DeviceFmm:
                  P(self.s_start), P(self.s_count), nl, P(self.s_centers), P(self.check_base),
                  n_c, P(phi), s)
         la.chain(nl * R, phi, n_c, Linalg.solve_stages(self.up_inv, self.side[d]), mult[d], n_e)
+        mark("p2m")
         if overlap and p2p_after == "p2m":
             fork_p2p()
         loc = b["loc"]
@@ -948,7 +966,9 @@ class DeviceFmm:
             st = self.level_streams[lvl]
             st.wait_stream(main)
             with torch.cuda.stream(st):
+                mark("m2l")
                 m2l(lvl)
+                mark("m2l")
             forked[lvl] = st
 
         # KIFMM_FINE_M2L_AT: fork the finest level's M2L right after P2M
@@ -958,6 +978,7 @@ class DeviceFmm:
         if overlap and d >= 3 and fine_at == "p2m":
             fork_m2l(d)
         phase("m2m")
+        mark("m2m")
         # M2M down to level 2 (levels 0-1 carry no M2L): children stacked in
         # the chain's loader, kernel product, then the up_inv solve.
         for lvl in range(d, 2, -1):
@@ -968,6 +989,7 @@ class DeviceFmm:
                      a_child=self.src_child[lvl], child_w=n_e, a_nrhs=R)
             if overlap and lvl - 1 >= 3:
                 fork_m2l(lvl - 1)
+        mark("m2m")
         if overlap and d >= 3 and fine_at == "m2m":
             fork_m2l(d)
         if overlap and p2p_after == "m2m":
@@ -976,9 +998,13 @@ class DeviceFmm:
             n_t = self.n_tgt[lvl]
             phase(f"m2l{lvl}")
             if lvl not in forked and lvl not in calls:
+                mark("m2l")
                 m2l(lvl)
+                mark("m2l")
             if lvl == 2:
+                mark("m2l")
                 solve_level(2)
+                mark("m2l")
             if lvl < d:
                 # the level's M2L check potentials must exist before the L2L
                 # adds to them
@@ -986,8 +1012,11 @@ class DeviceFmm:
                     main.wait_stream(forked[lvl + 1])
                 else:
                     phase(f"m2l{lvl + 1}")
+                    mark("m2l")
                     m2l(lvl + 1)
+                    mark("m2l")
                 phase(f"l2l{lvl}")
+                mark("l2l")
                 # child check potentials (parent row x 8 children x n_c) into
                 # scratch, then added to the level's M2L check rows
                 # child parts of t (parent row x 8 children x rf) into scratch,
@@ -1006,20 +1035,29 @@ class DeviceFmm:
                     launch(f"kifmm_scatter_add_rows_{sfx}", P(l2l_tmp),
                            P(self._l2l_rowmap(lvl + 1, R)), n_t * R * 8, rf, P(t_c), s)
                 solve_level(lvl + 1)
+                mark("l2l")
         for st in forked.values():
             main.wait_stream(st)
         calls = [calls[l] for l in sorted(calls)]
         phase("leaf")
         if overlap:
             main.wait_stream(side)
+            mark("l2p")
             l2p_final(s)
+            mark("l2p")
         elif mut is not None:
             phase("p2p")
+            mark("p2p")
             p2p_pass(s)
+            mark("p2p")
             phase("l2p")
+            mark("l2p")
             l2p_final(s)
+            mark("l2p")
         else:
+            mark("p2p")
             launch(leaf_name, *leaf_args(3), s)                      # fused L2P + P2P
+            mark("p2p")
         phase("end")
         self.last_m2l_calls = calls
         self._events = ev
@@ -1034,6 +1072,7 @@ class DeviceFmm:
         (graph, static float64 charge buffer (n_src*R,), output tensor(s))."""
         if not hasattr(self, "_graphs"):
             self._graphs = {}
+            self._graph_marks = {}
         key = (nrhs, bool(gradient))
         if key not in self._graphs:
             static_q = torch.zeros(self.sx.shape[0] * nrhs, dtype=torch.float64,
@@ -1051,13 +1090,17 @@ class DeviceFmm:
             import gc
             was_enabled = gc.isenabled()
             gc.disable()
+            marks = {} if os.environ.get("KIFMM_GRAPH_TIMINGS", "1") != "0" else None
+            self._marks = marks
             try:
                 with torch.cuda.graph(g):
                     out = self.evaluate_device(static_q, nrhs, gradient=gradient)
             finally:
+                self._marks = None
                 if was_enabled:
                     gc.enable()
             self._graphs[key] = (g, static_q, out)
+            self._graph_marks[key] = marks
         return self._graphs[key]
 
     def evaluate_graphed(self, q_dev, nrhs, gradient=False):
@@ -1067,6 +1110,24 @@ class DeviceFmm:
         static_q.copy_(q_dev.reshape(-1))
         g.replay()
         return out
+
+    def graph_timings(self, nrhs, gradient=False):
+        """Operator seconds of the last replay of the (nrhs, gradient) graph,
+        from the events recorded inside it, as a thunk (read on first use
+        of ``FmmInstance.timings``; the replay must have completed).  The
+        passes overlap on several streams, so the six intervals are each an
+        operator's own span and may add up to more than the evaluate.  l2p
+        is 0 when it is fused into the near-field pass."""
+        marks = getattr(self, "_graph_marks", {}).get((nrhs, bool(gradient)))
+
+        def read():
+            t = {k: 0.0 for k in ("p2m", "m2m", "m2l", "l2l", "l2p", "p2p")}
+            if not marks:
+                return t
+            for k, evs in marks.items():
+                t[k] = sum(a.elapsed_time(b) for a, b in zip(evs[0::2], evs[1::2])) / 1e3
+            return t
+        return read
 
     def collect_timings(self):
         ev = getattr(self, "_events", None)

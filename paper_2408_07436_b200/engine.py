@@ -190,7 +190,7 @@ class FmmInstance:
     fft_ops: m2l_fft.M2lFftOperators | None = None
     halo_plans: dict = field(default_factory=dict)
     near: NearFieldPlan | None = None
-    timings: dict = field(default_factory=dict)
+    _timings: dict = field(default_factory=dict, repr=False)
     setup_seconds: float = 0.0
     m2l_calls: list = field(default_factory=list)
     n_near_pairs: int = 0
@@ -198,12 +198,25 @@ class FmmInstance:
     _device: object = None
     # sources and targets are one point set (the mutual near field applies)
     self_interaction: bool = False
-    # per-operator CUDA-event timings (operator_timings) cost an eager,
-    # un-graphed evaluate; off by default
+    # profile=True: an eager, un-graphed evaluate with a CUDA event between
+    # every phase (sequential phase times) instead of the graph's own events
     profile: bool = False
 
     def evaluate(self, charges, gradient=False):
         return evaluate(self, charges, gradient)
+
+    @property
+    def timings(self) -> dict:
+        """Seconds per operator class of the last evaluate (the reference's
+        six timers, engine.py:289-399).  Filled on every evaluate from CUDA
+        events recorded inside the evaluate's graph, read on first access."""
+        if callable(self._timings):
+            self._timings = self._timings()
+        return self._timings
+
+    @timings.setter
+    def timings(self, value):
+        self._timings = value
 
     def attach_charges(self, charges):
         return evaluate(self, charges)
@@ -364,8 +377,8 @@ def evaluate(inst: FmmInstance, charges, gradient=False):
     inst._last_charges = q
     res = inst.device.evaluate_host(q, timings=inst.profile, gradient=gradient)
     out, grad = res if gradient else (res, None)
-    if inst.profile:
-        inst.timings = dict(inst.device.last_timings)
+    inst.timings = (dict(inst.device.last_timings) if inst.profile
+                    else inst.device.graph_timings(q.shape[1], gradient))
     inst.m2l_calls = list(inst.device.last_m2l_calls)
     if q_in.ndim == 1 and q.shape[1] == 1:
         out = out[:, 0]

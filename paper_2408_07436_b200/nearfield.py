@@ -31,6 +31,32 @@ class MutualSlots:
     near_dst: np.ndarray     # (len(near.leaves),) int32: base[B] + slot * n_B for upper entries, else -1
     total: int               # floats per right-hand side
 
+    def pack(self, near_offsets, near_leaves, leaf_starts, leaf_counts) -> np.ndarray:
+        """(len(near.leaves), 4) int32 device table of csrc/p2p_mutual.cu:
+        (start, count, dst, leaf) per near entry; the own entry (first of
+        each list) carries the leaf's slot base as dst."""
+        lv = np.asarray(near_leaves, dtype=np.int64)
+        off = np.asarray(near_offsets, dtype=np.int64)
+        dst = self.near_dst.astype(np.int64).copy()
+        nonempty = np.diff(off) > 0
+        dst[off[:-1][nonempty]] = self.base[np.flatnonzero(nonempty)]
+        out = np.stack([np.asarray(leaf_starts, np.int64)[lv], np.asarray(leaf_counts, np.int64)[lv],
+                        dst, lv], axis=1)
+        return np.ascontiguousarray(out.astype(np.int32))
+
+
+def mutual_order(near_offsets, near_leaves, leaf_counts) -> np.ndarray:
+    """Leaves by descending mutual-pass work (targets x (own + upper
+    columns)): the launch order of csrc/p2p_mutual.cu (longest first)."""
+    off = np.asarray(near_offsets, dtype=np.int64)
+    lv = np.asarray(near_leaves, dtype=np.int64)
+    n = np.asarray(leaf_counts, dtype=np.int64)
+    owner = np.repeat(np.arange(n.shape[0]), np.diff(off))
+    up = lv > owner
+    cols = np.bincount(owner[up], weights=n[lv[up]], minlength=n.shape[0])
+    work = n * (cols + n)
+    return np.argsort(-work, kind="stable").astype(np.int32)
+
 
 def mutual_slots(near_offsets, near_leaves, leaf_counts) -> MutualSlots:
     off = np.asarray(near_offsets, dtype=np.int64)

@@ -508,7 +508,8 @@ def test_mutual_near_field(cuda, monkeypatch, n, depth, nrhs, clustered, merge):
     if clustered:
         pts = pts ** 3
     if merge:
-        pts[:2] = [[0.5 - 1e-12, 0.3, 0.3], [0.5 + 1e-12, 0.3, 0.3]]
+        # domain [0, 1]^3 (its centre 0.5 is a leaf boundary at every level)
+        pts[:4] = [[0.5 - 1e-12, 0.3, 0.3], [0.5 + 1e-12, 0.3, 0.3], [0, 0, 0], [1, 1, 1]]
     q = rng.random((n, nrhs)) if nrhs > 1 else rng.random(n)
     kw = dict(depth=depth, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6)
     res = {}
@@ -529,3 +530,22 @@ def test_mutual_near_field(cuda, monkeypatch, n, depth, nrhs, clustered, merge):
     if nrhs == 1:
         want, _ = _reference_run(pts, q, kw)
         assert parity_report(res["mutual"], want)["max_rel"] <= TOL["f32"]
+
+
+def test_operator_timings_filled_by_default(cuda):
+    """inst.timings carries the reference's six operator timers after every
+    evaluate (engine.py:289-399, 454-459), from events inside the graph."""
+    from paper_2408_07436_b200 import FmmConfig, setup
+    from paper_2408_07436_b200.engine import OPERATOR_NAMES
+    pts = np.random.default_rng(2).random((30000, 3))
+    q = np.random.default_rng(3).random(30000)
+    for kw in (dict(depth=4, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6),
+               dict(depth=3, order_equiv=4, backend="fft", precision="f64")):
+        inst = setup(pts, pts, FmmConfig(**kw))
+        inst.evaluate(q)
+        t = inst.operator_timings()
+        assert set(OPERATOR_NAMES) <= set(t) and t["setup"] > 0
+        for k in ("p2m", "m2m", "m2l", "l2l", "p2p"):
+            assert 0 < t[k] < 1.0, (kw, k, t)
+        again = inst.evaluate(2 * q)
+        assert np.all(np.isfinite(again)) and inst.timings["m2l"] > 0
