@@ -209,7 +209,7 @@ def cpu_reference_run(pts, q, steps=1, warmup=0, kw=None):
         pot = run(q)
         times.append(time.perf_counter() - t0)
     return dict(kind=kind, cores=cores, times=times, potentials=pot,
-                timings=getattr(inst, "timings", {}))
+                timings=getattr(inst, "timings", {}), instance=inst)
 
 
 def run_reference_arm(args):
@@ -236,6 +236,157 @@ def run_reference_arm(args):
                 operator_seconds={k: float(v) for k, v in res["timings"].items()})
     print(json.dumps(line), flush=True)
     return 0
+
+
+# --------------------------------------------------------------- config 3
+C3_CONFIG = dict(depth=5, order_equiv=8, backend="fft", precision="f64")
+
+
+def c3_inputs(n=N_POINTS):
+    """BASELINE config 3: the config-2 points, charges U[-1, 1) (seed 11)."""
+    pts = np.random.default_rng(POINT_SEED).random((n, 3))
+    return pts, np.random.default_rng(CHARGE_SEED).uniform(-1, 1, n)
+
+
+def run_ref_subprocess(name, out_path):
+    """The reference evaluate of a named config in a fresh process: all
+    cores for its OpenMP loops with OMP_WAIT_POLICY=ACTIVE (libgomp reads it
+    once, at load).  See ref_config_main."""
+    n = str(os.cpu_count() or 1)
+    env = dict(os.environ, OMP_NUM_THREADS=n, KIFMM_THREADS=n, OMP_WAIT_POLICY="ACTIVE")
+    env.pop("OPENBLAS_NUM_THREADS", None)
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--ref-config", name,
+                        "--ref-out", out_path], env=env, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"reference {name} run failed: {r.stderr[-2000:]}")
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def ref_config_main(name, out_path):
+    """Two reference evaluates of one instance: the timed one with
+    single-threaded OpenBLAS (the fastest policy measured: it does not
+    oversubscribe the cores against the OpenMP team), and one with threaded
+    OpenBLAS.  The two differ by BLAS rounding alone, which bounds how
+    closely ANY implementation can be said to match "the reference" per
+    target (signed charges: near-zero potentials amplify it)."""
+    from threadpoolctl import threadpool_limits
+    pts, q = c3_inputs() if name == "c3" else inputs()
+    kw = C3_CONFIG if name == "c3" else CONFIG
+    t0 = time.perf_counter()
+    with threadpool_limits(limits=1, user_api="blas"):
+        res = cpu_reference_run(pts, q, steps=1, kw=kw)
+    inst = res["instance"]
+    pot_mt = np.asarray(inst.evaluate(q))
+    np.savez(out_path, timed=np.asarray(res["potentials"]), blas_threaded=pot_mt)
+    print(json.dumps(dict(kind=res["kind"], cores=res["cores"], seconds=min(res["times"]),
+                          total_seconds=time.perf_counter() - t0,
+                          operator_seconds={k: float(v) for k, v in res["timings"].items()})))
+    return 0
+
+
+def parity_stats(got, want, tol):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    d = np.abs(got - want)
+    rel = d / np.abs(want)
+    scale = np.abs(want).max()
+    return dict(tol=tol, max_rel=float(rel.max()), strict_failures=int((rel > tol).sum()),
+                normwise=float(d.max() / scale),
+                floored_max=float((d / np.maximum(np.abs(want), 1e-3 * scale)).max()))
+
+
+def hadamard_work(inst, lvl):
+    """SURVEY 8(d) FFT-M2L algorithmic work at one level, n_rhs = 1:
+    F_had = 8 n_freq sum(admissible pairs) flop, B_had = 2 w n_freq
+    (N_s + 26 * 64 + N_t) bytes (source spectra, the 26 x 64 kernel
+    spectra, target spectra)."""
+    ops, plan = inst.fft_ops, inst.halo_plans[lvl]
+    kh = np.asarray(ops.khat)
+    nz = np.any(kh != 0, axis=0).sum(axis=(1, 2))                 # admissible (tau, sigma) per offset
+    pairs = int((nz[None, :] * (np.asarray(plan.halo) >= 0)).sum())
+    w = np.dtype(inst.config.dtype).itemsize
+    n_s = inst.source_tree.level_keys(lvl).shape[0]
+    n_t = inst.target_tree.level_keys(lvl).shape[0]
+    return dict(pairs=pairs, flops=8.0 * ops.n_freq * pairs,
+                bytes=2.0 * w * ops.n_freq * (n_s + 26 * 64 + n_t))
+
+
+def run_config3(args, flush, peaks, with_reference=True):
+    """BASELINE config 3 on the same GPU: 1M uniform points, charges
+    U[-1, 1), float64, p = 8, FFT-M2L, depth 5, potential and gradient."""
+    import torch
+    from paper_2408_07436_b200 import FmmConfig, setup
+    from paper_2408_07436_b200.device import profile_launches
+    pts, q = c3_inputs()
+    t0 = time.perf_counter()
+    inst = setup(pts, pts, FmmConfig(**C3_CONFIG))
+    setup_s = time.perf_counter() - t0
+    dev = inst.device
+    q_dev = torch.from_numpy(q).cuda()
+    timed = {}
+    for grad in (True, False):
+        for _ in range(max(3, args.warmup)):
+            dev.evaluate_graphed(q_dev, 1, gradient=grad)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record()
+            dev.evaluate_graphed(q_dev, 1, gradient=grad)
+            e1.record()
+        torch.cuda.synchronize()
+        timed[grad] = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    flush.zero_()
+    with profile_launches() as prof:
+        dev.evaluate_device(q_dev, 1, timings=True)
+    launches = prof.times()
+    per_kernel = {}
+    for name, tag, t in launches:
+        per_kernel[name.replace("kifmm_", "")] = per_kernel.get(name.replace("kifmm_", ""), 0.0) + t
+    lvl = inst.config.depth
+    had_ms = sum(t for n, tag, t in launches if "hadamard" in n and tag == f"m2l{lvl}")
+    work = hadamard_work(inst, lvl)
+    dmma = probe_peak(3)
+    had = dict(kernel=f"hadamard_tiled_c128 (level {lvl})", ms=had_ms,
+               algorithmic=f"F_had = 8 n_freq sum(pairs) = {work['flops']:.4g} flop, "
+                           f"B_had = 2 w n_freq (N_s + 26*64 + N_t) = {work['bytes']:.4g} B "
+                           f"(SURVEY 8d), {work['pairs']} admissible pairs",
+               fp64_tflops=work["flops"] / (had_ms / 1e3) / 1e12, dmma_peak_tflops=dmma,
+               dmma_frac=work["flops"] / (had_ms / 1e3) / 1e12 / dmma,
+               hbm_gbs=work["bytes"] / (had_ms / 1e3) / 1e9, hbm_peak_gbs=peaks["hbm_gbs"],
+               hbm_frac=work["bytes"] / (had_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+               peak_source="kifmm_probe DMMA m8n8k4 measured in this run; HBM "
+                           + peaks["source"])
+    pot = dev.evaluate_device(q_dev, 1).cpu().numpy()[:, 0].astype(np.float64)
+    rec = dict(workload="BASELINE config 3: N=1,000,000 uniform [0,1]^3, charges U[-1,1), "
+                        "float64, p=8 (296-point surfaces), FFT-M2L on the 2p grid, depth 5, "
+                        "potential and gradient", config=C3_CONFIG, setup_seconds=setup_s,
+               ms_per_evaluate_gradient=timed[True], ms_per_evaluate_potential=timed[False],
+               value=N_POINTS / (timed[True] / 1e3) / 1e6, unit="Mpoints/s",
+               value_potential_only=N_POINTS / (timed[False] / 1e3) / 1e6,
+               kernel_ms=per_kernel, hadamard=had,
+               timing="CUDA graph replay, CUDA events, L2 flushed between steps")
+    if with_reference:
+        import tempfile
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "ref_c3.npz")
+            info = run_ref_subprocess("c3", path)
+            refs = dict(np.load(path))
+        rec["cpu_baseline"] = dict(
+            value=N_POINTS / info["seconds"] / 1e6, unit="Mpoints/s", seconds=info["seconds"],
+            cores=info["cores"], kind=info["kind"], operator_seconds=info["operator_seconds"],
+            sample="one full config-3 evaluate (potential; the reference has no gradient), "
+                   "all host threads, OMP_WAIT_POLICY=ACTIVE, single-threaded OpenBLAS")
+        rec["parity"] = dict(
+            vs_reference=parity_stats(pot, refs["timed"], 1e-10),
+            vs_reference_blas_threaded=parity_stats(pot, refs["blas_threaded"], 1e-10),
+            reference_vs_itself=parity_stats(refs["timed"], refs["blas_threaded"], 1e-10),
+            note="signed charges: near-zero potentials make the per-target ratio depend on "
+                 "rounding order alone; the reference's two BLAS threadings disagree by "
+                 "reference_vs_itself (SURVEY 8d); full-size records in "
+                 "profiles/r2/parity_full")
+    return rec
 
 
 # ------------------------------------------------------------------ ours
@@ -424,6 +575,9 @@ def run_single(args):
                    "(in the bench process; default thread policy)", seconds=csec,
                    operator_seconds={k: float(v) for k, v in res["timings"].items()},
                    parity_max_rel=float(rel.max()), parity_tol=1e-5)
+    c3 = None
+    if not args.no_config3:
+        c3 = run_config3(args, flush, peaks, with_reference=not args.no_cpu_baseline)
     line = dict(metric=METRIC, value=value, unit="Mpoints/s", n_gpus=1, steps=args.steps,
                 warmup=args.warmup, ms_per_step=ms, higher_is_better=True, scaling="strong",
                 vs_baseline=None, dtype="f32", data="synthetic (seeded; no dataset involved)",
@@ -440,7 +594,8 @@ def run_single(args):
                          h2d_bytes_per_step=int(q.nbytes),
                          d2h_bytes_per_step=int(out.nbytes)),
                 gpu_launches=n_launch * args.steps, clocks=clk.summary(),
-                setup_seconds=setup_s, p2p_interactions=inst.n_near_pairs)
+                setup_seconds=setup_s, p2p_interactions=inst.n_near_pairs,
+                configs={"c3": c3} if c3 is not None else {})
     print(json.dumps(line), flush=True)
     return 0
 
@@ -452,9 +607,15 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config3", action="store_true",
+                    help="skip the config-3 (FFT-M2L, float64) extra measurement")
+    ap.add_argument("--ref-config", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--ref-out", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--force-dist", action="store_true",
                     help="use the partitioned (torchrun) path even for one rank")
     args = ap.parse_args(argv)
+    if args.ref_config:
+        return ref_config_main(args.ref_config, args.ref_out)
     if args.impl == "reference":
         return run_reference_arm(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -300,14 +300,14 @@ int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, int6
                          const float* src4, int64_t npts, const int32_t* near_off,
                          const int32_t* near_pack, const int32_t* order, int64_t nrhs,
                          int64_t pstride, int guard, float* P, void* stream);
-/* Final pass of the mutual near field: out[perm[i]*nrhs + r] = L2P(i)
- * (engine.py:377-389) + sum_{s=0..nlow_b} P[r*pstride + base[b] + s*n_b + t]
- * (slot order), the un-permute of engine.py:399-404. */
-int kifmm_l2p_mutual_f32(const float* tx, const float* ty, const float* tz, const int32_t* tleaf_start,
-                         const int32_t* tleaf_count, int64_t n_tleaves, const double* centers,
-                         const double* base_e, int64_t ne, const float* local, int64_t nrhs,
-                         const int64_t* perm, const int32_t* base, const int32_t* nlow,
-                         int64_t pstride, const float* P, float* out, void* stream);
+/* Near-field totals of the mutual pass: out[perm[i]*nrhs + r] = (1/4 pi)
+ * sum_{s=0..nlow_b} P[r*pstride + base[b] + s*n_b + t] (slot order), for
+ * target i = leaf b's t-th point; the L2P pass then accumulates onto out
+ * (kifmm_leaf_pass_f32 with parts = 1 | 4). */
+int kifmm_p2p_mutual_reduce_f32(const int32_t* tleaf_start, const int32_t* tleaf_count,
+                                int64_t n_tleaves, int64_t nrhs, const int64_t* perm,
+                                const int32_t* base, const int32_t* nlow, int64_t pstride,
+                                const float* P, float* out, void* stream);
 
 /* Leaf pass: fused L2P + P2P + un-permute (engine.py:377-404).  For target
  * leaf b and target i in it:

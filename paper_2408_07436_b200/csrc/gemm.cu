@@ -531,13 +531,8 @@ int kifmm_gemm_f32(int64_t M, int64_t N, int64_t K, float alpha, const float* A,
                    float* C, int64_t ldc, const int32_t* rowmap, int accumulate, void* s) {
   if (M < 0 || N < 0 || K < 0 || asum < 1) return KIFMM_EARG;
   if (M == 0 || N == 0) return 0;
-  // tall shapes: the 128-row cp.async kernel (KIFMM_GEMM_TS=0: the SIMT tiles)
-  static int ts = -1;
-  if (ts < 0) {
-    const char* e = getenv("KIFMM_GEMM_TS");
-    ts = e ? atoi(e) : 1;
-  }
-  if (ts && M * ((N + SBN - 1) / SBN) >= 128 * 148)
+  // tall shapes: the 128-row cp.async kernel, else the SIMT tiles
+  if (M * ((N + SBN - 1) / SBN) >= 128 * 148)
     return gemm_ts(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,
                    accumulate, (cudaStream_t)s);
   return gemm<float>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,
@@ -547,13 +542,8 @@ int kifmm_gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, const double* 
                    int asum, int64_t astride, const double* B, int64_t ldb,
                    const double* colscale, double* C, int64_t ldc, const int32_t* rowmap,
                    int accumulate, void* s) {
-  // FP64 tensor cores for every tile-worthy shape (KIFMM_GEMM_DMMA=0: SIMT)
-  static int dmma = -1;
-  if (dmma < 0) {
-    const char* e = getenv("KIFMM_GEMM_DMMA");
-    dmma = e ? atoi(e) : 1;
-  }
-  if (dmma && M >= 256 && N >= 8 && K >= 4 && asum >= 1)
+  // FP64 tensor cores for every tile-worthy shape
+  if (M >= 256 && N >= 8 && K >= 4 && asum >= 1)
     return gemm_dmma(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,
                      accumulate, (cudaStream_t)s);
   return gemm<double>(M, N, K, alpha, A, lda, asum, astride, B, ldb, colscale, C, ldc, rowmap,

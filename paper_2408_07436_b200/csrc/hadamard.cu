@@ -472,12 +472,7 @@ int hadamard_tiled(const T* khat, const T* qhat, const int64_t* tile_begin, cons
                       UMAX * sizeof(int);
   dim3 grid((unsigned)n_tiles, ceil_div(nf, FCH), (unsigned)nrhs);
   if constexpr (sizeof(T) == 8) {
-    static int dmma = -1;
-    if (dmma < 0) {
-      const char* e = getenv("KIFMM_HADAMARD_DMMA");
-      dmma = e ? atoi(e) : 1;
-    }
-    if (dmma) {
+    {
       set_max_smem((const void*)hadamard_tiled_dmma_kernel, smem);
       hadamard_tiled_dmma_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(
           reinterpret_cast<const double2*>(khat), reinterpret_cast<const double2*>(qhat),

@@ -270,16 +270,10 @@ size_t forward_smem(int bpc) { return FftShape<T, P>::head + bpc * FftShape<T, P
 template <typename T, int P>
 size_t inverse_smem(int bpc) { return FftShape<T, P>::head + bpc * FftShape<T, P>::ibox; }
 
-// Boxes per CTA: the largest of 8/4/2/1 whose scratch fits, capped by
-// KIFMM_FFT_BPC (smaller CTAs -> more CTAs resident per SM).
+// Boxes per CTA: the largest of 8/4/2/1 whose scratch fits.
 int pick_bpc(size_t (*smem)(int), size_t limit) {
-  static int cap = -1;
-  if (cap < 0) {
-    const char* e = getenv("KIFMM_FFT_BPC");
-    cap = e ? atoi(e) : 8;
-  }
   for (int bpc = 8; bpc >= 1; bpc /= 2)
-    if (bpc <= cap && smem(bpc) <= limit) return bpc;
+    if (smem(bpc) <= limit) return bpc;
   return 0;
 }
 

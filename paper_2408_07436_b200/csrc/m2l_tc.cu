@@ -373,17 +373,8 @@ int kifmm_m2l_sweep_tc_f32(const float* qhi, const float* qlo, const float* bhi,
     return KIFMM_EARG;
   if (n_tiles == 0) return 0;
   const size_t stage_bytes = 2 * (size_t)TMT * KC * 4 + 2 * (size_t)n_out * KC * 4;
-  // Pipeline depth / CTAs per SM (tuning knobs, defaults measured on B200).
-  static int ctas_per_sm = -1, max_stages = -1, l1 = 0;
-  if (ctas_per_sm < 0) {
-    const char* e = getenv("KIFMM_TC_CTAS");
-    ctas_per_sm = e ? atoi(e) : 2;
-    if (ctas_per_sm < 1) ctas_per_sm = 1;
-    const char* f = getenv("KIFMM_TC_STAGES");
-    max_stages = f ? atoi(f) : 6;
-    const char* g = getenv("KIFMM_TC_L1");
-    l1 = g ? atoi(g) : 0;
-  }
+  // Pipeline depth / CTAs per SM (measured on B200)
+  constexpr int ctas_per_sm = 2, max_stages = 6, l1 = 0;
   // 3 * n_out accumulator columns > 256 take the whole 512-column TMEM:
   // one CTA per SM then (a second one would wait in tcgen05.alloc).
   const int ctas = 3 * n_out > 256 ? 1 : ctas_per_sm;

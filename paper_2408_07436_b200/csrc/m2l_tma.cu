@@ -466,26 +466,14 @@ int kifmm_m2l_sweep_tma_f32(const float* qhi, const float* qlo, const float* bhi
   if (!st) st = make_map(&tm_lo, split_smem ? qhi : qlo, (int)kin, (int)h, 8 * nrhs);
   if (st) return st;
   const size_t stage_bytes = 2 * (size_t)TMT * KC * 4 + 2 * (size_t)n_out * KC * 4;
-  static int max_stages = -1, ctas = -1;
-  if (max_stages < 0) {
-    const char* e = getenv("KIFMM_TMA_STAGES");
-    max_stages = e ? atoi(e) : 4;
-    const char* f = getenv("KIFMM_TMA_CTAS");
-    ctas = f ? atoi(f) : 2;
-    if (ctas < 1) ctas = 1;
-  }
+  constexpr int max_stages = 4, ctas = 2;   // measured on B200
   // 3 * n_out accumulator columns > 256 take the whole 512-column TMEM:
   // one CTA per SM then, with the shared memory for deeper pipelining.
-  static int mma2_env = -1;
-  if (mma2_env < 0) {
-    const char* g = getenv("KIFMM_TMA_MMA2");
-    mma2_env = g ? atoi(g) : 2;
-  }
-  // 2-MMA form (KIFMM_TMA_MMA2=2, default: single-buffered accumulator,
-  // 3 n_out TMEM columns, two CTAs/SM; =1: double-buffered, 5 n_out columns,
-  // one CTA/SM; =0: three MMAs per k-step) needs N = 2 n_out <= 256.
-  // Measured on B200 (config 2, level 5): =2 ~2% faster than =0, =1 ~50%
-  // slower (one CTA/SM).
+  // 2-MMA form (single-buffered accumulator, 3 n_out TMEM columns, two
+  // CTAs/SM) where N = 2 n_out <= 256, else three MMAs per k-step.
+  // Measured on B200 (config 2, level 5): ~2% faster than three MMAs; a
+  // double-buffered accumulator (5 n_out columns, one CTA/SM) ~50% slower.
+  constexpr int mma2_env = 2;
   const int mma2 = mma2_env && 2 * n_out <= 256 && 3 * n_out <= 256;
   const int nbuf = mma2 && mma2_env == 2 ? 1 : 2;
   const int cols = nbuf * (mma2 ? 2 : 1) * (int)n_out + (int)n_out;

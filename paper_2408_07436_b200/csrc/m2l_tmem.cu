@@ -46,8 +46,23 @@ using namespace kifmm;
 namespace {
 
 constexpr int TMT = 128;
-constexpr int NG = 2;             // groups per CTA (alternate vectors), each with its own TMEM A and D
-constexpr int NTHREADS = 32 + 128 * NG;
+#ifndef KIFMM_TMEM_MMA3
+#define KIFMM_TMEM_MMA3 0
+#endif
+// 1: per k-step three MMAs of N = KP into a KP-column accumulator,
+//    D += A_hi.B_hi + A_lo.B_hi + A_hi.B_lo (168 TMEM columns per group at
+//    KP = 56: three groups fit the 512 columns);
+// 0: two MMAs, A_hi.[B_hi | B_lo] (N = 2 KP) + A_lo.B_hi, into 2 KP columns
+constexpr bool MMA3 = KIFMM_TMEM_MMA3 != 0;
+#ifndef KIFMM_TMEM_NG
+#define KIFMM_TMEM_NG 2
+#endif
+// groups per CTA (interleaved vectors), each with its own TMEM A and D: the
+// requested count where their columns fit the 512-column TMEM, else 2
+template <int KP>
+constexpr int groups_for() {
+  return KIFMM_TMEM_NG * ((MMA3 ? KP : 2 * KP) + 2 * KP) <= 512 ? KIFMM_TMEM_NG : 2;
+}
 #ifndef KIFMM_TMEM_STW
 #define KIFMM_TMEM_STW 8           // widest tcgen05.st piece (8 / 16 / 32 columns)
 #endif
@@ -252,7 +267,7 @@ __device__ __forceinline__ TileGeom tile_geom(const TmemArgs& a, int slot) {
   return t;
 }
 
-template <int KP>
+template <int KP, int NG = groups_for<KP>(), int NTHREADS = 32 + 128 * NG>
 #ifdef KIFMM_TMEM_MAXNREG
 __global__ void __maxnreg__(KIFMM_TMEM_MAXNREG) m2l_sweep_tmem_kernel(
 #else
@@ -260,8 +275,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
 #endif
     const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm2,
     const __grid_constant__ CUtensorMap tm3, const TmemArgs a) {
-  constexpr int N1 = 2 * KP;
-  constexpr int N2 = (KP + 15) / 16 * 16;
+  constexpr int N1 = MMA3 ? KP : 2 * KP;
+  constexpr int N2 = MMA3 ? KP : (KP + 15) / 16 * 16;
   // source block: columns [0, 32) in a 128-byte-swizzled box, the rest
   // (KP - 32 columns) in a second box, swizzled when it is 32 wide and
   // linear (rows of (KP - 32) * 4 bytes, exact width) otherwise
@@ -284,6 +299,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
                                  : NEED <= 256 ? 256 : 512;
   static_assert(NEED <= 512, "TMEM budget");
   static_assert(KP % 8 == 0 && N1 <= 256, "shape");
+  static_assert(NG >= 2 && NG <= 3, "groups");
 
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -443,6 +459,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
             const uint64_t db = desc_nosw(bb + ks * 256, 128, SBO);
             mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, local | ks);
             mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
+            if (MMA3) {
+              // A_hi . B_lo: B_lo follows B_hi (KP / 8 groups of 8 rows)
+              const uint64_t dl = desc_nosw(bb + KP * KP * 4 + ks * 256, 128, SBO);
+              mma_tf32_ts(dcol, acol + ks * 8, dl, idesc1, 1);
+            }
           }
           mma_commit(&done[grp]);
           mma_commit(&empty[s]);
@@ -460,38 +481,42 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           for (int c = 0; c < KP / 8; ++c) {
             uint32_t u[8], w[8];
             tmem_ld8(dcol + lane_base + c * 8, u);
-            tmem_ld8(dcol + lane_base + KP + c * 8, w);
+            if (!MMA3) tmem_ld8(dcol + lane_base + KP + c * 8, w);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              acc[c * 8 + i] += __uint_as_float(u[i]) + __uint_as_float(w[i]);
+              acc[c * 8 + i] += MMA3 ? __uint_as_float(u[i])
+                                     : __uint_as_float(u[i]) + __uint_as_float(w[i]);
           }
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         }
       }
-      // combine the two groups' partial sums in shared memory, 8 columns at
-      // a time, and let group 0 write the item's result (one output slot per
+      // combine the groups' partial sums in shared memory, 8 columns at a
+      // time, and let group 0 write the item's result (one output slot per
       // vector split)
       float4* red = reinterpret_cast<float4*>(tmem_slot + 4);     // 128 x 8 floats
 #pragma unroll
       for (int c = 0; c < KP; c += 8) {
-        if (grp == 1) {
-          red[2 * m] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-          red[2 * m + 1] = make_float4(acc[c + 4], acc[c + 5], acc[c + 6], acc[c + 7]);
+#pragma unroll
+        for (int g2 = 1; g2 < NG; ++g2) {
+          if (grp == g2) {
+            red[2 * m] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+            red[2 * m + 1] = make_float4(acc[c + 4], acc[c + 5], acc[c + 6], acc[c + 7]);
+          }
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + NG), "r"(128 * NG) : "memory");
+          if (grp == 0) {
+            const float4 u = red[2 * m], w = red[2 * m + 1];
+            acc[c] += u.x;
+            acc[c + 1] += u.y;
+            acc[c + 2] += u.z;
+            acc[c + 3] += u.w;
+            acc[c + 4] += w.x;
+            acc[c + 5] += w.y;
+            acc[c + 6] += w.z;
+            acc[c + 7] += w.w;
+          }
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + NG), "r"(128 * NG) : "memory");
         }
-        asm volatile("bar.sync 3, 256;" ::: "memory");
-        if (grp == 0) {
-          const float4 u = red[2 * m], w = red[2 * m + 1];
-          acc[c] += u.x;
-          acc[c + 1] += u.y;
-          acc[c + 2] += u.z;
-          acc[c + 3] += u.w;
-          acc[c + 4] += w.x;
-          acc[c + 5] += w.y;
-          acc[c + 6] += w.z;
-          acc[c + 7] += w.w;
-        }
-        asm volatile("bar.sync 3, 256;" ::: "memory");
       }
       const int32_t tgt = a.tile_targets[(int64_t)x.slot * TMT + m];
       if (grp == 0 && tgt >= 0) {
@@ -568,29 +593,20 @@ int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   if (!st && W16) st = make_map(&tm2, a.q, KP, a.h, planes, 16, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!st && W8) st = make_map(&tm3, a.q, KP, a.h, planes, 8, CU_TENSOR_MAP_SWIZZLE_32B);
   if (st) return st;
-  static int ns_env = -1;
-  if (ns_env < 0) {
-    const char* e = getenv("KIFMM_TMEM_STAGES");
-    ns_env = e ? atoi(e) : 4;             // config 2 on B200: 4 ~ 3 stages (281-288 us), 2: 362 us
-    if (ns_env < 2) ns_env = 2;
-  }
+  constexpr int ns_env = 4;             // config 2 on B200: 4 ~ 3 stages (281-288 us), 2: 362 us
   const size_t sbytes = ((size_t)TMT * 128 + (size_t)TMT * W1 * 4 + 2ull * KP * KP * 4 + 1023) /
                         1024 * 1024;
   int ns = ns_env;
   while (ns > 2 && 1024 + ns * sbytes + 256 + 4096 > 227 * 1024) --ns;
   a.ns = ns;
+  constexpr int NG = groups_for<KP>();
   const size_t smem = 1024 + ns * sbytes + (2 * ns + NG) * 8 + 16 + 4096;
-  // persistent CTAs: one per SM, or KIFMM_TMEM_GRID (fewer leaves SMs to the
-  // concurrent small kernels of the other streams)
-  static int grid_env = -1;
-  if (grid_env < 0) {
-    const char* e = getenv("KIFMM_TMEM_GRID");
-    grid_env = e ? atoi(e) : 0;
-  }
-  const int g_max = grid_env > 0 && grid_env < sm_count() ? grid_env : sm_count();
+  // persistent CTAs: one per SM (capping the grid to leave SMs to the
+  // other streams' kernels measured within +-1%)
+  const int g_max = sm_count();
   const int grid = a.n_items < g_max ? a.n_items : g_max;
   set_max_smem((const void*)m2l_sweep_tmem_kernel<KP>, smem);
-  m2l_sweep_tmem_kernel<KP><<<grid, NTHREADS, smem, stream>>>(tm, tm2, tm3, a);
+  m2l_sweep_tmem_kernel<KP><<<grid, 32 + 128 * NG, smem, stream>>>(tm, tm2, tm3, a);
   return launch_status();
 }
 

@@ -20,8 +20,9 @@
 //   slot s = 1..nlow  the column sums contributed by the s-th lower
 //                     neighbour (B's near list is [B, neighbours ascending],
 //                     so the lower neighbours are entries 1..nlow)
-// at P[base_B + s n_B + t]; l2p_mutual_kernel adds the slots of each target
-// in slot order to its L2P far field and un-permutes (engine.py:377-404).
+// at P[base_B + s n_B + t]; mutual_reduce_kernel adds the slots of each
+// target in slot order into the caller-ordered output (un-permuted,
+// engine.py:399-404) and the L2P pass accumulates the far field onto it.
 //
 // Column sums inside a warp: a pass holds up to 32 targets of A, two per
 // lane (packed FP32 pairs, as leaf_pass_x2_kernel), in f = 32 / R groups of
@@ -63,39 +64,47 @@ __device__ __forceinline__ float4 pad_col() {
                      __int_as_float(0x7f800000), 0.f);
 }
 
-// Row-only sum over staged records [0, m) for the lane's two packed targets,
-// sources j = start, start + stride, ...; every record may coincide with a
-// target (the leaf's own block): r2 = 0 contributes 0.
-__device__ __forceinline__ void self_sum(const float4* buf, int m, int start, int stride,
-                                         float2 X, float2 Y, float2 Z, float2& acc) {
-  float2 acc2 = make_float2(0.f, 0.f);
-  auto body = [&](int j, float2& a_) {
-    const float4 s = buf[j];
-    const float2 dx = __fadd2_rn(X, make_float2(-s.x, -s.x));
-    const float2 dy = __fadd2_rn(Y, make_float2(-s.y, -s.y));
-    const float2 dz = __fadd2_rn(Z, make_float2(-s.z, -s.z));
-    const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-    float w0 = real_traits<float>::rsq(r2.x), w1 = real_traits<float>::rsq(r2.y);
+// Row-only sum over staged records [0, m) for the lane's four targets (two
+// packed pairs: X0 = targets (0, 1), X1 = (2, 3)), sources j = start,
+// start + stride, ...; every record may coincide with a target (the leaf's
+// own block): r2 = 0 contributes 0.
+struct Quad {
+  float2 X0, Y0, Z0, X1, Y1, Z1;
+};
+__device__ __forceinline__ float2 inv_r2(float2 X, float2 Y, float2 Z, const float4& s) {
+  const float2 dx = __fadd2_rn(X, make_float2(-s.x, -s.x));
+  const float2 dy = __fadd2_rn(Y, make_float2(-s.y, -s.y));
+  const float2 dz = __fadd2_rn(Z, make_float2(-s.z, -s.z));
+  return __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+}
+template <bool GUARD>
+__device__ __forceinline__ float2 rsq2f(float2 r2) {
+  float w0 = real_traits<float>::rsq(r2.x), w1 = real_traits<float>::rsq(r2.y);
+  if (GUARD) {
     w0 = r2.x > 0.f ? w0 : 0.f;
     w1 = r2.y > 0.f ? w1 : 0.f;
-    a_ = __ffma2_rn(make_float2(w0, w1), make_float2(s.w, s.w), a_);
-  };
-  int j = start;
-  for (; j + stride < m; j += 2 * stride) {
-    body(j, acc);
-    body(j + stride, acc2);
   }
-  if (j < m) body(j, acc);
-  acc = __fadd2_rn(acc, acc2);
+  return make_float2(w0, w1);
+}
+__device__ __forceinline__ void self_sum(const float4* buf, int m, int start, int stride,
+                                         const Quad& t, float2& acc0, float2& acc1) {
+  for (int j = start; j < m; j += stride) {
+    const float4 s = buf[j];
+    const float2 q = make_float2(s.w, s.w);
+    acc0 = __ffma2_rn(rsq2f<true>(inv_r2(t.X0, t.Y0, t.Z0, s)), q, acc0);
+    acc1 = __ffma2_rn(rsq2f<true>(inv_r2(t.X1, t.Y1, t.Z1, s)), q, acc1);
+  }
 }
 
 // Rounds of 32 staged columns (f chunks of R); group grp takes chunk
 // round * f + grp.  Chunk k occupies buf[2Rk, 2Rk + 2R) (the chunk twice).
+// Per step a lane meets one column with its four targets: one 16-byte
+// shared load and two shuffles feed four interactions.
 template <int R, bool GUARD>
 __device__ __forceinline__ void mutual_rounds(const float4* buf, const int32_t* dst, int m,
-                                              int grp, int ti, float2 X, float2 Y, float2 Z,
-                                              float2 QA, float2& phi, float* __restrict__ Pr,
-                                              bool rmw) {
+                                              int grp, int ti, const Quad& t, float2 QA0,
+                                              float2 QA1, float2& phi0, float2& phi1,
+                                              float* __restrict__ Pr, bool rmw) {
   for (int c0 = 0; c0 < m; c0 += 32) {
     const int k = c0 / R + grp;                    // R is a compile-time power of two
     const float4* p = buf + 2 * R * k + ti;
@@ -105,29 +114,20 @@ __device__ __forceinline__ void mutual_rounds(const float4* buf, const int32_t* 
     float* o = Pr + (col < m ? dst[col] : 0);
     const float old = (rmw && col < m) ? __ldcg(o) : 0.f;
     float2 psi = make_float2(0.f, 0.f);
-    float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int s = 0; s < R; ++s) {
       const float4 c = p[s];
-      const float2 dx = __fadd2_rn(X, make_float2(-c.x, -c.x));
-      const float2 dy = __fadd2_rn(Y, make_float2(-c.y, -c.y));
-      const float2 dz = __fadd2_rn(Z, make_float2(-c.z, -c.z));
-      const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-      float w0 = real_traits<float>::rsq(r2.x), w1 = real_traits<float>::rsq(r2.y);
-      if (GUARD) {
-        w0 = r2.x > 0.f ? w0 : 0.f;
-        w1 = r2.y > 0.f ? w1 : 0.f;
-      }
-      const float2 w = make_float2(w0, w1);
-      if (s & 1) acc2 = __ffma2_rn(w, make_float2(c.w, c.w), acc2);
-      else phi = __ffma2_rn(w, make_float2(c.w, c.w), phi);
-      psi = __ffma2_rn(w, QA, psi);
+      const float2 w0 = rsq2f<GUARD>(inv_r2(t.X0, t.Y0, t.Z0, c));
+      const float2 w1 = rsq2f<GUARD>(inv_r2(t.X1, t.Y1, t.Z1, c));
+      const float2 q = make_float2(c.w, c.w);
+      phi0 = __ffma2_rn(w0, q, phi0);
+      phi1 = __ffma2_rn(w1, q, phi1);
+      psi = __ffma2_rn(w1, QA1, __ffma2_rn(w0, QA0, psi));
       if (R > 1) {
         psi.x = __shfl_sync(kFull, psi.x, ti + 1, R);
         psi.y = __shfl_sync(kFull, psi.y, ti + 1, R);
       }
     }
-    phi = __fadd2_rn(phi, acc2);
     if (col < m) *o = old + (psi.x + psi.y);
   }
 }
@@ -189,12 +189,19 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
       float* Pr = P + r * pstride;
       for (int tb = 0; tb < tc; tb += 32) {
         const int n = min(32, tc - tb);
-        const int h = (n + 1) >> 1;
+        const int h = (n + 3) >> 2;                            // lanes per group: >= n / 4
         const int lr = h <= 1 ? 0 : 32 - __clz(h - 1);       // R = 2^lr
         const int R = 1 << lr;
         const int grp = lane >> lr, ti = lane & (R - 1), f = 32 >> lr;
-        const bool live0 = ti < n, live1 = ti + R < n;
-        const int64_t ia = t0 + tb + (live0 ? ti : 0), ib = t0 + tb + (live1 ? ti + R : 0);
+        // four targets per lane: ti, ti + R, ti + 2R, ti + 3R (dead ones
+        // repeat target 0 with charge 0)
+        bool live[4];
+        int64_t it[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          live[u] = ti + u * R < n;
+          it[u] = t0 + tb + (live[u] ? ti + u * R : 0);
+        }
         // stage one fill of columns [k kFC, ...) into buffer k & 1: each
         // column twice (2R-record chunks), padded to whole 32-column rounds
         auto stage = [&](int k) {
@@ -226,15 +233,21 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
         for (int k = lane; k < ms; k += 32) cp_async16(sm.self + k, srow + t0 + k, true);
         cp_async_commit();
         if (nfill) stage(0);
-        const float2 X = make_float2(tx[ia], tx[ib]), Y = make_float2(ty[ia], ty[ib]),
-                     Z = make_float2(tz[ia], tz[ib]);
-        const float2 QA = make_float2(live0 ? srow[ia].w : 0.f, live1 ? srow[ib].w : 0.f);
-        float2 phi = make_float2(0.f, 0.f);
+        Quad tq;
+        tq.X0 = make_float2(tx[it[0]], tx[it[1]]);
+        tq.Y0 = make_float2(ty[it[0]], ty[it[1]]);
+        tq.Z0 = make_float2(tz[it[0]], tz[it[1]]);
+        tq.X1 = make_float2(tx[it[2]], tx[it[3]]);
+        tq.Y1 = make_float2(ty[it[2]], ty[it[3]]);
+        tq.Z1 = make_float2(tz[it[2]], tz[it[3]]);
+        const float2 QA0 = make_float2(live[0] ? srow[it[0]].w : 0.f, live[1] ? srow[it[1]].w : 0.f);
+        const float2 QA1 = make_float2(live[2] ? srow[it[2]].w : 0.f, live[3] ? srow[it[3]].w : 0.f);
+        float2 phi0 = make_float2(0.f, 0.f), phi1 = make_float2(0.f, 0.f);
         // ---- own block (direct, guarded)
         if (nfill) cp_async_wait<1>();
         else cp_async_wait<0>();
         __syncwarp();
-        self_sum(sm.self, ms, grp, f, X, Y, Z, phi);
+        self_sum(sm.self, ms, grp, f, tq, phi0, phi1);
         for (int j0 = kSelf; j0 < tc; j0 += kSelf) {           // large leaves: more pieces
           const int m = min(kSelf, tc - j0);
           __syncwarp();
@@ -242,7 +255,7 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
           cp_async_commit();
           cp_async_wait<0>();                                  // (also completes fill 0)
           __syncwarp();
-          self_sum(sm.self, m, grp, f, X, Y, Z, phi);
+          self_sum(sm.self, m, grp, f, tq, phi0, phi1);
         }
         // ---- upper blocks: double-buffered fills
         const bool rmw = tb > 0;
@@ -258,23 +271,23 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
           const int32_t* db = sm.dst[k & 1];
           const int m = min(kFC, ncols - k * kFC);
           switch (lr) {
-            case 0: mutual_rounds<1, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
-            case 1: mutual_rounds<2, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
-            case 2: mutual_rounds<4, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
-            case 3: mutual_rounds<8, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
-            default: mutual_rounds<16, GUARD>(cb, db, m, grp, ti, X, Y, Z, QA, phi, Pr, rmw); break;
+            case 0: mutual_rounds<1, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
+            case 1: mutual_rounds<2, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
+            case 2: mutual_rounds<4, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
+            default: mutual_rounds<8, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
           }
           __syncwarp();
         }
         // ---- row sums of the pass: combine the f groups, slot 0
-        float pa = phi.x, pb = phi.y;
+        float ph[4] = {phi0.x, phi0.y, phi1.x, phi1.y};
         for (int off = R; off < 32; off <<= 1) {
-          pa += __shfl_xor_sync(kFull, pa, off);
-          pb += __shfl_xor_sync(kFull, pb, off);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ph[u] += __shfl_xor_sync(kFull, ph[u], off);
         }
         if (grp == 0) {
-          if (live0) Pr[own_base + tb + ti] = pa;
-          if (live1) Pr[own_base + tb + ti + R] = pb;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (live[u]) Pr[own_base + tb + ti + u * R] = ph[u];
         }
         __syncwarp();
       }
@@ -282,95 +295,38 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
   }
 }
 
-// Final pass: L2P (downward equivalent surface -> targets) + the near-field
-// slots of each target in slot order, un-permuted to caller order.
-constexpr int kLW = 8;
-__global__ void __launch_bounds__(32 * kLW) l2p_mutual_kernel(
-    const float* __restrict__ tx, const float* __restrict__ ty, const float* __restrict__ tz,
+// Near-field totals: out[perm[i]] = (1/4pi) sum_s P[slot s of i], slots in
+// order, for every target of leaf b (one warp per leaf, a lane per target);
+// runs right after the mutual pass, concurrently with the far field, and the
+// final L2P pass accumulates onto it (kifmm_leaf_pass_f32, parts = 1 | 4).
+constexpr int kRW = 8;
+__global__ void __launch_bounds__(32 * kRW, 4) mutual_reduce_kernel(
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
-    const double* __restrict__ centers, const double* __restrict__ ebase, int ne,
-    const float* __restrict__ local, int64_t nrhs, const int64_t* __restrict__ perm,
-    const int32_t* __restrict__ base, const int32_t* __restrict__ nlow, int64_t pstride,
-    const float* __restrict__ P, float* __restrict__ out) {
-  extern __shared__ __align__(16) float4 l2pm_buf[];
+    int64_t nrhs, const int64_t* __restrict__ perm, const int32_t* __restrict__ base,
+    const int32_t* __restrict__ nlow, int64_t pstride, const float* __restrict__ P,
+    float* __restrict__ out) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float4* buf = l2pm_buf + w * ne;
-  const int64_t b = (int64_t)blockIdx.x * kLW + w;
+  const int64_t b = (int64_t)blockIdx.x * kRW + w;
   if (b >= n_tleaves) return;
   const int64_t t0 = tstart[b];
   const int tc = tcount[b];
   const int slots = 1 + nlow[b];
   const int32_t pb0 = base[b];
-  const double cx = centers[b * 3], cy = centers[b * 3 + 1], cz = centers[b * 3 + 2];
-  for (int tb = 0; tb < tc; tb += 32) {
-    const int n = min(32, tc - tb);
-    const int h = (n + 1) >> 1;
-    const int R = h <= 1 ? 1 : 1 << (32 - __clz(h - 1));
-    const int f = 32 / R, sub = lane / R;
-    const int ti = lane % R;
-    const bool live0 = ti < n, live1 = ti + R < n;
-    const int64_t ia = t0 + tb + (live0 ? ti : 0), ib = t0 + tb + (live1 ? ti + R : 0);
-    const float2 X = make_float2(tx[ia], tx[ib]), Y = make_float2(ty[ia], ty[ib]),
-                 Z = make_float2(tz[ia], tz[ib]);
-    const int64_t oa = perm ? perm[ia] : ia, ob = perm ? perm[ib] : ib;
+  const float c = real_traits<float>::inv4pi();
+  for (int t = lane; t < tc; t += 32) {
+    const int64_t o = perm ? perm[t0 + t] : t0 + t;
     for (int64_t r = 0; r < nrhs; ++r) {
-      const float* loc = local + (b * nrhs + r) * ne;
-      // near field: the target's slots, spread over the f lane groups (group
-      // g adds slots g, g + f, ...; the groups are combined below with the
-      // far field); loads issued before the interaction loop
-      float na = 0.f, nb = 0.f;
-      {
-        const float* Pr = P + r * pstride + pb0 + tb + ti;
-        for (int s = sub; s < slots; s += f) {
-          if (live0) na += __ldg(Pr + (int64_t)s * tc);
-          if (live1) nb += __ldg(Pr + (int64_t)s * tc + R);
-        }
+      const float* Pr = P + r * pstride + pb0 + t;
+      float acc = 0.f;
+      // slots in order, eight loads in flight at a time
+      for (int s0 = 0; s0 < slots; s0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = s0 + u < slots ? __ldg(Pr + (s0 + u) * tc) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
       }
-      __syncwarp();
-      for (int k = lane; k < ne; k += 32)
-        buf[k] = make_float4(real_traits<float>::from_d(exact_add(cx, ebase[k * 3])),
-                             real_traits<float>::from_d(exact_add(cy, ebase[k * 3 + 1])),
-                             real_traits<float>::from_d(exact_add(cz, ebase[k * 3 + 2])), loc[k]);
-      __syncwarp();
-      float2 acc = make_float2(0.f, 0.f), acc2 = make_float2(0.f, 0.f);
-      int k = sub;
-      for (; k + f < ne; k += 2 * f) {
-        const float4 s = buf[k], s2 = buf[k + f];
-        float2 dx = __fadd2_rn(X, make_float2(-s.x, -s.x));
-        float2 dy = __fadd2_rn(Y, make_float2(-s.y, -s.y));
-        float2 dz = __fadd2_rn(Z, make_float2(-s.z, -s.z));
-        float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-        acc = __ffma2_rn(make_float2(real_traits<float>::rsq(r2.x), real_traits<float>::rsq(r2.y)),
-                         make_float2(s.w, s.w), acc);
-        dx = __fadd2_rn(X, make_float2(-s2.x, -s2.x));
-        dy = __fadd2_rn(Y, make_float2(-s2.y, -s2.y));
-        dz = __fadd2_rn(Z, make_float2(-s2.z, -s2.z));
-        r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-        acc2 = __ffma2_rn(make_float2(real_traits<float>::rsq(r2.x), real_traits<float>::rsq(r2.y)),
-                          make_float2(s2.w, s2.w), acc2);
-      }
-      if (k < ne) {
-        const float4 s = buf[k];
-        const float2 dx = __fadd2_rn(X, make_float2(-s.x, -s.x));
-        const float2 dy = __fadd2_rn(Y, make_float2(-s.y, -s.y));
-        const float2 dz = __fadd2_rn(Z, make_float2(-s.z, -s.z));
-        const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-        acc = __ffma2_rn(make_float2(real_traits<float>::rsq(r2.x), real_traits<float>::rsq(r2.y)),
-                         make_float2(s.w, s.w), acc);
-      }
-      acc = __fadd2_rn(acc, acc2);
-      float fa = acc.x, fb = acc.y;
-      for (int off = R; off < 32; off <<= 1) {
-        fa += __shfl_xor_sync(kFull, fa, off);
-        fb += __shfl_xor_sync(kFull, fb, off);
-        na += __shfl_xor_sync(kFull, na, off);
-        nb += __shfl_xor_sync(kFull, nb, off);
-      }
-      const float c = real_traits<float>::inv4pi();
-      if (sub == 0) {
-        if (live0) out[oa * nrhs + r] = fa * c + na * c;
-        if (live1) out[ob * nrhs + r] = fb * c + nb * c;
-      }
+      out[o * nrhs + r] = acc * c;
     }
   }
 }
@@ -401,19 +357,14 @@ int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, int6
   return launch_status();
 }
 
-// out[perm[i]] = L2P(i) + sum of i's near-field slots (slot order).
-int kifmm_l2p_mutual_f32(const float* tx, const float* ty, const float* tz, const int32_t* ts,
-                         const int32_t* tc, int64_t ntl, const double* centers,
-                         const double* ebase, int64_t ne, const float* local, int64_t nrhs,
-                         const int64_t* perm, const int32_t* base, const int32_t* nlow,
-                         int64_t pstride, const float* P, float* out, void* stream) {
-  if (ntl < 0 || ne < 1 || ne > 1024 || nrhs < 1) return KIFMM_EARG;
+// out[perm[i]] = (1/4pi) sum of i's near-field slots (slot order).
+int kifmm_p2p_mutual_reduce_f32(const int32_t* ts, const int32_t* tc, int64_t ntl, int64_t nrhs,
+                                const int64_t* perm, const int32_t* base, const int32_t* nlow,
+                                int64_t pstride, const float* P, float* out, void* stream) {
+  if (ntl < 0 || nrhs < 1) return KIFMM_EARG;
   if (ntl == 0) return 0;
-  const size_t smem = (size_t)kLW * ne * sizeof(float4);
-  set_max_smem((const void*)l2p_mutual_kernel, smem);
-  l2p_mutual_kernel<<<ceil_div(ntl, kLW), 32 * kLW, smem, (cudaStream_t)stream>>>(
-      tx, ty, tz, ts, tc, ntl, centers, ebase, (int)ne, local, nrhs, perm, base, nlow, pstride, P,
-      out);
+  mutual_reduce_kernel<<<ceil_div(ntl, kRW), 32 * kRW, 0, (cudaStream_t)stream>>>(
+      ts, tc, ntl, nrhs, perm, base, nlow, pstride, P, out);
   return launch_status();
 }
 

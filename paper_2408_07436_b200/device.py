@@ -144,9 +144,9 @@ class Linalg:
 
     # widest operator (elements) the fused chain kernel handles well; wider
     # chains (p >= 6 in float64) run as tiled GEMM stages instead
-    CHAIN_MAX_N = int(os.environ.get("KIFMM_CHAIN_MAX_N", "256"))
+    CHAIN_MAX_N = 256
     # row count from which the stages run as separate (throughput) GEMMs
-    CHAIN_GEMM_ROWS = int(os.environ.get("KIFMM_CHAIN_GEMM_ROWS", "16384"))
+    CHAIN_GEMM_ROWS = 16384
 
     def chain(self, M, A, lda, stages, C, ldc, rowmap=None, accumulate=False, asum=1,
               astride=0, a_child=None, child_w=0, a_nrhs=1):
@@ -384,12 +384,11 @@ class BlasDevice:
         self.k = k = ops.k
         self.n_e, self.n_c = ops.s.shape[0], ops.u.shape[0]
         if tensor_cores is None:
-            tensor_cores = os.environ.get("KIFMM_SWEEP", "tc") != "simt"
+            tensor_cores = True
         # float32: tcgen05 3xTF32 sweep (csrc/m2l_tc.cu); float64: FP64 SIMT sweep.
         # (3 TMEM accumulators of n_out <= 160 columns fit the 512-column TMEM;
         # above 256 columns the kernels run one CTA per SM)
         self.tc = bool(tensor_cores) and dt == np.float32 and -(-k // 16) * 16 <= 160
-        self.split_smem = os.environ.get("KIFMM_TMA_SPLIT", "host") == "smem"
         if self.tc:
             self.kin = -(-k // 8) * 8
             self.ko_pad = -(-k // 16) * 16
@@ -507,11 +506,9 @@ class BlasDevice:
         la = self.la
         la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
         hi, lo = dense
-        # KIFMM_TMA_SPLIT=smem: the dense array holds raw fp32 q~ and the sweep
-        # forms the TF32 hi/lo pair in shared memory (half the TMA bytes for A;
-        # measured slower on B200: the sweep is bound by shared-memory traffic,
-        # which the in-place split adds to)
-        lo = None if self.split_smem else lo
+        # TF32 hi/lo planes split here (splitting raw fp32 q~ in the sweep's
+        # shared memory halves the TMA bytes for A but measured slower on
+        # B200: the sweep is bound by shared-memory traffic)
         launch("kifmm_dense_split_tf32", P(qt), P(plan["src_slot"]), n_s, nrhs, self.kin,
                plan["h"], P(hi), P(lo), stream_handle())
         launch("kifmm_m2l_sweep_tma_f32", P(hi), P(lo), P(self.Bhi), P(self.Blo), self.kin,
@@ -669,7 +666,7 @@ class DeviceFmm:
                                self.np_dtype)
         self.blas_plan_dev = {l: upload_blas_plan(p) for l, p in plans.items()}
         # float32 engine path: TMA-fed sweep on dense sub-lattice arrays
-        self.tma = self.blas.tc and os.environ.get("KIFMM_SWEEP", "tma") == "tma"
+        self.tma = self.blas.tc
         if self.tma:
             st, tt = self.inst.source_tree, self.inst.target_tree
             self.tma_plan = {l: tma_level_plan(st.level_keys(l), tt.level_keys(l), l)
@@ -858,10 +855,10 @@ class DeviceFmm:
         # it runs on a low-priority side stream concurrently with the
         # far-field pipeline (mostly latency-bound small-level kernels), and
         # the L2P pass adds the far field at the end.  It is forked after the
-        # upward pass (KIFMM_P2P_AFTER=m2m; "pack"/"p2m" fork it earlier):
-        # forked at once its CTAs fill the machine and the P2M/M2M chain on
-        # the critical path waits for free slots (config 2: 0.904 -> 0.892 ms).  Eager timing/profiling
-        # passes keep the fused sequential leaf pass.
+        # upward pass: forked at once (after the pack or P2M), its CTAs fill
+        # the machine and the P2M/M2M chain on the critical path waits for
+        # free slots (config 2: 0.904 vs 0.892 ms).  Eager timing/profiling
+        # passes run the near field in sequence.
         out = b["out"]
         nt = self.tx.shape[0]
         if gradient and "grad" not in b:
@@ -882,26 +879,21 @@ class DeviceFmm:
 
         def p2p_pass(stream):
             if mut is not None:
-                # mutual near field into the partial-sum slots
+                # mutual near field into the partial-sum slots, then their
+                # per-target totals into out (caller order)
                 launch("kifmm_p2p_mutual_f32", P(self.tx), P(self.ty), P(self.tz),
                        self.n_tgt[d], P(b["src4"]), self.sx.shape[0], P(self.near_off),
                        P(mut["pack"]), P(mut["order"]), R, mut["total"], int(self.p2p_guard),
-                       P(b["pmut"]),
-                       stream)
+                       P(b["pmut"]), stream)
+                launch("kifmm_p2p_mutual_reduce_f32", P(self.t_start), P(self.t_count),
+                       self.n_tgt[d], R, P(self.t_perm), P(mut["base"]), P(mut["nlow"]),
+                       mut["total"], P(b["pmut"]), P(out), stream)
             else:
                 launch(leaf_name, *leaf_args(2), stream)             # P2P, overwrite
 
         def l2p_final(stream):
-            if mut is not None:
-                # L2P + the near-field slots, un-permuted
-                launch("kifmm_l2p_mutual_f32", P(self.tx), P(self.ty), P(self.tz),
-                       P(self.t_start), P(self.t_count), self.n_tgt[d], P(self.t_centers),
-                       P(self.equiv_base), n_e, P(b["loc"][d]), R, P(self.t_perm),
-                       P(mut["base"]), P(mut["nlow"]), mut["total"], P(b["pmut"]), P(out), stream)
-            else:
-                launch(leaf_name, *leaf_args(1 | 4), stream)         # L2P, accumulate
+            launch(leaf_name, *leaf_args(1 | 4), stream)             # L2P, accumulate
 
-        p2p_after = os.environ.get("KIFMM_P2P_AFTER", "m2m")
         side = self.side_stream
 
         def fork_p2p():
@@ -911,8 +903,6 @@ class DeviceFmm:
                 p2p_pass(side.cuda_stream)
                 mark("p2p")
 
-        if overlap and p2p_after == "pack":
-            fork_p2p()
         # P2M: check potentials, then the up_inv solve scaled by the leaf side.
         mult, phi, tmp = b["mult"], b["phi"], b["tmp"]
         nl = self.n_src[d]
@@ -921,8 +911,6 @@ class DeviceFmm:
                  n_c, P(phi), s)
         la.chain(nl * R, phi, n_c, Linalg.solve_stages(self.up_inv, self.side[d]), mult[d], n_e)
         mark("p2m")
-        if overlap and p2p_after == "p2m":
-            fork_p2p()
         loc = b["loc"]
         calls = {}
         # Each level's M2L leaves its check potentials (x 1/side) in
@@ -971,11 +959,10 @@ class DeviceFmm:
                 mark("m2l")
             forked[lvl] = st
 
-        # KIFMM_FINE_M2L_AT: fork the finest level's M2L right after P2M
-        # ("p2m") or after the M2M pass ("m2m": the persistent sweep then
-        # cannot hold the SMs the latency-bound M2M chain needs)
-        fine_at = os.environ.get("KIFMM_FINE_M2L_AT", "p2m")
-        if overlap and d >= 3 and fine_at == "p2m":
+        # the finest level's M2L is forked right after P2M (forking it after
+        # the M2M pass, so the persistent sweep cannot hold the SMs the
+        # latency-bound M2M chain needs, measured within +-1%)
+        if overlap and d >= 3:
             fork_m2l(d)
         phase("m2m")
         mark("m2m")
@@ -990,9 +977,7 @@ class DeviceFmm:
             if overlap and lvl - 1 >= 3:
                 fork_m2l(lvl - 1)
         mark("m2m")
-        if overlap and d >= 3 and fine_at == "m2m":
-            fork_m2l(d)
-        if overlap and p2p_after == "m2m":
+        if overlap:
             fork_p2p()
         for lvl in range(2, d + 1):
             n_t = self.n_tgt[lvl]

@@ -58,5 +58,9 @@ def test_full_size_parity_record(case):
     a, b = r["ours_vs_direct_4096"], r["reference_vs_direct_4096"]
     assert abs(a["mean"] - b["mean"]) <= tol, (a, b)
     assert abs(a["normwise"] - b["normwise"]) <= tol, (a, b)
-    # the record was produced on one host for both sides, with the GPU
+    # the reference against itself (single-threaded vs threaded OpenBLAS):
+    # for signed charges it, too, misses the strict per-target bound
+    ri = r["reference_vs_itself"]
+    assert ri["normwise"] <= tol and ri["floored_max"] <= tol, ri
+        # the record was produced on one host for both sides, with the GPU
     assert r["host"]["gpu"] and "B200" in r["host"]["gpu"]

@@ -94,7 +94,7 @@ def run_case(name):
     pts, q = make()
     rec = dict(case=name, n_points=int(pts.shape[0]), config=kw,
                seeds={"points": 7, "charges": 11}, host=dict(
-                   cpu_count=os.cpu_count(), cpu=platform.processor() or _cpu_model(),
+                   cpu_count=os.cpu_count(), cpu=_cpu_model() or platform.processor(),
                    gpu=torch.cuda.get_device_name(0) if torch.cuda.is_available() else None))
     # ---- ours (GPU)
     t0 = time.perf_counter()
@@ -121,6 +121,19 @@ def run_case(name):
     rec["reference_timings"] = {k: float(v) for k, v in ref.timings.items()}
     rec["reference_relative_error"] = list(ref.relative_error(want))
     rec["reference_vs_direct_4096"] = err_stats(np.asarray(want, np.float64)[idx], direct)
+    # the reference against itself: single-threaded OpenBLAS changes only
+    # BLAS rounding (bounds how closely any implementation can match it)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1, user_api="blas"):
+        want1 = np.asarray(ref.evaluate(q), np.float64)
+    w0 = np.asarray(want, np.float64)
+    d1 = np.abs(want1 - w0)
+    sc = np.abs(w0).max()
+    rec["reference_vs_itself"] = dict(
+        max_rel=float((d1 / np.abs(w0)).max()), normwise=float(d1.max() / sc),
+        floored_max=float((d1 / np.maximum(np.abs(w0), 1e-3 * sc)).max()),
+        strict_failures=int((d1 / np.abs(w0) > TOL[kw["precision"]]).sum()),
+        note="the reference evaluated again with single-threaded OpenBLAS")
     # ---- per-target comparison
     g = np.asarray(got, np.float64)
     w = np.asarray(want, np.float64)
