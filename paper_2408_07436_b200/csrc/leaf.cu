@@ -732,5 +732,4 @@ int kifmm_pack_sources_f64(const double* sx, const double* sy, const double* sz,
                            int64_t ns, int64_t nrhs, double* out, void* s) {
   return pack_sources<double>(sx, sy, sz, q, ns, nrhs, out, s);
 }
-
 }  // extern "C"

@@ -46,23 +46,8 @@ using namespace kifmm;
 namespace {
 
 constexpr int TMT = 128;
-#ifndef KIFMM_TMEM_MMA3
-#define KIFMM_TMEM_MMA3 0
-#endif
-// 1: per k-step three MMAs of N = KP into a KP-column accumulator,
-//    D += A_hi.B_hi + A_lo.B_hi + A_hi.B_lo (168 TMEM columns per group at
-//    KP = 56: three groups fit the 512 columns);
-// 0: two MMAs, A_hi.[B_hi | B_lo] (N = 2 KP) + A_lo.B_hi, into 2 KP columns
-constexpr bool MMA3 = KIFMM_TMEM_MMA3 != 0;
-#ifndef KIFMM_TMEM_NG
-#define KIFMM_TMEM_NG 2
-#endif
-// groups per CTA (interleaved vectors), each with its own TMEM A and D: the
-// requested count where their columns fit the 512-column TMEM, else 2
-template <int KP>
-constexpr int groups_for() {
-  return KIFMM_TMEM_NG * ((MMA3 ? KP : 2 * KP) + 2 * KP) <= 512 ? KIFMM_TMEM_NG : 2;
-}
+constexpr int NG = 2;             // groups per CTA (alternate vectors), each with its own TMEM A and D
+constexpr int NTHREADS = 32 + 128 * NG;
 #ifndef KIFMM_TMEM_STW
 #define KIFMM_TMEM_STW 8           // widest tcgen05.st piece (8 / 16 / 32 columns)
 #endif
@@ -71,13 +56,6 @@ constexpr int groups_for() {
 #endif
 constexpr int FLUSH_V = KIFMM_TMEM_FLUSH;   // vectors between promotions of a TMEM accumulator
 constexpr int BX = 4, BY = 4, BZ = 8;
-#ifndef KIFMM_TMEM_TAIL_LINEAR
-#define KIFMM_TMEM_TAIL_LINEAR 0
-#endif
-// 1: columns 32..KP of the source block in ONE linear box (2-way bank
-// conflicts on the loader reads); 0: 16- and 8-column boxes with the 64- and
-// 32-byte swizzles (conflict-free, one more TMA per stage)
-constexpr bool TAIL_LINEAR = KIFMM_TMEM_TAIL_LINEAR != 0;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -267,28 +245,21 @@ __device__ __forceinline__ TileGeom tile_geom(const TmemArgs& a, int slot) {
   return t;
 }
 
-template <int KP, int NG = groups_for<KP>(), int NTHREADS = 32 + 128 * NG>
+template <int KP>
 #ifdef KIFMM_TMEM_MAXNREG
 __global__ void __maxnreg__(KIFMM_TMEM_MAXNREG) m2l_sweep_tmem_kernel(
 #else
 __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
 #endif
     const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm2,
-    const __grid_constant__ CUtensorMap tm3, const TmemArgs a) {
-  constexpr int N1 = MMA3 ? KP : 2 * KP;
-  constexpr int N2 = MMA3 ? KP : (KP + 15) / 16 * 16;
+    const TmemArgs a) {
+  constexpr int N1 = 2 * KP;
+  constexpr int N2 = (KP + 15) / 16 * 16;
   // source block: columns [0, 32) in a 128-byte-swizzled box, the rest
   // (KP - 32 columns) in a second box, swizzled when it is 32 wide and
   // linear (rows of (KP - 32) * 4 bytes, exact width) otherwise
   constexpr int W1 = KP > 32 ? KP - 32 : 0;
   constexpr bool SW1 = W1 == 32;
-  // narrower remainders: a 16-column box with the 64-byte swizzle and/or an
-  // 8-column box with the 32-byte swizzle, so every loader read of the block
-  // is bank-conflict-free (a linear 24-column box costs 2-way conflicts)
-  constexpr int W16 = (!SW1 && !TAIL_LINEAR && W1 >= 16) ? 16 : 0;
-  constexpr int W8 = (!SW1 && !TAIL_LINEAR && W1 % 16 == 8) ? 8 : 0;
-  static_assert(SW1 || TAIL_LINEAR || W1 == W16 + W8, "remainder boxes");
-  constexpr uint32_t OFF8 = TMT * 128u + TMT * W16 * 4u;               // 8-column box
   constexpr uint32_t ABYTES = TMT * 128u + TMT * W1 * 4u;              // one source block
   constexpr uint32_t BBYTES = 2u * KP * KP * 4u;                       // one core pair
   constexpr uint32_t SBYTES = (ABYTES + BBYTES + 1023u) / 1024u * 1024u;
@@ -299,7 +270,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
                                  : NEED <= 256 ? 256 : 512;
   static_assert(NEED <= 512, "TMEM budget");
   static_assert(KP % 8 == 0 && N1 <= 256, "shape");
-  static_assert(NG >= 2 && NG <= 3, "groups");
 
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -320,8 +290,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
     for (int k = 0; k < NG; ++k) mbar_init(&done[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
-    if (SW1 || W16 || (TAIL_LINEAR && W1)) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2)) : "memory");
-    if (W8) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm3)) : "memory");
+    if (W1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2)) : "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -357,8 +326,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           const int sp = ((qx & 1) << 2) | ((qy & 1) << 1) | (qz & 1);
           const int cz = tg.iz0 + (qz >> 1), cy = tg.iy0 + (qy >> 1), cx = tg.ix0 + (qx >> 1);
           tma_load_5d(sb, &tm, 0, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
-          if (SW1 || W16 || (TAIL_LINEAR && W1)) tma_load_5d(sb + TMT * 128, &tm2, 32, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
-          if (W8) tma_load_5d(sb + OFF8, &tm3, 32 + W16, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
+          if (W1) tma_load_5d(sb + TMT * 128, &tm2, 32, cz, cy, cx, sp * a.nrhs + x.r, &full[s]);
           bulk_copy(sb + ABYTES, a.bpair + (int64_t)t * (2 * KP * KP), BBYTES, &full[s]);
         }
       }
@@ -418,21 +386,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           for (int i = 8; i < KP / 4; ++i)
             split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * 128 +
                                                        (((i & 7) ^ (m & 7)) << 4)));
-        } else if (TAIL_LINEAR) {
+        } else {
+          // linear second box: rows W1 * 4 bytes apart (measured faster than
+          // a conflict-free split into 16- and 8-column boxes with the 64- and
+          // 32-byte swizzles: 259 vs 265 us, one TMA fewer per stage; and
+          // than swapped chunk pairs: 284 vs 303 us)
 #pragma unroll
           for (int i = 8; i < KP / 4; ++i)
             split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * (W1 * 4) + (i - 8) * 16));
-        } else {
-          // 64-byte swizzle: 16-byte chunk c of row m at m * 64 + (c ^ (m >> 1 & 3)) * 16
-#pragma unroll
-          for (int i = 8; i < 8 + W16 / 4; ++i)
-            split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * 64 +
-                                                       (((i - 8) ^ ((m >> 1) & 3)) << 4)));
-          // 32-byte swizzle: chunk c of row m at m * 32 + (c ^ (m >> 2 & 1)) * 16
-#pragma unroll
-          for (int i = 8 + W16 / 4; i < KP / 4; ++i)
-            split4(i, *reinterpret_cast<const float4*>(sb + OFF8 + m * 32 +
-                                                       (((i - 8 - W16 / 4) ^ ((m >> 2) & 1)) << 4)));
         }
         // this group's previous MMAs done: A_k reusable (and D_k promoted below)
         if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);
@@ -459,11 +420,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
             const uint64_t db = desc_nosw(bb + ks * 256, 128, SBO);
             mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, local | ks);
             mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
-            if (MMA3) {
-              // A_hi . B_lo: B_lo follows B_hi (KP / 8 groups of 8 rows)
-              const uint64_t dl = desc_nosw(bb + KP * KP * 4 + ks * 256, 128, SBO);
-              mma_tf32_ts(dcol, acol + ks * 8, dl, idesc1, 1);
-            }
           }
           mma_commit(&done[grp]);
           mma_commit(&empty[s]);
@@ -481,12 +437,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           for (int c = 0; c < KP / 8; ++c) {
             uint32_t u[8], w[8];
             tmem_ld8(dcol + lane_base + c * 8, u);
-            if (!MMA3) tmem_ld8(dcol + lane_base + KP + c * 8, w);
+            tmem_ld8(dcol + lane_base + KP + c * 8, w);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              acc[c * 8 + i] += MMA3 ? __uint_as_float(u[i])
-                                     : __uint_as_float(u[i]) + __uint_as_float(w[i]);
+              acc[c * 8 + i] += __uint_as_float(u[i]) + __uint_as_float(w[i]);
           }
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         }
@@ -579,19 +534,14 @@ template <int KP>
 int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   TmemArgs a = a0;
   constexpr int W1 = KP > 32 ? KP - 32 : 0;
-  constexpr int W16 = (W1 != 32 && !TAIL_LINEAR && W1 >= 16) ? 16 : 0;
-  constexpr int W8 = (W1 != 32 && !TAIL_LINEAR && W1 % 16 == 8) ? 8 : 0;
-  CUtensorMap tm, tm2, tm3;
+  CUtensorMap tm, tm2;
   memset(&tm, 0, sizeof(tm));
   memset(&tm2, 0, sizeof(tm2));
-  memset(&tm3, 0, sizeof(tm3));
   const int64_t planes = 8 * (int64_t)a.nrhs;
   int st = make_map(&tm, a.q, KP, a.h, planes, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!st && W1 == 32) st = make_map(&tm2, a.q, KP, a.h, planes, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!st && TAIL_LINEAR && W1 && W1 != 32)
+  if (!st && W1 && W1 != 32)
     st = make_map(&tm2, a.q, KP, a.h, planes, W1, CU_TENSOR_MAP_SWIZZLE_NONE);
-  if (!st && W16) st = make_map(&tm2, a.q, KP, a.h, planes, 16, CU_TENSOR_MAP_SWIZZLE_64B);
-  if (!st && W8) st = make_map(&tm3, a.q, KP, a.h, planes, 8, CU_TENSOR_MAP_SWIZZLE_32B);
   if (st) return st;
   constexpr int ns_env = 4;             // config 2 on B200: 4 ~ 3 stages (281-288 us), 2: 362 us
   const size_t sbytes = ((size_t)TMT * 128 + (size_t)TMT * W1 * 4 + 2ull * KP * KP * 4 + 1023) /
@@ -599,14 +549,13 @@ int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   int ns = ns_env;
   while (ns > 2 && 1024 + ns * sbytes + 256 + 4096 > 227 * 1024) --ns;
   a.ns = ns;
-  constexpr int NG = groups_for<KP>();
   const size_t smem = 1024 + ns * sbytes + (2 * ns + NG) * 8 + 16 + 4096;
   // persistent CTAs: one per SM (capping the grid to leave SMs to the
   // other streams' kernels measured within +-1%)
   const int g_max = sm_count();
   const int grid = a.n_items < g_max ? a.n_items : g_max;
   set_max_smem((const void*)m2l_sweep_tmem_kernel<KP>, smem);
-  m2l_sweep_tmem_kernel<KP><<<grid, 32 + 128 * NG, smem, stream>>>(tm, tm2, tm3, a);
+  m2l_sweep_tmem_kernel<KP><<<grid, NTHREADS, smem, stream>>>(tm, tm2, a);
   return launch_status();
 }
 

@@ -907,8 +907,8 @@ class DeviceFmm:
         mult, phi, tmp = b["mult"], b["phi"], b["tmp"]
         nl = self.n_src[d]
         launch(f"kifmm_p2m_check_{sfx}", P(self.sx), P(self.sy), P(self.sz), P(q), R,
-                 P(self.s_start), P(self.s_count), nl, P(self.s_centers), P(self.check_base),
-                 n_c, P(phi), s)
+               P(self.s_start), P(self.s_count), nl, P(self.s_centers), P(self.check_base),
+               n_c, P(phi), s)
         la.chain(nl * R, phi, n_c, Linalg.solve_stages(self.up_inv, self.side[d]), mult[d], n_e)
         mark("p2m")
         loc = b["loc"]
@@ -1114,6 +1114,39 @@ class DeviceFmm:
             return t
         return read
 
+    # pageable host input: chunks copied into a pinned staging buffer by a
+    # few host threads (numpy releases the GIL for large copies), each chunk's
+    # H2D issued as soon as it is staged, so the copies overlap
+    STAGE_CHUNK = 1 << 18            # float64 elements (2 MB)
+    STAGE_THREADS = 4
+
+    def _stage_pageable(self, src, dst):
+        n = src.numel()
+        stage = getattr(self, "_stage_buf", None)
+        if stage is None or stage.numel() < n:
+            stage = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            self._stage_buf = stage
+            self._stage_np = stage.numpy()
+        if not hasattr(self, "_stage_pool"):
+            from concurrent.futures import ThreadPoolExecutor
+            self._stage_pool = ThreadPoolExecutor(self.STAGE_THREADS)
+        src_np = src.numpy()
+        # the previous call's H2D from the staging buffer must be done
+        ev = getattr(self, "_stage_done", None)
+        if ev is not None:
+            ev.synchronize()
+        step = self.STAGE_CHUNK
+        bounds = [(i, min(n, i + step)) for i in range(0, n, step)]
+
+        def copy(lo, hi):
+            np.copyto(self._stage_np[lo:hi], src_np[lo:hi])
+        futs = [self._stage_pool.submit(copy, lo, hi) for lo, hi in bounds]
+        for (lo, hi), f in zip(bounds, futs):
+            f.result()
+            dst[lo:hi].copy_(stage[lo:hi], non_blocking=True)
+        self._stage_done = torch.cuda.Event()
+        self._stage_done.record()
+
     def collect_timings(self):
         ev = getattr(self, "_events", None)
         if not ev:
@@ -1148,8 +1181,11 @@ class DeviceFmm:
                 return out[0].cpu().numpy().copy(), out[1].cpu().numpy().copy()
             return out.cpu().numpy().copy()
         g, static_q, out = self.graph_for(R, gradient)
-        # pinned host charges go over asynchronously, ordered before the replay
-        static_q.copy_(src, non_blocking=src.is_pinned())
+        if src.is_pinned():
+            # pinned host charges go over asynchronously, ordered before the replay
+            static_q.copy_(src, non_blocking=True)
+        else:
+            self._stage_pageable(src, static_q)
         g.replay()
         outs = out if gradient else (out,)
         # results land in fresh pinned buffers (the caller owns the arrays; the

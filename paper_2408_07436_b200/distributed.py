@@ -154,8 +154,10 @@ def make_rank_plans(inst, part: Partition):
             need, extra = _needed_sources(inst, lvl, lo, hi)
             if inst.config.backend == "blas":
                 tcodes = inst.target_tree.level_keys(lvl)
+                # tiles of the owned targets only: each rank sweeps its share
                 p.blas_plans[lvl] = level_plan_from_buckets(extra, tcodes.shape[0],
-                                                            child_index_codes(tcodes))
+                                                            child_index_codes(tcodes),
+                                                            owned=(lo, hi))
             else:
                 p.fft_clusters[lvl] = extra
             slo, shi = p.src_ranges[lvl]
@@ -238,6 +240,19 @@ class DistributedFmm:
                                                          inst.halo_plans[l].src_color,
                                                          inst.halo_plans[l].tgt_color[clo:chi]))
         del R
+
+    def _acc(self, lvl, nrhs):
+        """Sweep accumulator of this rank's plan at ``lvl`` (the rank tiles
+        only its own targets, so its vector split - and the accumulator
+        width - differ from the single-device plan's)."""
+        key = (lvl, nrhs)
+        if not hasattr(self, "_accs"):
+            self._accs = {}
+        if key not in self._accs:
+            d = self.dev
+            n = d.blas.acc_elems(d.n_tgt[lvl], nrhs, self.blas_plan_dev[lvl]["n_tiles"])
+            self._accs[key] = self.torch.zeros(max(n, 1), dtype=d.T, device=d.sx.device)
+        return self._accs[key]
 
     # -- exchange buffers: one flat buffer per peer holding all levels' rows
     def _pack_lists(self, kind):
@@ -348,7 +363,7 @@ class DistributedFmm:
                     bd = d.blas
                     plan = self.blas_plan_dev[lvl]
                     bd.run_level_rows(plan, mult[lvl], d.n_src[lvl], lo, hi, R, 1.0 / d.side[lvl],
-                                      check, b["qt_lv"][lvl], b["acc_lv"][lvl])
+                                      check, b["qt_lv"][lvl], self._acc(lvl, R))
                 else:
                     self._fft_level(lvl, mult[lvl], R, check)
                 d.la.solve(d.dn_inv, _View(check, lo * R * n_c, isz), (hi - lo) * R,

@@ -241,7 +241,9 @@ def infer_target_classes(buckets: TransferBuckets, n_targets: int) -> np.ndarray
 
 
 def level_plan_from_buckets(buckets: TransferBuckets, n_targets: int,
-                            target_classes=None) -> BlasLevelPlan:
+                            target_classes=None, owned=None) -> BlasLevelPlan:
+    """``owned`` (optional (lo, hi) target-row range): tile only those
+    targets (a rank of the partitioned evaluate sweeps its own tiles)."""
     if target_classes is None:
         target_classes = infer_target_classes(buckets, n_targets)
     table = class_transfer_table()                      # (8, 189)
@@ -251,8 +253,12 @@ def level_plan_from_buckets(buckets: TransferBuckets, n_targets: int,
     cls = np.asarray(target_classes, dtype=np.int64)
     order = []
     tile_class = []
+    keep = np.ones(cls.shape[0], dtype=bool)
+    if owned is not None:
+        keep[:] = False
+        keep[owned[0]:owned[1]] = True
     for c in range(8):
-        rows = np.flatnonzero(cls == c)
+        rows = np.flatnonzero((cls == c) & keep)
         n_t = (rows.shape[0] + TILE_TARGETS - 1) // TILE_TARGETS
         pad = np.full(n_t * TILE_TARGETS, -1, dtype=np.int64)
         pad[:rows.shape[0]] = rows
@@ -271,7 +277,10 @@ def level_plan_from_buckets(buckets: TransferBuckets, n_targets: int,
         j = pos_in_class[cls[rt], i]
         if np.any(j < 0):
             raise ValueError("bucket pair inadmissible for its target parity class")
-        src[slot_of_target[rt], j] = rs
+        sl = slot_of_target[rt]
+        if np.any(sl < 0):
+            raise ValueError("bucket pair targets a row outside the planned targets")
+        src[sl, j] = rs
         n_pairs += rs.shape[0]
     return BlasLevelPlan(buckets.level, n_targets, slots.astype(np.int32),
                          np.asarray(tile_class, dtype=np.int32), src, n_pairs)

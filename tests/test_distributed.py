@@ -77,6 +77,35 @@ def test_ghost_rows_cover_every_m2l_source(backend):
             assert need <= have, (p.rank, lvl, len(need - have))
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_rank_plans_tile_only_owned_targets(world):
+    """Each rank's BLAS-M2L plan tiles its own target rows only, so the
+    per-rank sweep work is its share of the level, and the plans
+    together hold every bucket pair of the level exactly once."""
+    from paper_2408_07436_b200.m2l_blas import level_plan_from_buckets
+    from paper_2408_07436_b200.octree import child_index_codes
+    inst = _instance("blas", n=20000, depth=4)
+    part = make_partition(inst.source_tree, inst.target_tree, world)
+    plans = make_rank_plans(inst, part)
+    for lvl in range(2, inst.config.depth + 1):
+        tcodes = inst.target_tree.level_keys(lvl)
+        full = level_plan_from_buckets(inst.buckets[lvl], tcodes.shape[0],
+                                       child_index_codes(tcodes))
+        tiles = 0
+        pairs = 0
+        for p in plans:
+            bp = p.blas_plans[lvl]
+            lo, hi = p.tgt_ranges[lvl]
+            t = bp.tile_targets[bp.tile_targets >= 0]
+            assert np.all((t >= lo) & (t < hi))
+            assert sorted(t.tolist()) == list(range(lo, hi))
+            tiles += bp.tile_class.shape[0]
+            pairs += bp.n_pairs
+        assert pairs == full.n_pairs
+        # ragged class tails per rank add at most 8 tiles per rank
+        assert tiles <= full.tile_class.shape[0] + 8 * world
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

@@ -442,9 +442,9 @@ def test_tmem_sweep_matches_tma_sweep_and_reference(cuda, monkeypatch, n, depth,
     <= 64) against the TMA-staged sweep on the same instance inputs, and
     against the reference; uniform and clustered (pruned boxes) clouds, 1 and
     2 right-hand sides; re-evaluation is bitwise deterministic.  The forced
-    ranks cover every source-block box split: k = 51 (KP 56: 32-column box
-    with the 128-byte swizzle + 16 (64-byte) + 8 (32-byte)), 36 (KP 40: + 8),
-    44 (KP 48: + 16), 60 (KP 64: two 128-byte boxes)."""
+    ranks cover every source-block box split: k = 51 (KP 56: a 32-column box
+    with the 128-byte swizzle + a linear 24-column box), 36 (KP 40: + 8),
+    44 (KP 48: + 16), 60 (KP 64: two 128-byte-swizzled boxes)."""
     from paper_2408_07436_b200 import FmmConfig, setup
     rng = np.random.default_rng(21)
     pts = rng.random((n, 3))

@@ -1,11 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 300 python tools/check_paths.py > gpurun_out/check_paths.log 2>&1; cat gpurun_out/check_paths.log
-C2="dict(depth=5, order_equiv=4, backend='blas', precision='f32', sigma_min=1e-6)"
-rm -f gpurun_out/variants.log
-for i in 1 2; do for v in default mma3 mma3ng3; do
-  if [ $v == default ]; then L=$PWD/paper_2408_07436_b200/libkifmm_b200.so; else L=$PWD/_variants/lib$v.so; fi
-  KIFMM_LIB=$L timeout 300 python tools/config_times.py 1000000 "$C2" > gpurun_out/var.log 2>&1
-  echo $v $(grep -h "evaluate\|p2p_mutual\|leaf_pass\|sweep m2l5" gpurun_out/var.log | head -6) >> gpurun_out/variants.log
-done; done
-cat gpurun_out/variants.log
-cat gpurun_out/var.log
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2_gputest7.log 2>&1; tail -3 gpurun_out/r2_gputest7.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/r2_bench7.json 2> gpurun_out/r2_bench7.err
+python -c "import json;d=json.loads(open('gpurun_out/r2_bench7.json').read().strip().splitlines()[-1]);print(d['value'],d['ms_per_step'],d['e2e'],d['roofline']['frac']);print(d['kernel_ms'])"
