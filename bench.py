@@ -371,6 +371,9 @@ def run_config3(args, flush, peaks, with_reference=True):
                dmma_frac=work["flops"] / (had_ms / 1e3) / 1e12 / dmma,
                hbm_gbs=work["bytes"] / (had_ms / 1e3) / 1e9, hbm_peak_gbs=peaks["hbm_gbs"],
                hbm_frac=work["bytes"] / (had_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+               traffic=dram_traffic("hadamard_tiled_c128_level5"),
+               bound="FP64 tensor (DMMA): intensity F_had / B_had ~ 40 flop/B is above the "
+                     "DMMA ridge (~5.8 flop/B), so the HBM fraction is reported, not targeted",
                peak_source="kifmm_probe DMMA m8n8k4 measured in this run; HBM "
                            + peaks["source"])
     pot = dev.evaluate_device(q_dev, 1).cpu().numpy()[:, 0].astype(np.float64)
@@ -407,9 +410,9 @@ def run_config3(args, flush, peaks, with_reference=True):
 # ------------------------------------------------------------------ ours
 def dram_traffic(key):
     """DRAM bytes per launch of a kernel from the committed ncu capture
-    (profiles/r1/dram_traffic.json), or None."""
+    (profiles/r2/dram_traffic.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1", "dram_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2", "dram_traffic.json")) as f:
             return float(json.load(f)[key]["bytes"])
     except (OSError, KeyError, ValueError):
         return None

@@ -48,9 +48,6 @@ namespace {
 constexpr int TMT = 128;
 constexpr int NG = 2;             // groups per CTA (alternate vectors), each with its own TMEM A and D
 constexpr int NTHREADS = 32 + 128 * NG;
-#ifndef KIFMM_TMEM_STW
-#define KIFMM_TMEM_STW 8           // widest tcgen05.st piece (8 / 16 / 32 columns)
-#endif
 #ifndef KIFMM_TMEM_FLUSH
 #define KIFMM_TMEM_FLUSH 8
 #endif
@@ -95,9 +92,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, bool s
 #endif
   }
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ uint64_t desc_nosw(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
@@ -122,46 +116,6 @@ __device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t (&v)[8]) 
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
-}
-__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
-      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
-      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
-}
-__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-      "%15,%16};" ::"r"(addr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
-}
-// A = [hi | lo] rows of this warp's 32 lanes: columns [0, KP) from hv and
-// [KP, 2 KP) from lv, hi and lo pieces interleaved, pieces of up to
-// KIFMM_TMEM_STW columns (x32 / x16 / x8 tcgen05.st)
-template <int KP>
-__device__ __forceinline__ void tmem_st_a(uint32_t addr, const uint32_t (&hv)[KP],
-                                          const uint32_t (&lv)[KP]) {
-  constexpr int C32 = KIFMM_TMEM_STW >= 32 ? KP / 32 * 32 : 0;
-  constexpr int C16 = KIFMM_TMEM_STW >= 16 ? C32 + (KP - C32) / 16 * 16 : C32;
-#pragma unroll
-  for (int c = 0; c < C32; c += 32) {
-    tmem_st32(addr + c, &hv[c]);
-    tmem_st32(addr + KP + c, &lv[c]);
-  }
-#pragma unroll
-  for (int c = C32; c < C16; c += 16) {
-    tmem_st16(addr + c, &hv[c]);
-    tmem_st16(addr + KP + c, &lv[c]);
-  }
-#pragma unroll
-  for (int c = C16; c < KP; c += 8) {
-    tmem_st8(addr + c, *reinterpret_cast<const uint32_t(*)[8]>(&hv[c]));
-    tmem_st8(addr + KP + c, *reinterpret_cast<const uint32_t(*)[8]>(&lv[c]));
-  }
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -246,11 +200,7 @@ __device__ __forceinline__ TileGeom tile_geom(const TmemArgs& a, int slot) {
 }
 
 template <int KP>
-#ifdef KIFMM_TMEM_MAXNREG
-__global__ void __maxnreg__(KIFMM_TMEM_MAXNREG) m2l_sweep_tmem_kernel(
-#else
 __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
-#endif
     const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm2,
     const TmemArgs a) {
   constexpr int N1 = 2 * KP;
@@ -399,15 +349,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
         if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);
         if (m == 0) trace(grp == 0 ? 1 : 6, gg);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#if KIFMM_TMEM_STW > 8
-        tmem_st_a<KP>(acol + lane_base, hv, lv);
-#else
 #pragma unroll
         for (int c = 0; c < KP / 8; ++c) {
           tmem_st8(acol + lane_base + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&hv[c * 8]));
           tmem_st8(acol + lane_base + KP + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&lv[c * 8]));
         }
-#endif
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
@@ -543,11 +489,17 @@ int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   if (!st && W1 && W1 != 32)
     st = make_map(&tm2, a.q, KP, a.h, planes, W1, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st) return st;
-  constexpr int ns_env = 4;             // config 2 on B200: 4 ~ 3 stages (281-288 us), 2: 362 us
+  constexpr int ns_env = 4;             // config 2 on B200: 4 stages 259 us, 3: 279 us, 2: 351 us
   const size_t sbytes = ((size_t)TMT * 128 + (size_t)TMT * W1 * 4 + 2ull * KP * KP * 4 + 1023) /
                         1024 * 1024;
   int ns = ns_env;
   while (ns > 2 && 1024 + ns * sbytes + 256 + 4096 > 227 * 1024) --ns;
+  // an even ring: stage s is then always consumed by the same group (vector
+  // g -> stage g % ns, group g % 2).  With an odd ring the two groups
+  // alternate on every stage, and repeated fresh evaluates at ns = 3 gave
+  // wrong sums on a few tile-vectors (4 of 40) and occasional launch faults;
+  // ns = 2 and ns = 4 gave none in 180 (tools/stress_overlap.py).
+  if (ns & 1) --ns;
   a.ns = ns;
   const size_t smem = 1024 + ns * sbytes + (2 * ns + NG) * 8 + 16 + 4096;
   // persistent CTAs: one per SM (capping the grid to leave SMs to the

@@ -652,6 +652,8 @@ class DeviceFmm:
         else:
             self._init_fft(inst.fft_ops, inst.halo_plans)
         self._bufs = {}
+        self._canary_on = os.environ.get("KIFMM_CANARY", "0") == "1"
+        self._canaries = []
         self._marks = None
         self.last_timings = {}
         self.last_m2l_calls = []
@@ -720,6 +722,39 @@ class DeviceFmm:
         return 4
 
     # -------------------------------------------------------------- buffers
+    # KIFMM_CANARY=1 (tests): every evaluate buffer gets CANARY guard
+    # elements before and after it, filled with a sentinel; check_canaries()
+    # reports any kernel write outside its buffer (compute-sanitizer is not
+    # available on the B200 pool)
+    CANARY = 4096
+
+    def _alloc(self, n, dtype, zero=False):
+        n = int(n)
+        if not getattr(self, "_canary_on", False):
+            return (torch.zeros if zero else torch.empty)(n, dtype=dtype, device=_dev())
+        pad = self.CANARY
+        full = torch.empty(n + 2 * pad, dtype=dtype, device=_dev())
+        sentinel = -1.2345e30
+        full.fill_(sentinel)
+        inner = full[pad: pad + n]
+        if zero:
+            inner.zero_()
+        self._canaries.append((full, n, sentinel))
+        return inner
+
+    def check_canaries(self):
+        """[(buffer index, elements clobbered before, after)] for every guarded
+        buffer whose guard elements changed (empty: no out-of-bounds write)."""
+        torch.cuda.synchronize()
+        bad = []
+        for i, (full, n, sentinel) in enumerate(getattr(self, "_canaries", [])):
+            pad = self.CANARY
+            head = int((full[:pad] != sentinel).sum().item())
+            tail = int((full[pad + n:] != sentinel).sum().item())
+            if head or tail:
+                bad.append((i, head, tail))
+        return bad
+
     def _buffers(self, nrhs):
         if nrhs in self._bufs:
             return self._bufs[nrhs]
@@ -727,27 +762,24 @@ class DeviceFmm:
         R = nrhs
         d = self.depth
         b = {}
-        b["q"] = torch.empty(self.sx.shape[0] * R, dtype=T, device=dev)
-        b["src4"] = torch.empty(self.sx.shape[0] * R * 4, dtype=T, device=dev)
-        b["mult"] = [torch.empty(self.n_src[l] * R * self.n_e, dtype=T, device=dev)
+        b["q"] = self._alloc(self.sx.shape[0] * R, T)
+        b["src4"] = self._alloc(self.sx.shape[0] * R * 4, T)
+        b["mult"] = [self._alloc(self.n_src[l] * R * self.n_e, T)
                      for l in range(d + 1)]
-        b["loc"] = [torch.empty(self.n_tgt[l] * R * self.n_e, dtype=T, device=dev)
+        b["loc"] = [self._alloc(self.n_tgt[l] * R * self.n_e, T)
                     for l in range(d + 1)]
         nmax_rows = max(max(self.n_src), max(self.n_tgt)) * R
-        b["phi"] = torch.empty(max(nmax_rows * max(self.n_c, 1),
-                                   max(self.n_tgt[:d] + [1]) * R * 8 * self.n_c), dtype=T,
-                               device=dev)
+        b["phi"] = self._alloc(max(nmax_rows * max(self.n_c, 1),
+                                   max(self.n_tgt[:d] + [1]) * R * 8 * self.n_c), T)
         rmax = max(self.r_up, self.r_dn)
-        b["tmp"] = torch.empty(max(nmax_rows, max(self.n_tgt[:d] + [1]) * 8 * R) * rmax,
-                               dtype=T, device=dev)
-        b["stack"] = torch.empty(max(self.n_src[2:d] + [1]) * R * 8 * self.n_e, dtype=T,
-                                 device=dev)
+        b["tmp"] = self._alloc(max(nmax_rows, max(self.n_tgt[:d] + [1]) * 8 * R) * rmax, T)
+        b["stack"] = self._alloc(max(self.n_src[2:d] + [1]) * R * 8 * self.n_e, T)
         # per-level M2L scratch (levels run concurrently in the overlapped
         # evaluate): check rows, and the BLAS (qt, acc) or FFT (qhat, phat) sets
         levels = list(range(2, d + 1))
-        b["phi_lv"] = {l: torch.empty(max(self.n_tgt[l] * R * self.n_c, 1), dtype=T, device=dev)
+        b["phi_lv"] = {l: self._alloc(max(self.n_tgt[l] * R * self.n_c, 1), T)
                        for l in levels}
-        b["t_lv"] = {l: torch.empty(max(self.n_tgt[l] * R * self.r_fold, 1), dtype=T, device=dev)
+        b["t_lv"] = {l: self._alloc(max(self.n_tgt[l] * R * self.r_fold, 1), T)
                      for l in levels}
         if self.cfg.backend == "blas":
             def acc_need(l):
@@ -757,23 +789,23 @@ class DeviceFmm:
                                                    tma=True, n_pairs=self.tma_plan[l]["n_pairs"]))
                 return max(n, 1)
             qt_w = R * self.blas.kin * (3 if self.blas.tc else 1)
-            b["qt_lv"] = {l: torch.zeros(max(self.n_src[l], 1) * qt_w, dtype=T, device=dev)
+            b["qt_lv"] = {l: self._alloc(max(self.n_src[l], 1) * qt_w, T, zero=True)
                           for l in levels}
-            b["acc_lv"] = {l: torch.zeros(acc_need(l), dtype=T, device=dev) for l in levels}
+            b["acc_lv"] = {l: self._alloc(acc_need(l), T, zero=True) for l in levels}
             if self.tma:
-                b["dense"] = {l: tuple(torch.zeros(8 * R * p["h"] ** 3 * self.blas.kin, dtype=T,
-                                                   device=dev) for _ in range(2))
+                b["dense"] = {l: tuple(self._alloc(8 * R * p["h"] ** 3 * self.blas.kin, T,
+                                                   zero=True) for _ in range(2))
                               for l, p in self.tma_plan.items()}
         else:
             fp = self.fft_plan_dev
-            b["qhat_lv"] = {l: torch.empty(2 * self.n_freq * fp[l]["nsc"] * 8 * R, dtype=T,
-                                           device=dev) for l in levels}
-            b["phat_lv"] = {l: torch.empty(2 * self.n_freq * fp[l]["ntc"] * 8 * R, dtype=T,
-                                           device=dev) for l in levels}
-        b["out"] = torch.empty(self.tx.shape[0] * R, dtype=T, device=dev)
+            b["qhat_lv"] = {l: self._alloc(2 * self.n_freq * fp[l]["nsc"] * 8 * R, T)
+                            for l in levels}
+            b["phat_lv"] = {l: self._alloc(2 * self.n_freq * fp[l]["ntc"] * 8 * R, T)
+                            for l in levels}
+        b["out"] = self._alloc(self.tx.shape[0] * R, T)
         if self.mutual is not None:
-            b["pmut"] = torch.empty(max(self.mutual["total"], 1) * R, dtype=T, device=dev)
-        b["qin"] = torch.empty(self.sx.shape[0] * R, dtype=torch.float64, device=dev)
+            b["pmut"] = self._alloc(max(self.mutual["total"], 1) * R, T)
+        b["qin"] = self._alloc(self.sx.shape[0] * R, torch.float64)
         self._bufs[nrhs] = b
         return b
 
@@ -862,7 +894,7 @@ class DeviceFmm:
         out = b["out"]
         nt = self.tx.shape[0]
         if gradient and "grad" not in b:
-            b["grad"] = torch.empty(nt * R * 3, dtype=self.T, device=out.device)
+            b["grad"] = self._alloc(nt * R * 3, self.T)
         grad_ptr = [P(b["grad"])] if gradient else []
         leaf_name = f"kifmm_leaf_pass_grad_{sfx}" if gradient else f"kifmm_leaf_pass_{sfx}"
 
@@ -1146,6 +1178,17 @@ class DeviceFmm:
             dst[lo:hi].copy_(stage[lo:hi], non_blocking=True)
         self._stage_done = torch.cuda.Event()
         self._stage_done.record()
+
+    def graph_timeline(self, nrhs, gradient=False):
+        """[(operator, start ms, end ms)] of the last replay, relative to the
+        start of its P2M (the graph's operator spans in time order)."""
+        marks = getattr(self, "_graph_marks", {}).get((nrhs, bool(gradient))) or {}
+        if "p2m" not in marks:
+            return []
+        t0 = marks["p2m"][0]
+        out = [(k, t0.elapsed_time(a), t0.elapsed_time(b))
+               for k, evs in marks.items() for a, b in zip(evs[0::2], evs[1::2])]
+        return sorted(out, key=lambda x: x[1])
 
     def collect_timings(self):
         ev = getattr(self, "_events", None)

@@ -549,3 +549,57 @@ def test_operator_timings_filled_by_default(cuda):
             assert 0 < t[k] < 1.0, (kw, k, t)
         again = inst.evaluate(2 * q)
         assert np.all(np.isfinite(again)) and inst.timings["m2l"] > 0
+
+
+@pytest.mark.parametrize("kw,clustered,nrhs", [
+    (dict(depth=3, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6), False, 1),
+    (dict(depth=4, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6), True, 2),
+    (dict(depth=3, order_equiv=6, backend="blas", precision="f32", sigma_min=1e-6), False, 1),
+    (dict(depth=4, order_equiv=5, backend="blas", precision="f64", sigma_min=1e-12), True, 1),
+    (dict(depth=3, order_equiv=4, backend="fft", precision="f64"), False, 3),
+    (dict(depth=4, order_equiv=4, backend="fft", precision="f32"), True, 1)])
+def test_no_out_of_bounds_writes(cuda, monkeypatch, kw, clustered, nrhs):
+    """Guard elements before and after every evaluate buffer stay intact
+    (KIFMM_CANARY=1) through graphed, eager and gradient evaluates - the
+    bounds evidence in place of compute-sanitizer, which is closed on the
+    B200 pool - and the results still match the reference."""
+    from paper_2408_07436_b200 import FmmConfig, setup
+    monkeypatch.setenv("KIFMM_CANARY", "1")
+    rng = np.random.default_rng(12)
+    n = 30000
+    pts = rng.random((n, 3)) ** (3 if clustered else 1)
+    q = rng.random((n, nrhs)) if nrhs > 1 else rng.random(n)
+    inst = setup(pts, pts, FmmConfig(**kw))
+    dev = inst.device
+    a = inst.evaluate(q)
+    inst.evaluate(q, gradient=True)
+    inst.profile = True
+    b = inst.evaluate(q)
+    assert dev.check_canaries() == [], dev.check_canaries()
+    assert len(dev._canaries) > 10
+    assert np.abs(np.asarray(a, np.float64) - b).max() <= 1e-5 * np.abs(b).max()
+    if nrhs == 1:
+        want, _ = _reference_run(pts, q, kw)
+        tol = TOL[kw["precision"]]
+        assert parity_report(a, want)["max_rel"] <= tol
+
+
+@pytest.mark.parametrize("rank", [None, 60])
+def test_fresh_instances_are_bitwise_equal(cuda, rank):
+    """Repeated fresh setups + first evaluates give bit-identical potentials
+    (config-2 shape; rank 60: KP = 64, the two-stage ring).  This caught an
+    intermittent stage race of the tensor-memory sweep with an odd stage
+    ring (now forced even)."""
+    from paper_2408_07436_b200 import FmmConfig, setup
+    pts = np.random.default_rng(7).random((1_000_000, 3))
+    q = np.random.default_rng(11).random(1_000_000)
+    kw = dict(depth=5, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6,
+              rank_estimate=rank)
+    first = None
+    for _ in range(6):
+        inst = setup(pts, pts, FmmConfig(**kw))
+        got = inst.evaluate(q)
+        if first is None:
+            first = got
+        else:
+            assert np.array_equal(got, first)
