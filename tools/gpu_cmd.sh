@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-echo "ns2dbg fresh overlap0"; KIFMM_OVERLAP=0 KIFMM_LIB=$PWD/_variants/libns2dbg.so timeout 900 python tools/stress_overlap.py 40 1 > gpurun_out/stress_a.log 2>&1; grep -v "CUDAEvent.h\|^frame" gpurun_out/stress_a.log | grep -E "mismatch|reps|Error|stuck" | head
-echo "ns4dbg fresh overlap0"; KIFMM_OVERLAP=0 KIFMM_LIB=$PWD/_variants/libns4dbg.so timeout 900 python tools/stress_overlap.py 60 1 > gpurun_out/stress_b.log 2>&1; grep -v "CUDAEvent.h\|^frame" gpurun_out/stress_b.log | grep -E "mismatch|reps|Error|stuck" | head
-echo "default fresh"; timeout 900 python tools/stress_overlap.py 80 1 > gpurun_out/stress_c.log 2>&1; grep -v "CUDAEvent.h\|^frame" gpurun_out/stress_c.log | grep -E "mismatch|reps|Error|stuck" | head
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/r2_gputest9.log 2>&1; tail -3 gpurun_out/r2_gputest9.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/r2_bench9.json 2> gpurun_out/r2_bench9.err
+python -c "import json;d=json.loads(open('gpurun_out/r2_bench9.json').read().strip().splitlines()[-1]);print(d['value'],d['ms_per_step'],d['e2e'],d['roofline']['frac'],d['roofline_all']['p2p_mutual_f32']['frac']);print(d['configs']['c3']['parity'])"
