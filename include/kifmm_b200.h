@@ -290,16 +290,15 @@ int kifmm_fft_inverse_f64(const double* phat, int64_t nrhs, int64_t order,
  * -> 0).  Results go to partial-sum slots (no atomics, deterministic):
  *   P[r*pstride + base[B] + s*n_B + t], s = 0: B's row sums, s = 1..nlow_B:
  *   the column sums of B's s-th lower neighbour (its entry s of B's near list);
- * For leaf A (points [leaf_start[A], +leaf_count[A]), slot base base[A]),
- * cols[col_off[A] .. col_off[A+1]) are its upper columns: every point of
- * every upper neighbour B > A, as int32 pairs (source row, base[B] + s*n_B
- * + t) with s = A's entry in B's near list.  order (n_leaves, or NULL): the
- * leaves in launch order (heaviest first balances the uneven per-leaf work).
- * guard != 0: also guard the cross-leaf pairs against r2 == 0. */
+ * near_pack[e] = (start, count, dst, leaf) of entry e of a near list (the
+ * CSR near_off): the entry leaf's first point and point count, and dst =
+ * base[B] + s*n_B for an upper entry (A, B > A), base[A] for the own entry
+ * (entry 0).  order (n_leaves, or NULL): the leaves in launch order
+ * (heaviest first balances the uneven per-leaf work).  guard != 0: also
+ * guard the cross-leaf pairs against r2 == 0. */
 int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, int64_t n_leaves,
-                         const float* src4, int64_t npts, const int32_t* leaf_start,
-                         const int32_t* leaf_count, const int32_t* base, const int64_t* col_off,
-                         const int32_t* cols, const int32_t* order, int64_t nrhs,
+                         const float* src4, int64_t npts, const int32_t* near_off,
+                         const int32_t* near_pack, const int32_t* order, int64_t nrhs,
                          int64_t pstride, int guard, float* P, void* stream);
 /* Near-field totals of the mutual pass: out[perm[i]*nrhs + r] = (1/4 pi)
  * sum_{s=0..nlow_b} P[r*pstride + base[b] + s*n_b + t] (slot order), for

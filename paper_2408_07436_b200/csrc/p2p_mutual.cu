@@ -141,16 +141,16 @@ struct WarpSmem {
   float4 col[2][2 * kFC];
   int32_t dst[2][kFC];
   float4 self[kSelf];
+  int2 seg[32];           // (source row - first column, dst - first column) of upper segment e
+  int32_t incl[32];       // inclusive end column of segment e (0-size for non-upper entries)
 };
 
 template <bool GUARD>
 __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
     const float* __restrict__ tx, const float* __restrict__ ty, const float* __restrict__ tz,
     int64_t n_leaves, const float4* __restrict__ src4, int64_t npts,
-    const int32_t* __restrict__ lstart, const int32_t* __restrict__ lcount,
-    const int32_t* __restrict__ base, const int64_t* __restrict__ col_off,
-    const int2* __restrict__ cols, const int32_t* __restrict__ order, int64_t nrhs,
-    int64_t pstride, float* __restrict__ P) {
+    const int32_t* __restrict__ near_off, const int4* __restrict__ near_pack,
+    const int32_t* __restrict__ order, int64_t nrhs, int64_t pstride, float* __restrict__ P) {
   __shared__ WarpSmem sm_all[kMW];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem& sm = sm_all[w];
@@ -158,14 +158,32 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
   const int64_t slot = (int64_t)blockIdx.x * kMW + w;
   if (slot >= n_leaves) return;
   const int64_t a = order ? order[slot] : slot;
-  // the leaf's points, slot base and upper columns: (source row, column-sum
-  // destination) of every point of its upper neighbours, in near-list order
-  const int t0 = lstart[a], tc = lcount[a];
-  const int32_t own_base = base[a];
-  const int64_t c_begin = col_off[a];
-  const int ncols = (int)(col_off[a + 1] - c_begin);
-  const int2* lcols = cols + c_begin;
+  // near entries of the first leaf: (start, count, dst, leaf); entry 0 is the
+  // leaf itself, its dst field holds the leaf's slot base
+  int4 ent = make_int4(0, 0, 0, -1);
+  int nent = 0;
   {
+    const int n0 = near_off[a];
+    nent = near_off[a + 1] - n0;
+    if (lane < nent) ent = near_pack[n0 + lane];
+  }
+  {
+    const int t0 = __shfl_sync(kFull, ent.x, 0), tc = __shfl_sync(kFull, ent.y, 0);
+    const int32_t own_base = __shfl_sync(kFull, ent.z, 0);
+    // upper segments: exclusive prefix of their sizes over the entries
+    const int ucnt = (lane > 0 && lane < nent && ent.w > a) ? ent.y : 0;
+    int incl = ucnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int ncols = __shfl_sync(kFull, incl, 31);
+    const int excl = incl - ucnt;
+    __syncwarp();
+    sm.seg[lane] = make_int2(ent.x - excl, ent.z - excl);
+    sm.incl[lane] = incl;
+    __syncwarp();
     for (int64_t r = 0; r < nrhs; ++r) {
       const float4* srow = src4 + r * npts;
       float* Pr = P + r * pstride;
@@ -193,10 +211,15 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
           for (int cc = lane; cc < mp; cc += 32) {
             const int e2 = ((cc >> lr) << (lr + 1)) + (cc & (R - 1));
             if (cc < m) {
-              const int2 cl = __ldg(lcols + c0 + cc);
-              cp_async16(cb + e2, srow + cl.x, true);
-              cp_async16(cb + e2 + R, srow + cl.x, true);
-              db[cc] = cl.y;
+              const int c = c0 + cc;
+              int e = 0;
+#pragma unroll
+              for (int st = 16; st > 0; st >>= 1)
+                if (sm.incl[e + st - 1] <= c) e += st;
+              const int2 sg = sm.seg[e];
+              cp_async16(cb + e2, srow + sg.x + c, true);
+              cp_async16(cb + e2 + R, srow + sg.x + c, true);
+              db[cc] = sg.y + c;
             } else {
               cb[e2] = pad_col();
               cb[e2 + R] = pad_col();
@@ -317,23 +340,20 @@ extern "C" {
 // = base_B + slot * n_B for an upper entry e of leaf A's near list (B > A),
 // unused otherwise; P: nrhs planes of pstride floats.
 int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, int64_t n_leaves,
-                         const float* src4, int64_t npts, const int32_t* lstart,
-                         const int32_t* lcount, const int32_t* base, const int64_t* col_off,
-                         const int32_t* cols, const int32_t* order, int64_t nrhs,
+                         const float* src4, int64_t npts, const int32_t* near_off,
+                         const int32_t* near_pack, const int32_t* order, int64_t nrhs,
                          int64_t pstride, int guard, float* P, void* stream) {
   if (n_leaves < 0 || npts < 0 || nrhs < 1 || pstride < npts) return KIFMM_EARG;
   if (n_leaves == 0) return 0;
   const auto* s4 = reinterpret_cast<const float4*>(src4);
-  const auto* c2 = reinterpret_cast<const int2*>(cols);
+  const auto* pk = reinterpret_cast<const int4*>(near_pack);
   const unsigned grid = ceil_div(n_leaves, kMW);
   if (guard)
     p2p_mutual_kernel<true><<<grid, 32 * kMW, 0, (cudaStream_t)stream>>>(
-        tx, ty, tz, n_leaves, s4, npts, lstart, lcount, base, col_off, c2, order, nrhs, pstride,
-        P);
+        tx, ty, tz, n_leaves, s4, npts, near_off, pk, order, nrhs, pstride, P);
   else
     p2p_mutual_kernel<false><<<grid, 32 * kMW, 0, (cudaStream_t)stream>>>(
-        tx, ty, tz, n_leaves, s4, npts, lstart, lcount, base, col_off, c2, order, nrhs, pstride,
-        P);
+        tx, ty, tz, n_leaves, s4, npts, near_off, pk, order, nrhs, pstride, P);
   return launch_status();
 }
 

@@ -614,10 +614,9 @@ class DeviceFmm:
                 and os.environ.get("KIFMM_P2P", "mutual") == "mutual"
                 and np.array_equal(st.perm, tt.perm)):
             ms = mutual_slots(inst.near.offsets, inst.near.leaves, st.leaf_counts)
-            col_off, cols = ms.columns(inst.near.offsets, inst.near.leaves, st.leaf_starts,
-                                       st.leaf_counts)
             self.mutual = dict(base=to_dev(ms.base), nlow=to_dev(ms.nlow), total=ms.total,
-                               col_off=to_dev(col_off), cols=to_dev(cols),
+                               pack=to_dev(ms.pack(inst.near.offsets, inst.near.leaves,
+                                                   st.leaf_starts, st.leaf_counts)),
                                order=to_dev(mutual_order(inst.near.offsets, inst.near.leaves,
                                                          st.leaf_counts)))
         # unit-box operators
@@ -915,10 +914,9 @@ class DeviceFmm:
                 # mutual near field into the partial-sum slots, then their
                 # per-target totals into out (caller order)
                 launch("kifmm_p2p_mutual_f32", P(self.tx), P(self.ty), P(self.tz),
-                       self.n_tgt[d], P(b["src4"]), self.sx.shape[0], P(self.t_start),
-                       P(self.t_count), P(mut["base"]), P(mut["col_off"]), P(mut["cols"]),
-                       P(mut["order"]), R, mut["total"], int(self.p2p_guard), P(b["pmut"]),
-                       stream)
+                       self.n_tgt[d], P(b["src4"]), self.sx.shape[0], P(self.near_off),
+                       P(mut["pack"]), P(mut["order"]), R, mut["total"], int(self.p2p_guard),
+                       P(b["pmut"]), stream)
                 launch("kifmm_p2p_mutual_reduce_f32", P(self.t_start), P(self.t_count),
                        self.n_tgt[d], R, P(self.t_perm), P(mut["base"]), P(mut["nlow"]),
                        mut["total"], P(b["pmut"]), P(out), stream)

@@ -31,28 +31,18 @@ class MutualSlots:
     near_dst: np.ndarray     # (len(near.leaves),) int32: base[B] + slot * n_B for upper entries, else -1
     total: int               # floats per right-hand side
 
-    def columns(self, near_offsets, near_leaves, leaf_starts, leaf_counts):
-        """Per leaf A, its upper columns - every point of every upper
-        neighbour B (B > A), in near-list order - as (source row, column-sum
-        destination base[B] + slot * n_B + t): ``col_off`` (n_leaves + 1)
-        int64 and ``cols`` (n_columns, 2) int32, the device table of
-        csrc/p2p_mutual.cu."""
-        off = np.asarray(near_offsets, dtype=np.int64)
+    def pack(self, near_offsets, near_leaves, leaf_starts, leaf_counts) -> np.ndarray:
+        """(len(near.leaves), 4) int32 device table of csrc/p2p_mutual.cu:
+        (start, count, dst, leaf) per near entry; the own entry (first of
+        each list) carries the leaf's slot base as dst."""
         lv = np.asarray(near_leaves, dtype=np.int64)
-        n = np.asarray(leaf_counts, dtype=np.int64)
-        starts = np.asarray(leaf_starts, dtype=np.int64)
-        owner = np.repeat(np.arange(n.shape[0], dtype=np.int64), np.diff(off))
-        up = np.flatnonzero(lv > owner)                       # upper entries, list order
-        cnt = n[lv[up]]
-        col_off = np.zeros(n.shape[0] + 1, dtype=np.int64)
-        np.add.at(col_off, owner[up] + 1, cnt)
-        col_off = np.cumsum(col_off)
-        seg_first = np.repeat(np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt)
-        k = np.arange(int(cnt.sum()), dtype=np.int64) - seg_first
-        src = np.repeat(starts[lv[up]], cnt) + k
-        dst = np.repeat(self.near_dst.astype(np.int64)[up], cnt) + k
-        cols = np.ascontiguousarray(np.stack([src, dst], axis=1).astype(np.int32))
-        return col_off, cols
+        off = np.asarray(near_offsets, dtype=np.int64)
+        dst = self.near_dst.astype(np.int64).copy()
+        nonempty = np.diff(off) > 0
+        dst[off[:-1][nonempty]] = self.base[np.flatnonzero(nonempty)]
+        out = np.stack([np.asarray(leaf_starts, np.int64)[lv], np.asarray(leaf_counts, np.int64)[lv],
+                        dst, lv], axis=1)
+        return np.ascontiguousarray(out.astype(np.int32))
 
 
 def mutual_order(near_offsets, near_leaves, leaf_counts) -> np.ndarray:

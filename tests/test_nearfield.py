@@ -148,22 +148,3 @@ def test_near_plan_digest_matches_reference_loop(case):
     assert near.n_pairs == want["n_near_pairs"]
     assert dig(offs) == want["near_offsets_sha256"]
     assert dig(rows) == want["near_idx_sha256"]
-
-
-def test_mutual_columns_table():
-    """The device column table lists, per leaf, every point of every upper
-    neighbour in near-list order with its column-sum destination."""
-    from paper_2408_07436_b200.nearfield import mutual_slots
-    pts = uniform_points(5000, seed=3)
-    st, tt, near = _trees(pts, 3)
-    ms = mutual_slots(near.offsets, near.leaves, st.leaf_counts)
-    col_off, cols = ms.columns(near.offsets, near.leaves, st.leaf_starts, st.leaf_counts)
-    assert col_off[0] == 0 and col_off[-1] == cols.shape[0]
-    for a in range(st.leaf_counts.shape[0]):
-        want = []
-        for e in range(near.offsets[a], near.offsets[a + 1]):
-            b = near.leaves[e]
-            if b > a:
-                want += [(st.leaf_starts[b] + k, ms.near_dst[e] + k)
-                         for k in range(st.leaf_counts[b])]
-        assert [tuple(x) for x in cols[col_off[a]:col_off[a + 1]]] == want
