@@ -1146,36 +1146,22 @@ class DeviceFmm:
             return t
         return read
 
-    # pageable host input: chunks copied into a pinned staging buffer by a
-    # few host threads (numpy releases the GIL for large copies), each chunk's
-    # H2D issued as soon as it is staged, so the copies overlap
-    STAGE_CHUNK = 1 << 18            # float64 elements (2 MB)
-    STAGE_THREADS = 4
-
+    # pageable host input: one (multi-threaded) torch host copy into a pinned
+    # staging buffer, then an asynchronous H2D (measured on the B200 host,
+    # 8 MB: 0.34 ms; a direct pageable copy 0.43 ms; a 4-thread chunked
+    # numpy pipeline 0.9 ms)
     def _stage_pageable(self, src, dst):
         n = src.numel()
         stage = getattr(self, "_stage_buf", None)
         if stage is None or stage.numel() < n:
             stage = torch.empty(n, dtype=torch.float64, pin_memory=True)
             self._stage_buf = stage
-            self._stage_np = stage.numpy()
-        if not hasattr(self, "_stage_pool"):
-            from concurrent.futures import ThreadPoolExecutor
-            self._stage_pool = ThreadPoolExecutor(self.STAGE_THREADS)
-        src_np = src.numpy()
         # the previous call's H2D from the staging buffer must be done
         ev = getattr(self, "_stage_done", None)
         if ev is not None:
             ev.synchronize()
-        step = self.STAGE_CHUNK
-        bounds = [(i, min(n, i + step)) for i in range(0, n, step)]
-
-        def copy(lo, hi):
-            np.copyto(self._stage_np[lo:hi], src_np[lo:hi])
-        futs = [self._stage_pool.submit(copy, lo, hi) for lo, hi in bounds]
-        for (lo, hi), f in zip(bounds, futs):
-            f.result()
-            dst[lo:hi].copy_(stage[lo:hi], non_blocking=True)
+        stage[:n].copy_(src)
+        dst.copy_(stage[:n], non_blocking=True)
         self._stage_done = torch.cuda.Event()
         self._stage_done.record()
 
