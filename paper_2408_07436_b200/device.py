@@ -470,24 +470,36 @@ class BlasDevice:
         return int(out.value)
 
     def run_level_tma(self, plan, mult, n_s, n_t, nrhs, level_scale, qt, dense, acc, solve,
-                      check=None):
+                      check=None, after_projection=None, coarse_ctas=0):
         """Engine path for float32: projection -> dense sub-lattice array ->
         tcgen05 sweep (A in tensor memory, or TMA-staged hi/lo planes) ->
-        fused epilogue into the locals."""
+        fused epilogue into the locals.
+
+        ``coarse_ctas`` > 0 (a level above the finest in the overlapped
+        evaluate): the persistent sweep is confined to about that many CTAs.
+        A persistent CTA owns its SM's shared memory, so a coarse level
+        spread over all SMs (a few vectors each) keeps the near field off the
+        whole machine for its duration; on a few SMs it takes longer but
+        runs in the near field's shadow."""
         la = self.la
         if self.tmem:
             nsplit = self.tmem_splits(plan["n_tiles"], plan["n_pairs"], nrhs)
+            if coarse_ctas > 0 and plan["n_tiles"] * nrhs <= coarse_ctas:
+                nsplit = min(nsplit, max(1, -(-coarse_ctas // (plan["n_tiles"] * nrhs))))
             # projection q~ = M S written straight into the dense parity
             # sub-lattice array (row map (box, rhs) -> plane p*R + r, cell)
             la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin,
                     dense[0], self.kin, rowmap=dense_rowmap(plan, nrhs))
+            if after_projection is not None:
+                after_projection()
             launch("kifmm_m2l_sweep_tmem_f32", P(dense[0]), P(self.Bpair), self.kin, plan["h"],
                    P(plan["tile_targets"]), P(plan["tile_ids"]), plan["n_tiles"],
                    P(plan["pairs"]), plan["n_pairs"], P(self.class_tv_local), P(self.offsets),
                    nrhs, nsplit, self.ko_pad, P(acc), stream_handle())
         else:
             nsplit = sweep_splits(plan["n_tiles"], 1)
-            self._run_tma(plan, mult, n_s, nrhs, qt, dense, acc, nsplit)
+            self._run_tma(plan, mult, n_s, nrhs, qt, dense, acc, nsplit,
+                          after_projection=after_projection)
         if solve is None:
             # t = check . U_dn in one product (acc . (U^T U_dn)); the caller
             # adds the L2L part and applies the rest of the solve
@@ -502,9 +514,11 @@ class BlasDevice:
                  asum=nsplit, astride=self.ko_pad)
         return 4
 
-    def _run_tma(self, plan, mult, n_s, nrhs, qt, dense, acc, nsplit):
+    def _run_tma(self, plan, mult, n_s, nrhs, qt, dense, acc, nsplit, after_projection=None):
         la = self.la
         la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
+        if after_projection is not None:
+            after_projection()
         hi, lo = dense
         # TF32 hi/lo planes split here (splitting raw fp32 q~ in the sweep's
         # shared memory halves the TMA bytes for A but measured slower on
@@ -577,6 +591,8 @@ class DeviceFmm:
         self.n_e, self.n_c = exp.n_equiv, exp.n_check
         # near field concurrent with the far field (see evaluate_device)
         self.overlap = os.environ.get("KIFMM_OVERLAP", "1") != "0"
+        self.p2p_fork = os.environ.get("KIFMM_P2P_FORK", "sweep")
+        self.coarse_ctas = int(os.environ.get("KIFMM_COARSE_CTAS", "32"))
         least, greatest = torch.cuda.Stream.priority_range()
         self.side_stream = torch.cuda.Stream(priority=least)
         self.hi_stream = torch.cuda.Stream(priority=greatest)
@@ -674,7 +690,8 @@ class DeviceFmm:
             self.tma_plan = {l: tma_level_plan(st.level_keys(l), tt.level_keys(l), l)
                              for l in plans}
 
-    def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None):
+    def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None, after_projection=None,
+                       coarse_ctas=0):
         """Each level has its own scratch (qt, acc): levels run concurrently
         in the overlapped evaluate."""
         b = self._buffers(nrhs)
@@ -683,7 +700,8 @@ class DeviceFmm:
             plan = self.tma_plan[lvl]
             return self.blas.run_level_tma(plan, mult, self.n_src[lvl], self.n_tgt[lvl], nrhs,
                                            1.0 / self.side[lvl], qt, b["dense"][lvl], acc, solve,
-                                           check=check)
+                                           check=check, after_projection=after_projection,
+                                           coarse_ctas=coarse_ctas)
         return self.blas.run_level(self.blas_plan_dev[lvl], mult, self.n_src[lvl],
                                    self.n_tgt[lvl], nrhs, 1.0 / self.side[lvl], check, qt, acc,
                                    solve=solve)
@@ -953,12 +971,14 @@ class DeviceFmm:
         # (engine.py:355, 370) and saves one solve per level.
         rf = self.r_fold
 
-        def m2l(lvl):
+        def m2l(lvl, after_projection=None):
             # t_l = check_l . U_dn (rank rf) from the level's M2L
             n_t = self.n_tgt[lvl]
             t_l = b["t_lv"][lvl][: n_t * R * rf]
             if self.cfg.backend == "blas" and self.tma:
-                calls[lvl] = self.m2l_blas_level(lvl, mult[lvl], R, t_l)
+                calls[lvl] = self.m2l_blas_level(
+                    lvl, mult[lvl], R, t_l, after_projection=after_projection,
+                    coarse_ctas=self.coarse_ctas if overlap and lvl < d else 0)
                 return
             check = b["phi_lv"][lvl][: n_t * R * n_c]
             if self.cfg.backend == "blas":
@@ -982,20 +1002,33 @@ class DeviceFmm:
         main = torch.cuda.current_stream()
         forked = {}
 
-        def fork_m2l(lvl):
+        def fork_m2l(lvl, after_projection=None):
             st = self.level_streams[lvl]
             st.wait_stream(main)
             with torch.cuda.stream(st):
                 mark("m2l")
-                m2l(lvl)
+                m2l(lvl, after_projection)
                 mark("m2l")
             forked[lvl] = st
 
         # the finest level's M2L is forked right after P2M (forking it after
         # the M2M pass, so the persistent sweep cannot hold the SMs the
         # latency-bound M2M chain needs, measured within +-1%)
+        # The near field is released when the finest level's projection ends,
+        # i.e. together with that level's persistent sweep: the sweep (higher
+        # priority) takes the SMs first and the near-field CTAs fill them as
+        # the sweep's CTAs retire, while the M2M chain, the coarse levels and
+        # the L2L chain (small latency-bound kernels on higher-priority
+        # streams) run in the near field's shadow.  Forked after the upward
+        # pass instead, the near field started ~60 us after the sweep's end
+        # (the M2M chain cannot get an SM while the sweep holds all of them).
+        p2p_forked = False
         if overlap and d >= 3:
-            fork_m2l(d)
+            if self.cfg.backend == "blas" and self.tma and self.p2p_fork == "sweep":
+                fork_m2l(d, after_projection=fork_p2p)
+                p2p_forked = True
+            else:
+                fork_m2l(d)
         phase("m2m")
         mark("m2m")
         # M2M down to level 2 (levels 0-1 carry no M2L): children stacked in
@@ -1009,7 +1042,7 @@ class DeviceFmm:
             if overlap and lvl - 1 >= 3:
                 fork_m2l(lvl - 1)
         mark("m2m")
-        if overlap:
+        if overlap and not p2p_forked:
             fork_p2p()
         for lvl in range(2, d + 1):
             n_t = self.n_tgt[lvl]
