@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           for (int i = 8; i < KP / 4; ++i)
             split4(i, *reinterpret_cast<const float4*>(sb + TMT * 128 + m * (W1 * 4) + (i - 8) * 16));
         }
+        if (m == 0 && grp == 0) trace(2, gg);
         // this group's previous MMAs done: A_k reusable (and D_k promoted below)
         if (nmine > 0) mbar_wait(&done[grp], (nmine - 1) & 1, false);
         if (m == 0) trace(grp == 0 ? 1 : 6, gg);
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           tmem_st8(acol + lane_base + KP + c * 8, *reinterpret_cast<const uint32_t(*)[8]>(&lv[c * 8]));
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (m == 0 && grp == 0) trace(7, gg);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
         if (issuer) {
@@ -369,6 +371,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
           }
           mma_commit(&done[grp]);
           mma_commit(&empty[s]);
+          if (grp == 0) trace(9, gg);
         }
         __syncwarp();
         ++nmine;
@@ -377,7 +380,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
         if (last_of_block) {
           // promote D_k: wait for this block's last MMAs, add into registers;
           // the next vector's MMA overwrites D_k only after the group barrier
+          if (m == 0 && grp == 0) trace(8, gg);
           mbar_wait(&done[grp], (nmine - 1) & 1, false);
+          if (m == 0 && grp == 0) trace(10, gg);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
           for (int c = 0; c < KP / 8; ++c) {
@@ -390,6 +395,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
               acc[c * 8 + i] += __uint_as_float(u[i]) + __uint_as_float(w[i]);
           }
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          if (m == 0 && grp == 0) trace(11, gg);
         }
       }
       // combine the groups' partial sums in shared memory, 8 columns at a
