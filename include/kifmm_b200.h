@@ -265,6 +265,13 @@ int kifmm_scatter_rows_f32(const float* src, const int32_t* rows, int64_t n_rows
                            float* dst, void* stream);
 int kifmm_scatter_rows_f64(const double* src, const int32_t* rows, int64_t n_rows, int64_t width,
                            double* dst, void* stream);
+/* dst[dst_rows[i]*width + e] = src[src_rows[i]*width + e]: the halo unpack of
+ * the all-gathered exchange buffer (distributed.py; the reference has no
+ * multi-GPU path, SPEC.md:139 - SURVEY 8(e)). */
+int kifmm_move_rows_f32(const float* src, const int32_t* src_rows, const int32_t* dst_rows,
+                        int64_t n_rows, int64_t width, float* dst, void* stream);
+int kifmm_move_rows_f64(const double* src, const int32_t* src_rows, const int32_t* dst_rows,
+                        int64_t n_rows, int64_t width, double* dst, void* stream);
 /* dst[rows[i]*width + e] += src[i*width + e] (rows[i] < 0: skipped): the L2L
  * child check potentials added to the M2L check potentials of a level before
  * the one down_inv solve (engine.py:355,370 merged). */

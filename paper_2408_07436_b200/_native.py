@@ -59,6 +59,8 @@ SIGNATURES = {
     "kifmm_gather_rows_f64": [_P, _P, _I, _I, _P, _P],
     "kifmm_scatter_rows_f32": [_P, _P, _I, _I, _P, _P],
     "kifmm_scatter_rows_f64": [_P, _P, _I, _I, _P, _P],
+    "kifmm_move_rows_f32": [_P, _P, _P, _I, _I, _P, _P],
+    "kifmm_move_rows_f64": [_P, _P, _P, _I, _I, _P, _P],
     "kifmm_fft_inverse_f32": [_P, _I, _I, _P, _I, _D, _P, _P],
     "kifmm_fft_inverse_f64": [_P, _I, _I, _P, _I, _D, _P, _P],
     "kifmm_leaf_pass_f32": [_P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P,

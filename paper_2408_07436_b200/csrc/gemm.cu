@@ -486,6 +486,28 @@ __global__ void rows_kernel(const T* __restrict__ src, const int32_t* __restrict
   }
 }
 
+// dst[dst_rows[i]] = src[src_rows[i]] (halo unpack straight out of an
+// all-gathered buffer: no intermediate copy)
+template <typename T>
+__global__ void move_rows_kernel(const T* __restrict__ src, const int32_t* __restrict__ src_rows,
+                                 const int32_t* __restrict__ dst_rows, int64_t n_rows,
+                                 int64_t width, T* __restrict__ dst) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_rows * width) return;
+  const int64_t i = idx / width, e = idx - i * width;
+  dst[(int64_t)dst_rows[i] * width + e] = src[(int64_t)src_rows[i] * width + e];
+}
+
+template <typename T>
+int move_rows(const T* src, const int32_t* src_rows, const int32_t* dst_rows, int64_t n_rows,
+              int64_t width, T* dst, void* stream) {
+  if (n_rows < 0 || width < 1) return KIFMM_EARG;
+  if (n_rows == 0) return 0;
+  move_rows_kernel<T><<<ceil_div(n_rows * width, 256), 256, 0, (cudaStream_t)stream>>>(
+      src, src_rows, dst_rows, n_rows, width, dst);
+  return launch_status();
+}
+
 template <typename T>
 int rows_op(const T* src, const int32_t* rows, int64_t n_rows, int64_t width, T* dst, int scatter,
             void* stream) {
@@ -515,6 +537,15 @@ int kifmm_scatter_rows_f32(const float* src, const int32_t* rows, int64_t n_rows
 int kifmm_scatter_rows_f64(const double* src, const int32_t* rows, int64_t n_rows, int64_t width,
                            double* dst, void* s) {
   return rows_op<double>(src, rows, n_rows, width, dst, 1, s);
+}
+
+int kifmm_move_rows_f32(const float* src, const int32_t* src_rows, const int32_t* dst_rows,
+                        int64_t n_rows, int64_t width, float* dst, void* s) {
+  return move_rows<float>(src, src_rows, dst_rows, n_rows, width, dst, s);
+}
+int kifmm_move_rows_f64(const double* src, const int32_t* src_rows, const int32_t* dst_rows,
+                        int64_t n_rows, int64_t width, double* dst, void* s) {
+  return move_rows<double>(src, src_rows, dst_rows, n_rows, width, dst, s);
 }
 
 int kifmm_scatter_add_rows_f32(const float* src, const int32_t* rows, int64_t n_rows,

@@ -57,6 +57,18 @@ def P(t):
     return None if t is None else t.data_ptr()
 
 
+class Off:
+    """A tensor's storage from element ``elems`` on, wherever the launch
+    helpers expect a tensor (they only take data_ptr()): the owned row range
+    of a rank in the multi-GPU evaluate."""
+
+    def __init__(self, t, elems):
+        self._p = t.data_ptr() + int(elems) * t.element_size()
+
+    def data_ptr(self):
+        return self._p
+
+
 # Optional per-launch event profiling (bench.py roofline): when _PROF is a
 # list, every launch appends (entry point, tag, start event, end event).
 _PROF = None
@@ -470,7 +482,7 @@ class BlasDevice:
         return int(out.value)
 
     def run_level_tma(self, plan, mult, n_s, n_t, nrhs, level_scale, qt, dense, acc, solve,
-                      check=None, after_projection=None, coarse_ctas=0):
+                      check=None, after_projection=None, coarse_ctas=0, rows=None):
         """Engine path for float32: projection -> dense sub-lattice array ->
         tcgen05 sweep (A in tensor memory, or TMA-staged hi/lo planes) ->
         fused epilogue into the locals.
@@ -503,9 +515,12 @@ class BlasDevice:
         if solve is None:
             # t = check . U_dn in one product (acc . (U^T U_dn)); the caller
             # adds the L2L part and applies the rest of the solve
+            # (rows: the owned target range of a rank plan)
             r = self.UTU.shape[1]
-            la.gemm(n_t * nrhs, r, self.k, level_scale, acc, nsplit * self.ko_pad,
-                    self.UTU, r, check, r, asum=nsplit, astride=self.ko_pad)
+            lo, hi = rows if rows is not None else (0, n_t)
+            ld = nsplit * self.ko_pad
+            la.gemm((hi - lo) * nrhs, r, self.k, level_scale, Off(acc, lo * nrhs * ld), ld,
+                    self.UTU, r, Off(check, lo * nrhs * r), r, asum=nsplit, astride=self.ko_pad)
             return 3
         inv, side, loc = solve
         la.chain(n_t * nrhs, acc, nsplit * self.ko_pad,

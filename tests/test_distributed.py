@@ -14,7 +14,8 @@ import torch.multiprocessing as mp
 from conftest import uniform_points
 from oracle import port
 from paper_2408_07436_b200 import FmmConfig, setup
-from paper_2408_07436_b200.distributed import (TorchExchanger, make_partition, make_rank_plans,
+from paper_2408_07436_b200.distributed import (HaloExchange, TorchCollectives, TorchExchanger,
+                                                make_partition, make_rank_plans,
                                                restrict_buckets)
 
 
@@ -147,6 +148,26 @@ def _rank_main(rank, world, port_no, backend, result):
                 mult[l][rows] = flat[off: off + rows.shape[0] * width].reshape(rows.shape[0],
                                                                               *mult[l].shape[1:])
                 off += rows.shape[0] * width
+        # the all-gather exchange of the device path (HaloExchange tables):
+        # one buffer per group and rank, every rank receives all of them and
+        # moves out the rows it needs - must deliver the same ghosts
+        plans_all = make_rank_plans(inst, part)
+        halo = HaloExchange(plans_all, rank, inst.config.depth)
+        mult_ag = {l: np.full_like(mult_full[l], np.nan) for l in mult}
+        for l in mult_ag:
+            lo, hi = plan.src_ranges[l]
+            mult_ag[l][lo:hi] = mult_full[l][lo:hi]
+        coll = TorchCollectives()
+        for group, g in halo.groups.items():
+            if not g["levels"]:
+                continue
+            send = torch.from_numpy(halo.pack_host(group, mult_ag))
+            recv = torch.empty((world * g["smax"], send.shape[1]), dtype=send.dtype)
+            coll.all_gather(send, recv)
+            halo.unpack_host(group, recv.numpy(), mult_ag)
+        for l in levels:
+            assert np.array_equal(np.isnan(mult_ag[l]), np.isnan(mult[l])), l
+            assert np.array_equal(np.nan_to_num(mult_ag[l]), np.nan_to_num(mult[l])), l
         # every owned target's M2L input is now exact; compare the level checks
         worst = 0.0
         for l in levels:

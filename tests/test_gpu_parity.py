@@ -7,6 +7,8 @@ SURVEY.md 8(d) prescribes, because near-zero potentials make a strict
 per-target bound depend on rounding order alone.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -284,6 +286,45 @@ def test_partitioned_evaluate_matches_single_device(cuda, backend, precision):
         got = evaluate_local(inst, world, q)[:, 0]
         rel = np.abs(got - ref) / np.abs(ref)
         assert rel.max() <= TOL[precision], (world, rel.max())
+
+
+def test_rank_graph_with_nccl_collectives(cuda):
+    """The rank path over a real NCCL process group (world size 1 - one GPU
+    is all there is here): its stream DAG with the three all-gathers is
+    captured as ONE CUDA graph and replays to the single-device result,
+    bitwise on re-replay.  (Ranks > 1 are covered by the in-process
+    emulation above and the gloo exchange test.)"""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2408_07436_b200 import FmmConfig, setup
+    from paper_2408_07436_b200.distributed import (DistributedFmm, TorchCollectives,
+                                                    make_partition, make_rank_plans)
+    from conftest import uniform_points
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port_no = so.getsockname()[1]
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port_no)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        pts = uniform_points(40000, seed=43)
+        q = np.random.default_rng(44).random(40000)
+        inst = setup(pts, pts, FmmConfig(depth=4, order_equiv=4, backend="blas",
+                                         precision="f32", sigma_min=1e-6))
+        ref = inst.evaluate(q)
+        plans = make_rank_plans(inst, make_partition(inst.source_tree, inst.target_tree, 1))
+        rk = DistributedFmm(inst, plans[0], all_plans=plans)
+        coll = TorchCollectives()
+        assert rk.graph_for(1, coll) is not None, "NCCL collectives were not captured"
+        qd = torch.from_numpy(q).cuda()
+        a = rk.evaluate_graphed(qd, 1, coll).clone()
+        b = rk.evaluate_graphed(qd, 1, coll).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+        got = a.cpu().numpy()[:, 0].astype(np.float64)
+        assert (np.abs(got - ref) / np.abs(ref)).max() <= 1e-5
+    finally:
+        dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ gradient
