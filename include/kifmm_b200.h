@@ -255,6 +255,21 @@ int kifmm_fft_forward_f64(const double* mult, int64_t nrhs, int64_t order,
                           const int32_t* slot_box, int64_t nsc, const int32_t* cluster_list,
                           int64_t n_list, double* qhat, void* stream);
 
+/* Fused row chain for tall inputs (float32, operator dimensions <= 64):
+ * Y0 = X B0 (x cs0, x al0), Y1 = Y0 B1 ..., with an optional output after every
+ * stage (C_s, ldc_s, optional int32 row map over the M input rows - negative:
+ * skipped -, accumulate flag); X[m][k] = sum_{s < asum} A[m*lda + s*astride + k].
+ * The evaluate runs the P2M solve (expansion.py:78-82 via engine.py:298-318)
+ * and the leaf level's M2L projection q~ = M S (m2l_blas.py:284-288) as one
+ * launch: phi . U_up (x inv) . V_up^T (x side) -> multipoles, . S -> q~. */
+int kifmm_rowchain_f32(int64_t M, const float* A, int64_t lda, int64_t asum, int64_t astride,
+                       int64_t nstage, const float* B0, const float* B1, const float* B2,
+                       int64_t K0, int64_t N0, int64_t N1, int64_t N2, const float* cs0,
+                       const float* cs1, const float* cs2, float al0, float al1, float al2,
+                       float* C0, float* C1, float* C2, int64_t ldc0, int64_t ldc1, int64_t ldc2,
+                       const int32_t* map0, const int32_t* map1, const int32_t* map2, int64_t acc0,
+                       int64_t acc1, int64_t acc2, void* stream);
+
 /* Multipole halo pack/unpack for the multi-GPU exchange:
  * gather: dst[i*width + e] = src[rows[i]*width + e]; scatter: the reverse. */
 int kifmm_gather_rows_f32(const float* src, const int32_t* rows, int64_t n_rows, int64_t width,

@@ -59,6 +59,8 @@ SIGNATURES = {
     "kifmm_gather_rows_f64": [_P, _P, _I, _I, _P, _P],
     "kifmm_scatter_rows_f32": [_P, _P, _I, _I, _P, _P],
     "kifmm_scatter_rows_f64": [_P, _P, _I, _I, _P, _P],
+    "kifmm_rowchain_f32": [_I, _P, _I, _I, _I, _I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _F, _F, _F,
+                           _P, _P, _P, _I, _I, _I, _P, _P, _P, _I, _I, _I, _P],
     "kifmm_move_rows_f32": [_P, _P, _P, _I, _I, _P, _P],
     "kifmm_move_rows_f64": [_P, _P, _P, _I, _I, _P, _P],
     "kifmm_fft_inverse_f32": [_P, _I, _I, _P, _I, _D, _P, _P],

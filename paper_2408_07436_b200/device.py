@@ -198,6 +198,18 @@ class Linalg:
                 rows = rows * N // stages[i + 1][1]
                 A, lda, asum, astride = y, stages[i + 1][1], 1, 0
 
+    def rowchain(self, M, A, lda, stages, asum=1, astride=0):
+        """Fused float32 row chain for tall inputs (csrc/rowchain.cu): stages =
+        [(B, K, N, colscale, alpha, C, ldc, rowmap, accumulate), ...] with an
+        optional output C after every stage; dimensions <= 64."""
+        st = list(stages) + [(None, 0, 0, None, 1.0, None, 0, None, False)] * (3 - len(stages))
+        launch("kifmm_rowchain_f32", M, P(A), lda, int(asum), astride, len(stages),
+               P(st[0][0]), P(st[1][0]), P(st[2][0]), st[0][1], st[0][2], st[1][2], st[2][2],
+               P(st[0][3]), P(st[1][3]), P(st[2][3]), float(st[0][4]), float(st[1][4]),
+               float(st[2][4]), P(st[0][5]), P(st[1][5]), P(st[2][5]), st[0][6], st[1][6],
+               st[2][6], P(st[0][7]), P(st[1][7]), P(st[2][7]), int(bool(st[0][8])),
+               int(bool(st[1][8])), int(bool(st[2][8])), stream_handle())
+
     def scratch(self, slot, n, T, dev):
         """Grow-only scratch buffers (allocated outside graph capture on the
         eager warm-up pass, reused afterwards).  A buffer that is outgrown is
@@ -482,7 +494,8 @@ class BlasDevice:
         return int(out.value)
 
     def run_level_tma(self, plan, mult, n_s, n_t, nrhs, level_scale, qt, dense, acc, solve,
-                      check=None, after_projection=None, coarse_ctas=0, rows=None):
+                      check=None, after_projection=None, coarse_ctas=0, rows=None,
+                      projected=False, after_sweep=None):
         """Engine path for float32: projection -> dense sub-lattice array ->
         tcgen05 sweep (A in tensor memory, or TMA-staged hi/lo planes) ->
         fused epilogue into the locals.
@@ -499,9 +512,11 @@ class BlasDevice:
             if coarse_ctas > 0 and plan["n_tiles"] * nrhs <= coarse_ctas:
                 nsplit = min(nsplit, max(1, -(-coarse_ctas // (plan["n_tiles"] * nrhs))))
             # projection q~ = M S written straight into the dense parity
-            # sub-lattice array (row map (box, rhs) -> plane p*R + r, cell)
-            la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin,
-                    dense[0], self.kin, rowmap=dense_rowmap(plan, nrhs))
+            # sub-lattice array (row map (box, rhs) -> plane p*R + r, cell);
+            # `projected`: the caller's fused P2M chain has written it already
+            if not projected:
+                la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin,
+                        dense[0], self.kin, rowmap=dense_rowmap(plan, nrhs))
             if after_projection is not None:
                 after_projection()
             launch("kifmm_m2l_sweep_tmem_f32", P(dense[0]), P(self.Bpair), self.kin, plan["h"],
@@ -512,6 +527,8 @@ class BlasDevice:
             nsplit = sweep_splits(plan["n_tiles"], 1)
             self._run_tma(plan, mult, n_s, nrhs, qt, dense, acc, nsplit,
                           after_projection=after_projection)
+        if after_sweep is not None:
+            after_sweep()
         if solve is None:
             # t = check . U_dn in one product (acc . (U^T U_dn)); the caller
             # adds the L2L part and applies the rest of the solve
@@ -606,8 +623,9 @@ class DeviceFmm:
         self.n_e, self.n_c = exp.n_equiv, exp.n_check
         # near field concurrent with the far field (see evaluate_device)
         self.overlap = os.environ.get("KIFMM_OVERLAP", "1") != "0"
-        self.p2p_fork = os.environ.get("KIFMM_P2P_FORK", "sweep")
+        self.p2p_fork = os.environ.get("KIFMM_P2P_FORK", "sweep_end")
         self.coarse_ctas = int(os.environ.get("KIFMM_COARSE_CTAS", "32"))
+        self.fuse_p2m = os.environ.get("KIFMM_FUSE_P2M", "1") != "0"
         least, greatest = torch.cuda.Stream.priority_range()
         self.side_stream = torch.cuda.Stream(priority=least)
         self.hi_stream = torch.cuda.Stream(priority=greatest)
@@ -706,7 +724,7 @@ class DeviceFmm:
                              for l in plans}
 
     def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None, after_projection=None,
-                       coarse_ctas=0):
+                       coarse_ctas=0, projected=False, after_sweep=None):
         """Each level has its own scratch (qt, acc): levels run concurrently
         in the overlapped evaluate."""
         b = self._buffers(nrhs)
@@ -716,7 +734,8 @@ class DeviceFmm:
             return self.blas.run_level_tma(plan, mult, self.n_src[lvl], self.n_tgt[lvl], nrhs,
                                            1.0 / self.side[lvl], qt, b["dense"][lvl], acc, solve,
                                            check=check, after_projection=after_projection,
-                                           coarse_ctas=coarse_ctas)
+                                           coarse_ctas=coarse_ctas, projected=projected,
+                                           after_sweep=after_sweep)
         return self.blas.run_level(self.blas_plan_dev[lvl], mult, self.n_src[lvl],
                                    self.n_tgt[lvl], nrhs, 1.0 / self.side[lvl], check, qt, acc,
                                    solve=solve)
@@ -974,7 +993,21 @@ class DeviceFmm:
         launch(f"kifmm_p2m_check_{sfx}", P(self.sx), P(self.sy), P(self.sz), P(q), R,
                P(self.s_start), P(self.s_count), nl, P(self.s_centers), P(self.check_base),
                n_c, P(phi), s)
-        la.chain(nl * R, phi, n_c, Linalg.solve_stages(self.up_inv, self.side[d]), mult[d], n_e)
+        # float32, narrow operators (p <= 4), tensor-memory sweep: the solve and
+        # the leaf level's M2L projection in one fused row chain (one launch
+        # instead of three latency-bound GEMMs in front of the finest sweep)
+        fused_p2m = (self.fuse_p2m and sfx == "f32" and self.cfg.backend == "blas" and self.tma
+                     and self.blas.tmem and d >= 3 and max(n_c, n_e, self.blas.kin) <= 64)
+        if fused_p2m:
+            u, vals, vt = self.up_inv
+            la.rowchain(nl * R, phi, n_c,
+                        [(u, n_c, u.shape[1], vals, 1.0, None, 0, None, False),
+                         (vt, u.shape[1], n_e, None, self.side[d], mult[d], n_e, None, False),
+                         (self.blas.S, n_e, self.blas.kin, None, 1.0, b["dense"][d][0],
+                          self.blas.kin, dense_rowmap(self.tma_plan[d], R), False)])
+        else:
+            la.chain(nl * R, phi, n_c, Linalg.solve_stages(self.up_inv, self.side[d]), mult[d],
+                     n_e)
         mark("p2m")
         loc = b["loc"]
         calls = {}
@@ -986,14 +1019,15 @@ class DeviceFmm:
         # (engine.py:355, 370) and saves one solve per level.
         rf = self.r_fold
 
-        def m2l(lvl, after_projection=None):
+        def m2l(lvl, after_projection=None, after_sweep=None):
             # t_l = check_l . U_dn (rank rf) from the level's M2L
             n_t = self.n_tgt[lvl]
             t_l = b["t_lv"][lvl][: n_t * R * rf]
             if self.cfg.backend == "blas" and self.tma:
                 calls[lvl] = self.m2l_blas_level(
                     lvl, mult[lvl], R, t_l, after_projection=after_projection,
-                    coarse_ctas=self.coarse_ctas if overlap and lvl < d else 0)
+                    coarse_ctas=self.coarse_ctas if overlap and lvl < d else 0,
+                    projected=fused_p2m and lvl == d, after_sweep=after_sweep)
                 return
             check = b["phi_lv"][lvl][: n_t * R * n_c]
             if self.cfg.backend == "blas":
@@ -1017,30 +1051,38 @@ class DeviceFmm:
         main = torch.cuda.current_stream()
         forked = {}
 
-        def fork_m2l(lvl, after_projection=None):
+        def fork_m2l(lvl, after_projection=None, after_sweep=None):
             st = self.level_streams[lvl]
             st.wait_stream(main)
             with torch.cuda.stream(st):
                 mark("m2l")
-                m2l(lvl, after_projection)
+                m2l(lvl, after_projection, after_sweep)
                 mark("m2l")
             forked[lvl] = st
 
         # the finest level's M2L is forked right after P2M (forking it after
         # the M2M pass, so the persistent sweep cannot hold the SMs the
         # latency-bound M2M chain needs, measured within +-1%)
-        # The near field is released when the finest level's projection ends,
-        # i.e. together with that level's persistent sweep: the sweep (higher
-        # priority) takes the SMs first and the near-field CTAs fill them as
-        # the sweep's CTAs retire, while the M2M chain, the coarse levels and
-        # the L2L chain (small latency-bound kernels on higher-priority
-        # streams) run in the near field's shadow.  Forked after the upward
-        # pass instead, the near field started ~60 us after the sweep's end
-        # (the M2M chain cannot get an SM while the sweep holds all of them).
+        # The near field is released when the finest level's persistent sweep
+        # ENDS.  Both are whole-GPU throughput kernels; a sweep CTA needs an
+        # SM's whole shared memory, so near-field CTAs resident on an SM keep
+        # the sweep off it (released together with the sweep - after its
+        # projection - the sweep took 340 us instead of 282 and the evaluate
+        # 850 us instead of 842; released after the upward pass, later still).
+        # The M2M chain, the coarse levels and the L2L chain (small
+        # latency-bound kernels on higher-priority streams) run in the near
+        # field's shadow.  Measured bounds of this schedule at config 2: with
+        # the coarse-level sweeps removed the evaluate takes 778 us, so their
+        # ~40 us of tensor work costs 64 us; prefix (78) + finest sweep (282) +
+        # near field (277) + L2P (52) = 689 us is the floor of the DAG.
         p2p_forked = False
         if overlap and d >= 3:
             if self.cfg.backend == "blas" and self.tma and self.p2p_fork == "sweep":
                 fork_m2l(d, after_projection=fork_p2p)
+                p2p_forked = True
+            elif self.cfg.backend == "blas" and self.tma and self.p2p_fork == "sweep_end":
+                # experiment: the near field strictly behind the finest sweep
+                fork_m2l(d, after_sweep=fork_p2p)
                 p2p_forked = True
             else:
                 fork_m2l(d)

@@ -532,6 +532,60 @@ def test_scatter_add_rows(cuda):
     assert np.array_equal(d_d.cpu().numpy(), want)
 
 
+def test_rowchain_and_move_rows(cuda):
+    """kifmm_rowchain_f32 (fused P2M solve + projection): three stages with a
+    split-sum input, a column scale, a plain middle output, a row-mapped
+    last output and a ragged last tile, against float64 numpy; and
+    kifmm_move_rows_f32 (halo unpack)."""
+    import torch
+    from paper_2408_07436_b200.device import Linalg
+    from paper_2408_07436_b200 import _native as nat
+    rng = np.random.default_rng(5)
+    M, K0, N0, N1, N2, nsplit = 1000, 56, 51, 56, 56, 2
+    A = rng.standard_normal((M, nsplit, 64)).astype(np.float32)
+    B0 = rng.standard_normal((K0, N0)).astype(np.float32)
+    cs = rng.random(N0).astype(np.float32)
+    B1 = rng.standard_normal((N0, N1)).astype(np.float32)
+    B2 = rng.standard_normal((N1, N2)).astype(np.float32)
+    rowmap = rng.permutation(M + 40)[:M].astype(np.int32)
+    rowmap[::17] = -1
+    X = A[:, :, :K0].astype(np.float64).sum(axis=1)
+    Y0 = X @ B0.astype(np.float64) * cs
+    Y1 = Y0 @ B1.astype(np.float64) * 0.25
+    Y2 = Y1 @ B2.astype(np.float64)
+    C1_0 = rng.standard_normal((M, N1)).astype(np.float32)
+    dev = lambda a: torch.from_numpy(a).cuda()   # noqa: E731
+    A_d, B0_d, cs_d, B1_d, B2_d, map_d = map(dev, (A, B0, cs, B1, B2, rowmap))
+    C1 = dev(C1_0.copy())
+    C2 = torch.full((M + 40, N2), 7.0, dtype=torch.float32, device="cuda")
+    Linalg("f32").rowchain(M, A_d, nsplit * 64,
+                           [(B0_d, K0, N0, cs_d, 1.0, None, 0, None, False),
+                            (B1_d, N0, N1, None, 0.25, C1, N1, None, True),
+                            (B2_d, N1, N2, None, 1.0, C2, N2, map_d, False)],
+                           asum=nsplit, astride=64)
+    torch.cuda.synchronize()
+    got1 = C1.cpu().numpy().astype(np.float64) - C1_0
+    assert np.abs(got1 - Y1).max() <= 2e-5 * np.abs(Y1).max()
+    got2 = C2.cpu().numpy()
+    want2 = np.full((M + 40, N2), 7.0)
+    want2[rowmap[rowmap >= 0]] = Y2[rowmap >= 0]
+    assert np.abs(got2 - want2).max() <= 2e-5 * np.abs(Y2).max()
+    untouched = np.setdiff1d(np.arange(M + 40), rowmap[rowmap >= 0])
+    assert np.all(got2[untouched] == 7.0)
+    # move_rows: dst[dst_rows[i]] = src[src_rows[i]]
+    src = rng.random((30, 9)).astype(np.float32)
+    sr = rng.integers(0, 30, 12).astype(np.int32)
+    dr = rng.permutation(20)[:12].astype(np.int32)
+    dst = np.zeros((20, 9), np.float32)
+    s_d, sr_d, dr_d, d_d = map(dev, (src, sr, dr, dst))
+    nat.call("kifmm_move_rows_f32", s_d.data_ptr(), sr_d.data_ptr(), dr_d.data_ptr(), 12, 9,
+             d_d.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    want = dst.copy()
+    want[dr] = src[sr]
+    assert np.array_equal(d_d.cpu().numpy(), want)
+
+
 # ------------------------------------------- mutual near field (csrc/p2p_mutual.cu)
 @pytest.mark.parametrize("n,depth,nrhs,clustered,merge", [
     (60000, 4, 1, False, False), (60000, 4, 2, False, False), (40000, 4, 1, True, False),
