@@ -255,6 +255,28 @@ int kifmm_fft_forward_f64(const double* mult, int64_t nrhs, int64_t order,
                           const int32_t* slot_box, int64_t nsc, const int32_t* cluster_list,
                           int64_t n_list, double* qhat, void* stream);
 
+/* Factored float64 BLAS-M2L sweep (reference m2l_blas.py:291-320 applies
+ * (q~[rows_s] vbar_t) ubar_t^T per bucket: 4 k k_t flop per pair; the dense
+ * sweep above spends 2 k^2).  Two passes over an HBM intermediate W:
+ * compress: W[pair] = q~[rows1[pair]] . vbar_t for the n_tiles 128-pair chunks
+ *   of one width class (ktp_t = 16 * ntw * n_slabs); vbar block t = (kin x ktp_t)
+ *   at voff[t]; W block t at 16-byte offset wbase16[t], one plane (w_plane
+ *   elements) per right-hand side.
+ * expand: acc[target] += sum_t W[pair(target, t)] . ubar_t^T, target-stationary
+ *   on the tile plan of kifmm_m2l_sweep_f64 (woff: 16-byte W offset per
+ *   (tile, vector position, row), -1 none; ubar^T block t = (ktp_t x ko_pad) at
+ *   uoff[t]); optional sparse lists as kifmm_m2l_sweep_sparse_f64. */
+int kifmm_m2l_compress_f64(const double* qt, int64_t kin, int64_t nrhs, const double* vbar,
+                           const int64_t* voff, const int32_t* ktp, const int32_t* tile_t,
+                           const int32_t* tile_first, const int32_t* rows1, int64_t n_tiles,
+                           int64_t ntw, int64_t n_slabs, const int64_t* wbase16, double* W,
+                           int64_t w_plane, void* stream);
+int kifmm_m2l_expand_f64(const double* W, int64_t w_plane, const double* ubT, const int64_t* uoff,
+                         const int32_t* ktp, int64_t ko_pad, const int32_t* tile_targets,
+                         const int32_t* tile_class, const int32_t* woff, const int32_t* class_tv,
+                         int64_t n_tiles, int64_t nrhs, int64_t nsplit, const uint16_t* gmask,
+                         const int16_t* jlist, const int32_t* jcount, double* acc, void* stream);
+
 /* Fused row chain for tall inputs (float32, operator dimensions <= 64):
  * Y0 = X B0 (x cs0, x al0), Y1 = Y0 B1 ..., with an optional output after every
  * stage (C_s, ldc_s, optional int32 row map over the M input rows - negative:

@@ -59,6 +59,9 @@ SIGNATURES = {
     "kifmm_gather_rows_f64": [_P, _P, _I, _I, _P, _P],
     "kifmm_scatter_rows_f32": [_P, _P, _I, _I, _P, _P],
     "kifmm_scatter_rows_f64": [_P, _P, _I, _I, _P, _P],
+    "kifmm_m2l_compress_f64": [_P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _I, _P],
+    "kifmm_m2l_expand_f64": [_P, _I, _P, _P, _P, _I, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P,
+                             _P],
     "kifmm_rowchain_f32": [_I, _P, _I, _I, _I, _I, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _F, _F, _F,
                            _P, _P, _P, _I, _I, _I, _P, _P, _P, _I, _I, _I, _P],
     "kifmm_move_rows_f32": [_P, _P, _P, _I, _I, _P, _P],

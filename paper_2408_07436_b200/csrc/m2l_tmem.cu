@@ -47,7 +47,11 @@ namespace {
 
 constexpr int TMT = 128;
 constexpr int NG = 2;             // groups per CTA (alternate vectors), each with its own TMEM A and D
-constexpr int NTHREADS = 32 + 128 * NG;
+#ifndef KIFMM_TMEM_ISSUER
+#define KIFMM_TMEM_ISSUER 1      // 1: one dedicated MMA-issuing warp per group; 0: the group's first thread issues
+#endif
+constexpr bool ISSUER_WARPS = KIFMM_TMEM_ISSUER != 0;
+constexpr int NTHREADS = 32 + 128 * NG + (ISSUER_WARPS ? 32 * NG : 0);
 #ifndef KIFMM_TMEM_FLUSH
 #define KIFMM_TMEM_FLUSH 8
 #endif
@@ -230,14 +234,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * SBYTES);
   uint64_t* empty = full + ns;          // the consuming group's MMAs have read the stage
   uint64_t* done = empty + ns;          // [NG]: group k's MMAs of its last vector completed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + NG);   // + 16 B, then 4 KB reduction buffer
+  uint64_t* aready = done + NG;         // [NG]: group k's 128 loaders have stored the vector's A
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aready + NG);   // + 16 B, then 4 KB reduction buffer
 
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int k = 0; k < NG; ++k) mbar_init(&done[k], 1);
+    for (int k = 0; k < NG; ++k) {
+      mbar_init(&done[k], 1);
+      mbar_init(&aready[k], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
     if (W1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm2)) : "memory");
@@ -358,20 +366,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         if (m == 0 && grp == 0) trace(7, gg);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
-        if (issuer) {
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (grp == 0) trace(3, gg);
-          const uint32_t bb = smem_u32(smem + s * SBYTES + ABYTES);
+        if (ISSUER_WARPS) {
+          // hand the vector over to the group's issuer warp and go on to the
+          // next source block (the issuing thread waits on the tensor pipe
+          // for ~1100 clk per vector: as a loader thread it held its warp -
+          // and through the group barrier the whole group - back)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&aready[grp]))
+                       : "memory");
+        } else {
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+          if (issuer) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (grp == 0) trace(3, gg);
+            const uint32_t bb = smem_u32(smem + s * SBYTES + ABYTES);
 #pragma unroll
-          for (int ks = 0; ks < KP / 8; ++ks) {
-            const uint64_t db = desc_nosw(bb + ks * 256, 128, SBO);
-            mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, local | ks);
-            mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
+            for (int ks = 0; ks < KP / 8; ++ks) {
+              const uint64_t db = desc_nosw(bb + ks * 256, 128, SBO);
+              mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, local | ks);
+              mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
+            }
+            mma_commit(&done[grp]);
+            mma_commit(&empty[s]);
+            if (grp == 0) trace(9, gg);
           }
-          mma_commit(&done[grp]);
-          mma_commit(&empty[s]);
-          if (grp == 0) trace(9, gg);
         }
         __syncwarp();
         ++nmine;
@@ -434,6 +451,48 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
       }
       g += x.nv;
     }
+  }
+  else if (ISSUER_WARPS && warp >= 1 + 4 * NG) {
+    // ------- issuer warp of group k: per vector of the group, wait for the
+    // loaders' A, issue the MMAs into D_k, commit (A_k / D_k free, stage free)
+    const int grp = warp - (1 + 4 * NG);
+    if (lane == 0) {
+      const uint32_t dcol = tmem + (uint32_t)(grp * GCOLS);
+      const uint32_t acol = dcol + N1;
+      constexpr uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) |
+                                  ((uint32_t)(N1 >> 3) << 17) | ((uint32_t)(TMT >> 4) << 24);
+      constexpr uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) |
+                                  ((uint32_t)(N2 >> 3) << 17) | ((uint32_t)(TMT >> 4) << 24);
+      constexpr uint32_t SBO = (KP / 4) * 128;
+      int g = 0, nmine = 0;
+      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+        const Item x = item_of(a, it);
+        int local = 0;
+        for (int v = grp; v < x.nv; v += NG) {
+          const int gg = g + v;
+          const int s = gg % ns;
+          mbar_wait(&full[s], (gg / ns) & 1, false);        // the stage's core pair has landed
+          mbar_wait(&aready[grp], nmine & 1, false);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (grp == 0) trace(3, gg);
+          const uint32_t bb = smem_u32(smem + s * SBYTES + ABYTES);
+#pragma unroll
+          for (int ks = 0; ks < KP / 8; ++ks) {
+            const uint64_t db = desc_nosw(bb + ks * 256, 128, SBO);
+            mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, local | ks);
+            mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
+          }
+          mma_commit(&done[grp]);
+          mma_commit(&empty[s]);
+          if (grp == 0) trace(9, gg);
+          ++nmine;
+          const bool last_of_block = local == FLUSH_V - 1 || v + NG >= x.nv;
+          local = last_of_block ? 0 : local + 1;
+        }
+        g += x.nv;
+      }
+    }
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -507,7 +566,7 @@ int launch_tmem(const TmemArgs& a0, cudaStream_t stream) {
   // ns = 2 and ns = 4 gave none in 180 (tools/stress_overlap.py).
   if (ns & 1) --ns;
   a.ns = ns;
-  const size_t smem = 1024 + ns * sbytes + (2 * ns + NG) * 8 + 16 + 4096;
+  const size_t smem = 1024 + ns * sbytes + (2 * ns + 2 * NG) * 8 + 16 + 4096;
   // persistent CTAs: one per SM (capping the grid to leave SMs to the
   // other streams' kernels measured within +-1%)
   const int g_max = sm_count();

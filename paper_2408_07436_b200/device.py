@@ -286,6 +286,72 @@ def upload_blas_plan(plan):
     return out
 
 
+def factored_widths(ranks):
+    """Padded rank ktp_t of every transfer vector for the factored float64
+    sweep (csrc/m2l_factored.cu) and its width class (ntw, slabs): ktp =
+    16 * ntw * slabs, one slab up to 160 columns."""
+    k16 = -(-np.asarray(ranks, dtype=np.int64) // 16) * 16
+    slabs = np.maximum(1, -(-k16 // 160))
+    ntw = -(-(k16 // 16) // slabs)
+    ntw = np.where(k16 == 0, 0, ntw)
+    return (16 * ntw * slabs).astype(np.int32), ntw.astype(np.int32), slabs.astype(np.int32)
+
+
+def factored_plan(plan_dev, class_tv, ktp, ntw, slabs):
+    """Pair tables of the factored sweep from a target-stationary plan, built
+    on the device: every (tile, vector, row) with a source is a pair; the
+    pairs of a vector t form its W block (rows padded to 128, ktp_t wide) in
+    (tile, vector position, row) order.  Returns None when the W offsets do
+    not fit int32 (the dense sweep is used then)."""
+    n_tiles = plan_dev["n_tiles"]
+    src = plan_dev["src"].reshape(n_tiles, 189, TILE_TARGETS)   # int32 source row or -1
+    dev = src.device
+    tv = class_tv.to(dev).long()[plan_dev["tile_class"].long()]       # (n_tiles, 189)
+    valid = src >= 0
+    t_flat = tv[:, :, None].expand(n_tiles, 189, TILE_TARGETS)[valid]
+    src_flat = src[valid]
+    n_pairs = int(t_flat.numel())
+    ktp_d = torch.from_numpy(np.asarray(ktp, np.int64)).to(dev)
+    counts = torch.bincount(t_flat, minlength=316)
+    rows_pad = (counts + TILE_TARGETS - 1) // TILE_TARGETS * TILE_TARGETS
+    w16 = rows_pad * (ktp_d // 2)                            # 16-byte units per block
+    wbase16 = torch.cumsum(w16, 0) - w16
+    w_elems = int(w16.sum().item()) * 2
+    if int(w16.sum().item()) >= 2 ** 31:
+        return None
+    order = torch.argsort(t_flat, stable=True)
+    t_sorted = t_flat[order]
+    start = torch.cumsum(counts, 0) - counts
+    idx_sorted = torch.arange(n_pairs, device=dev) - start[t_sorted]
+    pairidx = torch.empty_like(idx_sorted)
+    pairidx[order] = idx_sorted
+    woff = torch.full(src.shape, -1, dtype=torch.int32, device=dev)
+    woff[valid] = (wbase16[t_flat] + pairidx * (ktp_d[t_flat] // 2)).to(torch.int32)
+    rowbase = torch.cumsum(rows_pad, 0) - rows_pad
+    rows1 = torch.full((int(rows_pad.sum().item()),), -1, dtype=torch.int32, device=dev)
+    rows1[rowbase[t_sorted] + idx_sorted] = src_flat[order]
+    nt = (rows_pad // TILE_TARGETS).cpu().numpy()
+    tile_t = np.repeat(np.arange(316), nt).astype(np.int32)
+    tile_first = (np.concatenate([np.arange(n) for n in nt]) * TILE_TARGETS).astype(np.int32) \
+        if tile_t.size else np.zeros(0, np.int32)
+    rows1 = rows1.view(-1, TILE_TARGETS)
+    classes = []
+    for key in sorted({(int(ntw[t]), int(slabs[t])) for t in np.unique(tile_t)}):
+        sel = np.flatnonzero((ntw[tile_t] == key[0]) & (slabs[tile_t] == key[1]))
+        # launch order: by position along the (Morton-ordered) targets first,
+        # vector second, so the CTAs in flight at one time gather the q~ rows
+        # of one neighbourhood (L2 hits); vector-major order streams the whole
+        # q~ array from HBM once per vector
+        frac = (tile_first[sel] // TILE_TARGETS) / np.maximum(nt[tile_t[sel]], 1)
+        sel = sel[np.lexsort((tile_t[sel], np.floor(frac * max(n_tiles, 1))))]
+        sel_d = torch.from_numpy(sel).to(dev)
+        classes.append(dict(ntw=key[0], slabs=key[1], n=int(sel.size),
+                            tile_t=to_dev(tile_t[sel]), tile_first=to_dev(tile_first[sel]),
+                            rows1=rows1[sel_d].contiguous()))
+    return dict(woff=woff, wbase16=wbase16.contiguous(), w_elems=max(w_elems, 2),
+                classes=classes, n_pairs=n_pairs, W={})
+
+
 def tf32_split(x: np.ndarray):
     """Host twin of cvt.rna.tf32.f32: x (float32) -> (hi, lo) with hi, lo
     TF32-representable and x = hi + lo + O(2^-22 |x|)."""
@@ -445,6 +511,37 @@ class BlasDevice:
         dt_pad[:, :k, :k] = cores.transpose(0, 2, 1)
         self.Dt = to_dev(dt_pad)
         self.class_tv = to_dev(class_transfer_table(), np.int32)
+        # Factored float64 sweep (csrc/m2l_factored.cu): (q~ vbar_t) ubar_t^T in
+        # two passes, 2 ktp (kin + ko_pad) flop per pair instead of the dense
+        # 2 kin ko_pad; used when the padded ranks make it clearly cheaper
+        # (KIFMM_F64_SWEEP = auto | dense | factored)
+        self.factored = False
+        mode = os.environ.get("KIFMM_F64_SWEEP", "auto")
+        if dt == np.float64 and mode != "dense":
+            ktp, ntw, slabs = factored_widths(ops.ranks)
+            live = ktp[ktp > 0]
+            cheaper = live.size and live.mean() * (self.kin + self.ko_pad) < \
+                0.7 * self.kin * self.ko_pad
+            if mode == "factored" or cheaper:
+                self.factored = True
+                self.ktp, self.f_ntw, self.f_slabs = ktp, ntw, slabs
+                voff = np.concatenate([[0], np.cumsum(self.kin * ktp.astype(np.int64))])
+                uoff = np.concatenate([[0], np.cumsum(self.ko_pad * ktp.astype(np.int64))])
+                vb = np.zeros(max(int(voff[-1]), 1), dtype=np.float64)
+                ub = np.zeros(max(int(uoff[-1]), 1), dtype=np.float64)
+                for t in range(cores.shape[0]):
+                    kt = ops.ubar[t].shape[1]
+                    if not kt:
+                        continue
+                    v = np.zeros((self.kin, ktp[t]))
+                    v[:k, :kt] = ops.vbar[t]
+                    vb[voff[t]: voff[t + 1]] = v.ravel()
+                    u = np.zeros((ktp[t], self.ko_pad))
+                    u[:kt, :k] = np.asarray(ops.ubar[t]).T
+                    ub[uoff[t]: uoff[t + 1]] = u.ravel()
+                self.vbar, self.ubT = to_dev(vb), to_dev(ub)
+                self.voff, self.uoff = to_dev(voff[:-1], np.int64), to_dev(uoff[:-1], np.int64)
+                self.ktp_dev = to_dev(ktp, np.int32)
 
     def run_level_rows(self, plan, mult, n_s, lo, hi, nrhs, level_scale, check, qt, acc):
         """Multi-GPU variant: ``plan`` covers only the target rows [lo, hi)
@@ -463,11 +560,8 @@ class BlasDevice:
                        self.kin, self.ko_pad, P(plan["tile_targets"]), P(plan["tile_class"]),
                        P(plan["src"]), P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc),
                        stream_handle())
-        elif plan["n_tiles"] and self.sfx == "f64" and "gmask" in plan:
-            launch("kifmm_m2l_sweep_sparse_f64", P(qt), P(self.Dt), self.kin, self.ko_pad,
-                   P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
-                   P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(plan["gmask"]),
-                   P(plan["jlist"]), P(plan["jcount"]), P(acc), stream_handle())
+        elif self.sfx == "f64":
+            self.sweep_f64(plan, qt, nrhs, nsplit, acc)
         elif plan["n_tiles"]:
             launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
                    P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
@@ -484,6 +578,45 @@ class BlasDevice:
                 self.UT, self.n_c, _Off(check, lo * nrhs * self.n_c), self.n_c, asum=nsplit,
                 astride=self.ko_pad)
         return 3
+
+    def sweep_f64(self, plan, qt, nrhs, nsplit, acc):
+        """The float64 bucket sweep of one level plan: factored (compress +
+        expand) when the operators call for it, else the dense DMMA sweep
+        (sparse variant on plans with unused vectors / row groups)."""
+        if not plan["n_tiles"]:
+            return
+        sparse = "gmask" in plan
+        if self.factored:
+            if "fact" not in plan:
+                plan["fact"] = factored_plan(plan, self.class_tv, self.ktp, self.f_ntw,
+                                             self.f_slabs)
+            f = plan["fact"]
+        else:
+            f = None
+        if f is not None:
+            if nrhs not in f["W"]:
+                f["W"][nrhs] = torch.empty(f["w_elems"] * nrhs, dtype=torch.float64,
+                                           device=qt.device)
+            W = f["W"][nrhs]
+            for c in f["classes"]:
+                launch("kifmm_m2l_compress_f64", P(qt), self.kin, nrhs, P(self.vbar),
+                       P(self.voff), P(self.ktp_dev), P(c["tile_t"]), P(c["tile_first"]),
+                       P(c["rows1"]), c["n"], c["ntw"], c["slabs"], P(f["wbase16"]), P(W),
+                       f["w_elems"], stream_handle())
+            launch("kifmm_m2l_expand_f64", P(W), f["w_elems"], P(self.ubT), P(self.uoff),
+                   P(self.ktp_dev), self.ko_pad, P(plan["tile_targets"]), P(plan["tile_class"]),
+                   P(f["woff"]), P(self.class_tv), plan["n_tiles"], nrhs, nsplit,
+                   P(plan["gmask"]) if sparse else None, P(plan["jlist"]) if sparse else None,
+                   P(plan["jcount"]) if sparse else None, P(acc), stream_handle())
+        elif sparse:
+            launch("kifmm_m2l_sweep_sparse_f64", P(qt), P(self.Dt), self.kin, self.ko_pad,
+                   P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
+                   P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(plan["gmask"]),
+                   P(plan["jlist"]), P(plan["jcount"]), P(acc), stream_handle())
+        else:
+            launch("kifmm_m2l_sweep_f64", P(qt), P(self.Dt), self.kin, self.ko_pad,
+                   P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
+                   P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc), stream_handle())
 
     def tmem_splits(self, n_tiles, n_pairs, nrhs):
         """Vector-range split of the persistent tensor-memory sweep (host-side
@@ -582,11 +715,8 @@ class BlasDevice:
                        self.kin, self.ko_pad, P(plan["tile_targets"]), P(plan["tile_class"]),
                        P(plan["src"]), P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc),
                        stream_handle())
-        elif plan["n_tiles"] and self.sfx == "f64" and "gmask" in plan:
-            launch("kifmm_m2l_sweep_sparse_f64", P(qt), P(self.Dt), self.kin, self.ko_pad,
-                   P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
-                   P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(plan["gmask"]),
-                   P(plan["jlist"]), P(plan["jcount"]), P(acc), stream_handle())
+        elif self.sfx == "f64":
+            self.sweep_f64(plan, qt, nrhs, nsplit, acc)
         elif plan["n_tiles"]:
             launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
                    P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),

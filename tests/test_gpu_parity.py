@@ -268,6 +268,43 @@ def test_sparse_float64_sweep_on_a_surface(cuda):
     assert parity_report(got, want)["floored"] <= 1e-10
 
 
+@pytest.mark.parametrize("shape,n,depth,order,sigma,nrhs", [
+    ("uniform", 30000, 4, 6, 1e-6, 1),      # config-4-like operators: k = 147, mean k_t ~ 30
+    ("uniform", 20000, 3, 5, 1e-12, 2),     # ranks close to k, two right-hand sides
+    ("sphere", 30000, 5, 5, 1e-12, 1)])     # config-5-like geometry: sparse lists + masks
+def test_factored_float64_sweep(cuda, monkeypatch, shape, n, depth, order, sigma, nrhs):
+    """The factored float64 BLAS-M2L sweep (compress W = q~ vbar_t, expand
+    acc += W ubar_t^T; csrc/m2l_factored.cu) against the dense-core DMMA
+    sweep on the same instance inputs and against the oracle, bitwise on
+    re-evaluation; `auto` picks it for the config-4 operators."""
+    from oracle import port
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(21)
+    if shape == "sphere":
+        v = rng.standard_normal((n, 3))
+        pts = (v / np.linalg.norm(v, axis=1)[:, None] + 1) / 2
+    else:
+        pts = rng.random((n, 3))
+    q = rng.standard_normal((n, nrhs))
+    cfg = FmmConfig(depth=depth, order_equiv=order, backend="blas", precision="f64",
+                    sigma_min=sigma)
+    res = {}
+    for mode in ("dense", "factored"):
+        monkeypatch.setenv("KIFMM_F64_SWEEP", mode)
+        inst = setup(pts, pts, cfg)
+        assert inst.device.blas.factored == (mode == "factored")
+        res[mode] = inst.evaluate(q)
+        if mode == "factored":
+            assert np.array_equal(inst.evaluate(q), res[mode])
+            want = port.evaluate(inst, q)
+            assert parity_report(res[mode], want)["floored"] <= 1e-10
+    scale = np.abs(res["dense"]).max()
+    assert np.abs(res["factored"] - res["dense"]).max() <= 1e-13 * scale
+    if order == 6:
+        monkeypatch.setenv("KIFMM_F64_SWEEP", "auto")
+        assert setup(pts, pts, cfg).device.blas.factored
+
+
 @pytest.mark.parametrize("backend,precision", [("blas", "f32"), ("blas", "f64"), ("fft", "f64")])
 def test_partitioned_evaluate_matches_single_device(cuda, backend, precision):
     """Every device code path of the multi-GPU evaluate (owned ranges, rank

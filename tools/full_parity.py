@@ -105,6 +105,12 @@ def run_case(name):
     got = inst.evaluate(q)
     rec["ours_evaluate_s"] = time.perf_counter() - t0
     rec["ours_relative_error"] = list(inst.relative_error(got))
+    if kw["backend"] == "blas":
+        bd = inst.device.blas
+        rec["ours_sweep"] = ("tcgen05 3xTF32 (tensor memory)" if getattr(bd, "tmem", False) else
+                             "tcgen05 3xTF32 (TMA)" if bd.tc else
+                             "DMMA factored (compress + expand)" if getattr(bd, "factored", False)
+                             else "DMMA dense cores")
     idx = np.sort(np.random.default_rng(5).choice(pts.shape[0], 4096, replace=False))
     direct = direct_sample(pts, q, idx)
     rec["ours_vs_direct_4096"] = err_stats(np.asarray(got, np.float64)[idx], direct)
