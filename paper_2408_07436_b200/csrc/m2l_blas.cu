@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(256, MINB) m2l_sweep_dmma_kernel(
   constexpr int BK = BKT;                             // k-chunk per pipeline stage
   constexpr int GS = BK + 4;                          // row stride = 32 mod 128 bytes: conflict-free A
   constexpr int KOB = 16 * NTW;
-  constexpr int DS = KOB + 8;                         // Ds row stride: rows k, k+1 in opposite bank halves
+  constexpr int DS = KOB + 4;                         // Ds row stride = 4 mod 16 doubles: the 16 lanes of a
+                                                      // half-warp (rows lane & 3, columns lane >> 2) hit 16
+                                                      // distinct 8-byte bank pairs (KOB + 8: rows k, k + 2 collide)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Gs = reinterpret_cast<double*>(smem_raw);   // [STG][TMT][GS]
   double* Ds = Gs + STG * TMT * GS;                   // [STG][BK][DS]
@@ -374,7 +376,7 @@ int sweep_dmma(const double* qt, const double* Dt, int64_t kin, int64_t ko_pad,
   const int bk = wide ? 32 : 16;
   const int nchunks = (int)((kin + bk - 1) / bk);
   auto smem_of = [&](int st) {
-    return sizeof(double) * (size_t)st * (TMT * (bk + 4) + bk * (kob + 8));
+    return sizeof(double) * (size_t)st * (TMT * (bk + 4) + bk * (kob + 4));
   };
   const int stg = (wide && smem_of(3) <= 227 * 1024) ? 3 : 2;
   const size_t smem = smem_of(stg);
