@@ -544,38 +544,22 @@ class BlasDevice:
                 self.ktp_dev = to_dev(ktp, np.int32)
 
     def run_level_rows(self, plan, mult, n_s, lo, hi, nrhs, level_scale, check, qt, acc):
-        """Multi-GPU variant: ``plan`` covers only the target rows [lo, hi)
-        (global row numbering); the expansion runs on those rows only."""
+        """Multi-GPU variant for the generic bucket plans (float64, and float32
+        ranks above 160): ``plan`` covers only the target rows [lo, hi) (global
+        row numbering); the expansion runs on those rows only.  (float32 ranks
+        up to 160 take the class-tile plans: run_level_tma with ``rows``.)"""
         la = self.la
         nsplit = sweep_splits(plan["n_tiles"], self.n_slabs)
         ld = nsplit * self.ko_pad
-        isz = qt.element_size()
         la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
-        if self.tc:
-            nq = n_s * nrhs * self.kin
-            qhi, qlo = qt[nq: 2 * nq], qt[2 * nq: 3 * nq]
-            launch("kifmm_split_tf32", P(qt), nq, P(qhi), P(qlo), stream_handle())
-            if plan["n_tiles"]:
-                launch("kifmm_m2l_sweep_tc_f32", P(qhi), P(qlo), P(self.Bhi), P(self.Blo),
-                       self.kin, self.ko_pad, P(plan["tile_targets"]), P(plan["tile_class"]),
-                       P(plan["src"]), P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc),
-                       stream_handle())
-        elif self.sfx == "f64":
+        if self.sfx == "f64":
             self.sweep_f64(plan, qt, nrhs, nsplit, acc)
         elif plan["n_tiles"]:
             launch(f"kifmm_m2l_sweep_{self.sfx}", P(qt), P(self.Dt), self.kin, self.ko_pad,
                    P(plan["tile_targets"]), P(plan["tile_class"]), P(plan["src"]),
                    P(self.class_tv), plan["n_tiles"], nrhs, nsplit, P(acc), stream_handle())
-
-        class _Off:
-            def __init__(self, t, elems):
-                self.p = t.data_ptr() + elems * isz
-
-            def data_ptr(self):
-                return self.p
-
-        la.gemm((hi - lo) * nrhs, self.n_c, self.k, level_scale, _Off(acc, lo * nrhs * ld), ld,
-                self.UT, self.n_c, _Off(check, lo * nrhs * self.n_c), self.n_c, asum=nsplit,
+        la.gemm((hi - lo) * nrhs, self.n_c, self.k, level_scale, Off(acc, lo * nrhs * ld), ld,
+                self.UT, self.n_c, Off(check, lo * nrhs * self.n_c), self.n_c, asum=nsplit,
                 astride=self.ko_pad)
         return 3
 
