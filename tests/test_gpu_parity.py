@@ -325,6 +325,33 @@ def test_partitioned_evaluate_matches_single_device(cuda, backend, precision):
         assert rel.max() <= TOL[precision], (world, rel.max())
 
 
+@pytest.mark.parametrize("kw,shape,n,nrhs,world", [
+    (dict(depth=4, order_equiv=4, backend="blas", precision="f32", sigma_min=1e-6), "clustered",
+     60000, 2, 3),                                     # pruned boxes, 2 RHS, uneven partition
+    (dict(depth=5, order_equiv=5, backend="blas", precision="f64", sigma_min=1e-12), "sphere",
+     30000, 1, 8),                                     # sparse sweep lists per rank
+    (dict(depth=4, order_equiv=6, backend="blas", precision="f64", sigma_min=1e-6), "clustered",
+     40000, 2, 7),                                     # factored float64 sweep on rank plans
+    (dict(depth=4, order_equiv=4, backend="fft", precision="f32"), "clustered", 60000, 2, 6)])
+def test_partitioned_evaluate_irregular(cuda, kw, shape, n, nrhs, world):
+    """The partitioned evaluate on clustered / surface clouds, several
+    right-hand sides and rank counts that do not divide the level-2 boxes."""
+    from paper_2408_07436_b200 import FmmConfig, setup
+    from paper_2408_07436_b200.distributed import evaluate_local
+    rng = np.random.default_rng(7)
+    pts = rng.random((n, 3))
+    if shape == "clustered":
+        pts = pts ** 3
+    else:
+        v = rng.standard_normal((n, 3))
+        pts = (v / np.linalg.norm(v, axis=1)[:, None] + 1) / 2
+    q = rng.random((n, nrhs)) + 0.1
+    inst = setup(pts, pts, FmmConfig(**kw))
+    ref = np.asarray(inst.evaluate(q), dtype=np.float64).reshape(n, nrhs)
+    got = np.asarray(evaluate_local(inst, world, q), dtype=np.float64)
+    assert (np.abs(got - ref) / np.abs(ref)).max() <= TOL[kw["precision"]]
+
+
 def test_rank_graph_with_nccl_collectives(cuda):
     """The rank path over a real NCCL process group (world size 1 - one GPU
     is all there is here): its stream DAG with the three all-gathers is
