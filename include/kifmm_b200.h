@@ -344,6 +344,10 @@ int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, int6
                          const float* src4, int64_t npts, const int32_t* near_off,
                          const int32_t* near_pack, const int32_t* order, int64_t nrhs,
                          int64_t pstride, int guard, float* P, void* stream);
+int kifmm_p2p_mutual_f64(const double* tx, const double* ty, const double* tz, int64_t n_leaves,
+                         const double* src4, int64_t npts, const int32_t* near_off,
+                         const int32_t* near_pack, const int32_t* order, int64_t nrhs,
+                         int64_t pstride, int guard, double* P, void* stream);
 /* Near-field totals of the mutual pass: out[perm[i]*nrhs + r] = (1/4 pi)
  * sum_{s=0..nlow_b} P[r*pstride + base[b] + s*n_b + t] (slot order), for
  * target i = leaf b's t-th point; the L2P pass then accumulates onto out
@@ -352,6 +356,10 @@ int kifmm_p2p_mutual_reduce_f32(const int32_t* tleaf_start, const int32_t* tleaf
                                 int64_t n_tleaves, int64_t nrhs, const int64_t* perm,
                                 const int32_t* base, const int32_t* nlow, int64_t pstride,
                                 const float* P, float* out, void* stream);
+int kifmm_p2p_mutual_reduce_f64(const int32_t* tleaf_start, const int32_t* tleaf_count,
+                                int64_t n_tleaves, int64_t nrhs, const int64_t* perm,
+                                const int32_t* base, const int32_t* nlow, int64_t pstride,
+                                const double* P, double* out, void* stream);
 
 /* Leaf pass: fused L2P + P2P + un-permute (engine.py:377-404).  For target
  * leaf b and target i in it:

@@ -94,7 +94,9 @@ SIGNATURES = {
     "kifmm_scatter_add_rows_f32": [_P, _P, _I, _I, _P, _P],
     "kifmm_scatter_add_rows_f64": [_P, _P, _I, _I, _P, _P],
     "kifmm_p2p_mutual_f32": [_P, _P, _P, _I, _P, _I, _P, _P, _P, _I, _I, _C, _P, _P],
+    "kifmm_p2p_mutual_f64": [_P, _P, _P, _I, _P, _I, _P, _P, _P, _I, _I, _C, _P, _P],
     "kifmm_p2p_mutual_reduce_f32": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P],
+    "kifmm_p2p_mutual_reduce_f64": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P],
     "kifmm_sm_target": [],
     "kifmm_probe": [_C, _I, _I, _I, _P, _P],
 }

@@ -1,4 +1,5 @@
-// Mutual (symmetric) near field for sources == targets, float32, potential.
+// Mutual (symmetric) near field for sources == targets, potential (float32 on
+// packed FP32 pairs, float64 on the FP64 pipe: the same kernel, templated).
 //
 // The reference's P2P (_hot.pyx:91-138 over the gather plan of
 // engine.py:224-256) evaluates, for every target leaf A, K(t_i, s_j) for all
@@ -58,71 +59,119 @@ constexpr int kMW = KIFMM_MUT_WARPS;
 #endif
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ float4 pad_col() {
-  // far-away, chargeless: r2 = inf -> rsqrt = 0, no contribution either way
-  return make_float4(__int_as_float(0x7f800000), __int_as_float(0x7f800000),
-                     __int_as_float(0x7f800000), 0.f);
+// Pairs of targets: float -> packed FP32 (FADD2 / FMUL2 / FFMA2), double ->
+// two scalars.
+template <typename T> struct pr;
+template <> struct pr<float> {
+  using P2 = float2;
+  using Rec = float4;
+  static __device__ __forceinline__ P2 mk(float a, float b) { return make_float2(a, b); }
+  static __device__ __forceinline__ P2 add(P2 a, P2 b) { return __fadd2_rn(a, b); }
+  static __device__ __forceinline__ P2 mul(P2 a, P2 b) { return __fmul2_rn(a, b); }
+  static __device__ __forceinline__ P2 fma(P2 a, P2 b, P2 c) { return __ffma2_rn(a, b, c); }
+  static __device__ __forceinline__ float inf() { return __int_as_float(0x7f800000); }
+  static constexpr int kFC = 128;                 // columns per fill
+};
+template <> struct pr<double> {
+  using P2 = double2;
+  using Rec = double4;
+  static __device__ __forceinline__ P2 mk(double a, double b) { return make_double2(a, b); }
+  static __device__ __forceinline__ P2 add(P2 a, P2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+  static __device__ __forceinline__ P2 mul(P2 a, P2 b) { return make_double2(a.x * b.x, a.y * b.y); }
+  static __device__ __forceinline__ P2 fma(P2 a, P2 b, P2 c) {
+    return make_double2(::fma(a.x, b.x, c.x), ::fma(a.y, b.y, c.y));
+  }
+  // (finite: the Newton steps of the float64 rsqrt turn inf * 0 into NaN;
+  // r2 = 3e300 gives w ~ 6e-151, times the pad's zero charge = 0, and the
+  // pad's own column sum is never stored)
+  static __device__ __forceinline__ double inf() { return 1e150; }
+  static constexpr int kFC = 64;                  // 32-byte records: the same bytes per fill
+};
+
+template <typename T>
+__device__ __forceinline__ typename pr<T>::Rec pad_col() {
+  // far-away, chargeless: r2 = inf (float64: 3e300) -> no contribution either way
+  typename pr<T>::Rec c;
+  c.x = c.y = c.z = pr<T>::inf();
+  c.w = T(0);
+  return c;
+}
+template <typename T>
+__device__ __forceinline__ void cp_async_rec(typename pr<T>::Rec* dst, const typename pr<T>::Rec* src) {
+  cp_async16(dst, src, true);
+  if (sizeof(T) == 8)
+    cp_async16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16, true);
 }
 
 // Row-only sum over staged records [0, m) for the lane's four targets (two
-// packed pairs: X0 = targets (0, 1), X1 = (2, 3)), sources j = start,
+// pairs: X0 = targets (0, 1), X1 = (2, 3)), sources j = start,
 // start + stride, ...; every record may coincide with a target (the leaf's
 // own block): r2 = 0 contributes 0.
+template <typename T>
 struct Quad {
-  float2 X0, Y0, Z0, X1, Y1, Z1;
+  typename pr<T>::P2 X0, Y0, Z0, X1, Y1, Z1;
 };
-__device__ __forceinline__ float2 inv_r2(float2 X, float2 Y, float2 Z, const float4& s) {
-  const float2 dx = __fadd2_rn(X, make_float2(-s.x, -s.x));
-  const float2 dy = __fadd2_rn(Y, make_float2(-s.y, -s.y));
-  const float2 dz = __fadd2_rn(Z, make_float2(-s.z, -s.z));
-  return __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+template <typename T>
+__device__ __forceinline__ typename pr<T>::P2 inv_r2(typename pr<T>::P2 X, typename pr<T>::P2 Y,
+                                                     typename pr<T>::P2 Z,
+                                                     const typename pr<T>::Rec& s) {
+  using O = pr<T>;
+  const auto dx = O::add(X, O::mk(-s.x, -s.x));
+  const auto dy = O::add(Y, O::mk(-s.y, -s.y));
+  const auto dz = O::add(Z, O::mk(-s.z, -s.z));
+  return O::fma(dz, dz, O::fma(dy, dy, O::mul(dx, dx)));
 }
-template <bool GUARD>
-__device__ __forceinline__ float2 rsq2f(float2 r2) {
-  float w0 = real_traits<float>::rsq(r2.x), w1 = real_traits<float>::rsq(r2.y);
+template <typename T, bool GUARD>
+__device__ __forceinline__ typename pr<T>::P2 rsq2f(typename pr<T>::P2 r2) {
+  T w0 = real_traits<T>::rsq(r2.x), w1 = real_traits<T>::rsq(r2.y);
   if (GUARD) {
-    w0 = r2.x > 0.f ? w0 : 0.f;
-    w1 = r2.y > 0.f ? w1 : 0.f;
+    w0 = r2.x > T(0) ? w0 : T(0);
+    w1 = r2.y > T(0) ? w1 : T(0);
   }
-  return make_float2(w0, w1);
+  return pr<T>::mk(w0, w1);
 }
-__device__ __forceinline__ void self_sum(const float4* buf, int m, int start, int stride,
-                                         const Quad& t, float2& acc0, float2& acc1) {
+template <typename T>
+__device__ __forceinline__ void self_sum(const typename pr<T>::Rec* buf, int m, int start,
+                                         int stride, const Quad<T>& t, typename pr<T>::P2& acc0,
+                                         typename pr<T>::P2& acc1) {
+  using O = pr<T>;
   for (int j = start; j < m; j += stride) {
-    const float4 s = buf[j];
-    const float2 q = make_float2(s.w, s.w);
-    acc0 = __ffma2_rn(rsq2f<true>(inv_r2(t.X0, t.Y0, t.Z0, s)), q, acc0);
-    acc1 = __ffma2_rn(rsq2f<true>(inv_r2(t.X1, t.Y1, t.Z1, s)), q, acc1);
+    const typename O::Rec s = buf[j];
+    const auto q = O::mk(s.w, s.w);
+    acc0 = O::fma(rsq2f<T, true>(inv_r2<T>(t.X0, t.Y0, t.Z0, s)), q, acc0);
+    acc1 = O::fma(rsq2f<T, true>(inv_r2<T>(t.X1, t.Y1, t.Z1, s)), q, acc1);
   }
 }
 
 // Rounds of 32 staged columns (f chunks of R); group grp takes chunk
 // round * f + grp.  Chunk k occupies buf[2Rk, 2Rk + 2R) (the chunk twice).
-// Per step a lane meets one column with its four targets: one 16-byte
-// shared load and two shuffles feed four interactions.
-template <int R, bool GUARD>
-__device__ __forceinline__ void mutual_rounds(const float4* buf, const int32_t* dst, int m,
-                                              int grp, int ti, const Quad& t, float2 QA0,
-                                              float2 QA1, float2& phi0, float2& phi1,
-                                              float* __restrict__ Pr, bool rmw) {
+// Per step a lane meets one column with its four targets: one record load
+// and two shuffles feed four interactions.
+template <typename T, int R, bool GUARD>
+__device__ __forceinline__ void mutual_rounds(const typename pr<T>::Rec* buf, const int32_t* dst,
+                                              int m, int grp, int ti, const Quad<T>& t,
+                                              typename pr<T>::P2 QA0, typename pr<T>::P2 QA1,
+                                              typename pr<T>::P2& phi0, typename pr<T>::P2& phi1,
+                                              T* __restrict__ Pr, bool rmw) {
+  using O = pr<T>;
   for (int c0 = 0; c0 < m; c0 += 32) {
     const int k = c0 / R + grp;                    // R is a compile-time power of two
-    const float4* p = buf + 2 * R * k + ti;
+    const typename O::Rec* p = buf + 2 * R * k + ti;
     const int col = k * R + ti;
     // a later target pass of the same leaf adds to the column sums of the
     // earlier ones: fetch them before the chain of steps
-    float* o = Pr + (col < m ? dst[col] : 0);
-    const float old = (rmw && col < m) ? __ldcg(o) : 0.f;
-    float2 psi = make_float2(0.f, 0.f);
+    T* o = Pr + (col < m ? dst[col] : 0);
+    const T old = (rmw && col < m) ? __ldcg(o) : T(0);
+    auto psi = O::mk(T(0), T(0));
 #pragma unroll
     for (int s = 0; s < R; ++s) {
-      const float4 c = p[s];
-      const float2 w0 = rsq2f<GUARD>(inv_r2(t.X0, t.Y0, t.Z0, c));
-      const float2 w1 = rsq2f<GUARD>(inv_r2(t.X1, t.Y1, t.Z1, c));
-      const float2 q = make_float2(c.w, c.w);
-      phi0 = __ffma2_rn(w0, q, phi0);
-      phi1 = __ffma2_rn(w1, q, phi1);
-      psi = __ffma2_rn(w1, QA1, __ffma2_rn(w0, QA0, psi));
+      const typename O::Rec c = p[s];
+      const auto w0 = rsq2f<T, GUARD>(inv_r2<T>(t.X0, t.Y0, t.Z0, c));
+      const auto w1 = rsq2f<T, GUARD>(inv_r2<T>(t.X1, t.Y1, t.Z1, c));
+      const auto q = O::mk(c.w, c.w);
+      phi0 = O::fma(w0, q, phi0);
+      phi1 = O::fma(w1, q, phi1);
+      psi = O::fma(w1, QA1, O::fma(w0, QA0, psi));
       if (R > 1) {
         psi.x = __shfl_sync(kFull, psi.x, ti + 1, R);
         psi.y = __shfl_sync(kFull, psi.y, ti + 1, R);
@@ -135,25 +184,31 @@ __device__ __forceinline__ void mutual_rounds(const float4* buf, const int32_t* 
 // Per-warp shared memory: two column buffers (fills of kFC columns, staged
 // twice: 2 kFC records) with their destinations, the own-leaf records and
 // the upper-segment table of the current leaf.
-constexpr int kFC = 128;
 constexpr int kSelf = 64;
+template <typename T>
 struct WarpSmem {
-  float4 col[2][2 * kFC];
+  static constexpr int kFC = pr<T>::kFC;
+  typename pr<T>::Rec col[2][2 * kFC];
   int32_t dst[2][kFC];
-  float4 self[kSelf];
+  typename pr<T>::Rec self[kSelf];
   int2 seg[32];           // (source row - first column, dst - first column) of upper segment e
   int32_t incl[32];       // inclusive end column of segment e (0-size for non-upper entries)
 };
 
-template <bool GUARD>
-__global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
-    const float* __restrict__ tx, const float* __restrict__ ty, const float* __restrict__ tz,
-    int64_t n_leaves, const float4* __restrict__ src4, int64_t npts,
+template <typename T, bool GUARD>
+__global__ void __launch_bounds__(32 * kMW, sizeof(T) == 4 ? KIFMM_MUT_MINB : KIFMM_MUT_MINB / 2)
+p2p_mutual_kernel(
+    const T* __restrict__ tx, const T* __restrict__ ty, const T* __restrict__ tz,
+    int64_t n_leaves, const typename pr<T>::Rec* __restrict__ src4, int64_t npts,
     const int32_t* __restrict__ near_off, const int4* __restrict__ near_pack,
-    const int32_t* __restrict__ order, int64_t nrhs, int64_t pstride, float* __restrict__ P) {
-  __shared__ WarpSmem sm_all[kMW];
+    const int32_t* __restrict__ order, int64_t nrhs, int64_t pstride, T* __restrict__ P) {
+  using O = pr<T>;
+  using Rec = typename O::Rec;
+  using P2 = typename O::P2;
+  constexpr int kFC = O::kFC;
+  __shared__ WarpSmem<T> sm_all[kMW];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  WarpSmem& sm = sm_all[w];
+  WarpSmem<T>& sm = sm_all[w];
   // one leaf per warp, heaviest first (order: leaves by descending work)
   const int64_t slot = (int64_t)blockIdx.x * kMW + w;
   if (slot >= n_leaves) return;
@@ -185,8 +240,8 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
     sm.incl[lane] = incl;
     __syncwarp();
     for (int64_t r = 0; r < nrhs; ++r) {
-      const float4* srow = src4 + r * npts;
-      float* Pr = P + r * pstride;
+      const Rec* srow = src4 + r * npts;
+      T* Pr = P + r * pstride;
       for (int tb = 0; tb < tc; tb += 32) {
         const int n = min(32, tc - tb);
         const int h = (n + 3) >> 2;                            // lanes per group: >= n / 4
@@ -205,7 +260,7 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
         // stage one fill of columns [k kFC, ...) into buffer k & 1: each
         // column twice (2R-record chunks), padded to whole 32-column rounds
         auto stage = [&](int k) {
-          float4* cb = sm.col[k & 1];
+          Rec* cb = sm.col[k & 1];
           int32_t* db = sm.dst[k & 1];
           const int c0 = k * kFC, m = min(kFC, ncols - c0), mp = (m + 31) & ~31;
           for (int cc = lane; cc < mp; cc += 32) {
@@ -217,12 +272,12 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
               for (int st = 16; st > 0; st >>= 1)
                 if (sm.incl[e + st - 1] <= c) e += st;
               const int2 sg = sm.seg[e];
-              cp_async16(cb + e2, srow + sg.x + c, true);
-              cp_async16(cb + e2 + R, srow + sg.x + c, true);
+              cp_async_rec<T>(cb + e2, srow + sg.x + c);
+              cp_async_rec<T>(cb + e2 + R, srow + sg.x + c);
               db[cc] = sg.y + c;
             } else {
-              cb[e2] = pad_col();
-              cb[e2 + R] = pad_col();
+              cb[e2] = pad_col<T>();
+              cb[e2 + R] = pad_col<T>();
             }
           }
           cp_async_commit();
@@ -230,32 +285,32 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
         const int nfill = (ncols + kFC - 1) / kFC;
         // own leaf (first kSelf records) and the first fill in flight together
         const int ms = min(kSelf, tc);
-        for (int k = lane; k < ms; k += 32) cp_async16(sm.self + k, srow + t0 + k, true);
+        for (int k = lane; k < ms; k += 32) cp_async_rec<T>(sm.self + k, srow + t0 + k);
         cp_async_commit();
         if (nfill) stage(0);
-        Quad tq;
-        tq.X0 = make_float2(tx[it[0]], tx[it[1]]);
-        tq.Y0 = make_float2(ty[it[0]], ty[it[1]]);
-        tq.Z0 = make_float2(tz[it[0]], tz[it[1]]);
-        tq.X1 = make_float2(tx[it[2]], tx[it[3]]);
-        tq.Y1 = make_float2(ty[it[2]], ty[it[3]]);
-        tq.Z1 = make_float2(tz[it[2]], tz[it[3]]);
-        const float2 QA0 = make_float2(live[0] ? srow[it[0]].w : 0.f, live[1] ? srow[it[1]].w : 0.f);
-        const float2 QA1 = make_float2(live[2] ? srow[it[2]].w : 0.f, live[3] ? srow[it[3]].w : 0.f);
-        float2 phi0 = make_float2(0.f, 0.f), phi1 = make_float2(0.f, 0.f);
+        Quad<T> tq;
+        tq.X0 = O::mk(tx[it[0]], tx[it[1]]);
+        tq.Y0 = O::mk(ty[it[0]], ty[it[1]]);
+        tq.Z0 = O::mk(tz[it[0]], tz[it[1]]);
+        tq.X1 = O::mk(tx[it[2]], tx[it[3]]);
+        tq.Y1 = O::mk(ty[it[2]], ty[it[3]]);
+        tq.Z1 = O::mk(tz[it[2]], tz[it[3]]);
+        const P2 QA0 = O::mk(live[0] ? srow[it[0]].w : T(0), live[1] ? srow[it[1]].w : T(0));
+        const P2 QA1 = O::mk(live[2] ? srow[it[2]].w : T(0), live[3] ? srow[it[3]].w : T(0));
+        P2 phi0 = O::mk(T(0), T(0)), phi1 = O::mk(T(0), T(0));
         // ---- own block (direct, guarded)
         if (nfill) cp_async_wait<1>();
         else cp_async_wait<0>();
         __syncwarp();
-        self_sum(sm.self, ms, grp, f, tq, phi0, phi1);
+        self_sum<T>(sm.self, ms, grp, f, tq, phi0, phi1);
         for (int j0 = kSelf; j0 < tc; j0 += kSelf) {           // large leaves: more pieces
           const int m = min(kSelf, tc - j0);
           __syncwarp();
-          for (int k = lane; k < m; k += 32) cp_async16(sm.self + k, srow + t0 + j0 + k, true);
+          for (int k = lane; k < m; k += 32) cp_async_rec<T>(sm.self + k, srow + t0 + j0 + k);
           cp_async_commit();
           cp_async_wait<0>();                                  // (also completes fill 0)
           __syncwarp();
-          self_sum(sm.self, m, grp, f, tq, phi0, phi1);
+          self_sum<T>(sm.self, m, grp, f, tq, phi0, phi1);
         }
         // ---- upper blocks: double-buffered fills
         const bool rmw = tb > 0;
@@ -267,19 +322,19 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
             cp_async_wait<0>();
           }
           __syncwarp();
-          const float4* cb = sm.col[k & 1];
+          const Rec* cb = sm.col[k & 1];
           const int32_t* db = sm.dst[k & 1];
           const int m = min(kFC, ncols - k * kFC);
           switch (lr) {
-            case 0: mutual_rounds<1, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
-            case 1: mutual_rounds<2, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
-            case 2: mutual_rounds<4, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
-            default: mutual_rounds<8, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
+            case 0: mutual_rounds<T, 1, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
+            case 1: mutual_rounds<T, 2, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
+            case 2: mutual_rounds<T, 4, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
+            default: mutual_rounds<T, 8, GUARD>(cb, db, m, grp, ti, tq, QA0, QA1, phi0, phi1, Pr, rmw); break;
           }
           __syncwarp();
         }
         // ---- row sums of the pass: combine the f groups, slot 0
-        float ph[4] = {phi0.x, phi0.y, phi1.x, phi1.y};
+        T ph[4] = {phi0.x, phi0.y, phi1.x, phi1.y};
         for (int off = R; off < 32; off <<= 1) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) ph[u] += __shfl_xor_sync(kFull, ph[u], off);
@@ -300,11 +355,12 @@ __global__ void __launch_bounds__(32 * kMW, KIFMM_MUT_MINB) p2p_mutual_kernel(
 // runs right after the mutual pass, concurrently with the far field, and the
 // final L2P pass accumulates onto it (kifmm_leaf_pass_f32, parts = 1 | 4).
 constexpr int kRW = 8;
+template <typename T>
 __global__ void __launch_bounds__(32 * kRW, 4) mutual_reduce_kernel(
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
     int64_t nrhs, const int64_t* __restrict__ perm, const int32_t* __restrict__ base,
-    const int32_t* __restrict__ nlow, int64_t pstride, const float* __restrict__ P,
-    float* __restrict__ out) {
+    const int32_t* __restrict__ nlow, int64_t pstride, const T* __restrict__ P,
+    T* __restrict__ out) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * kRW + w;
   if (b >= n_tleaves) return;
@@ -312,23 +368,52 @@ __global__ void __launch_bounds__(32 * kRW, 4) mutual_reduce_kernel(
   const int tc = tcount[b];
   const int slots = 1 + nlow[b];
   const int32_t pb0 = base[b];
-  const float c = real_traits<float>::inv4pi();
+  const T c = real_traits<T>::inv4pi();
   for (int t = lane; t < tc; t += 32) {
     const int64_t o = perm ? perm[t0 + t] : t0 + t;
     for (int64_t r = 0; r < nrhs; ++r) {
-      const float* Pr = P + r * pstride + pb0 + t;
-      float acc = 0.f;
+      const T* Pr = P + r * pstride + pb0 + t;
+      T acc = T(0);
       // slots in order, eight loads in flight at a time
       for (int s0 = 0; s0 < slots; s0 += 8) {
-        float v[8];
+        T v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = s0 + u < slots ? __ldg(Pr + (s0 + u) * tc) : 0.f;
+        for (int u = 0; u < 8; ++u) v[u] = s0 + u < slots ? __ldg(Pr + (s0 + u) * tc) : T(0);
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc += v[u];
       }
       out[o * nrhs + r] = acc * c;
     }
   }
+}
+
+template <typename T>
+int p2p_mutual(const T* tx, const T* ty, const T* tz, int64_t n_leaves, const T* src4, int64_t npts,
+               const int32_t* near_off, const int32_t* near_pack, const int32_t* order,
+               int64_t nrhs, int64_t pstride, int guard, T* P, void* stream) {
+  if (n_leaves < 0 || npts < 0 || nrhs < 1 || pstride < npts) return KIFMM_EARG;
+  if (n_leaves == 0) return 0;
+  const auto* s4 = reinterpret_cast<const typename pr<T>::Rec*>(src4);
+  const auto* pk = reinterpret_cast<const int4*>(near_pack);
+  const unsigned grid = ceil_div(n_leaves, kMW);
+  if (guard)
+    p2p_mutual_kernel<T, true><<<grid, 32 * kMW, 0, (cudaStream_t)stream>>>(
+        tx, ty, tz, n_leaves, s4, npts, near_off, pk, order, nrhs, pstride, P);
+  else
+    p2p_mutual_kernel<T, false><<<grid, 32 * kMW, 0, (cudaStream_t)stream>>>(
+        tx, ty, tz, n_leaves, s4, npts, near_off, pk, order, nrhs, pstride, P);
+  return launch_status();
+}
+
+template <typename T>
+int mutual_reduce(const int32_t* ts, const int32_t* tc, int64_t ntl, int64_t nrhs,
+                  const int64_t* perm, const int32_t* base, const int32_t* nlow, int64_t pstride,
+                  const T* P, T* out, void* stream) {
+  if (ntl < 0 || nrhs < 1) return KIFMM_EARG;
+  if (ntl == 0) return 0;
+  mutual_reduce_kernel<T><<<ceil_div(ntl, kRW), 32 * kRW, 0, (cudaStream_t)stream>>>(
+      ts, tc, ntl, nrhs, perm, base, nlow, pstride, P, out);
+  return launch_status();
 }
 
 }  // namespace
@@ -338,34 +423,32 @@ extern "C" {
 // Mutual near field into the partial-sum slots P (layout above); sources ==
 // targets, tree order.  src4: (nrhs, npts) records (x, y, z, q); near_dst[e]
 // = base_B + slot * n_B for an upper entry e of leaf A's near list (B > A),
-// unused otherwise; P: nrhs planes of pstride floats.
+// unused otherwise; P: nrhs planes of pstride elements.
 int kifmm_p2p_mutual_f32(const float* tx, const float* ty, const float* tz, int64_t n_leaves,
                          const float* src4, int64_t npts, const int32_t* near_off,
                          const int32_t* near_pack, const int32_t* order, int64_t nrhs,
                          int64_t pstride, int guard, float* P, void* stream) {
-  if (n_leaves < 0 || npts < 0 || nrhs < 1 || pstride < npts) return KIFMM_EARG;
-  if (n_leaves == 0) return 0;
-  const auto* s4 = reinterpret_cast<const float4*>(src4);
-  const auto* pk = reinterpret_cast<const int4*>(near_pack);
-  const unsigned grid = ceil_div(n_leaves, kMW);
-  if (guard)
-    p2p_mutual_kernel<true><<<grid, 32 * kMW, 0, (cudaStream_t)stream>>>(
-        tx, ty, tz, n_leaves, s4, npts, near_off, pk, order, nrhs, pstride, P);
-  else
-    p2p_mutual_kernel<false><<<grid, 32 * kMW, 0, (cudaStream_t)stream>>>(
-        tx, ty, tz, n_leaves, s4, npts, near_off, pk, order, nrhs, pstride, P);
-  return launch_status();
+  return p2p_mutual<float>(tx, ty, tz, n_leaves, src4, npts, near_off, near_pack, order, nrhs,
+                           pstride, guard, P, stream);
+}
+int kifmm_p2p_mutual_f64(const double* tx, const double* ty, const double* tz, int64_t n_leaves,
+                         const double* src4, int64_t npts, const int32_t* near_off,
+                         const int32_t* near_pack, const int32_t* order, int64_t nrhs,
+                         int64_t pstride, int guard, double* P, void* stream) {
+  return p2p_mutual<double>(tx, ty, tz, n_leaves, src4, npts, near_off, near_pack, order, nrhs,
+                            pstride, guard, P, stream);
 }
 
 // out[perm[i]] = (1/4pi) sum of i's near-field slots (slot order).
 int kifmm_p2p_mutual_reduce_f32(const int32_t* ts, const int32_t* tc, int64_t ntl, int64_t nrhs,
                                 const int64_t* perm, const int32_t* base, const int32_t* nlow,
                                 int64_t pstride, const float* P, float* out, void* stream) {
-  if (ntl < 0 || nrhs < 1) return KIFMM_EARG;
-  if (ntl == 0) return 0;
-  mutual_reduce_kernel<<<ceil_div(ntl, kRW), 32 * kRW, 0, (cudaStream_t)stream>>>(
-      ts, tc, ntl, nrhs, perm, base, nlow, pstride, P, out);
-  return launch_status();
+  return mutual_reduce<float>(ts, tc, ntl, nrhs, perm, base, nlow, pstride, P, out, stream);
+}
+int kifmm_p2p_mutual_reduce_f64(const int32_t* ts, const int32_t* tc, int64_t ntl, int64_t nrhs,
+                                const int64_t* perm, const int32_t* base, const int32_t* nlow,
+                                int64_t pstride, const double* P, double* out, void* stream) {
+  return mutual_reduce<double>(ts, tc, ntl, nrhs, perm, base, nlow, pstride, P, out, stream);
 }
 
 }  // extern "C"

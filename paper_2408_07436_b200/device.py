@@ -770,10 +770,10 @@ class DeviceFmm:
         # near-field pair is guarded against r2 == 0 (reference _hot.pyx:44-50)
         self.p2p_guard = self.sfx == "f32" and f32_cross_leaf_coincident(tt, st)
         # sources == targets (one point set): the mutual near field evaluates
-        # each pair of adjacent leaves once (csrc/p2p_mutual.cu); float32
-        # potential path (KIFMM_P2P=direct keeps the per-target-leaf pass)
+        # each pair of adjacent leaves once (csrc/p2p_mutual.cu); potential
+        # path, both precisions (KIFMM_P2P=direct keeps the per-target-leaf pass)
         self.mutual = None
-        if (self.sfx == "f32" and getattr(inst, "self_interaction", False)
+        if (getattr(inst, "self_interaction", False)
                 and os.environ.get("KIFMM_P2P", "mutual") == "mutual"
                 and np.array_equal(st.perm, tt.perm)):
             ms = mutual_slots(inst.near.offsets, inst.near.leaves, st.leaf_counts)
@@ -1079,11 +1079,11 @@ class DeviceFmm:
             if mut is not None:
                 # mutual near field into the partial-sum slots, then their
                 # per-target totals into out (caller order)
-                launch("kifmm_p2p_mutual_f32", P(self.tx), P(self.ty), P(self.tz),
+                launch(f"kifmm_p2p_mutual_{sfx}", P(self.tx), P(self.ty), P(self.tz),
                        self.n_tgt[d], P(b["src4"]), self.sx.shape[0], P(self.near_off),
                        P(mut["pack"]), P(mut["order"]), R, mut["total"], int(self.p2p_guard),
                        P(b["pmut"]), stream)
-                launch("kifmm_p2p_mutual_reduce_f32", P(self.t_start), P(self.t_count),
+                launch(f"kifmm_p2p_mutual_reduce_{sfx}", P(self.t_start), P(self.t_count),
                        self.n_tgt[d], R, P(self.t_perm), P(mut["base"]), P(mut["nlow"]),
                        mut["total"], P(b["pmut"]), P(out), stream)
             else:

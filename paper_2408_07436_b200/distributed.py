@@ -502,11 +502,11 @@ class DistributedFmm:
                 return
             if self.mut_order is not None:
                 mut = d.mutual
-                launch("kifmm_p2p_mutual_f32", P(d.tx), P(d.ty), P(d.tz),
+                launch(f"kifmm_p2p_mutual_{sfx}", P(d.tx), P(d.ty), P(d.tz),
                        int(self.mut_order.numel()), P(b["src4"]), npts, P(d.near_off),
                        P(mut["pack"]), P(self.mut_order), R, mut["total"], int(d.p2p_guard),
                        P(b["pmut"]), stream)
-                launch("kifmm_p2p_mutual_reduce_f32", P(d.t_start) + 4 * tlo,
+                launch(f"kifmm_p2p_mutual_reduce_{sfx}", P(d.t_start) + 4 * tlo,
                        P(d.t_count) + 4 * tlo, thi - tlo, R, None, P(mut["base"]) + 4 * tlo,
                        P(mut["nlow"]) + 4 * tlo, mut["total"], P(b["pmut"]), out_base, stream)
             else:

@@ -691,6 +691,34 @@ def test_mutual_near_field(cuda, monkeypatch, n, depth, nrhs, clustered, merge):
         assert parity_report(res["mutual"], want)["max_rel"] <= TOL["f32"]
 
 
+@pytest.mark.parametrize("backend,n,depth,nrhs,clustered", [
+    ("fft", 60000, 4, 1, False), ("blas", 40000, 4, 2, True)])
+def test_mutual_near_field_float64(cuda, monkeypatch, backend, n, depth, nrhs, clustered):
+    """The float64 instantiation of the mutual near field (FP64 pipe, two
+    scalar pairs per lane) against the per-target-leaf pass and the oracle."""
+    from oracle import port
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(33)
+    pts = rng.random((n, 3))
+    if clustered:
+        pts = pts ** 3
+    q = rng.standard_normal((n, nrhs)) if nrhs > 1 else rng.random(n)
+    kw = dict(depth=depth, order_equiv=4, backend=backend, precision="f64", sigma_min=1e-10)
+    res = {}
+    for mode in ("direct", "mutual"):
+        monkeypatch.setenv("KIFMM_P2P", mode)
+        inst = setup(pts, pts, FmmConfig(**kw))
+        assert (inst.device.mutual is not None) == (mode == "mutual")
+        assert not inst.device.p2p_guard
+        res[mode] = np.asarray(inst.evaluate(q), dtype=np.float64)
+        if mode == "mutual":
+            assert np.array_equal(res[mode], inst.evaluate(q))        # deterministic
+            want = port.evaluate(inst, q)
+            assert parity_report(res[mode].reshape(want.shape), want)["floored"] <= TOL["f64"]
+    scale = np.abs(res["direct"]).max()
+    assert np.abs(res["mutual"] - res["direct"]).max() <= 1e-12 * scale
+
+
 def test_operator_timings_filled_by_default(cuda):
     """inst.timings carries the reference's six operator timers after every
     evaluate (engine.py:289-399, 454-459), from events inside the graph."""
