@@ -31,7 +31,13 @@ __device__ __forceinline__ void cfma(C& acc, C a, C b) {
   acc.y += a.x * b.y + a.y * b.x;
 }
 
-constexpr int kThreads = 256;
+#ifndef KIFMM_FFT_THREADS
+#define KIFMM_FFT_THREADS 512
+#endif
+#ifndef KIFMM_FFT_MAXBPC
+#define KIFMM_FFT_MAXBPC 8
+#endif
+constexpr int kThreads = KIFMM_FFT_THREADS;
 constexpr int kMaxP = 12;
 
 // Surface lattice of the p^3 cube in lexicographic order -> flat index
@@ -60,11 +66,17 @@ __device__ void build_lattice(int p, int* lat) {
 // read is (row base + immediate).
 template <typename T>
 __device__ void build_twiddles(int n, typename cx<T>::v* tw) {
+  // the n roots once (row k = 1 of the table), then the table by index: one
+  // sincospi per root instead of one per entry
+  for (int m = threadIdx.x; m < n; m += blockDim.x) {
+    double s, c;
+    sincospi(2.0 * m / n, &s, &c);
+    tw[n + m] = typename cx<T>::v{(T)c, (T)(-s)};
+  }
+  __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int k = e / n, m = e % n;
-    double s, c;
-    sincospi(2.0 * ((k * m) % n) / n, &s, &c);
-    tw[e] = typename cx<T>::v{(T)c, (T)(-s)};
+    if (k != 1) tw[e] = tw[n + (k * m) % n];
   }
 }
 
@@ -131,7 +143,7 @@ __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restri
 #pragma unroll
     for (int i2 = 0; i2 < P; ++i2) line[i2] = CUBE(b)[i01 * P + i2];
     C* out = X1(b) + i01 * NH;
-#pragma unroll 1
+#pragma unroll 2
     for (int k2 = 0; k2 < NH; ++k2) {
       const C* w = tw + k2 * N + P;
       C acc{0, 0};
@@ -151,7 +163,7 @@ __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restri
     C in[P];
 #pragma unroll
     for (int i1 = 0; i1 < P; ++i1) in[i1] = X1(b)[(i0 * P + i1) * NH + k2];
-#pragma unroll 1
+#pragma unroll 2
     for (int k1 = 0; k1 < N; ++k1) {
       const C* w = tw + k1 * N + P;
       C acc{0, 0};
@@ -169,7 +181,7 @@ __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restri
     for (int i0 = 0; i0 < P; ++i0) in[i0] = X2(b)[i0 * N * NH + k12];
     C* dst = qhat + (((int64_t)k12 * nsc + cluster) * 8 + child0 + b) * nrhs + r;
     const int64_t fstride = (int64_t)N * NH * nsc * 8 * nrhs;
-#pragma unroll 1
+#pragma unroll 2
     for (int k0 = 0; k0 < N; ++k0) {
       const C* w = tw + k0 * N + P;
       C acc{0, 0};
@@ -211,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) fft_inverse_kernel(const typename cx
     C in[N];
 #pragma unroll
     for (int k0 = 0; k0 < N; ++k0) in[k0] = src[k0 * fstride];
-#pragma unroll 1
+#pragma unroll 2
     for (int i0 = 0; i0 < P; ++i0) {
       C acc{0, 0};
 #pragma unroll
@@ -231,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) fft_inverse_kernel(const typename cx
     C in[N];
 #pragma unroll
     for (int k1 = 0; k1 < N; ++k1) in[k1] = Y1(b)[(i0 * N + k1) * NH + k2];
-#pragma unroll 1
+#pragma unroll 2
     for (int i1 = 0; i1 < P; ++i1) {
       C acc{0, 0};
 #pragma unroll
@@ -272,7 +284,7 @@ size_t inverse_smem(int bpc) { return FftShape<T, P>::head + bpc * FftShape<T, P
 
 // Boxes per CTA: the largest of 8/4/2/1 whose scratch fits.
 int pick_bpc(size_t (*smem)(int), size_t limit) {
-  for (int bpc = 8; bpc >= 1; bpc /= 2)
+  for (int bpc = KIFMM_FFT_MAXBPC; bpc >= 1; bpc /= 2)
     if (smem(bpc) <= limit) return bpc;
   return 0;
 }
