@@ -31,13 +31,9 @@ __device__ __forceinline__ void cfma(C& acc, C a, C b) {
   acc.y += a.x * b.y + a.y * b.x;
 }
 
-#ifndef KIFMM_FFT_THREADS
-#define KIFMM_FFT_THREADS 512
-#endif
-#ifndef KIFMM_FFT_MAXBPC
-#define KIFMM_FFT_MAXBPC 8
-#endif
-constexpr int kThreads = KIFMM_FFT_THREADS;
+// 512 threads per CTA (config 3 level 5: forward 670 us; 256: 1000 us, 1024
+// spills: 700 / 1160 us; 4 or 2 boxes per CTA for more CTAs per SM: slower)
+constexpr int kThreads = 512;
 constexpr int kMaxP = 12;
 
 // Surface lattice of the p^3 cube in lexicographic order -> flat index
@@ -284,7 +280,7 @@ size_t inverse_smem(int bpc) { return FftShape<T, P>::head + bpc * FftShape<T, P
 
 // Boxes per CTA: the largest of 8/4/2/1 whose scratch fits.
 int pick_bpc(size_t (*smem)(int), size_t limit) {
-  for (int bpc = KIFMM_FFT_MAXBPC; bpc >= 1; bpc /= 2)
+  for (int bpc = 8; bpc >= 1; bpc /= 2)
     if (smem(bpc) <= limit) return bpc;
   return 0;
 }

@@ -26,14 +26,17 @@
 //
 // Persistent: gridDim.x CTAs (one per SM) walk the work items (rhs, tile,
 // vector split) round-robin through a ring of NS stages (source block + core
-// pair, 53 KB at KP = 56).  Roles (288 threads): warp 0 lane 0 loads the
-// stages; warps 1..4 and 5..8 are two groups taking alternate vectors: each
-// loads, splits and stores its source rows into its own TMEM A buffer,
-// issues its own MMAs (one elected thread) into its own TMEM accumulator,
-// promotes it into registers every FLUSH_V of its vectors; at the end of an
+// pair, 53 KB at KP = 56).  Roles (352 threads): warp 0 lane 0 loads the
+// stages; warps 1..4 and 5..8 are two loader groups taking alternate vectors:
+// each loads, splits and stores its source rows into its own TMEM A buffer
+// and hands the vector to its issuer warp (warps 9, 10: one thread issues the
+// group's MMAs into the group's own TMEM accumulator), and promotes the
+// accumulator into registers every FLUSH_V of its vectors; at the end of an
 // item the two partial sums are combined through shared memory and group 0
 // writes the result.  Groups never share a TMEM accumulator, so no MMA
-// ordering between issuing threads is needed.
+// ordering between the issuing threads is needed - and the two groups'
+// dependent MMA chains interleave on the tensor pipe, which hides the
+// accumulate-to-accumulate latency of either (profiles/r2/sweep_bounds.md).
 #include <cuda.h>
 
 #include <cstdlib>
@@ -47,11 +50,7 @@ namespace {
 
 constexpr int TMT = 128;
 constexpr int NG = 2;             // groups per CTA (alternate vectors), each with its own TMEM A and D
-#ifndef KIFMM_TMEM_ISSUER
-#define KIFMM_TMEM_ISSUER 1      // 1: one dedicated MMA-issuing warp per group; 0: the group's first thread issues
-#endif
-constexpr bool ISSUER_WARPS = KIFMM_TMEM_ISSUER != 0;
-constexpr int NTHREADS = 32 + 128 * NG + (ISSUER_WARPS ? 32 * NG : 0);
+constexpr int NTHREADS = 32 + 128 * NG + 32 * NG;   // producer, loader groups, issuer warps
 #ifndef KIFMM_TMEM_FLUSH
 #define KIFMM_TMEM_FLUSH 8
 #endif
@@ -302,7 +301,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
     const int q4 = warp & 3;                       // TMEM lane quarter of this warp
     const int m = q4 * 32 + lane;                  // tile row = TMEM lane
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-    const bool issuer = (warp == 1 + 4 * grp) && lane == 0;
     const uint32_t dcol = tmem + (uint32_t)(grp * GCOLS);
     const uint32_t acol = dcol + N1;
     constexpr uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N1 >> 3) << 17) |
@@ -366,30 +364,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         if (m == 0 && grp == 0) trace(7, gg);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        if (ISSUER_WARPS) {
-          // hand the vector over to the group's issuer warp and go on to the
-          // next source block (the issuing thread waits on the tensor pipe
-          // for ~1100 clk per vector: as a loader thread it held its warp -
-          // and through the group barrier the whole group - back)
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&aready[grp]))
-                       : "memory");
-        } else {
-          asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
-          if (issuer) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (grp == 0) trace(3, gg);
-            const uint32_t bb = smem_u32(smem + s * SBYTES + ABYTES);
-#pragma unroll
-            for (int ks = 0; ks < KP / 8; ++ks) {
-              const uint64_t db = desc_nosw(bb + ks * 256, 128, SBO);
-              mma_tf32_ts(dcol, acol + ks * 8, db, idesc1, local | ks);
-              mma_tf32_ts(dcol, acol + KP + ks * 8, db, idesc2, 1);
-            }
-            mma_commit(&done[grp]);
-            mma_commit(&empty[s]);
-            if (grp == 0) trace(9, gg);
-          }
-        }
+        // hand the vector over to the group's issuer warp and go on to the
+        // next source block (the issuing thread waits on the tensor pipe for
+        // ~1100 clk per vector: as a loader thread it held its warp - and
+        // through a group barrier the whole group - back)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&aready[grp]))
+                     : "memory");
         __syncwarp();
         ++nmine;
         const bool last_of_block = local == FLUSH_V - 1 || v + NG >= x.nv;
@@ -452,7 +432,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_sweep_tmem_kernel(
       g += x.nv;
     }
   }
-  else if (ISSUER_WARPS && warp >= 1 + 4 * NG) {
+  else if (warp >= 1 + 4 * NG) {
     // ------- issuer warp of group k: per vector of the group, wait for the
     // loaders' A, issue the MMAs into D_k, commit (A_k / D_k free, stage free)
     const int grp = warp - (1 + 4 * NG);

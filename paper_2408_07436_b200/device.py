@@ -611,8 +611,8 @@ class BlasDevice:
         return int(out.value)
 
     def run_level_tma(self, plan, mult, n_s, n_t, nrhs, level_scale, qt, dense, acc, solve,
-                      check=None, after_projection=None, coarse_ctas=0, rows=None,
-                      projected=False, after_sweep=None):
+                      check=None, coarse_ctas=0, rows=None, projected=False,
+                      after_sweep=None):
         """Engine path for float32: projection -> dense sub-lattice array ->
         tcgen05 sweep (A in tensor memory, or TMA-staged hi/lo planes) ->
         fused epilogue into the locals.
@@ -634,16 +634,13 @@ class BlasDevice:
             if not projected:
                 la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin,
                         dense[0], self.kin, rowmap=dense_rowmap(plan, nrhs))
-            if after_projection is not None:
-                after_projection()
             launch("kifmm_m2l_sweep_tmem_f32", P(dense[0]), P(self.Bpair), self.kin, plan["h"],
                    P(plan["tile_targets"]), P(plan["tile_ids"]), plan["n_tiles"],
                    P(plan["pairs"]), plan["n_pairs"], P(self.class_tv_local), P(self.offsets),
                    nrhs, nsplit, self.ko_pad, P(acc), stream_handle())
         else:
             nsplit = sweep_splits(plan["n_tiles"], 1)
-            self._run_tma(plan, mult, n_s, nrhs, qt, dense, acc, nsplit,
-                          after_projection=after_projection)
+            self._run_tma(plan, mult, n_s, nrhs, qt, dense, acc, nsplit)
         if after_sweep is not None:
             after_sweep()
         if solve is None:
@@ -663,11 +660,9 @@ class BlasDevice:
                  asum=nsplit, astride=self.ko_pad)
         return 4
 
-    def _run_tma(self, plan, mult, n_s, nrhs, qt, dense, acc, nsplit, after_projection=None):
+    def _run_tma(self, plan, mult, n_s, nrhs, qt, dense, acc, nsplit):
         la = self.la
         la.gemm(n_s * nrhs, self.kin, self.n_e, 1.0, mult, self.n_e, self.S, self.kin, qt, self.kin)
-        if after_projection is not None:
-            after_projection()
         hi, lo = dense
         # TF32 hi/lo planes split here (splitting raw fp32 q~ in the sweep's
         # shared memory halves the TMA bytes for A but measured slower on
@@ -737,9 +732,9 @@ class DeviceFmm:
         self.n_e, self.n_c = exp.n_equiv, exp.n_check
         # near field concurrent with the far field (see evaluate_device)
         self.overlap = os.environ.get("KIFMM_OVERLAP", "1") != "0"
-        self.p2p_fork = os.environ.get("KIFMM_P2P_FORK", "sweep_end")
-        self.coarse_ctas = int(os.environ.get("KIFMM_COARSE_CTAS", "32"))
-        self.fuse_p2m = os.environ.get("KIFMM_FUSE_P2M", "1") != "0"
+        # persistent CTAs of a coarse level's sweep in the overlapped evaluate
+        # (measured: 32; all SMs keeps the near field off the whole machine)
+        self.coarse_ctas = 32
         least, greatest = torch.cuda.Stream.priority_range()
         self.side_stream = torch.cuda.Stream(priority=least)
         self.hi_stream = torch.cuda.Stream(priority=greatest)
@@ -837,8 +832,8 @@ class DeviceFmm:
             self.tma_plan = {l: tma_level_plan(st.level_keys(l), tt.level_keys(l), l)
                              for l in plans}
 
-    def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None, after_projection=None,
-                       coarse_ctas=0, projected=False, after_sweep=None):
+    def m2l_blas_level(self, lvl, mult, nrhs, check, solve=None, coarse_ctas=0,
+                       projected=False, after_sweep=None):
         """Each level has its own scratch (qt, acc): levels run concurrently
         in the overlapped evaluate."""
         b = self._buffers(nrhs)
@@ -847,8 +842,8 @@ class DeviceFmm:
             plan = self.tma_plan[lvl]
             return self.blas.run_level_tma(plan, mult, self.n_src[lvl], self.n_tgt[lvl], nrhs,
                                            1.0 / self.side[lvl], qt, b["dense"][lvl], acc, solve,
-                                           check=check, after_projection=after_projection,
-                                           coarse_ctas=coarse_ctas, projected=projected,
+                                           check=check, coarse_ctas=coarse_ctas,
+                                           projected=projected,
                                            after_sweep=after_sweep)
         return self.blas.run_level(self.blas_plan_dev[lvl], mult, self.n_src[lvl],
                                    self.n_tgt[lvl], nrhs, 1.0 / self.side[lvl], check, qt, acc,
@@ -1110,7 +1105,7 @@ class DeviceFmm:
         # float32, narrow operators (p <= 4), tensor-memory sweep: the solve and
         # the leaf level's M2L projection in one fused row chain (one launch
         # instead of three latency-bound GEMMs in front of the finest sweep)
-        fused_p2m = (self.fuse_p2m and sfx == "f32" and self.cfg.backend == "blas" and self.tma
+        fused_p2m = (sfx == "f32" and self.cfg.backend == "blas" and self.tma
                      and self.blas.tmem and d >= 3 and max(n_c, n_e, self.blas.kin) <= 64)
         if fused_p2m:
             u, vals, vt = self.up_inv
@@ -1133,13 +1128,13 @@ class DeviceFmm:
         # (engine.py:355, 370) and saves one solve per level.
         rf = self.r_fold
 
-        def m2l(lvl, after_projection=None, after_sweep=None):
+        def m2l(lvl, after_sweep=None):
             # t_l = check_l . U_dn (rank rf) from the level's M2L
             n_t = self.n_tgt[lvl]
             t_l = b["t_lv"][lvl][: n_t * R * rf]
             if self.cfg.backend == "blas" and self.tma:
                 calls[lvl] = self.m2l_blas_level(
-                    lvl, mult[lvl], R, t_l, after_projection=after_projection,
+                    lvl, mult[lvl], R, t_l,
                     coarse_ctas=self.coarse_ctas if overlap and lvl < d else 0,
                     projected=fused_p2m and lvl == d, after_sweep=after_sweep)
                 return
@@ -1165,12 +1160,12 @@ class DeviceFmm:
         main = torch.cuda.current_stream()
         forked = {}
 
-        def fork_m2l(lvl, after_projection=None, after_sweep=None):
+        def fork_m2l(lvl, after_sweep=None):
             st = self.level_streams[lvl]
             st.wait_stream(main)
             with torch.cuda.stream(st):
                 mark("m2l")
-                m2l(lvl, after_projection, after_sweep)
+                m2l(lvl, after_sweep)
                 mark("m2l")
             forked[lvl] = st
 
@@ -1191,11 +1186,7 @@ class DeviceFmm:
         # near field (277) + L2P (52) = 689 us is the floor of the DAG.
         p2p_forked = False
         if overlap and d >= 3:
-            if self.cfg.backend == "blas" and self.tma and self.p2p_fork == "sweep":
-                fork_m2l(d, after_projection=fork_p2p)
-                p2p_forked = True
-            elif self.cfg.backend == "blas" and self.tma and self.p2p_fork == "sweep_end":
-                # experiment: the near field strictly behind the finest sweep
+            if self.cfg.backend == "blas" and self.tma:
                 fork_m2l(d, after_sweep=fork_p2p)
                 p2p_forked = True
             else:

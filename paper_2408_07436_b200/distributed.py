@@ -517,20 +517,20 @@ class DistributedFmm:
             with torch.cuda.stream(side):
                 p2p_pass(side.cuda_stream)
 
-        def m2l(lvl, after_projection=None):
+        def m2l(lvl, after_sweep=None):
             """t_l = check_l . U_dn on the owned target rows of the level."""
             lo_, hi_ = tr[lvl]
             n_t = d.n_tgt[lvl]
             t_l = b["t_lv"][lvl]
             scale = 1.0 / d.side[lvl]
             if hi_ <= lo_:
-                if after_projection is not None:
-                    after_projection()
+                if after_sweep is not None:
+                    after_sweep()
                 return
             if self.inst.config.backend == "blas" and d.tma:
                 d.blas.run_level_tma(self.tma_plan[lvl], mult[lvl], d.n_src[lvl], n_t, R, scale,
                                      b["qt_lv"][lvl], b["dense"][lvl], rb["acc"][lvl], None,
-                                     check=t_l, after_projection=after_projection,
+                                     check=t_l, after_sweep=after_sweep,
                                      rows=(lo_, hi_))
                 return
             check = b["phi_lv"][lvl]
@@ -539,8 +539,8 @@ class DistributedFmm:
                                       R, scale, check, b["qt_lv"][lvl], rb["acc"][lvl])
             else:
                 self._fft_level(lvl, mult[lvl], R, check)
-            if after_projection is not None:
-                after_projection()
+            if after_sweep is not None:
+                after_sweep()
             la.gemm((hi_ - lo_) * R, rf, n_c, 1.0, Off(check, lo_ * R * n_c), n_c, d.dn_u, rf,
                     Off(t_l, lo_ * R * rf), rf)
 
@@ -552,19 +552,19 @@ class DistributedFmm:
 
         forked = {}
 
-        def fork_m2l(lvl, after_projection=None, wait=()):
+        def fork_m2l(lvl, after_sweep=None, wait=()):
             st = d.level_streams[lvl]
             st.wait_stream(main)
             for w in wait:
                 st.wait_stream(w)
             with torch.cuda.stream(st):
-                m2l(lvl, after_projection)
+                m2l(lvl, after_sweep)
             forked[lvl] = st
 
         # the leaf level's M2L waits for its ghosts; the near field is
-        # released behind its projection (as in the single-device evaluate)
+        # released behind its sweep (as in the single-device evaluate)
         if depth >= 3:
-            fork_m2l(depth, after_projection=fork_p2p,
+            fork_m2l(depth, after_sweep=fork_p2p,
                      wait=(comm,) if self.halo is not None else ())
         # ---- M2M of the owned subtrees
         for lvl in range(depth, 2, -1):
