@@ -360,6 +360,27 @@ int kifmm_p2p_mutual_reduce_f64(const int32_t* tleaf_start, const int32_t* tleaf
                                 int64_t n_tleaves, int64_t nrhs, const int64_t* perm,
                                 const int32_t* base, const int32_t* nlow, int64_t pstride,
                                 const double* P, double* out, void* stream);
+/* Potential + gradient variants (BASELINE config 3 asks for both; the reference
+ * is potential-only): P holds four component planes per right-hand side
+ * (potential, d/dx, d/dy, d/dz: P[(r*4 + c)*pstride + slot]); grad is
+ * (target, rhs, 3) in the caller's order, like kifmm_leaf_pass_grad_*. */
+int kifmm_p2p_mutual_grad_f32(const float* tx, const float* ty, const float* tz, int64_t n_leaves,
+                              const float* src4, int64_t npts, const int32_t* near_off,
+                              const int32_t* near_pack, const int32_t* order, int64_t nrhs,
+                              int64_t pstride, int guard, float* P, void* stream);
+int kifmm_p2p_mutual_grad_f64(const double* tx, const double* ty, const double* tz,
+                              int64_t n_leaves, const double* src4, int64_t npts,
+                              const int32_t* near_off, const int32_t* near_pack,
+                              const int32_t* order, int64_t nrhs, int64_t pstride, int guard,
+                              double* P, void* stream);
+int kifmm_p2p_mutual_reduce_grad_f32(const int32_t* tleaf_start, const int32_t* tleaf_count,
+                                     int64_t n_tleaves, int64_t nrhs, const int64_t* perm,
+                                     const int32_t* base, const int32_t* nlow, int64_t pstride,
+                                     const float* P, float* out, float* grad, void* stream);
+int kifmm_p2p_mutual_reduce_grad_f64(const int32_t* tleaf_start, const int32_t* tleaf_count,
+                                     int64_t n_tleaves, int64_t nrhs, const int64_t* perm,
+                                     const int32_t* base, const int32_t* nlow, int64_t pstride,
+                                     const double* P, double* out, double* grad, void* stream);
 
 /* Leaf pass: fused L2P + P2P + un-permute (engine.py:377-404).  For target
  * leaf b and target i in it:

@@ -97,6 +97,10 @@ SIGNATURES = {
     "kifmm_p2p_mutual_f64": [_P, _P, _P, _I, _P, _I, _P, _P, _P, _I, _I, _C, _P, _P],
     "kifmm_p2p_mutual_reduce_f32": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P],
     "kifmm_p2p_mutual_reduce_f64": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P],
+    "kifmm_p2p_mutual_grad_f32": [_P, _P, _P, _I, _P, _I, _P, _P, _P, _I, _I, _C, _P, _P],
+    "kifmm_p2p_mutual_grad_f64": [_P, _P, _P, _I, _P, _I, _P, _P, _P, _I, _I, _C, _P, _P],
+    "kifmm_p2p_mutual_reduce_grad_f32": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P],
+    "kifmm_p2p_mutual_reduce_grad_f64": [_P, _P, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P],
     "kifmm_sm_target": [],
     "kifmm_probe": [_C, _I, _I, _I, _P, _P],
 }

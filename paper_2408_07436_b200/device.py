@@ -1068,19 +1068,23 @@ class DeviceFmm:
                     P(self.s_count), P(self.near_off), P(self.near_leaf), R, P(self.t_perm),
                     parts | guard_bit, P(out)] + grad_ptr
 
-        mut = self.mutual if not gradient else None
+        mut = self.mutual
+        if mut is not None and gradient and "pmut4" not in b:
+            b["pmut4"] = self._alloc(max(mut["total"], 1) * R * 4, self.T)
 
         def p2p_pass(stream):
             if mut is not None:
                 # mutual near field into the partial-sum slots, then their
                 # per-target totals into out (caller order)
-                launch(f"kifmm_p2p_mutual_{sfx}", P(self.tx), P(self.ty), P(self.tz),
+                g_ = "grad_" if gradient else ""
+                pm = b["pmut4"] if gradient else b["pmut"]
+                launch(f"kifmm_p2p_mutual_{g_}{sfx}", P(self.tx), P(self.ty), P(self.tz),
                        self.n_tgt[d], P(b["src4"]), self.sx.shape[0], P(self.near_off),
                        P(mut["pack"]), P(mut["order"]), R, mut["total"], int(self.p2p_guard),
-                       P(b["pmut"]), stream)
-                launch(f"kifmm_p2p_mutual_reduce_{sfx}", P(self.t_start), P(self.t_count),
+                       P(pm), stream)
+                launch(f"kifmm_p2p_mutual_reduce_{g_}{sfx}", P(self.t_start), P(self.t_count),
                        self.n_tgt[d], R, P(self.t_perm), P(mut["base"]), P(mut["nlow"]),
-                       mut["total"], P(b["pmut"]), P(out), stream)
+                       mut["total"], P(pm), P(out), *grad_ptr, stream)
             else:
                 launch(leaf_name, *leaf_args(2), stream)             # P2P, overwrite
 

@@ -719,6 +719,40 @@ def test_mutual_near_field_float64(cuda, monkeypatch, backend, n, depth, nrhs, c
     assert np.abs(res["mutual"] - res["direct"]).max() <= 1e-12 * scale
 
 
+@pytest.mark.parametrize("precision,nrhs,clustered", [("f32", 1, False), ("f64", 2, True)])
+def test_mutual_near_field_gradient(cuda, monkeypatch, precision, nrhs, clustered):
+    """Potential + gradient with the mutual near field (each adjacent leaf
+    pair once: row sums -G, column sums +H per component) against the
+    per-target-leaf gradient pass, and the potentials against the
+    potential-only evaluate."""
+    from paper_2408_07436_b200 import FmmConfig, setup
+    rng = np.random.default_rng(35)
+    n = 40000
+    pts = rng.random((n, 3))
+    if clustered:
+        pts = pts ** 3
+    q = rng.standard_normal((n, nrhs)) if nrhs > 1 else rng.random(n)
+    kw = dict(depth=4, order_equiv=4, backend="fft", precision=precision)
+    res = {}
+    for mode in ("direct", "mutual"):
+        monkeypatch.setenv("KIFMM_P2P", mode)
+        inst = setup(pts, pts, FmmConfig(**kw))
+        phi, grad = inst.evaluate(q, gradient=True)
+        res[mode] = (np.asarray(phi, np.float64), np.asarray(grad, np.float64))
+        if mode == "mutual":
+            assert inst.device.mutual is not None
+            phi2, grad2 = inst.evaluate(q, gradient=True)
+            assert np.array_equal(phi, phi2) and np.array_equal(grad, grad2)
+            # (the L2P part of the gradient pass sums in another order)
+            ptol = 1e-6 if precision == "f32" else 1e-13
+            assert np.allclose(np.asarray(inst.evaluate(q)), np.asarray(phi), rtol=ptol,
+                               atol=ptol * np.abs(phi).max())
+    tol = 2e-5 if precision == "f32" else 1e-11
+    for a, b in zip(res["mutual"], res["direct"]):
+        assert a.shape == b.shape
+        assert np.abs(a - b).max() <= tol * np.abs(b).max()
+
+
 def test_operator_timings_filled_by_default(cuda):
     """inst.timings carries the reference's six operator timers after every
     evaluate (engine.py:289-399, 454-459), from events inside the graph."""
