@@ -425,6 +425,16 @@ int kifmm_leaf_pass_grad_f64(const double* tx, const double* ty, const double* t
                              const int64_t* perm, int parts, double* out, double* grad,
                              void* stream);
 
+/* Charge intake in one pass (engine.py:283-287: charges to tree order and the
+ * working type) fused with the source pack below: qt[i*nrhs + r] =
+ * (T) q_in[perm[i]*nrhs + r], src4[(r*n + i)*4 ..] = (x_i, y_i, z_i, q). */
+int kifmm_gather_pack_f32(const double* q_in, const int64_t* perm, const float* sx,
+                          const float* sy, const float* sz, int64_t n, int64_t nrhs, float* qt,
+                          float* src4, void* stream);
+int kifmm_gather_pack_f64(const double* q_in, const int64_t* perm, const double* sx,
+                          const double* sy, const double* sz, int64_t n, int64_t nrhs, double* qt,
+                          double* src4, void* stream);
+
 /* AoS source records for the leaf pass (16/32-byte aligned):
  * src4[(r*ns + j)*4 + {0,1,2,3}] = (x_j, y_j, z_j, q[j*nrhs + r]). */
 int kifmm_pack_sources_f32(const float* sx, const float* sy, const float* sz, const float* q,

@@ -78,6 +78,8 @@ SIGNATURES = {
                                  _P, _I, _P, _C, _P, _P, _P],
     "kifmm_pack_sources_f32": [_P, _P, _P, _P, _I, _I, _P, _P],
     "kifmm_pack_sources_f64": [_P, _P, _P, _P, _I, _I, _P, _P],
+    "kifmm_gather_pack_f32": [_P, _P, _P, _P, _P, _I, _I, _P, _P, _P],
+    "kifmm_gather_pack_f64": [_P, _P, _P, _P, _P, _I, _I, _P, _P, _P],
     "kifmm_gather_charges_f32": [_P, _P, _I, _I, _P, _P],
     "kifmm_gather_charges_f64": [_P, _P, _I, _I, _P, _P],
     "kifmm_split_tf32": [_P, _I, _P, _P, _P],

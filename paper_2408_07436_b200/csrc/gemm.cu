@@ -469,6 +469,39 @@ __global__ void gather_charges_kernel(const double* __restrict__ qin,
   qt[idx] = (T)qin[perm[i] * nrhs + r];
 }
 
+// Charge intake in one pass: qt[i*nrhs + r] = (T) qin[perm[i]*nrhs + r] (caller
+// order, float64 -> tree order, working type) and the packed source record
+// src4[r*n + i] = (x_i, y_i, z_i, q).  Four points per thread, a block-stride
+// apart: four independent gather chains in flight (the permuted read is
+// latency-bound) with every access still coalesced across the warp.
+template <typename T, typename V4>
+__global__ void __launch_bounds__(256) gather_pack_kernel(
+    const double* __restrict__ qin, const int64_t* __restrict__ perm, const T* __restrict__ sx,
+    const T* __restrict__ sy, const T* __restrict__ sz, int64_t n, int64_t nrhs,
+    T* __restrict__ qt, V4* __restrict__ src4) {
+  const int64_t base = (int64_t)blockIdx.x * (4 * 256) + threadIdx.x;
+  int64_t pi[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t i = base + u * 256;
+    pi[u] = i < n ? perm[i] : 0;
+  }
+  for (int64_t r = 0; r < nrhs; ++r) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = base + u * 256 < n ? qin[pi[u] * nrhs + r] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = base + u * 256;
+      if (i < n) {
+        const T qv = (T)v[u];
+        qt[i * nrhs + r] = qv;
+        src4[r * n + i] = V4{sx[i], sy[i], sz[i], qv};
+      }
+    }
+  }
+}
+
 // Row gather/scatter of width-element rows (multipole halo pack/unpack).
 template <typename T>
 __global__ void rows_kernel(const T* __restrict__ src, const int32_t* __restrict__ rows,
@@ -587,6 +620,24 @@ int kifmm_stack_children_f32(const float* mult, const int32_t* child, int64_t n_
 int kifmm_stack_children_f64(const double* mult, const int32_t* child, int64_t n_par,
                              int64_t nrhs, int64_t ne, double* out, void* s) {
   return stack<double>(mult, child, n_par, nrhs, ne, out, s);
+}
+int kifmm_gather_pack_f32(const double* qin, const int64_t* perm, const float* sx, const float* sy,
+                          const float* sz, int64_t n, int64_t nrhs, float* qt, float* src4,
+                          void* s) {
+  if (n < 0 || nrhs < 1) return KIFMM_EARG;
+  if (n == 0) return 0;
+  gather_pack_kernel<float, float4><<<ceil_div(n, 4 * 256), 256, 0, (cudaStream_t)s>>>(
+      qin, perm, sx, sy, sz, n, nrhs, qt, reinterpret_cast<float4*>(src4));
+  return launch_status();
+}
+int kifmm_gather_pack_f64(const double* qin, const int64_t* perm, const double* sx,
+                          const double* sy, const double* sz, int64_t n, int64_t nrhs, double* qt,
+                          double* src4, void* s) {
+  if (n < 0 || nrhs < 1) return KIFMM_EARG;
+  if (n == 0) return 0;
+  gather_pack_kernel<double, double4><<<ceil_div(n, 4 * 256), 256, 0, (cudaStream_t)s>>>(
+      qin, perm, sx, sy, sz, n, nrhs, qt, reinterpret_cast<double4*>(src4));
+  return launch_status();
 }
 int kifmm_gather_charges_f32(const double* qin, const int64_t* perm, int64_t n, int64_t nrhs,
                              float* qt, void* s) {

@@ -1040,10 +1040,8 @@ class DeviceFmm:
         phase("p2m")
         mark("p2m")
         q = b["q"]
-        launch(f"kifmm_gather_charges_{sfx}", P(q_dev), P(self.s_perm), self.sx.shape[0], R,
-               P(q), s)
-        launch(f"kifmm_pack_sources_{sfx}", P(self.sx), P(self.sy), P(self.sz), P(q),
-               self.sx.shape[0], R, P(b["src4"]), s)
+        launch(f"kifmm_gather_pack_{sfx}", P(q_dev), P(self.s_perm), P(self.sx), P(self.sy),
+               P(self.sz), self.sx.shape[0], R, P(q), P(b["src4"]), s)
         # The near field (P2P) needs only the packed sources: with `overlap`
         # it runs on a low-priority side stream concurrently with the
         # far-field pipeline (mostly latency-bound small-level kernels), and

@@ -465,10 +465,8 @@ class DistributedFmm:
         q = b["q"]
         npts = d.sx.shape[0]
         # charges of the whole cloud (the near-field halo reads its neighbours')
-        launch(f"kifmm_gather_charges_{sfx}", P(q_dev), P(d.s_perm), npts, R, P(q),
-               stream_handle())
-        launch(f"kifmm_pack_sources_{sfx}", P(d.sx), P(d.sy), P(d.sz), P(q), npts, R,
-               P(b["src4"]), stream_handle())
+        launch(f"kifmm_gather_pack_{sfx}", P(q_dev), P(d.s_perm), P(d.sx), P(d.sy), P(d.sz), npts,
+               R, P(q), P(b["src4"]), stream_handle())
         # ---- P2M of the owned leaves
         lo, hi = sr[depth]
         if hi > lo:

@@ -20,7 +20,7 @@ def main(path, out=None):
     tot = sum(v[1] for v in agg.values())
     for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"| {k} | {n} | {t:.1f} | {100 * t / tot:.1f}% |")
-    starts = [i for i, s in enumerate(seq) if s[0].startswith("gather_charges")]
+    starts = [i for i, s in enumerate(seq) if s[0].startswith(("gather_charges", "gather_pack"))]
     if len(starts) >= 2:
         lines += ["", "One evaluate (second in the run), in launch order:", "",
                   "| kernel | grid | block | us |", "|---|---|---|---|"]
