@@ -435,6 +435,16 @@ int kifmm_gather_pack_f64(const double* q_in, const int64_t* perm, const double*
                           const double* sy, const double* sz, int64_t n, int64_t nrhs, double* qt,
                           double* src4, void* stream);
 
+/* L2P with an addend in tree order: out[perm[i]*nrhs + r] = addend[i*nrhs + r] +
+ * sum_e K(t_i, center_b + base_e) local[(b*nrhs + r)*ne + e] (engine.py:377-389,
+ * 399-404).  The overlapped evaluate passes the near-field totals
+ * (kifmm_p2p_mutual_reduce_f32 with perm = NULL): both passes then touch the
+ * totals coalesced and only the final store is permuted. */
+int kifmm_l2p_add_f32(const float* tx, const float* ty, const float* tz, const int32_t* tleaf_start,
+                      const int32_t* tleaf_count, int64_t n_tleaves, const double* centers,
+                      const double* base, int64_t ne, const float* local, int64_t nrhs,
+                      const int64_t* perm, const float* addend, float* out, void* stream);
+
 /* AoS source records for the leaf pass (16/32-byte aligned):
  * src4[(r*ns + j)*4 + {0,1,2,3}] = (x_j, y_j, z_j, q[j*nrhs + r]). */
 int kifmm_pack_sources_f32(const float* sx, const float* sy, const float* sz, const float* q,

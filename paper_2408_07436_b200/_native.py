@@ -78,6 +78,7 @@ SIGNATURES = {
                                  _P, _I, _P, _C, _P, _P, _P],
     "kifmm_pack_sources_f32": [_P, _P, _P, _P, _I, _I, _P, _P],
     "kifmm_pack_sources_f64": [_P, _P, _P, _P, _I, _I, _P, _P],
+    "kifmm_l2p_add_f32": [_P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _I, _P, _P, _P, _P],
     "kifmm_gather_pack_f32": [_P, _P, _P, _P, _P, _I, _I, _P, _P, _P],
     "kifmm_gather_pack_f64": [_P, _P, _P, _P, _P, _I, _I, _P, _P, _P],
     "kifmm_gather_charges_f32": [_P, _P, _I, _I, _P, _P],

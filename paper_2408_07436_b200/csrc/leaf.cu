@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(32 * kL2pWarps) l2p_x2_kernel(
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
     const double* __restrict__ centers, const double* __restrict__ base, int ne,
     const float* __restrict__ local, int64_t nrhs, const int64_t* __restrict__ perm,
-    int accumulate, float* __restrict__ out) {
+    int accumulate, const float* __restrict__ addend, float* __restrict__ out) {
   extern __shared__ __align__(16) float4 l2p_buf[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float4* buf = l2p_buf + w * ne;
@@ -511,8 +511,13 @@ __global__ void __launch_bounds__(32 * kL2pWarps) l2p_x2_kernel(
     const int64_t oa = perm ? perm[ia] : ia, ob = perm ? perm[ib] : ib;
     for (int64_t r = 0; r < nrhs; ++r) {
       const float* loc = local + (b * nrhs + r) * ne;
+      // addend: the near-field totals in TREE order (coalesced, and no load
+      // that depends on perm); else the values already in out (caller order)
       float pa = 0.f, pb = 0.f;
-      if (accumulate && sub == 0) {
+      if (sub == 0 && addend) {
+        if (live0) pa = addend[ia * nrhs + r];
+        if (live1) pb = addend[ib * nrhs + r];
+      } else if (accumulate && sub == 0) {
         if (live0) pa = out[oa * nrhs + r];
         if (live1) pb = out[ob * nrhs + r];
       }
@@ -532,8 +537,8 @@ __global__ void __launch_bounds__(32 * kL2pWarps) l2p_x2_kernel(
       }
       const float c = real_traits<float>::inv4pi();
       if (sub == 0) {
-        if (live0) out[oa * nrhs + r] = accumulate ? pa + fa * c : fa * c;
-        if (live1) out[ob * nrhs + r] = accumulate ? pb + fb * c : fb * c;
+        if (live0) out[oa * nrhs + r] = (accumulate || addend) ? pa + fa * c : fa * c;
+        if (live1) out[ob * nrhs + r] = (accumulate || addend) ? pb + fb * c : fb * c;
       }
     }
   }
@@ -638,7 +643,7 @@ int leaf_pass(const T* tx, const T* ty, const T* tz, const int32_t* ts, const in
       const size_t smem = (size_t)kL2pWarps * ne * sizeof(float4);
       l2p_x2_kernel<<<ceil_div(ntl, kL2pWarps), 32 * kL2pWarps, smem, (cudaStream_t)stream>>>(
           tx, ty, tz, ts, tcnt, ntl, centers, base, (int)ne, local, nrhs, perm, (parts & 4) != 0,
-          out);
+          nullptr, out);
       return launch_status();
     }
     if (!grad) {
@@ -693,6 +698,19 @@ int kifmm_leaf_pass_f32(const float* tx, const float* ty, const float* tz, const
                         float* out, void* s) {
   return leaf_pass<float>(tx, ty, tz, ts, tc, ntl, centers, base, ne, local, src4, ns, ss, sc, no,
                           nlf, nrhs, perm, parts, out, nullptr, s);
+}
+// L2P + addend: out[perm[i]] = addend[i] + L2P(i), addend in tree order (the
+// near-field totals of kifmm_p2p_mutual_reduce_f32 with perm = NULL).
+int kifmm_l2p_add_f32(const float* tx, const float* ty, const float* tz, const int32_t* ts,
+                      const int32_t* tc, int64_t ntl, const double* centers, const double* base,
+                      int64_t ne, const float* local, int64_t nrhs, const int64_t* perm,
+                      const float* addend, float* out, void* s) {
+  if (ntl < 0 || ne < 1 || ne > 256 || nrhs < 1 || !addend) return KIFMM_EARG;
+  if (ntl == 0) return 0;
+  const size_t smem = (size_t)kL2pWarps * ne * sizeof(float4);
+  l2p_x2_kernel<<<ceil_div(ntl, kL2pWarps), 32 * kL2pWarps, smem, (cudaStream_t)s>>>(
+      tx, ty, tz, ts, tc, ntl, centers, base, (int)ne, local, nrhs, perm, 0, addend, out);
+  return launch_status();
 }
 int kifmm_leaf_pass_f64(const double* tx, const double* ty, const double* tz, const int32_t* ts,
                         const int32_t* tc, int64_t ntl, const double* centers, const double* base,

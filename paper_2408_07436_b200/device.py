@@ -1067,6 +1067,11 @@ class DeviceFmm:
                     parts | guard_bit, P(out)] + grad_ptr
 
         mut = self.mutual
+        near_sorted = None
+        if mut is not None and not gradient and sfx == "f32" and n_e <= 256:
+            if "near_sorted" not in b:
+                b["near_sorted"] = self._alloc(nt * R, self.T)
+            near_sorted = b["near_sorted"]
         if mut is not None and gradient and "pmut4" not in b:
             b["pmut4"] = self._alloc(max(mut["total"], 1) * R * 4, self.T)
 
@@ -1080,14 +1085,22 @@ class DeviceFmm:
                        self.n_tgt[d], P(b["src4"]), self.sx.shape[0], P(self.near_off),
                        P(mut["pack"]), P(mut["order"]), R, mut["total"], int(self.p2p_guard),
                        P(pm), stream)
+                # float32 potential: totals in tree order (coalesced), added by
+                # the final L2P pass, which alone un-permutes
                 launch(f"kifmm_p2p_mutual_reduce_{g_}{sfx}", P(self.t_start), P(self.t_count),
-                       self.n_tgt[d], R, P(self.t_perm), P(mut["base"]), P(mut["nlow"]),
-                       mut["total"], P(pm), P(out), *grad_ptr, stream)
+                       self.n_tgt[d], R, None if near_sorted is not None else P(self.t_perm),
+                       P(mut["base"]), P(mut["nlow"]), mut["total"], P(pm),
+                       P(near_sorted) if near_sorted is not None else P(out), *grad_ptr, stream)
             else:
                 launch(leaf_name, *leaf_args(2), stream)             # P2P, overwrite
 
         def l2p_final(stream):
-            launch(leaf_name, *leaf_args(1 | 4), stream)             # L2P, accumulate
+            if near_sorted is not None:
+                launch("kifmm_l2p_add_f32", P(self.tx), P(self.ty), P(self.tz), P(self.t_start),
+                       P(self.t_count), self.n_tgt[d], P(self.t_centers), P(self.equiv_base), n_e,
+                       P(b["loc"][d]), R, P(self.t_perm), P(near_sorted), P(out), stream)
+            else:
+                launch(leaf_name, *leaf_args(1 | 4), stream)         # L2P, accumulate
 
         side = self.side_stream
 
