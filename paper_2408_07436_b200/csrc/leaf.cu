@@ -481,8 +481,10 @@ __global__ void __launch_bounds__(32 * kWarps, KIFMM_LEAF_MINB) leaf_pass_x2_ker
 // the near-field machinery, 8 warps per CTA and 0.9 KB of shared memory per
 // warp, so many leaves are in flight at once (the pass is latency-bound:
 // ~56 interactions per target).
-constexpr int kL2pWarps = 8;
-__global__ void __launch_bounds__(32 * kL2pWarps) l2p_x2_kernel(
+// one warp (= one leaf) per CTA, 32 CTAs per SM: a warp that is done frees
+// its slot at once (config 2: 43.5 us; 8-warp CTAs 53 us, 4-warp x 10: 47.6 us)
+constexpr int kL2pWarps = 1;
+__global__ void __launch_bounds__(32 * kL2pWarps, 32) l2p_x2_kernel(
     const float* __restrict__ tx, const float* __restrict__ ty, const float* __restrict__ tz,
     const int32_t* __restrict__ tstart, const int32_t* __restrict__ tcount, int64_t n_tleaves,
     const double* __restrict__ centers, const double* __restrict__ base, int ne,
@@ -547,14 +549,16 @@ __global__ void __launch_bounds__(32 * kL2pWarps) l2p_x2_kernel(
 // float32 P2M check potentials on packed FP32: every lane evaluates two
 // check points (c, c + 32) of its leaf against the leaf's sources, staged
 // once per warp (one 16-byte shared load feeds two interactions).
-__global__ void __launch_bounds__(32 * kWarps) p2m_check_x2_kernel(
+// (single-warp CTAs as for the L2P pass: 37 vs 40 us at config 2)
+constexpr int kP2mWarps = 1;
+__global__ void __launch_bounds__(32 * kP2mWarps, 32) p2m_check_x2_kernel(
     const float* __restrict__ sx, const float* __restrict__ sy, const float* __restrict__ sz,
     const float* __restrict__ q, int64_t nrhs, const int32_t* __restrict__ leaf_start,
     const int32_t* __restrict__ leaf_count, int64_t n_leaves, const double* __restrict__ centers,
     const double* __restrict__ base, int64_t nc, float* __restrict__ phi) {
-  __shared__ __align__(16) float4 buf[kWarps][64];
+  __shared__ __align__(16) float4 buf[kP2mWarps][64];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t leaf = (int64_t)blockIdx.x * kWarps + w;
+  const int64_t leaf = (int64_t)blockIdx.x * kP2mWarps + w;
   if (leaf >= n_leaves) return;
   const int64_t s0 = leaf_start[leaf];
   const int cnt = leaf_count[leaf];
@@ -620,7 +624,7 @@ int p2m_check(const T* sx, const T* sy, const T* sz, const T* q, int64_t nrhs, c
   if (nl < 0 || nc < 1 || nrhs < 1) return KIFMM_EARG;
   if (nl == 0) return 0;
   if constexpr (sizeof(T) == 4) {
-    p2m_check_x2_kernel<<<ceil_div(nl, kWarps), 32 * kWarps, 0, (cudaStream_t)stream>>>(
+    p2m_check_x2_kernel<<<ceil_div(nl, kP2mWarps), 32 * kP2mWarps, 0, (cudaStream_t)stream>>>(
         sx, sy, sz, q, nrhs, ls, lc, nl, centers, base, nc, phi);
     return launch_status();
   }
