@@ -29,7 +29,9 @@ template <typename T> struct vec4;
 template <> struct vec4<float> { using v = float4; };
 template <> struct vec4<double> { using v = double4; };
 
-constexpr int kWarps = 4;
+// one warp (= one leaf) per CTA: a finished leaf frees its slot at once (config 3:
+// gradient L2P 840 -> 707 us, P2M check 422 -> 385 us against 4-warp CTAs)
+constexpr int kWarps = 1;
 
 template <typename T>
 __global__ void __launch_bounds__(32 * kWarps) p2m_check_kernel(
