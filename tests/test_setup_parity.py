@@ -174,3 +174,20 @@ def test_tmem_core_packing_layout():
             dense = blk.transpose(0, 2, 1, 3).reshape(kp, kp)
             assert np.array_equal(dense[:13, :13], src[t])
             assert not dense[13:].any() and not dense[:, 13:].any()
+
+
+def test_factored_sweep_widths():
+    """Width classes of the factored float64 sweep (device.factored_widths):
+    ktp = 16 * ntw * slabs covers the rank with at most 10 fragments per slab
+    (csrc/m2l_factored.cu dispatches ntw = 1..10); rank 0 stays 0."""
+    from paper_2408_07436_b200.device import factored_widths
+    ranks = np.array([0, 1, 16, 17, 54, 160, 161, 198, 320, 321, 483])
+    ktp, ntw, slabs = factored_widths(ranks)
+    assert ktp[0] == 0 and ntw[0] == 0
+    live = ranks > 0
+    assert np.all(ktp[live] >= ranks[live]) and np.all(ktp % 16 == 0)
+    assert np.all(ktp[live] == 16 * ntw[live] * slabs[live])
+    assert np.all((ntw[live] >= 1) & (ntw[live] <= 10))
+    # no more padding than one 16-column step per slab
+    assert np.all(ktp[live] - ranks[live] < 16 * slabs[live] + 16)
+    assert list(ktp[[2, 3, 5, 6, 7]]) == [16, 32, 160, 192, 224]
