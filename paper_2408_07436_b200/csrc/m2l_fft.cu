@@ -31,9 +31,24 @@ __device__ __forceinline__ void cfma(C& acc, C a, C b) {
   acc.y += a.x * b.y + a.y * b.x;
 }
 
-// 512 threads per CTA (config 3 level 5: forward 670 us; 256: 1000 us, 1024
-// spills: 700 / 1160 us; 4 or 2 boxes per CTA for more CTAs per SM: slower)
-constexpr int kThreads = 512;
+// Threads per CTA: the y pass has bpc * P * (P + 1) work items (576 at p = 8
+// with 8 boxes per CTA) and the x pass twice that, so the block is sized to
+// that count rounded up to a warp (one round of the y pass, two of the x
+// pass), within [128, kMaxThreads].  (config 3 level 5 with 512 threads:
+// forward 670 us; 256: 1000 us; 1024 spills: 700 / 1160 us; 4 or 2 boxes
+// per CTA for more CTAs per SM: slower)
+constexpr int kMaxThreads = 640;
+constexpr size_t kSmemLimit = 227 * 1024;
+// Boxes per CTA: the largest of 8/4/2/1 whose scratch fits (0: none).
+constexpr int boxes_per_cta(size_t head, size_t box) {
+  for (int bpc = 8; bpc >= 1; bpc /= 2)
+    if (head + bpc * box <= kSmemLimit) return bpc;
+  return 0;
+}
+constexpr int fft_threads(int bpc, int p) {
+  const int t = (bpc * p * (p + 1) + 31) / 32 * 32;
+  return t < 128 ? 128 : (t > kMaxThreads ? kMaxThreads : t);
+}
 constexpr int kMaxP = 12;
 
 // Surface lattice of the p^3 cube in lexicographic order -> flat index
@@ -97,10 +112,13 @@ struct FftShape {
   // inverse: Y1 [P][N][NH], Y2 [P][P][NH]
   static constexpr size_t iy1 = (size_t)P * N * NH * sizeof(C);
   static constexpr size_t ibox = pad_box<C>(iy1 + (size_t)P * P * NH * sizeof(C));
+  static constexpr int fbpc = boxes_per_cta(head, fbox), ibpc = boxes_per_cta(head, ibox);
+  static constexpr int fthreads = fft_threads(fbpc ? fbpc : 1, P);
+  static constexpr int ithreads = fft_threads(ibpc ? ibpc : 1, P);
 };
 
 template <typename T, int P>
-__global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restrict__ mult,
+__global__ void __launch_bounds__(FftShape<T, P>::fthreads) fft_forward_kernel(const T* __restrict__ mult,
                                                                int64_t nrhs, int bpc,
                                                                const int32_t* __restrict__ slot_box,
                                                                int64_t nsc,
@@ -124,16 +142,16 @@ __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restri
   const int64_t r = blockIdx.y;
   build_twiddles<T>(N, tw);
   build_lattice(P, lat);
-  for (int e = threadIdx.x; e < bpc * P3; e += kThreads) CUBE(e % bpc)[e / bpc] = T(0);
+  for (int e = threadIdx.x; e < bpc * P3; e += (int)blockDim.x) CUBE(e % bpc)[e / bpc] = T(0);
   __syncthreads();
-  for (int e = threadIdx.x; e < bpc * NE; e += kThreads) {
+  for (int e = threadIdx.x; e < bpc * NE; e += (int)blockDim.x) {
     const int b = e / NE, s = e - b * NE;
     const int32_t box = slot_box[cluster * 8 + child0 + b];
     if (box >= 0) CUBE(b)[lat[s]] = mult[((int64_t)box * nrhs + r) * NE + s];
   }
   __syncthreads();
   // z: X1[i0][i1][k2] = sum_{i2} cube[i0][i1][i2] w^{k2 (i2 + P)}; thread per line.
-  for (int e = threadIdx.x; e < bpc * P * P; e += kThreads) {
+  for (int e = threadIdx.x; e < bpc * P * P; e += (int)blockDim.x) {
     const int b = e % bpc, i01 = e / bpc;
     T line[P];
 #pragma unroll
@@ -153,7 +171,7 @@ __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restri
   }
   __syncthreads();
   // y: X2[i0][k1][k2] = sum_{i1} X1[i0][i1][k2] w^{k1 (i1 + P)} (overwrites the cube).
-  for (int e = threadIdx.x; e < bpc * P * NH; e += kThreads) {
+  for (int e = threadIdx.x; e < bpc * P * NH; e += (int)blockDim.x) {
     const int b = e % bpc, rem = e / bpc;
     const int k2 = rem % NH, i0 = rem / NH;
     C in[P];
@@ -170,7 +188,7 @@ __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restri
   }
   __syncthreads();
   // x: spectrum[k0][k1][k2] = sum_{i0} X2[i0][k1][k2] w^{k0 (i0 + P)}, child fastest.
-  for (int e = threadIdx.x; e < N * NH * bpc; e += kThreads) {
+  for (int e = threadIdx.x; e < N * NH * bpc; e += (int)blockDim.x) {
     const int b = e % bpc, k12 = e / bpc;
     C in[P];
 #pragma unroll
@@ -189,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) fft_forward_kernel(const T* __restri
 }
 
 template <typename T, int P>
-__global__ void __launch_bounds__(kThreads) fft_inverse_kernel(const typename cx<T>::v* __restrict__ phat,
+__global__ void __launch_bounds__(FftShape<T, P>::ithreads) fft_inverse_kernel(const typename cx<T>::v* __restrict__ phat,
                                                                int64_t nrhs, int bpc,
                                                                const int32_t* __restrict__ slot_box,
                                                                int64_t ntc, T scale,
@@ -212,7 +230,7 @@ __global__ void __launch_bounds__(kThreads) fft_inverse_kernel(const typename cx
   build_lattice(P, lat);
   __syncthreads();
   // x: Y1[i0][k1][k2] = sum_{k0} X[k0][k1][k2] w^{-k0 i0}, i0 < P; child fastest.
-  for (int e = threadIdx.x; e < N * NH * bpc; e += kThreads) {
+  for (int e = threadIdx.x; e < N * NH * bpc; e += (int)blockDim.x) {
     const int b = e % bpc, k12 = e / bpc;
     const C* src = phat + (((int64_t)k12 * ntc + cluster) * 8 + child0 + b) * nrhs + r;
     const int64_t fstride = (int64_t)N * NH * ntc * 8 * nrhs;
@@ -233,7 +251,7 @@ __global__ void __launch_bounds__(kThreads) fft_inverse_kernel(const typename cx
   }
   __syncthreads();
   // y: Y2[i0][i1][k2] = sum_{k1} Y1[i0][k1][k2] w^{-k1 i1}, i1 < P.
-  for (int e = threadIdx.x; e < P * NH * bpc; e += kThreads) {
+  for (int e = threadIdx.x; e < P * NH * bpc; e += (int)blockDim.x) {
     const int b = e % bpc, rem = e / bpc;
     const int k2 = rem % NH, i0 = rem / NH;
     C in[N];
@@ -256,7 +274,7 @@ __global__ void __launch_bounds__(kThreads) fft_inverse_kernel(const typename cx
   // k2 = 0 and Nyquist bins are ignored as in pocketfft's c2r), read the
   // lattice, normalise by n^3 and apply the level scale.
   const T norm = T(1) / (T)(N * N * N);
-  for (int e = threadIdx.x; e < NE * bpc; e += kThreads) {
+  for (int e = threadIdx.x; e < NE * bpc; e += (int)blockDim.x) {
     const int b = e % bpc, s = e / bpc;
     const int32_t box = slot_box[cluster * 8 + child0 + b];
     if (box < 0) continue;
@@ -278,23 +296,16 @@ size_t forward_smem(int bpc) { return FftShape<T, P>::head + bpc * FftShape<T, P
 template <typename T, int P>
 size_t inverse_smem(int bpc) { return FftShape<T, P>::head + bpc * FftShape<T, P>::ibox; }
 
-// Boxes per CTA: the largest of 8/4/2/1 whose scratch fits.
-int pick_bpc(size_t (*smem)(int), size_t limit) {
-  for (int bpc = 8; bpc >= 1; bpc /= 2)
-    if (smem(bpc) <= limit) return bpc;
-  return 0;
-}
-
 template <typename T, int P>
 int forward_p(const T* mult, int64_t nrhs, const int32_t* slot_box, int64_t nsc,
               const int32_t* cluster_list, int64_t nclusters, T* qhat, cudaStream_t stream) {
   using C = typename cx<T>::v;
-  const int bpc = pick_bpc(forward_smem<T, P>, 227 * 1024);
+  constexpr int bpc = FftShape<T, P>::fbpc;
   if (!bpc) return KIFMM_EARG;
   const size_t smem = forward_smem<T, P>(bpc);
   set_max_smem((const void*)fft_forward_kernel<T, P>, smem);
   dim3 grid((unsigned)(nclusters * (8 / bpc)), (unsigned)nrhs);
-  fft_forward_kernel<T, P><<<grid, kThreads, smem, stream>>>(
+  fft_forward_kernel<T, P><<<grid, FftShape<T, P>::fthreads, smem, stream>>>(
       mult, nrhs, bpc, slot_box, nsc, cluster_list, reinterpret_cast<C*>(qhat));
   return launch_status();
 }
@@ -303,12 +314,12 @@ template <typename T, int P>
 int inverse_p(const T* phat, int64_t nrhs, const int32_t* slot_box, int64_t ntc, double scale,
               T* check, cudaStream_t stream) {
   using C = typename cx<T>::v;
-  const int bpc = pick_bpc(inverse_smem<T, P>, 227 * 1024);
+  constexpr int bpc = FftShape<T, P>::ibpc;
   if (!bpc) return KIFMM_EARG;
   const size_t smem = inverse_smem<T, P>(bpc);
   set_max_smem((const void*)fft_inverse_kernel<T, P>, smem);
   dim3 grid((unsigned)(ntc * (8 / bpc)), (unsigned)nrhs);
-  fft_inverse_kernel<T, P><<<grid, kThreads, smem, stream>>>(
+  fft_inverse_kernel<T, P><<<grid, FftShape<T, P>::ithreads, smem, stream>>>(
       reinterpret_cast<const C*>(phat), nrhs, bpc, slot_box, ntc, (T)scale, check);
   return launch_status();
 }
