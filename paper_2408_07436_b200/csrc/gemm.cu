@@ -297,7 +297,7 @@ int gemm_ts(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_
 // the fragment loads conflict-free.
 constexpr int DBM = 128, DBN = 64, DBK = 16;
 constexpr int DAS = DBK + 4;    // A tile row stride (doubles)
-constexpr int DBS = DBN + 8;    // B tile row stride (doubles)
+constexpr int DBS = DBN + 4;    // B tile row stride (doubles): = 4 mod 16, the 16 lanes of a half-warp (rows lane & 3, columns lane >> 2) hit 16 distinct bank pairs
 
 __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
