@@ -384,7 +384,10 @@ __global__ void __launch_bounds__(256, 1) hadamard_tiled_dmma_kernel(
     C* kd = ks + b * 26 * 64;
     for (int e = tid; e < 26 * 64; e += 256) {
       const int o = e >> 6, tau = (e >> 3) & 7, sg = e & 7;
-      cp_async_c(kd + (o * 8 + sg) * 8 + tau, kf + e, true);
+      // tau ^ 2 in odd sigma rows: a B-fragment load touches rows sigma,
+      // sigma + 1 (16 doubles apart: the same banks) at columns tau, tau + 1 -
+      // the swizzle moves the odd row's pair to the other bank group
+      cp_async_c(kd + (o * 8 + sg) * 8 + (tau ^ ((sg & 1) << 1)), kf + e, true);
     }
     C* qd = qs + b * QROWS * 8;
     const C* qf = qhat + f * nsc * 8 * nrhs + r;
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(256, 1) hadamard_tiled_dmma_kernel(
 #pragma unroll
           for (int jn = 0; jn < 2; ++jn) {
             const int tau = 4 * jn + (g8 >> 1);
-            const double v = ko[(sga * 8 + tau) * 2 + comp];
+            const double v = ko[(sga * 8 + (tau ^ ((sga & 1) << 1))) * 2 + comp];
             bf[jn] = __longlong_as_double(__double_as_longlong(v) ^ (long long)neg);
           }
 #pragma unroll
